@@ -1,0 +1,146 @@
+/*
+ * vpipg.h -- C-ABI of the B200 point-inclusion engine (libvpipg.so).
+ *
+ * This is the drop-in boundary for the reference's hot path (arxiv 2007.15385,
+ * the `vpip` C++ library, /root/reference/proj). Each entry point names the
+ * reference interface it replaces. The reference has no FFI of its own; its
+ * callers are C++ (the CLI, the bench harness, the tests), so the binding a
+ * maintainer adds is the C++ shim in include/vpip/ headers (same signatures as
+ * proj/include/vpip/, implemented over this ABI), or a ctypes/cffi stub
+ * from Python -- see INTEGRATION.md.
+ *
+ * Conventions
+ *  - Return 0 on success. 1..7 are vpip::ErrorCode in declaration order
+ *    (proj/include/vpip/error.hpp:23-31): 1 TooFewVertices, 2 NotConvex,
+ *    3 DegenerateEdge, 4 NonFinite, 5 GeneratorCollision, 6 InvalidParameter,
+ *    7 ParseError. 100 + cudaError_t for CUDA failures, 300 when the device
+ *    is not an sm_100 part. No exception crosses the ABI.
+ *  - `stream` is a cudaStream_t passed as void* (NULL = legacy default).
+ *    Device-pointer calls are asynchronous on that stream; the caller owns
+ *    point, mask and count buffers; the library owns a handle's tables.
+ *  - Handles are immutable after prepare: any number of threads and streams
+ *    may use one handle concurrently (engines.hpp:80-84).
+ *  - Masks: `mask_words` holds ceil(m/32) little-endian u32 words; bit b of
+ *    word w is point 32w+b. As a byte stream this is exactly the PIPM payload
+ *    (io.cpp:272-279: bit j of the payload is point j, LSB-first).
+ *    `mask_bytes` is the reference InclusionMask layout (engines.hpp:53-54):
+ *    one byte per point, 1 = inside. Either may be NULL.
+ *  - `d_inside` (device u64, may be NULL) is ACCUMULATED into: the fused
+ *    count_inside (engines.cpp:215-217). Zero it before the first call.
+ *  - dtype VPIPG_F64: the reference's own fp64 arithmetic, operation for
+ *    operation (no FMA contraction) -> masks bit-identical to the reference.
+ *    dtype VPIPG_F32: float32 points, fast affine kernels; masks equal the
+ *    reference's on the same (f32-rounded) points for every point farther than
+ *    1e-5 * max(1,|x|,|y|,extent) from every edge line.
+ */
+#ifndef VPIPG_H
+#define VPIPG_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define VPIPG_ABI_VERSION 1
+
+/* engines: vpip::EngineKind order (engines.hpp:64-73) */
+#define VPIPG_ENGINE_VORONOI 0
+#define VPIPG_ENGINE_OFFSET 1
+#define VPIPG_ENGINE_CROSSING 2
+
+/* preparation kinds (bit set) */
+#define VPIPG_KIND_VORONOI (1u << 0)
+#define VPIPG_KIND_OFFSET (1u << 1)
+#define VPIPG_KIND_CROSSING (1u << 2)
+#define VPIPG_KIND_ALL 7u
+
+/* point dtypes */
+#define VPIPG_F64 0
+#define VPIPG_F32 1
+
+#define VPIPG_ERR_CUDA 100
+#define VPIPG_ERR_ARCH 300
+
+typedef struct vpipg_poly vpipg_poly;
+
+/* Human-readable text for a return code (error.hpp:33-45 for 1..7). */
+const char* vpipg_strerror(int code);
+int vpipg_abi_version(void);
+
+/* Replaces: validate_polygon (geometry.cpp:53-98, geometry.hpp:110-111) +
+ * to_voronoi (voronoi.cpp:60-71, voronoi.hpp:67-70) + the sign-of-offset and
+ * ray-crossing per-edge setup hoisted out of engines.cpp:146-149, :176-186.
+ * Vertices are host f64 arrays. When `kinds` includes VORONOI or OFFSET the
+ * polygon is validated with the reference rules (error codes 1-4) and, for
+ * VORONOI, converted on the device (centroid + one reflection per edge, the
+ * reference's operation order; code 5 on a collision). CROSSING alone takes
+ * the raw vertices unvalidated, any orientation (vpip.cpp:120-128). The
+ * call is synchronous (it returns the status) and uses `stream`. */
+int vpipg_prepare(const double* vx, const double* vy, uint32_t n, uint32_t kinds, int device,
+                  void* stream, vpipg_poly** out);
+
+/* Replaces the GeneratorSet argument of voronoi_contains_batch
+ * (engines.hpp:90-96): a handle built from an explicit generator set
+ * (inner point, n outer points) instead of a polygon. VORONOI only. */
+int vpipg_prepare_generators(const double* inner_xy, const double* outer_xy, uint32_t n,
+                             int device, void* stream, vpipg_poly** out);
+
+void vpipg_destroy(vpipg_poly* poly);
+
+/* n, prepared kinds, and whether validation reversed a clockwise input
+ * (ConvexPolygon::was_reversed, geometry.hpp:95). Any pointer may be NULL. */
+int vpipg_poly_info(const vpipg_poly* poly, uint32_t* n, uint32_t* kinds, int* reversed);
+
+/* Reads back the generator set built on the device (GeneratorSet,
+ * voronoi.hpp:58-65): inner_xy[2], outer_xy[2n]. Synchronous. */
+int vpipg_poly_generators(const vpipg_poly* poly, double* inner_xy, double* outer_xy);
+
+/* Reads back the validated CCW vertices (ConvexPolygon::vertices). */
+int vpipg_poly_vertices(const vpipg_poly* poly, double* vx, double* vy);
+
+/* Replaces voronoi_contains_batch (engines.cpp:243-254),
+ * sign_of_offset_contains_batch (:320-329), ray_crossing_contains_batch
+ * (:369-378) and count_inside (:215-217), fused. xs, ys, mask_words,
+ * mask_bytes, d_inside are DEVICE pointers. Asynchronous on `stream`. */
+int vpipg_test(const vpipg_poly* poly, int engine, int dtype, const void* xs, const void* ys,
+               uint64_t m, uint32_t* mask_words, uint8_t* mask_bytes,
+               unsigned long long* d_inside, void* stream);
+
+/* Same with HOST buffers (pageable or pinned): chunked host->device copies,
+ * the test kernel and device->host mask copies are pipelined over two
+ * streams on `device`. Synchronous; *inside receives the count (may be NULL).
+ * This is the path the vpip:: C++ shim uses. */
+int vpipg_test_host(const vpipg_poly* poly, int engine, int dtype, const void* xs,
+                    const void* ys, uint64_t m, uint32_t* mask_words, uint8_t* mask_bytes,
+                    uint64_t* inside);
+
+/* Instrumented work counters of voronoi_contains_batch(..., BatchStats&)
+ * (engines.cpp:256-273): the branch-free kernels perform exactly
+ * (n+1)*m distance evaluations and n*m comparisons. */
+int vpipg_voronoi_work(const vpipg_poly* poly, uint64_t m, uint64_t* distance_evaluations,
+                       uint64_t* comparisons);
+
+/* Counter-based uniform points on the device: point j (j = first..first+m-1)
+ * is (min_x + w*U(mix_seed(seed, 2j)), min_y + h*U(mix_seed(seed, 2j+1))),
+ * U = top-53-bit uniform (sampling.cpp:31-33), mix_seed = sampling.cpp:107-112,
+ * stored as f64 or rounded to f32. Input generation, not timed work. */
+int vpipg_fill_uniform_points(uint64_t seed, uint64_t first, uint64_t m, double min_x,
+                              double min_y, double max_x, double max_y, int dtype, void* xs,
+                              void* ys, void* stream);
+
+/* Host-side seeded polygon and point samplers with the reference's exact
+ * semantics (sampling.cpp:50-105), for building workloads. Vertices come
+ * back validated (CCW). */
+uint64_t vpipg_mix_seed(uint64_t seed, uint64_t salt);
+int vpipg_regular_polygon(uint32_t n, double r, double cx, double cy, double* vx, double* vy);
+int vpipg_random_convex_polygon(uint32_t n, uint64_t seed, double r, double cx, double cy,
+                                double* vx, double* vy);
+int vpipg_sample_points(uint64_t count, double min_x, double min_y, double max_x, double max_y,
+                        uint64_t seed, double* xs, double* ys);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* VPIPG_H */

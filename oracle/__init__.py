@@ -1,0 +1,301 @@
+"""CPU oracle for the B200 point-inclusion engine -- TEST INFRASTRUCTURE ONLY.
+
+Two checkers, both loaded with ctypes:
+  * `Oracle`    -- liboracle.so, the plain-C restatement of the reference path
+                   (oracle/vpip_oracle.c, every function cites its reference
+                   file:line), compiled with -ffp-contract=off;
+  * `Reference` -- oracle/_ref/libvpip_ref.so, the UNMODIFIED reference sources
+                   (/root/reference/proj/src) compiled by oracle/Makefile.
+
+Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline /
+--impl reference legs may import this package, and only as the checker or the
+CPU baseline -- never as the thing measured on the GPU path.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import subprocess
+from pathlib import Path
+
+import numpy as np
+
+HERE = Path(__file__).resolve().parent
+ORACLE_SO = HERE / "liboracle.so"
+REF_SO = HERE / "_ref" / "libvpip_ref.so"
+REF_ACCEPTANCE = HERE / "_ref" / "vpip_acceptance"
+REFERENCE_SRC = Path("/root/reference/proj")
+
+_D = C.POINTER(C.c_double)
+_U8 = C.POINTER(C.c_uint8)
+
+
+def _d(a):
+    return a.ctypes.data_as(_D)
+
+
+def build(ref: bool | None = None) -> None:
+    """Compile liboracle.so, and oracle/_ref when the reference tree is present."""
+    subprocess.run(["make", "-s", "-C", str(HERE), "all"], check=True)
+    if ref is None:
+        ref = REFERENCE_SRC.exists()
+    if ref:
+        subprocess.run(["make", "-s", "-C", str(HERE), "ref"], check=True)
+
+
+class Oracle:
+    """numpy-facing wrapper of the C restatement."""
+
+    def __init__(self):
+        if not ORACLE_SO.exists():
+            build(ref=False)
+        L = C.CDLL(str(ORACLE_SO))
+        sz = C.c_size_t
+        L.vo_mix_seed.restype = C.c_uint64
+        L.vo_mix_seed.argtypes = [C.c_uint64, C.c_uint64]
+        L.vo_sample_points.argtypes = [sz, C.c_double, C.c_double, C.c_double, C.c_double,
+                                       C.c_uint64, _D, _D]
+        L.vo_regular_polygon.argtypes = [sz, C.c_double, C.c_double, C.c_double, _D, _D]
+        L.vo_random_convex_polygon.argtypes = [sz, C.c_uint64, C.c_double, C.c_double,
+                                               C.c_double, _D, _D]
+        L.vo_validate_polygon.argtypes = [_D, _D, sz, C.c_double, C.POINTER(C.c_int)]
+        L.vo_centroid.argtypes = [_D, _D, sz, _D, _D]
+        L.vo_signed_area.restype = C.c_double
+        L.vo_signed_area.argtypes = [_D, _D, sz]
+        L.vo_edge_coefficients.argtypes = [C.c_double] * 4 + [_D]
+        L.vo_reflect_generator.argtypes = [C.c_double, C.c_double, _D, _D, _D]
+        L.vo_foot_of_perpendicular.argtypes = [C.c_double, C.c_double, _D, _D, _D]
+        L.vo_to_voronoi.argtypes = [_D, _D, sz, _D, _D]
+        L.vo_edge_line_distance.restype = C.c_double
+        L.vo_edge_line_distance.argtypes = [_D, _D, sz, C.c_double, C.c_double]
+        for f in ("vo_voronoi_batch",):
+            getattr(L, f).argtypes = [_D, _D, sz, _D, _D, sz, _U8]
+        for f in ("vo_offset_batch", "vo_ray_batch"):
+            getattr(L, f).argtypes = [_D, _D, sz, _D, _D, sz, _U8]
+        L.vo_voronoi_contains.argtypes = [_D, _D, sz, C.c_double, C.c_double]
+        for f in ("vo_offset_contains", "vo_ray_contains", "vo_ray_count"):
+            getattr(L, f).argtypes = [_D, _D, sz, C.c_double, C.c_double]
+        L.vo_count_inside.restype = C.c_uint64
+        L.vo_count_inside.argtypes = [_U8, sz]
+        L.vo_pack_mask_lsb.argtypes = [_U8, sz, _U8]
+        L.vo_counter_points_f32.argtypes = [C.c_uint64, C.c_uint64, sz, C.c_double, C.c_double,
+                                            C.c_double, C.c_double, C.POINTER(C.c_float),
+                                            C.POINTER(C.c_float)]
+        self.L = L
+
+    # sampling
+    def mix_seed(self, seed, salt):
+        return self.L.vo_mix_seed(seed, salt)
+
+    def sample_points(self, count, box, seed):
+        xs, ys = np.zeros(count), np.zeros(count)
+        rc = self.L.vo_sample_points(count, *map(float, box), seed, _d(xs), _d(ys))
+        if rc:
+            raise ValueError(rc)
+        return xs, ys
+
+    def regular_polygon(self, n, r=1.0, center=(0.0, 0.0)):
+        vx, vy = np.zeros(n), np.zeros(n)
+        rc = self.L.vo_regular_polygon(n, r, center[0], center[1], _d(vx), _d(vy))
+        if rc:
+            raise ValueError(rc)
+        return vx, vy
+
+    def random_convex_polygon(self, n, seed, r=1.0, center=(0.0, 0.0)):
+        vx, vy = np.zeros(n), np.zeros(n)
+        rc = self.L.vo_random_convex_polygon(n, seed, r, center[0], center[1], _d(vx), _d(vy))
+        if rc:
+            raise ValueError(rc)
+        return vx, vy
+
+    def counter_points_f32(self, seed, first, count, box):
+        xs, ys = np.zeros(count, np.float32), np.zeros(count, np.float32)
+        fp = C.POINTER(C.c_float)
+        self.L.vo_counter_points_f32(seed, first, count, *map(float, box),
+                                     xs.ctypes.data_as(fp), ys.ctypes.data_as(fp))
+        return xs, ys
+
+    # geometry / conversion
+    def validate(self, vx, vy, eps=1e-12):
+        vx, vy = np.array(vx, dtype=np.float64), np.array(vy, dtype=np.float64)
+        rev = C.c_int()
+        rc = self.L.vo_validate_polygon(_d(vx), _d(vy), vx.size, eps, C.byref(rev))
+        return rc, vx, vy, bool(rev.value)
+
+    def centroid(self, vx, vy):
+        cx, cy = C.c_double(), C.c_double()
+        self.L.vo_centroid(_d(vx), _d(vy), vx.size, C.byref(cx), C.byref(cy))
+        return cx.value, cy.value
+
+    def edge_coefficients(self, qi, qj):
+        abc = np.zeros(3)
+        rc = self.L.vo_edge_coefficients(qi[0], qi[1], qj[0], qj[1], _d(abc))
+        return rc, abc
+
+    def reflect(self, p, abc):
+        rx, ry = C.c_double(), C.c_double()
+        abc = np.asarray(abc, dtype=np.float64)
+        rc = self.L.vo_reflect_generator(p[0], p[1], _d(abc), C.byref(rx), C.byref(ry))
+        return rc, (rx.value, ry.value)
+
+    def foot(self, p, abc):
+        fx, fy = C.c_double(), C.c_double()
+        abc = np.asarray(abc, dtype=np.float64)
+        self.L.vo_foot_of_perpendicular(p[0], p[1], _d(abc), C.byref(fx), C.byref(fy))
+        return fx.value, fy.value
+
+    def to_voronoi(self, vx, vy):
+        inner, outer = np.zeros(2), np.zeros((vx.size, 2))
+        rc = self.L.vo_to_voronoi(_d(vx), _d(vy), vx.size, _d(inner), _d(outer))
+        return rc, inner, outer
+
+    def edge_line_distance(self, vx, vy, px, py):
+        return self.L.vo_edge_line_distance(_d(vx), _d(vy), vx.size, px, py)
+
+    def edge_line_distances(self, vx, vy, xs, ys):
+        """Vectorised min over edges of |a x + b y + c| / hypot(a, b) (voronoi.cpp:73-82)."""
+        xs = np.asarray(xs, dtype=np.float64)
+        ys = np.asarray(ys, dtype=np.float64)
+        d = np.full(xs.shape, np.inf)
+        n = vx.size
+        for k in range(n):
+            k1 = (k + 1) % n
+            a = vy[k] - vy[k1]
+            b = vx[k1] - vx[k]
+            c = -(a * vx[k] + b * vy[k])
+            d = np.minimum(d, np.abs(a * xs + b * ys + c) / np.hypot(a, b))
+        return d
+
+    # engines
+    def voronoi_batch(self, inner, outer, xs, ys):
+        xs, ys = np.ascontiguousarray(xs, np.float64), np.ascontiguousarray(ys, np.float64)
+        out = np.zeros(xs.size, np.uint8)
+        inner = np.ascontiguousarray(inner, np.float64)
+        outer = np.ascontiguousarray(outer, np.float64)
+        self.L.vo_voronoi_batch(_d(inner), _d(outer), outer.shape[0], _d(xs), _d(ys), xs.size,
+                                out.ctypes.data_as(_U8))
+        return out
+
+    def offset_batch(self, vx, vy, xs, ys):
+        xs, ys = np.ascontiguousarray(xs, np.float64), np.ascontiguousarray(ys, np.float64)
+        out = np.zeros(xs.size, np.uint8)
+        self.L.vo_offset_batch(_d(vx), _d(vy), vx.size, _d(xs), _d(ys), xs.size,
+                               out.ctypes.data_as(_U8))
+        return out
+
+    def ray_batch(self, vx, vy, xs, ys):
+        xs, ys = np.ascontiguousarray(xs, np.float64), np.ascontiguousarray(ys, np.float64)
+        vx, vy = np.ascontiguousarray(vx, np.float64), np.ascontiguousarray(vy, np.float64)
+        out = np.zeros(xs.size, np.uint8)
+        self.L.vo_ray_batch(_d(vx), _d(vy), vx.size, _d(xs), _d(ys), xs.size,
+                            out.ctypes.data_as(_U8))
+        return out
+
+    def masks(self, vx_raw, vy_raw, xs, ys):
+        """All three engines the way the reference CLI builds them (vpip.cpp:120-133)."""
+        rc, vx, vy, _ = self.validate(vx_raw, vy_raw)
+        if rc:
+            raise ValueError(rc)
+        rc, inner, outer = self.to_voronoi(vx, vy)
+        if rc:
+            raise ValueError(rc)
+        return (self.voronoi_batch(inner, outer, xs, ys), self.offset_batch(vx, vy, xs, ys),
+                self.ray_batch(np.asarray(vx_raw, np.float64), np.asarray(vy_raw, np.float64),
+                               xs, ys))
+
+    def pack(self, mask):
+        mask = np.ascontiguousarray(mask, np.uint8)
+        out = np.zeros((mask.size + 7) // 8, np.uint8)
+        self.L.vo_pack_mask_lsb(mask.ctypes.data_as(_U8), mask.size, out.ctypes.data_as(_U8))
+        return out
+
+
+class Reference:
+    """The unmodified reference library (oracle/_ref/libvpip_ref.so)."""
+
+    def __init__(self):
+        if not REF_SO.exists():
+            raise FileNotFoundError(f"{REF_SO} not built (needs /root/reference; run oracle.build())")
+        L = C.CDLL(str(REF_SO))
+        sz = C.c_size_t
+        L.vr_validate.argtypes = [_D, _D, sz, _D, _D, C.POINTER(C.c_int)]
+        L.vr_to_voronoi.argtypes = [_D, _D, sz, _D, _D]
+        L.vr_edge_coefficients.argtypes = [C.c_double] * 4 + [_D]
+        L.vr_reflect_generator.argtypes = [C.c_double, C.c_double, _D, _D]
+        L.vr_edge_line_distance.restype = C.c_double
+        L.vr_edge_line_distance.argtypes = [_D, _D, sz, C.c_double, C.c_double]
+        L.vr_mix_seed.restype = C.c_uint64
+        L.vr_mix_seed.argtypes = [C.c_uint64, C.c_uint64]
+        L.vr_sample_points.argtypes = [sz, C.c_double, C.c_double, C.c_double, C.c_double,
+                                       C.c_uint64, _D, _D]
+        L.vr_regular_polygon.argtypes = [sz, C.c_double, C.c_double, C.c_double, _D, _D]
+        L.vr_random_convex_polygon.argtypes = [sz, C.c_uint64, C.c_double, C.c_double,
+                                               C.c_double, _D, _D]
+        L.vr_batch_new.restype = C.c_void_p
+        L.vr_batch_new.argtypes = [_D, _D, sz]
+        L.vr_batch_free.argtypes = [C.c_void_p]
+        L.vr_poly_new.restype = C.c_void_p
+        L.vr_poly_new.argtypes = [_D, _D, sz, C.c_int, C.POINTER(C.c_int)]
+        L.vr_poly_free.argtypes = [C.c_void_p]
+        L.vr_run_engine.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_int, _U8,
+                                    C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]
+        L.vr_voronoi_batch_gens.argtypes = [_D, _D, sz, C.c_void_p, C.c_int, _U8,
+                                            C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]
+        L.vr_scalar.argtypes = [C.c_void_p, C.c_int, C.c_double, C.c_double]
+        self.L = L
+
+    def validate(self, vx, vy):
+        vx, vy = np.ascontiguousarray(vx, np.float64), np.ascontiguousarray(vy, np.float64)
+        ox, oy = np.zeros(vx.size), np.zeros(vx.size)
+        rev = C.c_int()
+        rc = self.L.vr_validate(_d(vx), _d(vy), vx.size, _d(ox), _d(oy), C.byref(rev))
+        return rc, ox, oy, bool(rev.value)
+
+    def to_voronoi(self, vx, vy):
+        vx, vy = np.ascontiguousarray(vx, np.float64), np.ascontiguousarray(vy, np.float64)
+        inner, outer = np.zeros(2), np.zeros((vx.size, 2))
+        rc = self.L.vr_to_voronoi(_d(vx), _d(vy), vx.size, _d(inner), _d(outer))
+        return rc, inner, outer
+
+    def sample_points(self, count, box, seed):
+        xs, ys = np.zeros(count), np.zeros(count)
+        rc = self.L.vr_sample_points(count, *map(float, box), seed, _d(xs), _d(ys))
+        if rc:
+            raise ValueError(rc)
+        return xs, ys
+
+    def regular_polygon(self, n, r=1.0, center=(0.0, 0.0)):
+        vx, vy = np.zeros(n), np.zeros(n)
+        rc = self.L.vr_regular_polygon(n, r, center[0], center[1], _d(vx), _d(vy))
+        if rc:
+            raise ValueError(rc)
+        return vx, vy
+
+    def random_convex_polygon(self, n, seed, r=1.0, center=(0.0, 0.0)):
+        vx, vy = np.zeros(n), np.zeros(n)
+        rc = self.L.vr_random_convex_polygon(n, seed, r, center[0], center[1], _d(vx), _d(vy))
+        if rc:
+            raise ValueError(rc)
+        return vx, vy
+
+    def masks(self, vx, vy, xs, ys, threads=1, engines=(0, 1, 2)):
+        """Masks of the requested engines (0 voronoi, 1 offset, 2 crossing) + timings (ns)."""
+        vx, vy = np.ascontiguousarray(vx, np.float64), np.ascontiguousarray(vy, np.float64)
+        xs, ys = np.ascontiguousarray(xs, np.float64), np.ascontiguousarray(ys, np.float64)
+        code = C.c_int()
+        p = self.L.vr_poly_new(_d(vx), _d(vy), vx.size, 1 if any(e != 2 for e in engines) else 0,
+                               C.byref(code))
+        if not p:
+            raise ValueError(code.value)
+        b = self.L.vr_batch_new(_d(xs), _d(ys), xs.size)
+        out, times = [], []
+        try:
+            for e in engines:
+                m = np.zeros(xs.size, np.uint8)
+                ns = C.c_uint64()
+                self.L.vr_run_engine(p, e, b, threads, m.ctypes.data_as(_U8), C.byref(ns), None)
+                out.append(m)
+                times.append(ns.value)
+        finally:
+            self.L.vr_batch_free(b)
+            self.L.vr_poly_free(p)
+        return out, times

@@ -1,0 +1,224 @@
+// ref_shim.cpp -- extern "C" access to the UNMODIFIED reference library.
+//
+// TEST INFRASTRUCTURE ONLY. oracle/Makefile compiles the reference's own
+// sources where they lie (/root/reference/proj/src/{geometry,voronoi,engines,
+// sampling}.cpp) together with this file into oracle/_ref/libvpip_ref.so.
+// It is used (a) to pin the C restatement (oracle/vpip_oracle.c) against the
+// reference itself, (b) to generate tests/golden/ fixtures, and (c) as the
+// CPU baseline arm of bench.py (`--impl reference`, cpu_baseline.kind =
+// "reference"). Nothing here is on the product path.
+#include <chrono>
+#include <cstdint>
+#include <cstring>
+#include <optional>
+#include <vector>
+
+#include "vpip/engines.hpp"
+#include "vpip/geometry.hpp"
+#include "vpip/sampling.hpp"
+#include "vpip/voronoi.hpp"
+
+namespace {
+
+std::vector<vpip::Point2> to_points(const double* vx, const double* vy, std::size_t n) {
+  std::vector<vpip::Point2> v(n);
+  for (std::size_t i = 0; i < n; ++i) v[i] = {vx[i], vy[i]};
+  return v;
+}
+
+int code_of(const vpip::Error& e) { return static_cast<int>(e.code()) + 1; }
+
+struct Poly {
+  std::vector<vpip::Point2> raw;              // as given (crossing engine input)
+  std::optional<vpip::ConvexPolygon> convex;  // validated (voronoi / offset)
+  std::optional<vpip::GeneratorSet> gens;
+};
+
+}  // namespace
+
+extern "C" {
+
+int vr_validate(const double* vx, const double* vy, std::size_t n, double* ox, double* oy,
+                int* reversed) {
+  try {
+    vpip::ConvexPolygon p = vpip::validate_polygon(to_points(vx, vy, n));
+    for (std::size_t i = 0; i < p.size(); ++i) {
+      ox[i] = p.vertex(i).x;
+      oy[i] = p.vertex(i).y;
+    }
+    *reversed = p.was_reversed() ? 1 : 0;
+    return 0;
+  } catch (const vpip::Error& e) {
+    return code_of(e);
+  }
+}
+
+int vr_to_voronoi(const double* vx, const double* vy, std::size_t n, double* inner_xy,
+                  double* outer_xy) {
+  try {
+    const vpip::GeneratorSet g = vpip::to_voronoi(vpip::validate_polygon(to_points(vx, vy, n)));
+    inner_xy[0] = g.inner.x;
+    inner_xy[1] = g.inner.y;
+    for (std::size_t k = 0; k < g.outer.size(); ++k) {
+      outer_xy[2 * k] = g.outer[k].x;
+      outer_xy[2 * k + 1] = g.outer[k].y;
+    }
+    return 0;
+  } catch (const vpip::Error& e) {
+    return code_of(e);
+  }
+}
+
+int vr_edge_coefficients(double qix, double qiy, double qjx, double qjy, double* abc) {
+  try {
+    const vpip::EdgeCoefficients e = vpip::edge_coefficients({qix, qiy}, {qjx, qjy});
+    abc[0] = e.a;
+    abc[1] = e.b;
+    abc[2] = e.c;
+    return 0;
+  } catch (const vpip::Error& e) {
+    return code_of(e);
+  }
+}
+
+int vr_reflect_generator(double px, double py, const double* abc, double* r) {
+  try {
+    const vpip::Point2 q = vpip::reflect_generator({px, py}, {abc[0], abc[1], abc[2]});
+    r[0] = q.x;
+    r[1] = q.y;
+    return 0;
+  } catch (const vpip::Error& e) {
+    return code_of(e);
+  }
+}
+
+double vr_edge_line_distance(const double* vx, const double* vy, std::size_t n, double px,
+                             double py) {
+  return vpip::edge_line_distance(vpip::validate_polygon(to_points(vx, vy, n)), {px, py});
+}
+
+uint64_t vr_mix_seed(uint64_t seed, uint64_t salt) { return vpip::mix_seed(seed, salt); }
+
+int vr_sample_points(std::size_t count, double min_x, double min_y, double max_x, double max_y,
+                     uint64_t seed, double* xs, double* ys) {
+  try {
+    const vpip::PointBatch b = vpip::sample_points(count, {min_x, min_y, max_x, max_y}, seed);
+    std::memcpy(xs, b.xs.data(), count * sizeof(double));
+    std::memcpy(ys, b.ys.data(), count * sizeof(double));
+    return 0;
+  } catch (const vpip::Error& e) {
+    return code_of(e);
+  }
+}
+
+int vr_regular_polygon(std::size_t n, double r, double cx, double cy, double* vx, double* vy) {
+  try {
+    const vpip::ConvexPolygon p = vpip::regular_polygon(n, r, {cx, cy});
+    for (std::size_t i = 0; i < n; ++i) {
+      vx[i] = p.vertex(i).x;
+      vy[i] = p.vertex(i).y;
+    }
+    return 0;
+  } catch (const vpip::Error& e) {
+    return code_of(e);
+  }
+}
+
+int vr_random_convex_polygon(std::size_t n, uint64_t seed, double r, double cx, double cy,
+                             double* vx, double* vy) {
+  try {
+    const vpip::ConvexPolygon p = vpip::random_convex_polygon(n, seed, r, {cx, cy});
+    for (std::size_t i = 0; i < n; ++i) {
+      vx[i] = p.vertex(i).x;
+      vy[i] = p.vertex(i).y;
+    }
+    return 0;
+  } catch (const vpip::Error& e) {
+    return code_of(e);
+  }
+}
+
+// ---- batch engines through opaque handles (input copies are untimed) ----
+
+void* vr_batch_new(const double* xs, const double* ys, std::size_t m) {
+  auto* b = new vpip::PointBatch;
+  b->xs.assign(xs, xs + m);
+  b->ys.assign(ys, ys + m);
+  return b;
+}
+
+void vr_batch_free(void* b) { delete static_cast<vpip::PointBatch*>(b); }
+
+// Builds the engine inputs the way the reference CLI does (vpip.cpp:120-133):
+// raw vertices for crossing, validate + to_voronoi for the others. Returns
+// nullptr and sets *code when validation or conversion throws.
+void* vr_poly_new(const double* vx, const double* vy, std::size_t n, int want_convex, int* code) {
+  auto* p = new Poly;
+  p->raw = to_points(vx, vy, n);
+  *code = 0;
+  if (want_convex) {
+    try {
+      p->convex.emplace(vpip::validate_polygon(p->raw));
+      p->gens.emplace(vpip::to_voronoi(*p->convex));
+    } catch (const vpip::Error& e) {
+      *code = code_of(e);
+      delete p;
+      return nullptr;
+    }
+  }
+  return p;
+}
+
+void vr_poly_free(void* p) { delete static_cast<Poly*>(p); }
+
+// engine: 0 voronoi, 1 sign_of_offset, 2 ray_crossing (vpip::EngineKind order).
+// Times only the *_contains_batch call, as run_benchmark does
+// (bench.cpp:196-199); copies the byte mask out afterwards when out != null.
+int vr_run_engine(void* poly, int engine, void* batch, int threads, uint8_t* out,
+                  uint64_t* ns, uint64_t* inside) {
+  const Poly& p = *static_cast<Poly*>(poly);
+  const vpip::PointBatch& b = *static_cast<vpip::PointBatch*>(batch);
+  if (engine != 2 && !p.convex) return 6;
+  vpip::InclusionMask mask;
+  const auto t0 = std::chrono::steady_clock::now();
+  switch (engine) {
+    case 0: mask = vpip::voronoi_contains_batch(*p.gens, b, threads); break;
+    case 1: mask = vpip::sign_of_offset_contains_batch(*p.convex, b, threads); break;
+    case 2: mask = vpip::ray_crossing_contains_batch(p.raw, b, threads); break;
+    default: return 6;
+  }
+  const auto t1 = std::chrono::steady_clock::now();
+  if (ns) *ns = static_cast<uint64_t>(std::chrono::duration_cast<std::chrono::nanoseconds>(t1 - t0).count());
+  if (inside) *inside = vpip::count_inside(mask);
+  if (out) std::memcpy(out, mask.data(), mask.size());
+  return 0;
+}
+
+// Voronoi batch on an explicit generator set (any GeneratorSet, e.g. one
+// read back from the GPU), plus the instrumented work counters.
+void vr_voronoi_batch_gens(const double* inner_xy, const double* outer_xy, std::size_t n,
+                           void* batch, int threads, uint8_t* out, uint64_t* evals,
+                           uint64_t* comps) {
+  vpip::GeneratorSet g;
+  g.inner = {inner_xy[0], inner_xy[1]};
+  for (std::size_t k = 0; k < n; ++k) g.outer.push_back({outer_xy[2 * k], outer_xy[2 * k + 1]});
+  vpip::BatchStats stats;
+  const vpip::InclusionMask mask =
+      vpip::voronoi_contains_batch(g, *static_cast<vpip::PointBatch*>(batch), stats, threads);
+  std::memcpy(out, mask.data(), mask.size());
+  if (evals) *evals = stats.distance_evaluations;
+  if (comps) *comps = stats.comparisons;
+}
+
+int vr_scalar(void* poly, int engine, double px, double py) {
+  const Poly& p = *static_cast<Poly*>(poly);
+  switch (engine) {
+    case 0: return vpip::voronoi_contains(*p.gens, {px, py});
+    case 1: return vpip::sign_of_offset_contains(*p.convex, {px, py});
+    case 2: return vpip::ray_crossing_contains(p.raw, {px, py});
+    case 3: return vpip::ray_crossing_count(p.raw, {px, py});
+    default: return -1;
+  }
+}
+
+}  // extern "C"

@@ -1,0 +1,411 @@
+// capi.cu -- host side of the C-ABI (include/vpipg.h).
+//
+// Owns handle lifetime, host-side polygon validation (the reference's
+// precondition, geometry.cpp:53-98, restated exactly), blob layout, kernel
+// dispatch and the pipelined host-buffer path. No compute on the point
+// stream happens here: every point test runs in a device kernel, and a
+// missing or wrong-architecture device is an error (no CPU fallback).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <mutex>
+#include <new>
+#include <numbers>
+#include <random>
+#include <vector>
+
+#include "vpipg.h"
+#include "vpipg_internal.h"
+
+using namespace vpipg;
+
+struct vpipg_poly {
+  int device = 0;
+  uint32_t n = 0;
+  uint32_t kinds = 0;
+  int reversed = 0;
+  void* blob = nullptr;
+  DevTables t{};
+  std::vector<double> vx, vy;  // validated (or raw, crossing-only) vertices
+  double inner_x = 0, inner_y = 0;
+};
+
+namespace {
+
+constexpr int kOk = 0;
+constexpr int kTooFew = 1, kNotConvex = 2, kDegenerate = 3, kNonFinite = 4;
+constexpr int kInvalid = 6;
+
+int cuda_code(cudaError_t e) { return e == cudaSuccess ? kOk : VPIPG_ERR_CUDA + static_cast<int>(e); }
+
+#define VPIPG_TRY(expr)                         \
+  do {                                          \
+    const cudaError_t e_ = (expr);              \
+    if (e_ != cudaSuccess) return cuda_code(e_); \
+  } while (0)
+
+// The kernels are built for sm_100a only; refuse anything else loudly.
+int check_device(int device) {
+  static std::mutex mu;
+  static std::vector<int> ok(64, -1);
+  if (device < 0 || device >= 64) return kInvalid;
+  std::lock_guard<std::mutex> lock(mu);
+  if (ok[device] < 0) {
+    cudaDeviceProp prop;
+    const cudaError_t e = cudaGetDeviceProperties(&prop, device);
+    if (e != cudaSuccess) return cuda_code(e);
+    ok[device] = (prop.major == 10 && prop.minor == 0) ? 1 : 0;
+  }
+  return ok[device] ? kOk : VPIPG_ERR_ARCH;
+}
+
+// validate_polygon (geometry.cpp:53-98): same checks in the same order, same
+// arithmetic (this TU is compiled with -fmad=false on the host side too).
+int validate(std::vector<double>& vx, std::vector<double>& vy, int* reversed) {
+  const size_t n = vx.size();
+  for (size_t i = 0; i < n; ++i)
+    if (!std::isfinite(vx[i]) || !std::isfinite(vy[i])) return kNonFinite;
+  if (n < 3) return kTooFew;
+  for (size_t i = 0, j = n - 1; i < n; j = i++) {
+    const double dx = vx[j] - vx[i], dy = vy[j] - vy[i];
+    if (dx * dx + dy * dy <= 1e-24) return kDegenerate;
+  }
+  double sum = 0.0;
+  for (size_t i = 0, j = n - 1; i < n; j = i++) sum += vx[j] * vy[i] - vx[i] * vy[j];
+  *reversed = 0;
+  if (sum < 0.0) {
+    std::reverse(vx.begin(), vx.end());
+    std::reverse(vy.begin(), vy.end());
+    *reversed = 1;
+  }
+  double total_turn = 0.0;
+  for (size_t i = 0; i < n; ++i) {
+    const size_t p = (i + n - 1) % n, q = (i + 1) % n;
+    const double inx = vx[i] - vx[p], iny = vy[i] - vy[p];
+    const double outx = vx[q] - vx[i], outy = vy[q] - vy[i];
+    const double cr = inx * outy - iny * outx;
+    if (cr <= 1e-12) return kNotConvex;
+    total_turn += std::atan2(cr, inx * outx + iny * outy);
+  }
+  if (total_turn >= 3.0 * std::numbers::pi) return kNotConvex;
+  return kOk;
+}
+
+size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+// Builds the blob, runs the prep kernel, reads back the status.
+int build(vpipg_poly* p, const double* vv, const double* vr, const double* gen, cudaStream_t s) {
+  const size_t n = p->n;
+  size_t off = 0;
+  auto take = [&](size_t bytes) { const size_t o = off; off = align256(off + bytes); return o; };
+  const size_t o_vv = take(2 * n * sizeof(double));
+  const size_t o_vr = take(2 * n * sizeof(double));
+  const size_t o_gen = take((2 + 2 * n) * sizeof(double));
+  const size_t o_outer = take(n * sizeof(double2));
+  const size_t o_off = take(n * sizeof(OffsetEdgeF64));
+  const size_t o_ray = take(n * sizeof(RayEdgeF64));
+  const size_t o_s0 = take((n + 4) * sizeof(float2));
+  const size_t o_s1 = take((n + 4) * sizeof(float2));
+  const size_t o_cross = take(n * sizeof(float4));
+  const size_t o_meta = take(sizeof(PrepMeta));
+  VPIPG_TRY(cudaMalloc(&p->blob, off));
+  char* b = static_cast<char*>(p->blob);
+  VPIPG_TRY(cudaMemsetAsync(b, 0, off, s));
+  PrepArgs a{};
+  a.n = p->n;
+  a.kinds = p->kinds;
+  if (vv) {
+    VPIPG_TRY(cudaMemcpyAsync(b + o_vv, vv, 2 * n * sizeof(double), cudaMemcpyHostToDevice, s));
+    a.vv = reinterpret_cast<const double*>(b + o_vv);
+  }
+  if (vr) {
+    VPIPG_TRY(cudaMemcpyAsync(b + o_vr, vr, 2 * n * sizeof(double), cudaMemcpyHostToDevice, s));
+    a.vr = reinterpret_cast<const double*>(b + o_vr);
+  }
+  if (gen) {
+    VPIPG_TRY(cudaMemcpyAsync(b + o_gen, gen, (2 + 2 * n) * sizeof(double), cudaMemcpyHostToDevice, s));
+    a.gen_in = reinterpret_cast<const double*>(b + o_gen);
+  }
+  a.outer = reinterpret_cast<double2*>(b + o_outer);
+  a.off = reinterpret_cast<OffsetEdgeF64*>(b + o_off);
+  a.ray = reinterpret_cast<RayEdgeF64*>(b + o_ray);
+  a.slab_coef[0] = reinterpret_cast<float2*>(b + o_s0);
+  a.slab_coef[1] = reinterpret_cast<float2*>(b + o_s1);
+  a.cross_vert = reinterpret_cast<float4*>(b + o_cross);
+  a.meta = reinterpret_cast<PrepMeta*>(b + o_meta);
+  VPIPG_TRY(launch_prep(a, s));
+  PrepMeta meta;
+  VPIPG_TRY(cudaMemcpyAsync(&meta, a.meta, sizeof(meta), cudaMemcpyDeviceToHost, s));
+  VPIPG_TRY(cudaStreamSynchronize(s));
+  if (meta.status != 0) return meta.status;
+
+  DevTables& t = p->t;
+  t.n = p->n;
+  t.kinds = p->kinds;
+  t.inner_x = meta.inner_x;
+  t.inner_y = meta.inner_y;
+  t.outer = a.outer;
+  t.off = a.off;
+  t.ray = a.ray;
+  t.ox = meta.ox;
+  t.oy = meta.oy;
+  for (int e = 0; e < 2; ++e) {
+    SlabTable& st = t.slab[e];
+    st.coef = a.slab_coef[e];
+    uint32_t acc = 0;
+    for (int g = 0; g < kGroups; ++g) {
+      st.off[g] = acc;
+      st.cnt[g] = meta.cnt[e][g];
+      acc += meta.cnt[e][g];
+    }
+    st.total = acc;
+  }
+  t.cross.vert = a.cross_vert;
+  t.cross.n = p->n;
+  p->inner_x = meta.inner_x;
+  p->inner_y = meta.inner_y;
+  return kOk;
+}
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+int dispatch(const vpipg_poly* p, int engine, int dtype, const TestArgs& a, cudaStream_t s) {
+  const uint32_t need = engine == VPIPG_ENGINE_VORONOI  ? kKindVoronoi
+                        : engine == VPIPG_ENGINE_OFFSET ? kKindOffset
+                        : engine == VPIPG_ENGINE_CROSSING ? kKindCrossing
+                                                          : 0u;
+  if (need == 0 || !(p->kinds & need)) return kInvalid;
+  if (dtype != VPIPG_F32 && dtype != VPIPG_F64) return kInvalid;
+  if (a.m == 0) return kOk;
+  if (!a.xs || !a.ys) return kInvalid;
+  const cudaError_t e = (dtype == VPIPG_F32) ? launch_test_f32(p->t, engine, a, s)
+                                             : launch_test_f64(p->t, engine, a, s);
+  return cuda_code(e);
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* vpipg_strerror(int code) {
+  switch (code) {
+    case 0: return "ok";
+    case 1: return "too few vertices";
+    case 2: return "not convex";
+    case 3: return "degenerate edge";
+    case 4: return "non-finite value";
+    case 5: return "generator collision";
+    case 6: return "invalid parameter";
+    case 7: return "parse error";
+    case VPIPG_ERR_ARCH: return "device is not an sm_100 (B200) GPU";
+    default: break;
+  }
+  if (code >= VPIPG_ERR_CUDA && code < VPIPG_ERR_ARCH)
+    return cudaGetErrorString(static_cast<cudaError_t>(code - VPIPG_ERR_CUDA));
+  return "unknown error";
+}
+
+int vpipg_abi_version(void) { return VPIPG_ABI_VERSION; }
+
+int vpipg_prepare(const double* vx, const double* vy, uint32_t n, uint32_t kinds, int device,
+                  void* stream, vpipg_poly** out) {
+  if (!out || (kinds & ~VPIPG_KIND_ALL) || kinds == 0) return kInvalid;
+  if (n > 0 && (!vx || !vy)) return kInvalid;
+  *out = nullptr;
+  int rc = check_device(device);
+  if (rc) return rc;
+  auto* p = new (std::nothrow) vpipg_poly;
+  if (!p) return kInvalid;
+  p->device = device;
+  p->n = n;
+  p->kinds = kinds;
+  std::vector<double> raw(2 * size_t(n)), val;
+  std::copy(vx, vx + n, raw.begin());
+  std::copy(vy, vy + n, raw.begin() + n);
+  const bool convex = kinds & (kKindVoronoi | kKindOffset);
+  if (convex) {
+    p->vx.assign(vx, vx + n);
+    p->vy.assign(vy, vy + n);
+    rc = validate(p->vx, p->vy, &p->reversed);
+    if (rc) {
+      delete p;
+      return rc;
+    }
+    val.resize(2 * size_t(n));
+    std::copy(p->vx.begin(), p->vx.end(), val.begin());
+    std::copy(p->vy.begin(), p->vy.end(), val.begin() + n);
+  } else {
+    p->vx.assign(vx, vx + n);
+    p->vy.assign(vy, vy + n);
+  }
+  DeviceGuard g(device);
+  rc = build(p, convex ? val.data() : nullptr, (kinds & kKindCrossing) ? raw.data() : nullptr,
+             nullptr, static_cast<cudaStream_t>(stream));
+  if (rc) {
+    vpipg_destroy(p);
+    return rc;
+  }
+  *out = p;
+  return kOk;
+}
+
+int vpipg_prepare_generators(const double* inner_xy, const double* outer_xy, uint32_t n,
+                             int device, void* stream, vpipg_poly** out) {
+  if (!out || !inner_xy || (n > 0 && !outer_xy)) return kInvalid;
+  *out = nullptr;
+  int rc = check_device(device);
+  if (rc) return rc;
+  auto* p = new (std::nothrow) vpipg_poly;
+  if (!p) return kInvalid;
+  p->device = device;
+  p->n = n;
+  p->kinds = kKindVoronoi;
+  std::vector<double> gen(2 + 2 * size_t(n));
+  gen[0] = inner_xy[0];
+  gen[1] = inner_xy[1];
+  std::copy(outer_xy, outer_xy + 2 * size_t(n), gen.begin() + 2);
+  DeviceGuard g(device);
+  rc = build(p, nullptr, nullptr, gen.data(), static_cast<cudaStream_t>(stream));
+  if (rc) {
+    vpipg_destroy(p);
+    return rc;
+  }
+  *out = p;
+  return kOk;
+}
+
+void vpipg_destroy(vpipg_poly* p) {
+  if (!p) return;
+  if (p->blob) {
+    DeviceGuard g(p->device);
+    cudaFree(p->blob);
+  }
+  delete p;
+}
+
+int vpipg_poly_info(const vpipg_poly* p, uint32_t* n, uint32_t* kinds, int* reversed) {
+  if (!p) return kInvalid;
+  if (n) *n = p->n;
+  if (kinds) *kinds = p->kinds;
+  if (reversed) *reversed = p->reversed;
+  return kOk;
+}
+
+int vpipg_poly_generators(const vpipg_poly* p, double* inner_xy, double* outer_xy) {
+  if (!p || !(p->kinds & kKindVoronoi) || !inner_xy || (p->n && !outer_xy)) return kInvalid;
+  DeviceGuard g(p->device);
+  inner_xy[0] = p->inner_x;
+  inner_xy[1] = p->inner_y;
+  if (p->n) VPIPG_TRY(cudaMemcpy(outer_xy, p->t.outer, p->n * sizeof(double2), cudaMemcpyDeviceToHost));
+  return kOk;
+}
+
+int vpipg_poly_vertices(const vpipg_poly* p, double* vx, double* vy) {
+  if (!p || (p->n && (!vx || !vy))) return kInvalid;
+  std::copy(p->vx.begin(), p->vx.end(), vx);
+  std::copy(p->vy.begin(), p->vy.end(), vy);
+  return kOk;
+}
+
+int vpipg_test(const vpipg_poly* p, int engine, int dtype, const void* xs, const void* ys,
+               uint64_t m, uint32_t* mask_words, uint8_t* mask_bytes,
+               unsigned long long* d_inside, void* stream) {
+  if (!p) return kInvalid;
+  DeviceGuard g(p->device);
+  TestArgs a{xs, ys, m, mask_words, mask_bytes, d_inside};
+  return dispatch(p, engine, dtype, a, static_cast<cudaStream_t>(stream));
+}
+
+int vpipg_test_host(const vpipg_poly* p, int engine, int dtype, const void* xs, const void* ys,
+                    uint64_t m, uint32_t* mask_words, uint8_t* mask_bytes, uint64_t* inside) {
+  if (!p) return kInvalid;
+  if (inside) *inside = 0;
+  if (m == 0) return kOk;
+  if (!xs || !ys) return kInvalid;
+  DeviceGuard g(p->device);
+  const size_t elt = dtype == VPIPG_F64 ? sizeof(double) : sizeof(float);
+  // chunks of 4 Mi points (32-aligned so word boundaries line up), two in flight
+  const uint64_t chunk = std::min<uint64_t>(m, uint64_t(1) << 22);
+  const uint64_t chunk_words = (chunk + 31) / 32;
+  cudaStream_t st[2];
+  for (auto& s : st) VPIPG_TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  struct Slot {
+    void* x = nullptr;
+    void* y = nullptr;
+    uint32_t* w = nullptr;
+    uint8_t* b = nullptr;
+    unsigned long long* c = nullptr;
+  } slot[2];
+  int rc = kOk;
+  auto fail = [&](cudaError_t e) {
+    if (e != cudaSuccess && rc == kOk) rc = cuda_code(e);
+    return rc != kOk;
+  };
+  for (int i = 0; i < 2 && rc == kOk; ++i) {
+    if (fail(cudaMallocAsync(&slot[i].x, chunk * elt, st[i]))) break;
+    if (fail(cudaMallocAsync(&slot[i].y, chunk * elt, st[i]))) break;
+    if (mask_words && fail(cudaMallocAsync(reinterpret_cast<void**>(&slot[i].w), chunk_words * 4, st[i]))) break;
+    if (mask_bytes && fail(cudaMallocAsync(reinterpret_cast<void**>(&slot[i].b), chunk, st[i]))) break;
+    if (fail(cudaMallocAsync(reinterpret_cast<void**>(&slot[i].c), 8, st[i]))) break;
+    if (fail(cudaMemsetAsync(slot[i].c, 0, 8, st[i]))) break;
+  }
+  const char* hx = static_cast<const char*>(xs);
+  const char* hy = static_cast<const char*>(ys);
+  for (uint64_t base = 0, c = 0; rc == kOk && base < m; base += chunk, ++c) {
+    const int i = static_cast<int>(c & 1);
+    const uint64_t len = std::min<uint64_t>(chunk, m - base);
+    if (fail(cudaMemcpyAsync(slot[i].x, hx + base * elt, len * elt, cudaMemcpyHostToDevice, st[i]))) break;
+    if (fail(cudaMemcpyAsync(slot[i].y, hy + base * elt, len * elt, cudaMemcpyHostToDevice, st[i]))) break;
+    TestArgs a{slot[i].x, slot[i].y, len, slot[i].w, slot[i].b, slot[i].c};
+    rc = dispatch(p, engine, dtype, a, st[i]);
+    if (rc) break;
+    if (mask_words && fail(cudaMemcpyAsync(mask_words + base / 32, slot[i].w, ((len + 31) / 32) * 4,
+                                           cudaMemcpyDeviceToHost, st[i]))) break;
+    if (mask_bytes && fail(cudaMemcpyAsync(mask_bytes + base, slot[i].b, len, cudaMemcpyDeviceToHost, st[i]))) break;
+  }
+  unsigned long long cnt[2] = {0, 0};
+  for (int i = 0; i < 2; ++i) {
+    if (rc == kOk && slot[i].c) fail(cudaMemcpyAsync(&cnt[i], slot[i].c, 8, cudaMemcpyDeviceToHost, st[i]));
+    for (void* ptr : {slot[i].x, slot[i].y, static_cast<void*>(slot[i].w), static_cast<void*>(slot[i].b),
+                      static_cast<void*>(slot[i].c)})
+      if (ptr) cudaFreeAsync(ptr, st[i]);
+  }
+  for (auto& s : st) {
+    fail(cudaStreamSynchronize(s));
+    cudaStreamDestroy(s);
+  }
+  if (rc == kOk && inside) *inside = cnt[0] + cnt[1];
+  return rc;
+}
+
+int vpipg_voronoi_work(const vpipg_poly* p, uint64_t m, uint64_t* evals, uint64_t* comps) {
+  if (!p || !(p->kinds & kKindVoronoi)) return kInvalid;
+  if (evals) *evals = (uint64_t(p->n) + 1) * m;
+  if (comps) *comps = uint64_t(p->n) * m;
+  return kOk;
+}
+
+int vpipg_fill_uniform_points(uint64_t seed, uint64_t first, uint64_t m, double min_x,
+                              double min_y, double max_x, double max_y, int dtype, void* xs,
+                              void* ys, void* stream) {
+  if ((dtype != VPIPG_F32 && dtype != VPIPG_F64) || (m && (!xs || !ys))) return kInvalid;
+  if (!(min_x < max_x && min_y < max_y)) return kInvalid;
+  return cuda_code(launch_fill_uniform(seed, first, m, min_x, min_y, max_x, max_y, dtype, xs, ys,
+                                       static_cast<cudaStream_t>(stream)));
+}
+
+}  // extern "C"

@@ -1,0 +1,279 @@
+// prep.cu -- polygon preprocessing kernel (the device half of vpipg_prepare).
+//
+// Replaces the reference's conversion step: centroid (geometry.cpp:106-120),
+// edge_coefficients (voronoi.cpp:23-31) and reflect_generator
+// (voronoi.cpp:46-58) composed by to_voronoi (voronoi.cpp:60-71), plus the
+// per-edge setup the reference batch kernels hoist out of their point loops
+// (engines.cpp:146-149, :176-186). One CTA per polygon.
+//
+// The f64 outputs (generators, offset and ray records) repeat the
+// reference's expressions operation for operation with explicitly rounded
+// intrinsics (__dmul_rn / __dadd_rn / __dsub_rn / __ddiv_rn are never
+// contracted into FMAs), so they are bit-identical to the reference's
+// -ffp-contract=off build. The fp32 slab tables are derived from those f64
+// values (accuracy matters there, bit-matching does not).
+#include <climits>
+#include <cmath>
+#include <cstdint>
+
+#include "vpipg_device.cuh"
+#include "vpipg_internal.h"
+
+namespace vpipg {
+
+namespace {
+
+constexpr int kPrepThreads = 256;
+enum : int { kNone = -1, kXlo = 0, kXhi = 1, kYlo = 2, kYhi = 3 };
+
+__device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ double ddiv(double a, double b) { return __ddiv_rn(a, b); }
+// std::min / std::max semantics (engines.cpp:183-186)
+__device__ __forceinline__ double smin(double a, double b) { return (b < a) ? b : a; }
+__device__ __forceinline__ double smax(double a, double b) { return (a < b) ? b : a; }
+
+// Half-plane a*x' + b*y' + c >= 0 (local frame) -> slab class and (B, C).
+__device__ int slab_classify(double a, double b, double c, float2* bc) {
+  if (a == 0.0 && b == 0.0) {
+    if (c >= 0.0) return kNone;          // no constraint (e.g. outer == inner)
+    *bc = make_float2(0.f, INFINITY);     // unsatisfiable: x' >= +inf
+    return kXlo;
+  }
+  if (fabs(a) >= fabs(b)) {
+    *bc = make_float2(static_cast<float>(-b / a), static_cast<float>(-c / a));
+    return a > 0.0 ? kXlo : kXhi;
+  }
+  *bc = make_float2(static_cast<float>(-a / b), static_cast<float>(-c / b));
+  return b > 0.0 ? kYlo : kYhi;
+}
+
+// Block-wide deterministic scatter of per-edge (class, coef) into the four
+// groups of one slab table, each padded to an even length with a neutral
+// entry. Edge order is preserved inside a group.
+__device__ void slab_scatter(int n, int (*cls_of)(int, const void*, float2*), const void* ctx,
+                             float2* out, uint32_t* cnt_out) {
+  __shared__ uint32_t s_base[kGroups];
+  __shared__ uint32_t s_warp[kGroups][kPrepThreads / 32];
+  __shared__ uint32_t s_count[kGroups];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid < kGroups) s_count[tid] = 0;
+  __syncthreads();
+  // pass 1: group sizes
+  for (int k = tid; k < n; k += kPrepThreads) {
+    float2 bc;
+    const int c = cls_of(k, ctx, &bc);
+    if (c >= 0) atomicAdd(&s_count[c], 1u);
+  }
+  __syncthreads();
+  if (tid == 0) {
+    uint32_t acc = 0;
+    for (int g = 0; g < kGroups; ++g) {
+      s_base[g] = acc;
+      const uint32_t padded = (s_count[g] + 1u) & ~1u;
+      cnt_out[g] = padded;
+      if (padded != s_count[g]) {  // neutral pad entry at the group's end
+        out[acc + padded - 1] = make_float2(0.f, (g == kXlo || g == kYlo) ? -INFINITY : INFINITY);
+      }
+      acc += padded;
+    }
+  }
+  __syncthreads();
+  // pass 2: ordered placement, one 256-edge chunk at a time
+  for (int k0 = 0; k0 < n; k0 += kPrepThreads) {
+    const int k = k0 + tid;
+    float2 bc = make_float2(0.f, 0.f);
+    const int c = (k < n) ? cls_of(k, ctx, &bc) : kNone;
+    uint32_t rank[kGroups];
+    for (int g = 0; g < kGroups; ++g) {
+      const unsigned bal = __ballot_sync(0xffffffffu, c == g);
+      rank[g] = __popc(bal & ((1u << lane) - 1u));
+      if (lane == 0) s_warp[g][warp] = __popc(bal);
+    }
+    __syncthreads();
+    if (c >= 0) {
+      uint32_t before = 0;
+      for (int w = 0; w < warp; ++w) before += s_warp[c][w];
+      out[s_base[c] + before + rank[c]] = bc;
+    }
+    __syncthreads();
+    if (tid < kGroups) {
+      uint32_t tot = 0;
+      for (int w = 0; w < kPrepThreads / 32; ++w) tot += s_warp[tid][w];
+      s_base[tid] += tot;
+    }
+    __syncthreads();
+  }
+}
+
+struct VorCtx {
+  const double2* outer;
+  double p0x, p0y, ox, oy;
+};
+
+// Voronoi half-plane k: |x - p0|^2 <= |x - pk|^2  <=>  d.(m - x) >= 0 with
+// d = pk - p0 and m the midpoint (the perpendicular bisector, Eq. 9).
+__device__ int vor_class(int k, const void* ctx, float2* bc) {
+  const VorCtx& v = *static_cast<const VorCtx*>(ctx);
+  const double2 pk = v.outer[k];
+  const double dx = pk.x - v.p0x, dy = pk.y - v.p0y;
+  const double mx = 0.5 * ((v.p0x - v.ox) + (pk.x - v.ox));
+  const double my = 0.5 * ((v.p0y - v.oy) + (pk.y - v.oy));
+  return slab_classify(-dx, -dy, dx * mx + dy * my, bc);
+}
+
+struct OffCtx {
+  const double* vx;
+  const double* vy;
+  int n;
+  double ox, oy;
+};
+
+// Sign-of-offset edge e (j = e-1 -> i = e): inside iff lhs >= rhs, i.e.
+// (q - v_j) x dv >= 0 (engines.cpp:150-152 with the flags == 0 branch).
+__device__ int off_class(int e, const void* ctx, float2* bc) {
+  const OffCtx& o = *static_cast<const OffCtx*>(ctx);
+  const int i = e, j = (e + o.n - 1) % o.n;
+  const double dvx = o.vx[i] - o.vx[j], dvy = o.vy[i] - o.vy[j];
+  const double wx = o.vx[j] - o.ox, wy = o.vy[j] - o.oy;
+  return slab_classify(-dvy, dvx, wx * dvy - wy * dvx, bc);
+}
+
+__global__ void __launch_bounds__(kPrepThreads) prep_kernel(PrepArgs a) {
+  __shared__ double s_inner[2];
+  __shared__ int s_fail;  // min over failing edges of (edge * 8 + code): the first throw wins
+  const int tid = threadIdx.x;
+  const int n = static_cast<int>(a.n);
+  if (tid == 0) {
+    s_fail = INT_MAX;
+    double cx = 0.0, cy = 0.0;
+    if (a.gen_in != nullptr) {  // explicit generator set
+      cx = a.gen_in[0];
+      cy = a.gen_in[1];
+    } else if (a.vv != nullptr) {
+      // centroid, geometry.cpp:106-120, sequential in the reference order
+      double area2 = 0.0, sx = 0.0, sy = 0.0;
+      for (int i = 0, j = n - 1; i < n; j = i++) {
+        const double d = dsub(dmul(a.vv[j], a.vv[n + i]), dmul(a.vv[i], a.vv[n + j]));
+        area2 = dadd(area2, d);
+        sx = dadd(sx, dmul(dadd(a.vv[j], a.vv[i]), d));
+        sy = dadd(sy, dmul(dadd(a.vv[n + j], a.vv[n + i]), d));
+      }
+      cx = ddiv(sx, dmul(3.0, area2));
+      cy = ddiv(sy, dmul(3.0, area2));
+    } else if (a.vr != nullptr && n > 0) {  // crossing only: vertex mean as frame origin
+      for (int i = 0; i < n; ++i) {
+        cx += a.vr[i];
+        cy += a.vr[n + i];
+      }
+      cx /= n;
+      cy /= n;
+    }
+    s_inner[0] = cx;
+    s_inner[1] = cy;
+    float ox = static_cast<float>(cx), oy = static_cast<float>(cy);
+    // a zero origin is stored as -0.0f so that x - ox never yields -0.0
+    if (ox == 0.f) ox = -0.f;
+    if (oy == 0.f) oy = -0.f;
+    a.meta->inner_x = cx;
+    a.meta->inner_y = cy;
+    a.meta->ox = ox;
+    a.meta->oy = oy;
+  }
+  __syncthreads();
+  const double p0x = s_inner[0], p0y = s_inner[1];
+  const double ox = static_cast<double>(a.meta->ox), oy = static_cast<double>(a.meta->oy);
+
+  // ---- Voronoi generators (voronoi.cpp:60-71) ----
+  if (a.kinds & kKindVoronoi) {
+    if (a.gen_in != nullptr) {
+      for (int k = tid; k < n; k += kPrepThreads)
+        a.outer[k] = make_double2(a.gen_in[2 + 2 * k], a.gen_in[3 + 2 * k]);
+    } else {
+      for (int k = tid; k < n; k += kPrepThreads) {
+        const int k1 = (k + 1) % n;
+        const double qix = a.vv[k], qiy = a.vv[n + k], qjx = a.vv[k1], qjy = a.vv[n + k1];
+        // edge_coefficients, voronoi.cpp:23-31
+        const double ea = dsub(qiy, qjy);
+        const double eb = dsub(qjx, qix);
+        const double ec = -dadd(dmul(ea, qix), dmul(eb, qiy));
+        const double denom = dadd(dmul(ea, ea), dmul(eb, eb));
+        if (denom <= 1e-24) {
+          atomicMin(&s_fail, k * 8 + 3);  // DegenerateEdge
+          continue;
+        }
+        // reflect_generator, voronoi.cpp:46-58 (Eq. 8, fused)
+        if (fabs(dadd(dadd(dmul(ea, p0x), dmul(eb, p0y)), ec)) <= dmul(1e-12, denom)) {
+          atomicMin(&s_fail, k * 8 + 5);  // GeneratorCollision
+          continue;
+        }
+        const double t1 = dmul(dsub(dmul(eb, eb), dmul(ea, ea)), p0x);
+        const double t2 = dmul(dmul(dmul(2.0, ea), eb), p0y);
+        const double t3 = dmul(dmul(2.0, ec), ea);
+        const double rx = ddiv(dsub(dsub(t1, t2), t3), denom);
+        const double u1 = dmul(dmul(dmul(-2.0, ea), eb), p0x);
+        const double u2 = dmul(dsub(dmul(ea, ea), dmul(eb, eb)), p0y);
+        const double u3 = dmul(dmul(2.0, ec), eb);
+        const double ry = ddiv(dsub(dadd(u1, u2), u3), denom);
+        a.outer[k] = make_double2(rx, ry);
+      }
+    }
+    __syncthreads();
+    VorCtx vc{a.outer, p0x, p0y, ox, oy};
+    slab_scatter(n, vor_class, &vc, a.slab_coef[0], a.meta->cnt[0]);
+  }
+
+  // ---- sign-of-offset (engines.cpp:146-149) ----
+  if (a.kinds & kKindOffset) {
+    for (int e = tid; e < n; e += kPrepThreads) {
+      const int i = e, j = (e + n - 1) % n;
+      const double dvx = dsub(a.vv[i], a.vv[j]);
+      const double dvy = dsub(a.vv[n + i], a.vv[n + j]);
+      const double rhs = dsub(dmul(a.vv[n + j], dvx), dmul(a.vv[j], dvy));
+      a.off[e] = OffsetEdgeF64{dvx, dvy, rhs, 0.0};
+    }
+    __syncthreads();
+    OffCtx oc{a.vv, a.vv + n, n, ox, oy};
+    slab_scatter(n, off_class, &oc, a.slab_coef[1], a.meta->cnt[1]);
+  }
+
+  // ---- ray crossing (engines.cpp:176-186), raw vertices ----
+  if (a.kinds & kKindCrossing) {
+    for (int e = tid; e < n; e += kPrepThreads) {
+      const int i = e, j = (e + n - 1) % n;
+      const double wx = a.vr[j], wy = a.vr[n + j], ux = a.vr[i], uy = a.vr[n + i];
+      const double dvx = dsub(ux, wx), dvy = dsub(uy, wy);
+      RayEdgeF64 r;
+      r.wy = wy;
+      r.uy = uy;
+      r.dvx = dvx;
+      r.dvy = dvy;
+      r.rhs = dsub(dmul(wy, dvx), dmul(wx, dvy));
+      r.min_x = smin(wx, ux);
+      r.max_x = smax(wx, ux);
+      r.min_y = smin(wy, uy);
+      r.max_y = smax(wy, uy);
+      r.going_up = uy > wy;
+      r.pad_ = 0;
+      a.ray[e] = r;
+      // fp32 crossing record for vertex i (edge j -> i)
+      // (+0.0 turns a -0.0 difference into +0.0: sign bits are tested directly)
+      const float xl = static_cast<float>((ux - ox) + 0.0);
+      const float yl = static_cast<float>((uy - oy) + 0.0);
+      const float bk = (dvy != 0.0) ? static_cast<float>(dvx / dvy) : 0.f;
+      a.cross_vert[i] = make_float4(xl, yl, bk, 0.f);
+    }
+  }
+  __syncthreads();
+  if (tid == 0) a.meta->status = (s_fail == INT_MAX) ? 0 : (s_fail & 7);
+}
+
+}  // namespace
+
+cudaError_t launch_prep(const PrepArgs& args, cudaStream_t stream) {
+  prep_kernel<<<1, kPrepThreads, 0, stream>>>(args);
+  return cudaGetLastError();
+}
+
+}  // namespace vpipg

@@ -1,0 +1,184 @@
+// test_f64.cu -- fp64 batched point-inclusion kernels that repeat the
+// reference's arithmetic operation for operation.
+//
+// The reference is compiled with -ffp-contract=off (proj/CMakeLists.txt:16),
+// so each of its expressions is a sequence of individually rounded IEEE
+// operations. These kernels issue the same sequence with __dsub_rn /
+// __dmul_rn / __dadd_rn (never fused), so every mask byte equals the
+// reference's for every input, boundary points included:
+//   voronoi_kernel (engines.cpp:65-104): inner_sq <= outer_sq for all k
+//   offset_kernel  (engines.cpp:136-160): flags in {0, n}
+//   ray_kernel     (engines.cpp:165-204): parity | on-segment latch
+// Same warp-tile / ballot / fused-count structure as test_f32.cu.
+#include <cstdint>
+
+#include "vpipg_device.cuh"
+#include "vpipg_internal.h"
+
+namespace vpipg {
+
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kWarps = kThreads / 32;
+
+__device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a, b); }
+
+template <int P>
+__device__ __forceinline__ uint32_t emit_words(const bool (&in)[P], uint64_t base, uint64_t m,
+                                               const TestArgs& a, int lane) {
+  uint32_t mine = 0;
+#pragma unroll
+  for (int p = 0; p < P; ++p) {
+    const uint32_t w = __ballot_sync(0xffffffffu, in[p]);
+    if (lane == p) mine = w;
+  }
+  const uint64_t w0 = base >> 5;
+  const uint64_t nwords = (m + 31) >> 5;
+  if (lane < P && w0 + lane < nwords && a.words) a.words[w0 + lane] = mine;
+  if (a.bytes) {
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+      const uint64_t idx = base + 32u * p + lane;
+      if (idx < m) a.bytes[idx] = in[p] ? 1 : 0;
+    }
+  }
+  return lane < P ? __popc(mine) : 0u;
+}
+
+__device__ __forceinline__ void flush_count(uint32_t cnt, const TestArgs& a) {
+#pragma unroll
+  for (int s = 16; s > 0; s >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, s);
+  if ((threadIdx.x & 31) == 0 && a.inside && cnt) atomicAdd(a.inside, (unsigned long long)cnt);
+}
+
+template <int kEngine, int P>
+__global__ void __launch_bounds__(kThreads) exact_kernel(const DevTables t, const TestArgs a) {
+  extern __shared__ double4 s_tab[];
+  const uint32_t n = t.n;
+  // stage the per-edge records
+  if (kEngine == 0) {
+    double2* s = reinterpret_cast<double2*>(s_tab);
+    for (uint32_t i = threadIdx.x; i < n; i += kThreads) s[i] = t.outer[i];
+  } else if (kEngine == 1) {
+    OffsetEdgeF64* s = reinterpret_cast<OffsetEdgeF64*>(s_tab);
+    for (uint32_t i = threadIdx.x; i < n; i += kThreads) s[i] = t.off[i];
+  } else {
+    RayEdgeF64* s = reinterpret_cast<RayEdgeF64*>(s_tab);
+    for (uint32_t i = threadIdx.x; i < n; i += kThreads) s[i] = t.ray[i];
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  const double* xs = static_cast<const double*>(a.xs);
+  const double* ys = static_cast<const double*>(a.ys);
+  const uint64_t tiles = (a.m + 32u * P - 1) / (32u * P);
+  uint32_t count = 0;
+  for (uint64_t tile = (uint64_t)blockIdx.x * kWarps + warp; tile < tiles;
+       tile += (uint64_t)gridDim.x * kWarps) {
+    const uint64_t base = tile * 32u * P;
+    double x[P], y[P];
+    bool in[P];
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+      const uint64_t idx = base + 32u * p + lane;
+      const bool ok = idx < a.m;
+      x[p] = ok ? __ldcs(xs + idx) : 0.0;
+      y[p] = ok ? __ldcs(ys + idx) : 0.0;
+    }
+    if (kEngine == 0) {
+      const double2* s = reinterpret_cast<const double2*>(s_tab);
+      double inner_sq[P];
+#pragma unroll
+      for (int p = 0; p < P; ++p) {
+        const double dx = dsub(x[p], t.inner_x), dy = dsub(y[p], t.inner_y);
+        inner_sq[p] = dadd(dmul(dx, dx), dmul(dy, dy));
+        in[p] = true;
+      }
+      for (uint32_t k = 0; k < n; ++k) {
+        const double2 g = s[k];
+#pragma unroll
+        for (int p = 0; p < P; ++p) {
+          const double dx = dsub(x[p], g.x), dy = dsub(y[p], g.y);
+          const double outer_sq = dadd(dmul(dx, dx), dmul(dy, dy));
+          in[p] &= inner_sq[p] <= outer_sq;
+        }
+      }
+    } else if (kEngine == 1) {
+      const OffsetEdgeF64* s = reinterpret_cast<const OffsetEdgeF64*>(s_tab);
+      uint32_t flags[P];
+#pragma unroll
+      for (int p = 0; p < P; ++p) flags[p] = 0;
+      for (uint32_t e = 0; e < n; ++e) {
+        const OffsetEdgeF64 r = s[e];
+#pragma unroll
+        for (int p = 0; p < P; ++p) {
+          const double lhs = dsub(dmul(y[p], r.dvx), dmul(x[p], r.dvy));
+          flags[p] += lhs < r.rhs;
+        }
+      }
+#pragma unroll
+      for (int p = 0; p < P; ++p) in[p] = (flags[p] == 0u) | (flags[p] == n);
+    } else {
+      const RayEdgeF64* s = reinterpret_cast<const RayEdgeF64*>(s_tab);
+      bool parity[P], on_edge[P];
+#pragma unroll
+      for (int p = 0; p < P; ++p) { parity[p] = false; on_edge[p] = false; }
+      for (uint32_t e = 0; e < n; ++e) {
+        const RayEdgeF64 r = s[e];
+#pragma unroll
+        for (int p = 0; p < P; ++p) {
+          const bool in_range = (r.uy > y[p]) != (r.wy > y[p]);
+          const double lhs = dsub(dmul(y[p], r.dvx), dmul(x[p], r.dvy));
+          const bool on_left = (lhs != r.rhs) & ((lhs > r.rhs) == (r.going_up != 0));
+          parity[p] ^= in_range & on_left;
+          on_edge[p] |= (lhs == r.rhs) & (x[p] >= r.min_x) & (x[p] <= r.max_x) &
+                        (y[p] >= r.min_y) & (y[p] <= r.max_y);
+        }
+      }
+#pragma unroll
+      for (int p = 0; p < P; ++p) in[p] = on_edge[p] | parity[p];
+    }
+#pragma unroll
+    for (int p = 0; p < P; ++p) in[p] = in[p] & (base + 32u * p + lane < a.m);
+    count += emit_words<P>(in, base, a.m, a, lane);
+  }
+  flush_count(count, a);
+}
+
+template <int kEngine>
+cudaError_t launch_one(const DevTables& t, const TestArgs& a, size_t rec_bytes,
+                       cudaStream_t stream) {
+  constexpr int P = 4;
+  auto k = exact_kernel<kEngine, P>;
+  const size_t smem = (size_t)t.n * rec_bytes;
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  int dev = 0, sms = 0, per_sm = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kThreads, smem);
+  if (per_sm < 1) per_sm = 1;
+  const uint64_t need = (a.m + kThreads * P - 1) / (kThreads * P);
+  const uint64_t cap = (uint64_t)sms * per_sm;
+  const int grid = static_cast<int>(need < cap ? (need ? need : 1) : cap);
+  k<<<grid, kThreads, smem, stream>>>(t, a);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+cudaError_t launch_test_f64(const DevTables& t, int engine, const TestArgs& a,
+                            cudaStream_t stream) {
+  switch (engine) {
+    case 0: return launch_one<0>(t, a, sizeof(double2), stream);
+    case 1: return launch_one<1>(t, a, sizeof(OffsetEdgeF64), stream);
+    default: return launch_one<2>(t, a, sizeof(RayEdgeF64), stream);
+  }
+}
+
+}  // namespace vpipg

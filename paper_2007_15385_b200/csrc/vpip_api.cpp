@@ -1,0 +1,439 @@
+// vpip_api.cpp -- the reference's C++ API (include/vpip/*.hpp) implemented
+// over the B200 C-ABI (include/vpipg.h).
+//
+// The batch engines and the polygon conversion run on the GPU; the scalar
+// early-exit tests, the small geometric helpers and the samplers stay on the
+// host, as in the reference (they are not on the batched hot path). Compiled
+// with -ffp-contract=off so every host expression rounds like the reference's
+// Release build.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <limits>
+#include <numbers>
+#include <random>
+#include <stdexcept>
+#include <string>
+
+#include <cuda_runtime.h>
+
+#include "vpip/engines.hpp"
+#include "vpip/error.hpp"
+#include "vpip/geometry.hpp"
+#include "vpip/sampling.hpp"
+#include "vpip/voronoi.hpp"
+#include "vpipg.h"
+
+namespace vpip {
+
+// ---------------------------------------------------------------- errors
+std::string_view error_code_name(ErrorCode code) {
+  return vpipg_strerror(static_cast<int>(code) + 1);
+}
+
+Error::Error(ErrorCode code, const std::string& message)
+    : std::runtime_error(std::string(error_code_name(code)) + ": " + message), code_(code) {}
+
+namespace {
+
+// C-ABI status -> the reference's exception types.
+void check(int rc, const char* what) {
+  if (rc == 0) return;
+  if (rc >= 1 && rc <= 7) throw Error(static_cast<ErrorCode>(rc - 1), what);
+  throw std::runtime_error(std::string(what) + ": " + vpipg_strerror(rc));
+}
+
+int current_device() {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) throw std::runtime_error("vpip: no CUDA device");
+  return dev;
+}
+
+struct Handle {
+  vpipg_poly* p = nullptr;
+  ~Handle() { vpipg_destroy(p); }
+};
+
+void split(std::span<const Point2> v, std::vector<double>& x, std::vector<double>& y) {
+  x.resize(v.size());
+  y.resize(v.size());
+  for (std::size_t i = 0; i < v.size(); ++i) {
+    x[i] = v[i].x;
+    y[i] = v[i].y;
+  }
+}
+
+InclusionMask run(const vpipg_poly* p, int engine, const PointBatch& points) {
+  if (points.xs.size() != points.ys.size())
+    throw Error(ErrorCode::InvalidParameter, "xs and ys differ in length");
+  InclusionMask mask(points.size());
+  if (points.empty()) return mask;
+  check(vpipg_test_host(p, engine, VPIPG_F64, points.xs.data(), points.ys.data(), points.size(),
+                        nullptr, mask.data(), nullptr),
+        "vpipg_test_host");
+  return mask;
+}
+
+double smin(double a, double b) { return std::min(a, b); }
+double smax(double a, double b) { return std::max(a, b); }
+
+}  // namespace
+
+// ---------------------------------------------------------------- geometry
+bool Box::valid() const {
+  return std::isfinite(min_x) && std::isfinite(min_y) && std::isfinite(max_x) &&
+         std::isfinite(max_y) && min_x < max_x && min_y < max_y;
+}
+
+Box Box::scaled(double factor) const {
+  const Point2 c = center();
+  const double hw = 0.5 * factor * width();
+  const double hh = 0.5 * factor * height();
+  return {c.x - hw, c.y - hh, c.x + hw, c.y + hh};
+}
+
+Box bounding_box(std::span<const Point2> points) {
+  if (points.empty()) throw Error(ErrorCode::InvalidParameter, "bounding box of an empty point set");
+  Box b{points[0].x, points[0].y, points[0].x, points[0].y};
+  for (const Point2& p : points) {
+    b.min_x = smin(b.min_x, p.x);
+    b.min_y = smin(b.min_y, p.y);
+    b.max_x = smax(b.max_x, p.x);
+    b.max_y = smax(b.max_y, p.y);
+  }
+  return b;
+}
+
+double signed_area(std::span<const Point2> v) {
+  double s = 0.0;
+  for (std::size_t i = 0, j = v.size() - 1; i < v.size(); j = i++) s += v[j].x * v[i].y - v[i].x * v[j].y;
+  return 0.5 * s;
+}
+
+double signed_area(const ConvexPolygon& polygon) { return signed_area(polygon.vertices()); }
+
+ConvexPolygon validate_polygon(std::vector<Point2> vertices, double convexity_epsilon) {
+  const std::size_t n = vertices.size();
+  for (std::size_t i = 0; i < n; ++i)
+    if (!is_finite(vertices[i])) throw Error(ErrorCode::NonFinite, "vertex " + std::to_string(i));
+  if (n < 3) throw Error(ErrorCode::TooFewVertices, std::to_string(n) + " vertices");
+  for (std::size_t i = 0, j = n - 1; i < n; j = i++)
+    if (squared_distance(vertices[j], vertices[i]) <= tol::kDegenerateEdgeSq)
+      throw Error(ErrorCode::DegenerateEdge, "vertices " + std::to_string(j) + " and " + std::to_string(i));
+  double twice = 0.0;
+  for (std::size_t i = 0, j = n - 1; i < n; j = i++)
+    twice += vertices[j].x * vertices[i].y - vertices[i].x * vertices[j].y;
+  const bool reversed = twice < 0.0;
+  if (reversed) std::reverse(vertices.begin(), vertices.end());
+  double turn = 0.0;
+  for (std::size_t i = 0; i < n; ++i) {
+    const Point2 in = vertices[i] - vertices[(i + n - 1) % n];
+    const Point2 out = vertices[(i + 1) % n] - vertices[i];
+    const double c = cross(in, out);
+    if (c <= convexity_epsilon)
+      throw Error(ErrorCode::NotConvex, "collinear or reflex vertex at index " + std::to_string(i));
+    turn += std::atan2(c, dot(in, out));
+  }
+  if (turn >= 3.0 * std::numbers::pi) throw Error(ErrorCode::NotConvex, "winds more than once");
+  return ConvexPolygon(std::move(vertices), reversed);
+}
+
+Point2 centroid(const ConvexPolygon& polygon) { return to_voronoi(polygon).inner; }
+
+// ---------------------------------------------------------------- voronoi helpers
+EdgeCoefficients edge_coefficients(Point2 qi, Point2 qj, double degenerate_sq) {
+  const double a = qi.y - qj.y;
+  const double b = qj.x - qi.x;
+  const double c = -(a * qi.x + b * qi.y);
+  if (a * a + b * b <= degenerate_sq) throw Error(ErrorCode::DegenerateEdge, "edge endpoints coincide");
+  return {a, b, c};
+}
+
+double line_distance(const EdgeCoefficients& e, Point2 p) {
+  return std::abs(e.a * p.x + e.b * p.y + e.c) / std::hypot(e.a, e.b);
+}
+
+Point2 foot_of_perpendicular(Point2 p0, const EdgeCoefficients& e) {
+  const double d = e.a * e.a + e.b * e.b;
+  return {(e.b * e.b * p0.x - e.a * e.b * p0.y - e.c * e.a) / d,
+          (-e.a * e.b * p0.x + e.a * e.a * p0.y - e.c * e.b) / d};
+}
+
+Point2 reflect_generator(Point2 p0, const EdgeCoefficients& e, double collision_rel) {
+  const double a = e.a, b = e.b, d = a * a + b * b;
+  if (std::abs(a * p0.x + b * p0.y + e.c) <= collision_rel * d)
+    throw Error(ErrorCode::GeneratorCollision, "point lies on the edge line");
+  return {((b * b - a * a) * p0.x - 2.0 * a * b * p0.y - 2.0 * e.c * a) / d,
+          (-2.0 * a * b * p0.x + (a * a - b * b) * p0.y - 2.0 * e.c * b) / d};
+}
+
+GeneratorSet to_voronoi(const ConvexPolygon& polygon) {
+  std::vector<double> x, y;
+  split(polygon.vertices(), x, y);
+  Handle h;
+  check(vpipg_prepare(x.data(), y.data(), static_cast<uint32_t>(x.size()), VPIPG_KIND_VORONOI,
+                      current_device(), nullptr, &h.p),
+        "to_voronoi");
+  std::vector<double> outer(2 * x.size());
+  double inner[2];
+  check(vpipg_poly_generators(h.p, inner, outer.data()), "to_voronoi");
+  GeneratorSet g;
+  g.inner = {inner[0], inner[1]};
+  g.outer.resize(x.size());
+  for (std::size_t k = 0; k < x.size(); ++k) g.outer[k] = {outer[2 * k], outer[2 * k + 1]};
+  return g;
+}
+
+double edge_line_distance(const ConvexPolygon& polygon, Point2 p) {
+  const auto v = polygon.vertices();
+  double nearest = std::numeric_limits<double>::infinity();
+  for (std::size_t k = 0; k < v.size(); ++k)
+    nearest = smin(nearest, line_distance(edge_coefficients(v[k], v[(k + 1) % v.size()]), p));
+  return nearest;
+}
+
+// ---------------------------------------------------------------- engines
+PointBatch PointBatch::from_points(std::span<const Point2> points) {
+  PointBatch b;
+  b.reserve(points.size());
+  for (const Point2& p : points) b.push_back(p);
+  return b;
+}
+
+std::size_t count_inside(const InclusionMask& mask) {
+  std::size_t s = 0;
+  for (std::uint8_t b : mask) s += b;
+  return s;
+}
+
+std::string_view engine_name(EngineKind kind) {
+  switch (kind) {
+    case EngineKind::Voronoi: return "voronoi";
+    case EngineKind::SignOfOffset: return "sign_of_offset";
+    case EngineKind::RayCrossing: return "ray_crossing";
+  }
+  return "unknown";
+}
+
+std::optional<EngineKind> parse_engine(std::string_view name) {
+  if (name == "voronoi") return EngineKind::Voronoi;
+  if (name == "sign_of_offset" || name == "offset") return EngineKind::SignOfOffset;
+  if (name == "ray_crossing" || name == "crossing") return EngineKind::RayCrossing;
+  return std::nullopt;
+}
+
+bool voronoi_contains(const GeneratorSet& g, Point2 p) {
+  const double inner_sq = squared_distance(p, g.inner);
+  for (const Point2& o : g.outer)
+    if (squared_distance(p, o) < inner_sq) return false;
+  return true;
+}
+
+InclusionMask voronoi_contains_batch(const GeneratorSet& g, const PointBatch& points, int) {
+  std::vector<double> outer(2 * g.outer.size());
+  for (std::size_t k = 0; k < g.outer.size(); ++k) {
+    outer[2 * k] = g.outer[k].x;
+    outer[2 * k + 1] = g.outer[k].y;
+  }
+  const double inner[2] = {g.inner.x, g.inner.y};
+  Handle h;
+  check(vpipg_prepare_generators(inner, outer.data(), static_cast<uint32_t>(g.outer.size()),
+                                 current_device(), nullptr, &h.p),
+        "voronoi_contains_batch");
+  return run(h.p, VPIPG_ENGINE_VORONOI, points);
+}
+
+InclusionMask voronoi_contains_batch(const GeneratorSet& g, const PointBatch& points,
+                                     BatchStats& stats, int threads) {
+  InclusionMask mask = voronoi_contains_batch(g, points, threads);
+  // the device kernel is branch-free: (n+1)*m evaluations, n*m comparisons
+  stats.distance_evaluations += (g.edge_count() + 1) * points.size();
+  stats.comparisons += g.edge_count() * points.size();
+  return mask;
+}
+
+InclusionMask voronoi_contains_batch_sqrt(const GeneratorSet& g, const PointBatch& points, int) {
+  InclusionMask mask(points.size());
+  for (std::size_t j = 0; j < points.size(); ++j) {
+    const double inner = std::sqrt(squared_distance(points.at(j), g.inner));
+    std::uint8_t in = 1;
+    for (const Point2& o : g.outer) in &= static_cast<std::uint8_t>(inner <= std::sqrt(squared_distance(points.at(j), o)));
+    mask[j] = in;
+  }
+  return mask;
+}
+
+SquaredDistanceTable squared_distance_table(const GeneratorSet& g, const PointBatch& points) {
+  const std::size_t rows = g.edge_count() + 1, cols = points.size();
+  SquaredDistanceTable t{rows, cols, std::vector<double>(rows * cols)};
+  for (std::size_t r = 0; r < rows; ++r) {
+    const Point2 q = r == 0 ? g.inner : g.outer[r - 1];
+    for (std::size_t j = 0; j < cols; ++j) t.values[r * cols + j] = squared_distance(points.at(j), q);
+  }
+  return t;
+}
+
+bool sign_of_offset_contains(const ConvexPolygon& polygon, Point2 p) {
+  const auto v = polygon.vertices();
+  for (std::size_t i = 0, j = v.size() - 1; i < v.size(); j = i++) {
+    const double dvx = v[i].x - v[j].x, dvy = v[i].y - v[j].y;
+    if (p.y * dvx - p.x * dvy < v[j].y * dvx - v[j].x * dvy) return false;
+  }
+  return true;
+}
+
+InclusionMask sign_of_offset_contains_batch(const ConvexPolygon& polygon, const PointBatch& points,
+                                            int) {
+  std::vector<double> x, y;
+  split(polygon.vertices(), x, y);
+  Handle h;
+  check(vpipg_prepare(x.data(), y.data(), static_cast<uint32_t>(x.size()), VPIPG_KIND_OFFSET,
+                      current_device(), nullptr, &h.p),
+        "sign_of_offset_contains_batch");
+  return run(h.p, VPIPG_ENGINE_OFFSET, points);
+}
+
+namespace {
+bool on_segment_or_cross(Point2 w, Point2 u, Point2 p, int& crossings) {
+  const double dvx = u.x - w.x, dvy = u.y - w.y;
+  const bool in_range = (u.y > p.y) != (w.y > p.y);
+  const double lhs = p.y * dvx - p.x * dvy;
+  const double rhs = w.y * dvx - w.x * dvy;
+  crossings += in_range && (lhs != rhs) && ((lhs > rhs) == (u.y > w.y));
+  return lhs == rhs && p.x >= smin(w.x, u.x) && p.x <= smax(w.x, u.x) && p.y >= smin(w.y, u.y) &&
+         p.y <= smax(w.y, u.y);
+}
+}  // namespace
+
+bool ray_crossing_contains(std::span<const Point2> v, Point2 p) {
+  int crossings = 0;
+  for (std::size_t i = 0, j = v.size() - 1; i < v.size(); j = i++)
+    if (on_segment_or_cross(v[j], v[i], p, crossings)) return true;
+  return (crossings & 1) != 0;
+}
+
+int ray_crossing_count(std::span<const Point2> v, Point2 p) {
+  int crossings = 0;
+  for (std::size_t i = 0, j = v.size() - 1; i < v.size(); j = i++) on_segment_or_cross(v[j], v[i], p, crossings);
+  return crossings;
+}
+
+InclusionMask ray_crossing_contains_batch(std::span<const Point2> vertices, const PointBatch& points,
+                                          int) {
+  std::vector<double> x, y;
+  split(vertices, x, y);
+  Handle h;
+  check(vpipg_prepare(x.data(), y.data(), static_cast<uint32_t>(x.size()), VPIPG_KIND_CROSSING,
+                      current_device(), nullptr, &h.p),
+        "ray_crossing_contains_batch");
+  return run(h.p, VPIPG_ENGINE_CROSSING, points);
+}
+
+// ---------------------------------------------------------------- sampling
+namespace {
+double unit_real(std::mt19937_64& rng) { return static_cast<double>(rng() >> 11) * 0x1.0p-53; }
+void check_params(std::size_t n, double r, Point2 c) {
+  if (n < 3) throw Error(ErrorCode::InvalidParameter, "polygon needs at least 3 vertices");
+  if (!std::isfinite(r) || r <= 0.0) throw Error(ErrorCode::InvalidParameter, "circumradius must be positive and finite");
+  if (!is_finite(c)) throw Error(ErrorCode::InvalidParameter, "center must be finite");
+}
+}  // namespace
+
+ConvexPolygon regular_polygon(std::size_t n, double r, Point2 c) {
+  check_params(n, r, c);
+  std::vector<Point2> v(n);
+  for (std::size_t k = 0; k < n; ++k) {
+    const double a = 2.0 * std::numbers::pi * static_cast<double>(k) / static_cast<double>(n) +
+                     std::numbers::pi / 2.0;
+    v[k] = {c.x + r * std::cos(a), c.y + r * std::sin(a)};
+  }
+  return validate_polygon(std::move(v));
+}
+
+ConvexPolygon random_convex_polygon(std::size_t n, std::uint64_t seed, double r, Point2 c) {
+  check_params(n, r, c);
+  std::mt19937_64 rng(seed);
+  const double min_gap = 2.0 * std::numbers::pi / (20.0 * static_cast<double>(n));
+  std::vector<double> ang(n);
+  for (int attempt = 0; attempt < 1024; ++attempt) {
+    for (double& a : ang) a = 2.0 * std::numbers::pi * unit_real(rng);
+    std::sort(ang.begin(), ang.end());
+    bool ok = ang.front() + 2.0 * std::numbers::pi - ang.back() >= min_gap;
+    for (std::size_t k = 1; ok && k < n; ++k) ok = ang[k] - ang[k - 1] >= min_gap;
+    if (!ok) continue;
+    std::vector<Point2> v(n);
+    for (std::size_t k = 0; k < n; ++k) v[k] = {c.x + r * std::cos(ang[k]), c.y + r * std::sin(ang[k])};
+    return validate_polygon(std::move(v));
+  }
+  throw Error(ErrorCode::InvalidParameter, "no well-spaced angle draw after 1024 attempts");
+}
+
+PointBatch sample_points(std::size_t count, const Box& box, std::uint64_t seed) {
+  if (!box.valid()) throw Error(ErrorCode::InvalidParameter, "sampling box is degenerate");
+  std::mt19937_64 rng(seed);
+  PointBatch b;
+  b.xs.resize(count);
+  b.ys.resize(count);
+  const double w = box.width(), h = box.height();
+  for (std::size_t j = 0; j < count; ++j) {
+    b.xs[j] = box.min_x + w * unit_real(rng);
+    b.ys[j] = box.min_y + h * unit_real(rng);
+  }
+  return b;
+}
+
+std::uint64_t mix_seed(std::uint64_t seed, std::uint64_t salt) { return vpipg_mix_seed(seed, salt); }
+
+}  // namespace vpip
+
+// ---------------------------------------------------------------- C-ABI samplers
+extern "C" {
+
+uint64_t vpipg_mix_seed(uint64_t seed, uint64_t salt) {
+  uint64_t z = seed + 0x9e3779b97f4a7c15ULL * (salt + 1);
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+  return z ^ (z >> 31);
+}
+
+static int sampler_status(const vpip::Error& e) { return static_cast<int>(e.code()) + 1; }
+
+static void copy_out(const vpip::ConvexPolygon& p, double* vx, double* vy) {
+  for (std::size_t i = 0; i < p.size(); ++i) {
+    vx[i] = p.vertex(i).x;
+    vy[i] = p.vertex(i).y;
+  }
+}
+
+int vpipg_regular_polygon(uint32_t n, double r, double cx, double cy, double* vx, double* vy) {
+  try {
+    copy_out(vpip::regular_polygon(n, r, {cx, cy}), vx, vy);
+    return 0;
+  } catch (const vpip::Error& e) {
+    return sampler_status(e);
+  }
+}
+
+int vpipg_random_convex_polygon(uint32_t n, uint64_t seed, double r, double cx, double cy,
+                                double* vx, double* vy) {
+  try {
+    copy_out(vpip::random_convex_polygon(n, seed, r, {cx, cy}), vx, vy);
+    return 0;
+  } catch (const vpip::Error& e) {
+    return sampler_status(e);
+  }
+}
+
+int vpipg_sample_points(uint64_t count, double min_x, double min_y, double max_x, double max_y,
+                        uint64_t seed, double* xs, double* ys) {
+  try {
+    const vpip::PointBatch b = vpip::sample_points(count, {min_x, min_y, max_x, max_y}, seed);
+    std::memcpy(xs, b.xs.data(), count * sizeof(double));
+    std::memcpy(ys, b.ys.data(), count * sizeof(double));
+    return 0;
+  } catch (const vpip::Error& e) {
+    return sampler_status(e);
+  }
+}
+
+}  // extern "C"

@@ -1,0 +1,165 @@
+"""Python host mirror of the vpip engine interface over the C-ABI.
+
+`PreparedPolygon` is the handle of include/vpipg.h (vpipg_prepare /
+vpipg_prepare_generators); `test()` is the fused batch test + count
+(vpipg_test) on device tensors, `test_host()` the host-buffer drop-in
+(vpipg_test_host). Names and argument meaning follow the reference API
+(proj/include/vpip/engines.hpp, voronoi.hpp); errors raise VpipError with the
+reference's ErrorCode. torch is used only for device memory and streams.
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from . import _lib
+from ._lib import (ENGINES, F32, F64, KIND_ALL, KIND_CROSSING, KIND_OFFSET, KIND_VORONOI,
+                   VpipError, check, load)
+
+__all__ = ["PreparedPolygon", "VpipError", "fill_uniform_points", "mix_seed",
+           "regular_polygon", "random_convex_polygon", "sample_points", "KIND_ALL",
+           "KIND_VORONOI", "KIND_OFFSET", "KIND_CROSSING", "F32", "F64"]
+
+
+def _dptr(a: np.ndarray):
+    return a.ctypes.data_as(C.POINTER(C.c_double))
+
+
+def _stream_ptr(stream) -> C.c_void_p:
+    if stream is None:
+        return C.c_void_p(None)
+    if isinstance(stream, int):
+        return C.c_void_p(stream)
+    return C.c_void_p(stream.cuda_stream)  # torch.cuda.Stream
+
+
+def _engine_id(engine) -> int:
+    return ENGINES[engine] if isinstance(engine, str) else int(engine)
+
+
+class PreparedPolygon:
+    """A polygon converted on the device (validate_polygon + to_voronoi + edge tables)."""
+
+    def __init__(self, handle: C.c_void_p, n: int):
+        self._h = handle
+        self.n = n
+
+    @classmethod
+    def prepare(cls, vx, vy, kinds: int = KIND_ALL, device: int = 0, stream=None):
+        vx = np.ascontiguousarray(vx, dtype=np.float64)
+        vy = np.ascontiguousarray(vy, dtype=np.float64)
+        if vx.shape != vy.shape or vx.ndim != 1:
+            raise VpipError(6, "prepare")
+        h = C.c_void_p()
+        check(load().vpipg_prepare(_dptr(vx), _dptr(vy), vx.size, kinds, device,
+                                   _stream_ptr(stream), C.byref(h)), "vpipg_prepare")
+        return cls(h, vx.size)
+
+    @classmethod
+    def from_generators(cls, inner, outer, device: int = 0, stream=None):
+        inner = np.ascontiguousarray(inner, dtype=np.float64).reshape(2)
+        outer = np.ascontiguousarray(outer, dtype=np.float64).reshape(-1, 2)
+        h = C.c_void_p()
+        check(load().vpipg_prepare_generators(_dptr(inner), _dptr(outer), outer.shape[0], device,
+                                              _stream_ptr(stream), C.byref(h)),
+              "vpipg_prepare_generators")
+        return cls(h, outer.shape[0])
+
+    def close(self) -> None:
+        if self._h:
+            load().vpipg_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    @property
+    def handle(self) -> C.c_void_p:
+        return self._h
+
+    def info(self):
+        n, kinds, rev = C.c_uint32(), C.c_uint32(), C.c_int()
+        check(load().vpipg_poly_info(self._h, C.byref(n), C.byref(kinds), C.byref(rev)))
+        return n.value, kinds.value, bool(rev.value)
+
+    def generators(self):
+        """(inner[2], outer[n, 2]) as built on the device (GeneratorSet)."""
+        inner = np.zeros(2)
+        outer = np.zeros((self.n, 2))
+        check(load().vpipg_poly_generators(self._h, _dptr(inner), _dptr(outer)), "generators")
+        return inner, outer
+
+    def vertices(self):
+        vx, vy = np.zeros(self.n), np.zeros(self.n)
+        check(load().vpipg_poly_vertices(self._h, _dptr(vx), _dptr(vy)))
+        return vx, vy
+
+    def test(self, engine, xs, ys, words=None, bytes_=None, count=None, stream=None) -> None:
+        """Fused batch test on device tensors (vpipg_test). Asynchronous.
+
+        xs, ys: 1-D CUDA tensors (float32 -> F32 kernels, float64 -> exact F64
+        kernels). words: int32 tensor of ceil(m/32) (PIPM bit order); bytes_:
+        uint8 tensor of m; count: int64 tensor of 1 (accumulated).
+        """
+        import torch
+        dtype = F32 if xs.dtype == torch.float32 else F64
+        m = xs.numel()
+        ptr = lambda t: C.c_void_p(t.data_ptr()) if t is not None else C.c_void_p(None)
+        check(load().vpipg_test(self._h, _engine_id(engine), dtype, ptr(xs), ptr(ys), m,
+                                ptr(words), ptr(bytes_), ptr(count), _stream_ptr(stream)),
+              "vpipg_test")
+
+    def test_host(self, engine, xs: np.ndarray, ys: np.ndarray, words: bool = True,
+                  bytes_: bool = False):
+        """Host-buffer drop-in (vpipg_test_host): returns (words|None, bytes|None, count)."""
+        dtype = F32 if xs.dtype == np.float32 else F64
+        m = xs.size
+        w = np.zeros((m + 31) // 32, dtype=np.uint32) if words else None
+        b = np.zeros(m, dtype=np.uint8) if bytes_ else None
+        cnt = C.c_uint64()
+        vp = lambda a: C.c_void_p(a.ctypes.data) if a is not None else C.c_void_p(None)
+        check(load().vpipg_test_host(self._h, _engine_id(engine), dtype, vp(xs), vp(ys), m,
+                                     vp(w), vp(b), C.byref(cnt)), "vpipg_test_host")
+        return w, b, cnt.value
+
+
+def fill_uniform_points(seed: int, first: int, xs, ys, box, stream=None) -> None:
+    """Counter-based device point stream (vpipg_fill_uniform_points)."""
+    import torch
+    dtype = F32 if xs.dtype == torch.float32 else F64
+    check(load().vpipg_fill_uniform_points(seed, first, xs.numel(), *map(float, box), dtype,
+                                           C.c_void_p(xs.data_ptr()), C.c_void_p(ys.data_ptr()),
+                                           _stream_ptr(stream)), "fill_uniform_points")
+
+
+def mix_seed(seed: int, salt: int) -> int:
+    return load().vpipg_mix_seed(seed, salt)
+
+
+def regular_polygon(n: int, r: float = 1.0, center=(0.0, 0.0)):
+    vx, vy = np.zeros(n), np.zeros(n)
+    check(load().vpipg_regular_polygon(n, r, center[0], center[1], _dptr(vx), _dptr(vy)))
+    return vx, vy
+
+
+def random_convex_polygon(n: int, seed: int, r: float = 1.0, center=(0.0, 0.0)):
+    vx, vy = np.zeros(n), np.zeros(n)
+    check(load().vpipg_random_convex_polygon(n, seed, r, center[0], center[1], _dptr(vx),
+                                             _dptr(vy)))
+    return vx, vy
+
+
+def sample_points(count: int, box, seed: int):
+    xs, ys = np.zeros(count), np.zeros(count)
+    check(load().vpipg_sample_points(count, *map(float, box), seed, _dptr(xs), _dptr(ys)))
+    return xs, ys

@@ -1,0 +1,96 @@
+"""CPU checks of the drop-in boundary: the C-ABI library loads, exports every
+symbol include/vpipg.h declares, carries sm_100a code, fails loudly without a
+B200, and its host-side samplers reproduce the reference bit for bit."""
+import re
+import subprocess
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+import paper_2007_15385_b200 as vp
+from paper_2007_15385_b200 import _lib
+
+ROOT = Path(__file__).resolve().parents[1]
+HEADER = ROOT / "include" / "vpipg.h"
+
+
+def header_symbols():
+    text = HEADER.read_text()
+    return sorted(set(re.findall(r"^[A-Za-z_][\w \*]*?\b(vpipg_\w+)\s*\(", text, re.M)))
+
+
+def test_header_symbols_all_exported():
+    lib = _lib.load()
+    names = header_symbols()
+    assert len(names) >= 15
+    for name in names:
+        assert hasattr(lib, name), name
+    assert sorted(_lib.SIGNATURES) == names
+
+
+def test_exported_dynamic_symbols_match_header():
+    out = subprocess.run(["nm", "-D", "--defined-only", str(_lib.LIB_PATH)], capture_output=True,
+                         text=True, check=True).stdout
+    exported = sorted(set(re.findall(r"\bT (vpipg_\w+)", out)))
+    assert exported == header_symbols()
+
+
+def test_library_contains_sm100a_cubin():
+    out = subprocess.run(["cuobjdump", "--list-elf", str(_lib.LIB_PATH)], capture_output=True,
+                         text=True, check=True).stdout
+    assert "sm_100a" in out
+
+
+def test_kernels_use_fma_and_3way_minmax():
+    """The slab kernel's inner loop is FFMA + FMNMX3 (two edges per FMNMX3)."""
+    sass = subprocess.run(["cuobjdump", "-sass", str(_lib.LIB_PATH)], capture_output=True,
+                          text=True, check=True).stdout
+    body = sass.split("slab_kernel")[1].split("Function :")[0]
+    assert "FMNMX3" in body and "FFMA" in body
+
+
+def test_strerror_and_version():
+    lib = _lib.load()
+    assert lib.vpipg_abi_version() == 1
+    assert lib.vpipg_strerror(0) == b"ok"
+    assert lib.vpipg_strerror(2) == b"not convex"
+    assert lib.vpipg_strerror(5) == b"generator collision"
+    assert b"sm_100" in lib.vpipg_strerror(300)
+
+
+def test_no_gpu_fails_loudly():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is present")
+    with pytest.raises(vp.VpipError) as e:
+        vp.PreparedPolygon.prepare([0, 1, 1, 0], [0, 0, 1, 1])
+    assert e.value.code >= 100  # CUDA error, never a silent CPU path
+
+
+def test_invalid_arguments_rejected_before_device():
+    lib = _lib.load()
+    import ctypes as C
+    h = C.c_void_p()
+    assert lib.vpipg_prepare(None, None, 3, 0, 0, None, C.byref(h)) == 6  # kinds == 0
+    assert lib.vpipg_prepare(None, None, 3, 8, 0, None, C.byref(h)) == 6  # unknown kind
+    assert lib.vpipg_test(None, 0, 1, None, None, 0, None, None, None, None) == 6
+
+
+def test_host_samplers_match_reference(golden):
+    for (s, t), want in zip(golden["mix_seed_in"], golden["mix_seed_out"]):
+        assert vp.mix_seed(int(s), int(t)) == int(want)
+    xs, ys = vp.sample_points(1000, (-1, -1, 2, 2), 4242)
+    assert np.array_equal(xs, golden["sample_xs"]) and np.array_equal(ys, golden["sample_ys"])
+    for n in range(3, 17):
+        assert np.array_equal(np.stack(vp.regular_polygon(n)), golden[f"regular_{n}"])
+    for i, (n, s) in enumerate(golden["rcp_params"]):
+        assert np.array_equal(np.stack(vp.random_convex_polygon(int(n), int(s))), golden[f"rcp_{i}"])
+
+
+def test_sampler_errors():
+    with pytest.raises(vp.VpipError) as e:
+        vp.regular_polygon(2)
+    assert e.value.code == 6
+    with pytest.raises(vp.VpipError):
+        vp.sample_points(4, (0, 0, 0, 1), 1)

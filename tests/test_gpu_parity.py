@@ -1,0 +1,264 @@
+"""GPU parity: the sm_100a kernels (through the C-ABI) against the oracle.
+
+* f64 engines repeat the reference arithmetic -> bit-exact masks and counts on
+  every input, boundary points included (tolerance: none).
+* f32 engines -> identical to the reference on the same f32-rounded inputs for
+  every point farther than EPS32 * max(1, |x|, |y|, polygon extent) from every
+  edge supporting line; disagreements inside that band are counted and
+  reported (north star: 1e-5 relative for fp32).
+"""
+import hashlib
+
+import numpy as np
+import pytest
+
+from conftest import case_names, unpack
+import workloads as W
+
+torch = pytest.importorskip("torch")
+import paper_2007_15385_b200 as vp  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+EPS32 = 1e-5
+DEV = "cuda:0"
+
+
+def run_device(poly, engine, xs, ys, words=True, bytes_=True):
+    xs_t = torch.as_tensor(np.ascontiguousarray(xs)).to(DEV)
+    ys_t = torch.as_tensor(np.ascontiguousarray(ys)).to(DEV)
+    m = xs_t.numel()
+    w = torch.zeros((m + 31) // 32, dtype=torch.int32, device=DEV) if words else None
+    b = torch.zeros(m, dtype=torch.uint8, device=DEV) if bytes_ else None
+    c = torch.zeros(1, dtype=torch.int64, device=DEV)
+    poly.test(engine, xs_t, ys_t, words=w, bytes_=b, count=c)
+    torch.cuda.synchronize()
+    wn = w.cpu().numpy().view(np.uint32) if words else None
+    bn = b.cpu().numpy() if bytes_ else None
+    return wn, bn, int(c.item())
+
+
+def words_to_mask(words, m):
+    return np.unpackbits(words.view(np.uint8), bitorder="little")[:m]
+
+
+def band_mask(orc, vx, vy, xs, ys):
+    ext = max(np.ptp(vx), np.ptp(vy))
+    s = np.maximum(np.maximum(1.0, np.abs(xs)), np.maximum(np.abs(ys), ext))
+    return orc.edge_line_distances(np.asarray(vx, float), np.asarray(vy, float), xs, ys) <= EPS32 * s
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    assert torch.cuda.is_available(), "GPU tests need a B200"
+    assert torch.cuda.get_device_capability(0) == (10, 0)
+
+
+def test_generators_bit_exact(golden):
+    for name in golden["conv_names"]:
+        vx, vy = golden[f"conv_{name}_v"]
+        with vp.PreparedPolygon.prepare(vx, vy, vp.KIND_VORONOI) as p:
+            inner, outer = p.generators()
+        assert np.array_equal(inner, golden[f"conv_{name}_inner"]), name
+        assert np.array_equal(outer, golden[f"conv_{name}_outer"]), name
+
+
+@pytest.mark.parametrize("name", ["too_few", "nonfinite", "degenerate", "collinear", "reflex",
+                                  "pentagram", "clockwise_square"])
+def test_validation_error_codes(golden, name):
+    vx, vy = golden[f"val_{name}_in"]
+    code = int(golden[f"val_{name}_code"])
+    if code:
+        with pytest.raises(vp.VpipError) as e:
+            vp.PreparedPolygon.prepare(vx, vy, vp.KIND_VORONOI | vp.KIND_OFFSET)
+        assert e.value.code == code
+    else:
+        with vp.PreparedPolygon.prepare(vx, vy, vp.KIND_ALL) as p:
+            ox, oy = p.vertices()
+            assert p.info()[2] == bool(golden[f"val_{name}_rev"])
+        assert np.array_equal(np.array([ox, oy]), golden[f"val_{name}_out"])
+
+
+def test_f64_engines_bit_exact_on_all_golden_cases(golden):
+    for name in case_names(golden):
+        pre = f"case_{name}_"
+        vx, vy = golden[pre + "v"]
+        xs, ys = golden[pre + "pts"].astype(np.float64)
+        want = [unpack(b, xs.size) for b in golden[pre + "masks"]]
+        with vp.PreparedPolygon.prepare(vx, vy, vp.KIND_ALL) as p:
+            for e in range(3):
+                w, b, c = run_device(p, e, xs, ys)
+                assert np.array_equal(b, want[e]), (name, e, np.flatnonzero(b != want[e])[:10])
+                assert np.array_equal(words_to_mask(w, xs.size), want[e]), (name, e)
+                assert c == int(want[e].sum())
+
+
+def test_f32_engines_match_outside_band(golden, orc):
+    total = {0: 0, 1: 0, 2: 0}
+    for name in case_names(golden):
+        pre = f"case_{name}_"
+        vx, vy = golden[pre + "v"]
+        xs64, ys64 = golden[pre + "pts"].astype(np.float64)
+        xs, ys = xs64.astype(np.float32), ys64.astype(np.float32)
+        if not bool(golden[pre + "f32"]):  # compare against the oracle on the rounded points
+            want = orc.masks(vx, vy, xs.astype(np.float64), ys.astype(np.float64))
+        else:
+            want = [unpack(b, xs.size) for b in golden[pre + "masks"]]
+        band = band_mask(orc, vx, vy, xs.astype(np.float64), ys.astype(np.float64))
+        with vp.PreparedPolygon.prepare(vx, vy, vp.KIND_ALL) as p:
+            for e in range(3):
+                w, b, c = run_device(p, e, xs, ys)
+                assert np.array_equal(words_to_mask(w, xs.size), b)
+                assert c == int(b.sum())
+                diff = b != want[e]
+                assert not np.any(diff & ~band), (name, e, np.flatnonzero(diff & ~band)[:10])
+                total[e] += int(diff.sum())
+                assert abs(c - int(want[e].sum())) <= int(diff.sum())
+    print("f32 band disagreements per engine:", total)
+
+
+def test_unit_square_known_answers():
+    # test_engines.cpp:49-71, :92-106, :128-137
+    with vp.PreparedPolygon.prepare([0, 1, 1, 0], [0, 0, 1, 1], vp.KIND_ALL) as p:
+        pts = np.array([[0.5, 0.5], [2, 2], [1, 0.5], [2, 0.5]])
+        for e in range(3):
+            _, b, _ = run_device(p, e, pts[:, 0].copy(), pts[:, 1].copy())
+            assert b.tolist() == [1, 0, 1, 0]
+            # vertices and edge midpoints are inside under all engines (f64 exact)
+            bx = np.array([0, 0.5, 1, 1, 1, 0.5, 0, 0.0])
+            by = np.array([0, 0, 0, 0.5, 1, 1, 1, 0.5])
+            _, b, c = run_device(p, e, bx, by)
+            assert b.tolist() == [1] * 8 and c == 8
+
+
+def test_concave_arrow_crossing(golden):
+    vx, vy = golden["arrow_v"]
+    xs, ys = golden["arrow_pts"]
+    with vp.PreparedPolygon.prepare(vx, vy, vp.KIND_CROSSING) as p:
+        _, b, _ = run_device(p, 2, xs.copy(), ys.copy())
+    assert b.tolist() == golden["arrow_inside"].tolist()
+    with pytest.raises(vp.VpipError) as e:  # not convex: voronoi / offset refuse it
+        vp.PreparedPolygon.prepare(vx, vy, vp.KIND_VORONOI)
+    assert e.value.code == 2
+
+
+@pytest.mark.parametrize("m", [0, 1, 31, 32, 33, 255, 256, 257, 1000, 2049, 4097])
+def test_ragged_sizes(orc, m):
+    vx, vy = W.c1_polygon()
+    xs, ys = orc.sample_points(max(m, 1), W.C1_BOX, 77 + m)
+    xs, ys = xs[:m], ys[:m]
+    want = orc.masks(vx, vy, xs, ys) if m else [np.zeros(0, np.uint8)] * 3
+    with vp.PreparedPolygon.prepare(vx, vy, vp.KIND_ALL) as p:
+        for e in range(3):
+            w, b, c = run_device(p, e, xs, ys)
+            assert np.array_equal(b, want[e]) and c == int(want[e].sum())
+            assert w.size == (m + 31) // 32
+            assert np.array_equal(words_to_mask(w, m), want[e])
+            w32, b32, c32 = run_device(p, e, xs.astype(np.float32), ys.astype(np.float32))
+            assert np.array_equal(words_to_mask(w32, m), b32) and c32 == int(b32.sum())
+
+
+def test_c1_full_f64_sha256(golden):
+    vx, vy = W.c1_polygon()
+    xs, ys = W.c1_points(vp.sample_points)
+    with vp.PreparedPolygon.prepare(vx, vy, vp.KIND_ALL) as p:
+        for e in range(3):
+            w, _, c = run_device(p, e, xs, ys, bytes_=False)
+            digest = hashlib.sha256(w.tobytes()[: (xs.size + 7) // 8]).hexdigest()
+            assert digest == str(golden["c1_full_sha256"][e]), e
+            assert c == int(golden["c1_full_counts"][e])
+
+
+def test_device_point_stream_matches_oracle(orc):
+    m, first = 100_003, 123_456_789
+    xs = torch.empty(m, dtype=torch.float32, device=DEV)
+    ys = torch.empty(m, dtype=torch.float32, device=DEV)
+    vp.fill_uniform_points(W.c5_point_seed(), first, xs, ys, W.C5_BOX)
+    ex, ey = orc.counter_points_f32(W.c5_point_seed(), first, m, W.C5_BOX)
+    assert np.array_equal(xs.cpu().numpy(), ex) and np.array_equal(ys.cpu().numpy(), ey)
+
+
+def test_large_batch_properties_and_shard_independence(orc):
+    """2^26 f32 points (C5 polygon): masks do not depend on the partitioning
+    (test_engines.cpp:227-241), popcount(words) == fused count, the three
+    engines agree up to band points, and a sampled subset matches the oracle."""
+    vx, vy = W.c5_polygon(vp.random_convex_polygon)
+    m = 1 << 26
+    xs = torch.empty(m, dtype=torch.float32, device=DEV)
+    ys = torch.empty(m, dtype=torch.float32, device=DEV)
+    vp.fill_uniform_points(W.c5_point_seed(), 0, xs, ys, W.C5_BOX)
+    counts = []
+    with vp.PreparedPolygon.prepare(vx, vy, vp.KIND_ALL) as p:
+        full = []
+        for e in range(3):
+            w = torch.zeros(m // 32, dtype=torch.int32, device=DEV)
+            c = torch.zeros(1, dtype=torch.int64, device=DEV)
+            p.test(e, xs, ys, words=w, count=c)
+            # the same batch as 4 uneven 32-aligned shards
+            ws = torch.zeros_like(w)
+            cs = torch.zeros(1, dtype=torch.int64, device=DEV)
+            cuts = [0, 32 * 1001, 32 * 777777, m - 32 * 5, m]
+            for lo, hi in zip(cuts[:-1], cuts[1:]):
+                p.test(e, xs[lo:hi], ys[lo:hi], words=ws[lo // 32: hi // 32], count=cs)
+            torch.cuda.synchronize()
+            assert torch.equal(w, ws) and c.item() == cs.item()
+            pop = int(np.unpackbits(w.cpu().numpy().view(np.uint8)).sum())
+            assert pop == c.item()
+            counts.append(c.item())
+            full.append(w.cpu().numpy().view(np.uint32))
+    # three engines: differences only in band (checked exactly on a sample below)
+    assert max(counts) - min(counts) <= m * 1e-5
+    idx = np.sort(np.random.default_rng(5).choice(m, 200_000, replace=False))
+    sx, sy = xs.cpu().numpy()[idx].astype(np.float64), ys.cpu().numpy()[idx].astype(np.float64)
+    want = orc.masks(vx.astype(np.float32).astype(np.float64),
+                     vy.astype(np.float32).astype(np.float64), sx, sy)
+    band = band_mask(orc, vx, vy, sx, sy)
+    for e in range(3):
+        got = words_to_mask(full[e], m)[idx]
+        assert not np.any((got != want[e]) & ~band), e
+
+
+def test_host_buffer_path_equals_device_path(orc):
+    vx, vy = W.c1_polygon()
+    xs, ys = orc.sample_points(5_000_001, W.C1_BOX, 99)
+    with vp.PreparedPolygon.prepare(vx, vy, vp.KIND_ALL) as p:
+        for e in range(3):
+            wd, bd, cd = run_device(p, e, xs, ys)
+            wh, bh, ch = p.test_host(e, xs, ys, words=True, bytes_=True)
+            assert np.array_equal(wd, wh) and np.array_equal(bd, bh) and cd == ch
+            wh32, _, ch32 = p.test_host(e, xs.astype(np.float32), ys.astype(np.float32))
+            wd32, _, cd32 = run_device(p, e, xs.astype(np.float32), ys.astype(np.float32),
+                                       bytes_=False)
+            assert np.array_equal(wd32, wh32) and cd32 == ch32
+
+
+def test_concurrent_streams_share_one_handle(orc):
+    # test_engines.cpp:243-257: one generator set serves concurrent callers
+    vx, vy = W.c1_polygon()
+    xs, ys = orc.sample_points(1 << 20, W.C1_BOX, 5)
+    xt = torch.as_tensor(xs.astype(np.float32), device=DEV)
+    yt = torch.as_tensor(ys.astype(np.float32), device=DEV)
+    with vp.PreparedPolygon.prepare(vx, vy, vp.KIND_ALL) as p:
+        ref = torch.zeros(xs.size // 32, dtype=torch.int32, device=DEV)
+        p.test(0, xt, yt, words=ref)
+        outs = [torch.zeros_like(ref) for _ in range(4)]
+        streams = [torch.cuda.Stream() for _ in range(4)]
+        torch.cuda.synchronize()
+        for s, o in zip(streams, outs):
+            p.test(0, xt, yt, words=o, stream=s)
+        torch.cuda.synchronize()
+        for o in outs:
+            assert torch.equal(o, ref)
+
+
+def test_generator_set_handle(golden):
+    # voronoi_contains_batch(GeneratorSet, ...): handle from explicit generators
+    name = "c1_sample"
+    vx, vy = golden[f"case_{name}_v"]
+    xs, ys = golden[f"case_{name}_pts"].astype(np.float64)
+    want = unpack(golden[f"case_{name}_masks"][0], xs.size)
+    inner, outer = golden["conv_c1_inner"], golden["conv_c1_outer"]
+    with vp.PreparedPolygon.from_generators(inner, outer) as p:
+        _, b, _ = run_device(p, 0, xs, ys)
+        assert np.array_equal(b, want)
+        with pytest.raises(vp.VpipError):  # offset tables were not prepared
+            run_device(p, 1, xs, ys)
