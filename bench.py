@@ -1,0 +1,432 @@
+#!/usr/bin/env python3
+"""Benchmark of the B200 point-inclusion engine (the BASELINE.json metric).
+
+Headline workload (BASELINE.json configs[4], the config the metric "at
+1/2/4/8 B200" is quoted on; it fits one GPU): one random convex 32-gon
+(vpip::random_convex_polygon(32, seed, 1.0)), 2^31 float32 points uniform in
+[-1.5, 1.5]^2 from the counter-based stream, sharded evenly (1024-aligned,
+contiguous) over the ranks. One step = all three engines (Voronoi,
+sign-of-offset, ray-crossing) over every point + one NCCL all-reduce of the
+three inside counts. value = 3 * 2^31 point-polygon tests per step / step
+time (max over ranks, CUDA events). Inputs (17 GB at N=1) are far larger than
+L2, so no flush is needed between steps.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+                    [--workload c5|c2|c3:<n>|c1]
+
+`--impl reference` times the reference's own CPU implementation
+(oracle/_ref/libvpip_ref.so, the unmodified reference sources; the oracle port
+when that library is absent) on a bounded sample of the same workload with all
+host threads, on rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+import workloads as W  # noqa: E402
+
+METRIC = "point-polygon tests/sec"
+UNIT = "tests/s"
+PEAKS_FILE = ROOT / "MEASURED_PEAKS.json"
+PIPE_PEAKS_FILE = ROOT / "profiles" / "pipe_peaks_r01.json"
+HBM_FALLBACK_GBS = 6650.0
+# FFMA lane-ops per SM per clock on sm_100a (tools/pipe_peaks.cu: 3.79 warp-inst/clk/SM)
+FFMA_PER_SM_CLK = 128
+CPU_SAMPLE = 1 << 25
+
+
+# ----------------------------------------------------------------- helpers
+def env_int(name, default):
+    v = os.environ.get(name)
+    return int(v) if v is not None else default
+
+
+def load_peaks():
+    hbm, src = HBM_FALLBACK_GBS, "fallback (B200_PROFILING.md)"
+    try:
+        j = json.loads(PEAKS_FILE.read_text())
+        hbm, src = float(j["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs (measured copy)"
+    except Exception:
+        pass
+    fma = None
+    try:
+        for line in PIPE_PEAKS_FILE.read_text().splitlines():
+            r = json.loads(line)
+            if r.get("op") == "ffma_reg":
+                fma = float(r["lane_ops_per_s"])
+    except Exception:
+        pass
+    return hbm, src, fma
+
+
+class ClockSampler:
+    """nvidia-smi sampled during the timed region (B200_PROFILING.md clocks line)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpus: str):
+        self.rows = []
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "-i", gpus,
+                                       "--format=csv,noheader,nounits", "-lms", "50"],
+                                      stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.p = None
+            return
+        self.t = threading.Thread(target=self._read, daemon=True)
+        self.t.start()
+
+    def _read(self):
+        for line in self.p.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) == 8:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        try:
+            self.p.wait(timeout=5)
+        except Exception:
+            self.p.kill()
+        self.t.join(timeout=2)
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons, mhz, mx, pw = set(), [], [], []
+        for r in self.rows:
+            try:
+                mhz.append(float(r[1]))
+                mx.append(float(r[2]))
+                pw.append(float(r[3]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, r[4:]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(mhz) if mhz else None,
+                "sm_max_mhz": max(mx) if mx else None,
+                "power_w_max": max(pw) if pw else None,
+                "samples": len(mhz), "reasons": sorted(reasons)}
+
+
+# ----------------------------------------------------------------- workloads
+def build_workload(name: str, lo: int, hi: int, torch, vp, stream):
+    """Polygon vertices (f64) + this rank's device-resident f32 points."""
+    dev = torch.device("cuda", torch.cuda.current_device())
+    if name == "c5":
+        vx, vy = W.c5_polygon(vp.random_convex_polygon)
+        m = hi - lo
+        xs = torch.empty(m, dtype=torch.float32, device=dev)
+        ys = torch.empty(m, dtype=torch.float32, device=dev)
+        vp.fill_uniform_points(W.c5_point_seed(), lo, xs, ys, W.C5_BOX, stream=stream)
+    elif name.startswith("c3"):
+        n = int(name.split(":")[1]) if ":" in name else 8
+        vx, vy = W.c3_polygon(n)
+        m = hi - lo
+        xs = torch.empty(m, dtype=torch.float32, device=dev)
+        ys = torch.empty(m, dtype=torch.float32, device=dev)
+        vp.fill_uniform_points(int(W.mix_seed_np(W.config_seed(3), 200 + n)), lo, xs, ys,
+                               W.C3_BOX, stream=stream)
+    elif name == "c2":
+        vx, vy = W.c2_polygon()
+        px, py = W.c2_points()
+        xs = torch.as_tensor(px[lo:hi], device=dev)
+        ys = torch.as_tensor(py[lo:hi], device=dev)
+    elif name == "c1":
+        vx, vy = W.c1_polygon()
+        px, py = W.c1_points(vp.sample_points)
+        xs = torch.as_tensor(px[lo:hi], device=dev)
+        ys = torch.as_tensor(py[lo:hi], device=dev)
+    else:
+        raise SystemExit(f"unknown workload {name}")
+    return vx, vy, xs, ys
+
+
+def workload_size(name: str) -> int:
+    return {"c5": W.C5_POINTS, "c2": W.C2_CLUSTERS * W.C2_PER_CLUSTER, "c1": W.C1_POINTS}.get(
+        name.split(":")[0], W.C3_POINTS)
+
+
+def workload_desc(name: str) -> str:
+    return {"c5": "C5 multi-GPU scaling: random convex 32-gon, 2^31 f32 points U[-1.5,1.5]^2, "
+                  "3 engines + NCCL all-reduce of inside counts",
+            "c2": "C2 vehicle footprint 12-gon, 2^24 f32 lidar-like clustered points",
+            "c1": "C1 random 8-angle hull, 2^20 points (f32 copy of the f64 oracle config)"}.get(
+        name.split(":")[0], f"C3 n-sweep regular {name} jittered hull, 2^28 f32 points")
+
+
+# ----------------------------------------------------------------- CPU reference
+def cpu_reference_sample(name: str, sample: int):
+    """Polygon (f64) + a bounded f64 sample (widened f32) of the workload's points."""
+    import oracle
+    orc = oracle.Oracle()
+    if name == "c5":
+        vx, vy = W.c5_polygon(orc.random_convex_polygon)
+        xs, ys = orc.counter_points_f32(W.c5_point_seed(), 0, sample, W.C5_BOX)
+    elif name.startswith("c3"):
+        n = int(name.split(":")[1]) if ":" in name else 8
+        vx, vy = W.c3_polygon(n)
+        xs, ys = orc.counter_points_f32(int(W.mix_seed_np(W.config_seed(3), 200 + n)), 0, sample,
+                                        W.C3_BOX)
+    elif name == "c2":
+        vx, vy = W.c2_polygon()
+        xs, ys = W.c2_points()
+        xs, ys = xs[:sample], ys[:sample]
+    else:
+        vx, vy = W.c1_polygon()
+        xs, ys = W.c1_points(orc.sample_points, min(sample, W.C1_POINTS))
+    return vx, vy, np.asarray(xs, np.float64), np.asarray(ys, np.float64)
+
+
+def time_cpu_reference(name: str, sample: int, reps: int, warmup: int):
+    """Times the three reference engines on the sample; returns (tests/s, kind, cores, s/rep)."""
+    import oracle
+    vx, vy, xs, ys = cpu_reference_sample(name, sample)
+    cores = os.cpu_count() or 1
+    try:
+        ref = oracle.Reference()
+        kind = "reference"
+    except FileNotFoundError:
+        ref, kind, cores = None, "port", 1
+    per_rep = []
+    for r in range(warmup + reps):
+        if ref is not None:
+            _, ns = ref.masks(vx, vy, xs, ys, threads=cores)
+            t = sum(ns) * 1e-9
+        else:
+            orc = oracle.Oracle()
+            t0 = time.perf_counter()
+            orc.masks(vx, vy, xs, ys)
+            t = time.perf_counter() - t0
+        if r >= warmup:
+            per_rep.append(t)
+    t = statistics.median(per_rep)
+    return 3 * xs.size / t, kind, cores, t
+
+
+def run_reference_arm(args, rank: int, world: int):
+    if rank != 0:
+        return
+    steps, warmup = args.steps, args.warmup
+    value, kind, cores, t = time_cpu_reference(args.workload, args.cpu_sample, steps, warmup)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": steps, "warmup": warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": config_block(args, world),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind,
+                         "sample": f"first {args.cpu_sample} points of the workload stream "
+                                   "(f32 rounded, widened to f64), 3 engines per step, "
+                                   "*_contains_batch(threads=cores) timed like bench.cpp:196-199"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def config_block(args, world):
+    return {"workload": workload_desc(args.workload), "points": workload_size(args.workload),
+            "engines": ["voronoi", "sign_of_offset", "ray_crossing"],
+            "parallelism": f"point shards x{world}",
+            "l2": ("inputs larger than L2" if workload_size(args.workload) * 8 > 4 * 126e6
+                   else "L2 flushed between steps (256 MB write)")}
+
+
+# ----------------------------------------------------------------- GPU arm
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--workload", default="c5")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--cpu-sample", type=int, default=CPU_SAMPLE)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--points", type=int, default=0, help="override the workload size (profiling)")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    rank, world = env_int("RANK", 0), env_int("WORLD_SIZE", 1)
+    local = env_int("LOCAL_RANK", 0)
+    if args.impl == "reference":
+        return run_reference_arm(args, rank, world)
+
+    import torch
+    import torch.distributed as dist
+    import paper_2007_15385_b200 as vp
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    stream = torch.cuda.Stream()
+    M = args.points or workload_size(args.workload)
+    lo, hi = W.shard(M, rank, world)
+    m = hi - lo
+    with torch.cuda.stream(stream):
+        vx, vy, xs, ys = build_workload(args.workload, lo, hi, torch, vp, stream)
+        poly = vp.PreparedPolygon.prepare(vx, vy, vp.KIND_ALL, device=local, stream=stream)
+        words = [torch.zeros((m + 31) // 32, dtype=torch.int32, device="cuda") for _ in range(3)]
+        counts = torch.zeros(3, dtype=torch.int64, device="cuda")
+        flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda") if M * 8 <= 4 * 126e6 else None
+    stream.synchronize()
+    n_edges = poly.n
+
+    kevents = []  # per step, per engine: (start, end) on the launch stream
+
+    def step(record: bool):
+        if flush is not None:
+            flush.fill_(1)
+        counts.zero_()
+        pairs = []
+        for e in range(3):
+            if record:
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+            poly.test(e, xs, ys, words=words[e], count=counts[e:e + 1], stream=stream)
+            if record:
+                b.record(stream)
+                pairs.append((a, b))
+        if world > 1:
+            dist.all_reduce(counts)
+        if record:
+            kevents.append(pairs)
+
+    with torch.cuda.stream(stream):
+        for _ in range(args.warmup):
+            step(False)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    gpus = os.environ.get("CUDA_VISIBLE_DEVICES", ",".join(str(i) for i in range(world)))
+    sampler = ClockSampler(gpus if rank == 0 else str(local)) if rank == 0 else None
+    time.sleep(0.2 if rank == 0 else 0)
+    t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    with torch.cuda.stream(stream):
+        t_start.record(stream)
+        for _ in range(args.steps):
+            step(True)
+        t_end.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = sampler.stop() if sampler else None
+    ms = t_start.elapsed_time(t_end)
+    ms_t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+    ms_max = float(ms_t.item())
+    per_kernel_ms = [statistics.mean(p[e][0].elapsed_time(p[e][1]) for p in kevents)
+                     for e in range(3)]
+    final_counts = counts.tolist()
+
+    # ---- end-to-end through the host-buffer C-ABI (pinned host memory) ----
+    e2e = None
+    if not args.no_e2e:
+        hx = torch.empty(m, dtype=torch.float32, pin_memory=True)
+        hy = torch.empty(m, dtype=torch.float32, pin_memory=True)
+        hx.copy_(xs)
+        hy.copy_(ys)
+        hw = [torch.empty((m + 31) // 32, dtype=torch.int32, pin_memory=True) for _ in range(3)]
+        torch.cuda.synchronize()
+        times = []
+        for r in range(1 + args.e2e_steps):
+            if world > 1:
+                dist.barrier()
+            t0 = time.perf_counter()
+            _, cnt = poly.test_host_multi(hx, hy, (0, 1, 2), words=hw)
+            if world > 1:
+                ct = torch.tensor(cnt, dtype=torch.int64, device="cuda")
+                dist.all_reduce(ct)
+                ct.cpu()
+            dt = time.perf_counter() - t0
+            if r > 0:
+                times.append(dt)
+        t_e2e = torch.tensor([statistics.mean(times)], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(t_e2e, op=dist.ReduceOp.MAX)
+        e2e = {"value": 3 * M / float(t_e2e.item()), "unit": UNIT,
+               "h2d_bytes_per_step": 2 * 4 * m, "d2h_bytes_per_step": 3 * 4 * ((m + 31) // 32),
+               "steps": args.e2e_steps,
+               "path": "vpipg_test_host_multi (C-ABI, pinned host buffers, 4 Mi-point chunks "
+                       "double-buffered over 2 streams, counts read back + NCCL all-reduce)"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        v, kind, cores, t = time_cpu_reference(args.workload, args.cpu_sample, reps=3, warmup=1)
+        cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": kind,
+               "sample": f"first {args.cpu_sample} points of the same stream (f32 widened to "
+                         f"f64), 3 engines, threads={cores}, median of 3 after 1 warm-up; "
+                         f"{t * 1e3:.1f} ms per 3-engine pass"}
+
+    if world > 1:
+        dist.barrier()
+    if rank != 0:
+        dist.destroy_process_group() if world > 1 else None
+        return
+
+    hbm_peak, hbm_src, fma_peak = load_peaks()
+    bytes_per_launch = m * 8 + 4 * ((m + 31) // 32)
+    pe = m * n_edges
+    kernels = []
+    for e, name in enumerate(("voronoi", "sign_of_offset", "ray_crossing")):
+        t = per_kernel_ms[e] * 1e-3
+        kernels.append({"engine": name, "ms": per_kernel_ms[e],
+                        "GB_per_s": bytes_per_launch / t / 1e9,
+                        "point_edge_per_s": pe / t,
+                        "tflops_alg": 4 * pe / t / 1e12})
+    dom = max(range(3), key=lambda e: per_kernel_ms[e])
+    dk = kernels[dom]
+    hbm_frac = dk["GB_per_s"] / hbm_peak
+    fma_tflops = 2 * fma_peak / 1e12 if fma_peak else 2 * FFMA_PER_SM_CLK * 148 * 1.965e9 / 1e12
+    fma_frac = dk["tflops_alg"] / fma_tflops
+    compute_bound = (4 * pe / (fma_tflops * 1e12)) > (bytes_per_launch / (hbm_peak * 1e9))
+    if compute_bound:
+        roof = {"bound": "fp32-fma", "achieved": dk["tflops_alg"], "peak": fma_tflops,
+                "unit": "TFLOP/s", "frac": fma_frac, "traffic": None}
+    else:
+        roof = {"bound": "hbm", "achieved": dk["GB_per_s"], "peak": hbm_peak, "unit": "GB/s",
+                "frac": hbm_frac, "traffic": None}
+    roof.update({"kernel": dk["engine"], "hbm_GB_per_s": dk["GB_per_s"], "hbm_frac": hbm_frac,
+                 "hbm_peak_source": hbm_src, "fma_frac": fma_frac,
+                 "fma_peak_source": "tools/pipe_peaks.cu FFMA lane-ops/s x2 (profiles/pipe_peaks_r01.json)",
+                 "per_unit": f"{bytes_per_launch / m:.3f} B and {4 * n_edges} flops per test "
+                             f"(n={n_edges} edges, 4 flops per point-edge)"})
+
+    step_s = ms_max * 1e-3 / args.steps
+    total_tests = 3 * M
+    line = {
+        "metric": METRIC, "value": total_tests / step_s, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_s * 1e3,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (seeded counter-based points, reference-sampler polygon)",
+        "config": config_block(args, world),
+        "gpu_launches": 3 * args.steps,
+        "roofline": roof, "kernels": kernels, "inside_counts": final_counts,
+        "clocks": clocks, "e2e": e2e, "cpu_baseline": cpu,
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

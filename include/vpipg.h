@@ -116,6 +116,14 @@ int vpipg_test_host(const vpipg_poly* poly, int engine, int dtype, const void* x
                     const void* ys, uint64_t m, uint32_t* mask_words, uint8_t* mask_bytes,
                     uint64_t* inside);
 
+/* Several engines over one host batch: the points cross PCIe once per chunk
+ * and each engine in the bit set `engines` (1 << VPIPG_ENGINE_*) tests them.
+ * mask_words / mask_bytes / inside are indexed by engine (arrays of 3; any
+ * entry, or the array itself, may be NULL). */
+int vpipg_test_host_multi(const vpipg_poly* poly, uint32_t engines, int dtype, const void* xs,
+                          const void* ys, uint64_t m, uint32_t* const* mask_words,
+                          uint8_t* const* mask_bytes, uint64_t* inside);
+
 /* Instrumented work counters of voronoi_contains_batch(..., BatchStats&)
  * (engines.cpp:256-273): the branch-free kernels perform exactly
  * (n+1)*m distance evaluations and n*m comparisons. */

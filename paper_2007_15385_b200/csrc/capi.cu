@@ -330,15 +330,21 @@ int vpipg_test(const vpipg_poly* p, int engine, int dtype, const void* xs, const
   return dispatch(p, engine, dtype, a, static_cast<cudaStream_t>(stream));
 }
 
-int vpipg_test_host(const vpipg_poly* p, int engine, int dtype, const void* xs, const void* ys,
-                    uint64_t m, uint32_t* mask_words, uint8_t* mask_bytes, uint64_t* inside) {
-  if (!p) return kInvalid;
-  if (inside) *inside = 0;
+int vpipg_test_host_multi(const vpipg_poly* p, uint32_t engines, int dtype, const void* xs,
+                          const void* ys, uint64_t m, uint32_t* const* mask_words,
+                          uint8_t* const* mask_bytes, uint64_t* inside) {
+  if (!p || engines == 0 || (engines & ~7u)) return kInvalid;
+  int eng[3], ne = 0;
+  for (int e = 0; e < 3; ++e) {
+    if (inside && (engines & (1u << e))) inside[e] = 0;
+    if (engines & (1u << e)) eng[ne++] = e;
+  }
   if (m == 0) return kOk;
   if (!xs || !ys) return kInvalid;
   DeviceGuard g(p->device);
   const size_t elt = dtype == VPIPG_F64 ? sizeof(double) : sizeof(float);
-  // chunks of 4 Mi points (32-aligned so word boundaries line up), two in flight
+  // chunks of 4 Mi points (32-aligned so mask words line up), two in flight:
+  // the points cross PCIe once and every requested engine tests them
   const uint64_t chunk = std::min<uint64_t>(m, uint64_t(1) << 22);
   const uint64_t chunk_words = (chunk + 31) / 32;
   cudaStream_t st[2];
@@ -346,8 +352,8 @@ int vpipg_test_host(const vpipg_poly* p, int engine, int dtype, const void* xs, 
   struct Slot {
     void* x = nullptr;
     void* y = nullptr;
-    uint32_t* w = nullptr;
-    uint8_t* b = nullptr;
+    uint32_t* w[3] = {nullptr, nullptr, nullptr};
+    uint8_t* b[3] = {nullptr, nullptr, nullptr};
     unsigned long long* c = nullptr;
   } slot[2];
   int rc = kOk;
@@ -358,10 +364,15 @@ int vpipg_test_host(const vpipg_poly* p, int engine, int dtype, const void* xs, 
   for (int i = 0; i < 2 && rc == kOk; ++i) {
     if (fail(cudaMallocAsync(&slot[i].x, chunk * elt, st[i]))) break;
     if (fail(cudaMallocAsync(&slot[i].y, chunk * elt, st[i]))) break;
-    if (mask_words && fail(cudaMallocAsync(reinterpret_cast<void**>(&slot[i].w), chunk_words * 4, st[i]))) break;
-    if (mask_bytes && fail(cudaMallocAsync(reinterpret_cast<void**>(&slot[i].b), chunk, st[i]))) break;
-    if (fail(cudaMallocAsync(reinterpret_cast<void**>(&slot[i].c), 8, st[i]))) break;
-    if (fail(cudaMemsetAsync(slot[i].c, 0, 8, st[i]))) break;
+    for (int k = 0; k < ne && rc == kOk; ++k) {
+      const int e = eng[k];
+      if (mask_words && mask_words[e])
+        fail(cudaMallocAsync(reinterpret_cast<void**>(&slot[i].w[e]), chunk_words * 4, st[i]));
+      if (mask_bytes && mask_bytes[e] && rc == kOk)
+        fail(cudaMallocAsync(reinterpret_cast<void**>(&slot[i].b[e]), chunk, st[i]));
+    }
+    if (rc == kOk && !fail(cudaMallocAsync(reinterpret_cast<void**>(&slot[i].c), 24, st[i])))
+      fail(cudaMemsetAsync(slot[i].c, 0, 24, st[i]));
   }
   const char* hx = static_cast<const char*>(xs);
   const char* hy = static_cast<const char*>(ys);
@@ -370,25 +381,46 @@ int vpipg_test_host(const vpipg_poly* p, int engine, int dtype, const void* xs, 
     const uint64_t len = std::min<uint64_t>(chunk, m - base);
     if (fail(cudaMemcpyAsync(slot[i].x, hx + base * elt, len * elt, cudaMemcpyHostToDevice, st[i]))) break;
     if (fail(cudaMemcpyAsync(slot[i].y, hy + base * elt, len * elt, cudaMemcpyHostToDevice, st[i]))) break;
-    TestArgs a{slot[i].x, slot[i].y, len, slot[i].w, slot[i].b, slot[i].c};
-    rc = dispatch(p, engine, dtype, a, st[i]);
-    if (rc) break;
-    if (mask_words && fail(cudaMemcpyAsync(mask_words + base / 32, slot[i].w, ((len + 31) / 32) * 4,
-                                           cudaMemcpyDeviceToHost, st[i]))) break;
-    if (mask_bytes && fail(cudaMemcpyAsync(mask_bytes + base, slot[i].b, len, cudaMemcpyDeviceToHost, st[i]))) break;
+    for (int k = 0; k < ne && rc == kOk; ++k) {
+      const int e = eng[k];
+      TestArgs a{slot[i].x, slot[i].y, len, slot[i].w[e], slot[i].b[e], slot[i].c + e};
+      rc = dispatch(p, e, dtype, a, st[i]);
+      if (rc) break;
+      if (slot[i].w[e] && fail(cudaMemcpyAsync(mask_words[e] + base / 32, slot[i].w[e],
+                                               ((len + 31) / 32) * 4, cudaMemcpyDeviceToHost, st[i])))
+        break;
+      if (slot[i].b[e] && fail(cudaMemcpyAsync(mask_bytes[e] + base, slot[i].b[e], len,
+                                               cudaMemcpyDeviceToHost, st[i])))
+        break;
+    }
   }
-  unsigned long long cnt[2] = {0, 0};
+  unsigned long long cnt[2][3] = {{0, 0, 0}, {0, 0, 0}};
   for (int i = 0; i < 2; ++i) {
-    if (rc == kOk && slot[i].c) fail(cudaMemcpyAsync(&cnt[i], slot[i].c, 8, cudaMemcpyDeviceToHost, st[i]));
-    for (void* ptr : {slot[i].x, slot[i].y, static_cast<void*>(slot[i].w), static_cast<void*>(slot[i].b),
-                      static_cast<void*>(slot[i].c)})
+    if (rc == kOk && slot[i].c) fail(cudaMemcpyAsync(cnt[i], slot[i].c, 24, cudaMemcpyDeviceToHost, st[i]));
+    void* ptrs[] = {slot[i].x, slot[i].y, slot[i].w[0], slot[i].w[1], slot[i].w[2],
+                    slot[i].b[0], slot[i].b[1], slot[i].b[2], slot[i].c};
+    for (void* ptr : ptrs)
       if (ptr) cudaFreeAsync(ptr, st[i]);
   }
   for (auto& s : st) {
     fail(cudaStreamSynchronize(s));
     cudaStreamDestroy(s);
   }
-  if (rc == kOk && inside) *inside = cnt[0] + cnt[1];
+  if (rc == kOk && inside)
+    for (int k = 0; k < ne; ++k) inside[eng[k]] = cnt[0][eng[k]] + cnt[1][eng[k]];
+  return rc;
+}
+
+int vpipg_test_host(const vpipg_poly* p, int engine, int dtype, const void* xs, const void* ys,
+                    uint64_t m, uint32_t* mask_words, uint8_t* mask_bytes, uint64_t* inside) {
+  if (engine < 0 || engine > 2) return kInvalid;
+  uint32_t* w[3] = {nullptr, nullptr, nullptr};
+  uint8_t* b[3] = {nullptr, nullptr, nullptr};
+  uint64_t cnt[3] = {0, 0, 0};
+  w[engine] = mask_words;
+  b[engine] = mask_bytes;
+  const int rc = vpipg_test_host_multi(p, 1u << engine, dtype, xs, ys, m, w, b, cnt);
+  if (inside) *inside = rc == kOk ? cnt[engine] : 0;
   return rc;
 }
 

@@ -1,21 +1,25 @@
 // test_f32.cu -- fp32 batched point-inclusion kernels for sm_100a.
 //
 // Replaces the reference's batch kernels for float32 point streams:
-//   voronoi_kernel   (engines.cpp:65-104)  -> slab kernel, Voronoi table
-//   offset_kernel    (engines.cpp:136-160) -> slab kernel, offset table
-//   ray_kernel       (engines.cpp:165-204) -> crossing kernel
+//   voronoi_kernel   (engines.cpp:65-104)  -> SlabEngine, Voronoi table
+//   offset_kernel    (engines.cpp:136-160) -> SlabEngine, offset table
+//   ray_kernel       (engines.cpp:165-204) -> CrossEngine
 //   count_inside     (engines.cpp:215-217) -> fused popc + one atomic per warp
 //
-// Work decomposition: a warp owns "warp tiles" of 32*P consecutive points;
-// lane l handles points base + 32*p + l (p < P), so the ballot of sub-tile p
-// is exactly mask word (base/32 + p) in the PIPM bit order (io.cpp:272-279)
-// and every global load / store is a fully coalesced 128-byte line per warp.
-// The polygon's coefficient table is staged once per CTA in shared memory and
-// read with warp-uniform (broadcast) 16-byte loads; every point-edge costs one
-// FFMA plus half an FMNMX3 (slab) -- no per-point data-dependent branches,
-// like the reference's branch-free kernels.
+// Streaming structure (stream_kernel): a persistent grid of CTAs, each with one
+// producer warp and kConsumers consumer warps. The producer's elected lane
+// moves 2048-point tiles of xs and ys into a kStages-deep shared-memory ring
+// with cp.async.bulk (TMA, evict-first) and arms a "full" mbarrier per stage;
+// consumer warps copy their 256-point slice into registers, release the stage
+// on its "empty" mbarrier and evaluate while the next tiles are in flight.
+// Lane l of a consumer warp owns points 32*p + l (p < P) of its slice, so the
+// ballot of sub-tile p is exactly one PIPM mask word (io.cpp:272-279, bit j =
+// point j) and word stores are coalesced. The polygon table is staged once per
+// CTA in shared memory and read with warp-uniform 16-byte broadcasts.
+// generic_kernel handles unaligned inputs with guarded direct loads.
 #include <cstdint>
 
+#include "tma_pipe.cuh"
 #include "vpipg_device.cuh"
 #include "vpipg_internal.h"
 
@@ -23,8 +27,12 @@ namespace vpipg {
 
 namespace {
 
-constexpr int kThreads = 256;
-constexpr int kWarps = kThreads / 32;
+constexpr int P = 8;                          // points per lane per tile
+constexpr int kConsumers = 8;                 // consumer warps per CTA
+constexpr int kThreads = (kConsumers + 1) * 32;
+constexpr int kWarpPts = 32 * P;              // 256 points per warp slice
+constexpr int kTile = kConsumers * kWarpPts;  // 2048 points per stage
+constexpr int kStages = 4;
 
 __device__ __forceinline__ float fmax3(float a, float b, float c) {
   float r;
@@ -37,14 +45,141 @@ __device__ __forceinline__ float fmin3(float a, float b, float c) {
   return r;
 }
 
-// Streaming loads: every point is read exactly once.
-__device__ __forceinline__ float ld_stream(const float* p) { return __ldcs(p); }
+// ---------------------------------------------------------------------------
+// Slab engine (Voronoi and sign-of-offset): inside iff
+//   max(XLO) <= x' <= min(XHI)  and  max(YLO) <= y' <= min(YHI)
+// where each group entry is t = B * (other coordinate) + C (see prep.cu).
+struct SlabEngine {
+  struct Params {
+    SlabTable tab;
+    float ox, oy;
+  };
+  static size_t table_bytes(const Params& p) { return (size_t)p.tab.total * sizeof(float2); }
 
-// Emits the P ballot words of one warp tile: lane p keeps word p; lanes
-// 0..P-1 store them (one coalesced 4P-byte store) and count their bits.
-template <int P>
-__device__ __forceinline__ uint32_t emit_words(const bool (&in)[P], uint64_t base, uint64_t m,
-                                               const TestArgs& a, int lane) {
+  __device__ static void stage(const Params& p, float4* s) {
+    const float4* src = reinterpret_cast<const float4*>(p.tab.coef);
+    for (uint32_t i = threadIdx.x; i < p.tab.total / 2; i += blockDim.x) s[i] = src[i];
+  }
+
+  // Two groups that bound the same coordinate (lo: max-reduced, hi: min-reduced),
+  // consumed in lockstep so each iteration carries 4 edges x P points of work.
+  __device__ __forceinline__ static void section(const float4* A, uint32_t na, const float4* B,
+                                                 uint32_t nb, const float (&v)[P], float (&lo)[P],
+                                                 float (&hi)[P]) {
+    const uint32_t nc = na < nb ? na : nb;
+    uint32_t i = 0;
+    for (; i < nc; ++i) {
+      const float4 a = A[i], b = B[i];
+#pragma unroll
+      for (int p = 0; p < P; ++p) {
+        lo[p] = fmax3(lo[p], fmaf(a.x, v[p], a.y), fmaf(a.z, v[p], a.w));
+        hi[p] = fmin3(hi[p], fmaf(b.x, v[p], b.y), fmaf(b.z, v[p], b.w));
+      }
+    }
+    for (uint32_t j = i; j < na; ++j) {
+      const float4 a = A[j];
+#pragma unroll
+      for (int p = 0; p < P; ++p) lo[p] = fmax3(lo[p], fmaf(a.x, v[p], a.y), fmaf(a.z, v[p], a.w));
+    }
+    for (uint32_t j = i; j < nb; ++j) {
+      const float4 b = B[j];
+#pragma unroll
+      for (int p = 0; p < P; ++p) hi[p] = fmin3(hi[p], fmaf(b.x, v[p], b.y), fmaf(b.z, v[p], b.w));
+    }
+  }
+
+  __device__ __forceinline__ static void eval(const Params& prm, const float4* s,
+                                              const float (&x)[P], const float (&y)[P],
+                                              bool (&in)[P]) {
+    const SlabTable& t = prm.tab;
+    float lo[P], hi[P];
+#pragma unroll
+    for (int p = 0; p < P; ++p) { lo[p] = -INFINITY; hi[p] = INFINITY; }
+    section(s + t.off[0] / 2, t.cnt[0] / 2, s + t.off[1] / 2, t.cnt[1] / 2, y, lo, hi);
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+      in[p] = (x[p] >= lo[p]) & (x[p] <= hi[p]);
+      lo[p] = -INFINITY;
+      hi[p] = INFINITY;
+    }
+    section(s + t.off[2] / 2, t.cnt[2] / 2, s + t.off[3] / 2, t.cnt[3] / 2, x, lo, hi);
+#pragma unroll
+    for (int p = 0; p < P; ++p) in[p] = in[p] & (y[p] >= lo[p]) & (y[p] <= hi[p]);
+  }
+};
+
+// ---------------------------------------------------------------------------
+// Crossing engine (engines.cpp:165-204). For edge w = v[k-1] -> u = v[k]:
+//   in_range <=> (u.y > qy) != (w.y > qy) <=> sign(h_k) ^ sign(h_{k-1}),
+//                h = qy - v.y (never -0.0, see prep.cu)
+//   on_left  <=> qx < x-of-edge-at-qy <=> d = (w.x - qx) + h_{k-1} * dvx/dvy > 0
+// crossing bit = (H_k ^ H_{k-1}) & ~D; parity accumulated by XOR in bit 31.
+// Points exactly on an edge line lie inside the 1e-5 parity band, so the
+// reference's closed-boundary latch (engines.cpp:194-196) is repeated only by
+// the exact f64 kernel.
+struct CrossEngine {
+  struct Params {
+    CrossTable tab;
+    float ox, oy;
+  };
+  static size_t table_bytes(const Params& p) { return (size_t)p.tab.n * sizeof(float4); }
+
+  __device__ static void stage(const Params& p, float4* s) {
+    for (uint32_t i = threadIdx.x; i < p.tab.n; i += blockDim.x) s[i] = p.tab.vert[i];
+  }
+
+  __device__ __forceinline__ static void eval(const Params& prm, const float4* s,
+                                              const float (&x)[P], const float (&y)[P],
+                                              bool (&in)[P]) {
+    const uint32_t n = prm.tab.n;
+    uint32_t par[P];
+#pragma unroll
+    for (int p = 0; p < P; ++p) par[p] = 0;
+    if (n > 0) {
+      const float4 last = s[n - 1];
+      float hp[P], gp[P];
+#pragma unroll
+      for (int p = 0; p < P; ++p) {
+        hp[p] = y[p] - last.y;
+        gp[p] = last.x - x[p];
+      }
+      uint32_t k = 0;
+      for (; k + 1 < n; k += 2) {
+        const float4 v0 = s[k], v1 = s[k + 1];
+#pragma unroll
+        for (int p = 0; p < P; ++p) {
+          const float h0 = y[p] - v0.y;
+          const float d0 = fmaf(hp[p], v0.z, gp[p]);
+          const float g0 = v0.x - x[p];
+          const float h1 = y[p] - v1.y;
+          const float d1 = fmaf(h0, v1.z, g0);
+          const uint32_t t0 = (__float_as_uint(h0) ^ __float_as_uint(hp[p])) & ~__float_as_uint(d0);
+          const uint32_t t1 = (__float_as_uint(h1) ^ __float_as_uint(h0)) & ~__float_as_uint(d1);
+          par[p] ^= t0 ^ t1;
+          hp[p] = h1;
+          gp[p] = v1.x - x[p];
+        }
+      }
+      if (k < n) {
+        const float4 v0 = s[k];
+#pragma unroll
+        for (int p = 0; p < P; ++p) {
+          const float h0 = y[p] - v0.y;
+          const float d0 = fmaf(hp[p], v0.z, gp[p]);
+          par[p] ^= (__float_as_uint(h0) ^ __float_as_uint(hp[p])) & ~__float_as_uint(d0);
+        }
+      }
+    }
+#pragma unroll
+    for (int p = 0; p < P; ++p) in[p] = (par[p] >> 31) != 0;
+  }
+};
+
+// ---------------------------------------------------------------------------
+// Output: ballot words (PIPM order), optional byte mask, per-lane bit counts.
+template <bool kGuard>
+__device__ __forceinline__ uint32_t emit(const bool (&in)[P], uint64_t base, const TestArgs& a,
+                                         int lane) {
   uint32_t mine = 0;
 #pragma unroll
   for (int p = 0; p < P; ++p) {
@@ -52,15 +187,12 @@ __device__ __forceinline__ uint32_t emit_words(const bool (&in)[P], uint64_t bas
     if (lane == p) mine = w;
   }
   const uint64_t w0 = base >> 5;
-  const uint64_t nwords = (m + 31) >> 5;
-  if (lane < P && w0 + lane < nwords) {
-    if (a.words) __stcs(a.words + w0 + lane, mine);
-  }
+  if (a.words && lane < P && (!kGuard || w0 + lane < ((a.m + 31) >> 5))) __stcs(a.words + w0 + lane, mine);
   if (a.bytes) {
 #pragma unroll
     for (int p = 0; p < P; ++p) {
       const uint64_t idx = base + 32u * p + lane;
-      if (idx < m) a.bytes[idx] = in[p] ? 1 : 0;
+      if (!kGuard || idx < a.m) a.bytes[idx] = in[p] ? 1 : 0;
     }
   }
   return lane < P ? __popc(mine) : 0u;
@@ -72,187 +204,159 @@ __device__ __forceinline__ void flush_count(uint32_t cnt, const TestArgs& a) {
   if ((threadIdx.x & 31) == 0 && a.inside && cnt) atomicAdd(a.inside, (unsigned long long)cnt);
 }
 
-// ---------------------------------------------------------------------------
-// Slab kernel: Voronoi and sign-of-offset (same arithmetic, different table).
-template <int P>
-__global__ void __launch_bounds__(kThreads) slab_kernel(const SlabTable tab, const float ox,
-                                                        const float oy, const TestArgs a) {
-  extern __shared__ float4 s_coef4[];  // (B0, C0, B1, C1) pairs of edges
-  {
-    const float4* src = reinterpret_cast<const float4*>(tab.coef);
-    for (uint32_t i = threadIdx.x; i < tab.total / 2; i += kThreads) s_coef4[i] = src[i];
-  }
-  __syncthreads();
-  const int lane = threadIdx.x & 31;
-  const int warp = threadIdx.x >> 5;
+// Guarded warp tile straight from global memory (tails, unaligned inputs).
+template <class Eng>
+__device__ __forceinline__ uint32_t guarded_tile(const typename Eng::Params& prm, const float4* tab,
+                                                 const TestArgs& a, uint64_t base, int lane) {
   const float* xs = static_cast<const float*>(a.xs);
   const float* ys = static_cast<const float*>(a.ys);
-  const uint64_t tiles = (a.m + 32u * P - 1) / (32u * P);
-  const uint32_t g0 = tab.off[0] / 2, n0 = tab.cnt[0] / 2;
-  const uint32_t g1 = tab.off[1] / 2, n1 = tab.cnt[1] / 2;
-  const uint32_t g2 = tab.off[2] / 2, n2 = tab.cnt[2] / 2;
-  const uint32_t g3 = tab.off[3] / 2, n3 = tab.cnt[3] / 2;
+  float x[P], y[P];
+  bool in[P];
+#pragma unroll
+  for (int p = 0; p < P; ++p) {
+    const uint64_t idx = base + 32u * p + lane;
+    const bool ok = idx < a.m;
+    x[p] = (ok ? __ldcs(xs + idx) : 0.f) - prm.ox;
+    y[p] = (ok ? __ldcs(ys + idx) : 0.f) - prm.oy;
+  }
+  Eng::eval(prm, tab, x, y, in);
+#pragma unroll
+  for (int p = 0; p < P; ++p) in[p] = in[p] & (base + 32u * p + lane < a.m);
+  return emit<true>(in, base, a, lane);
+}
+
+template <class Eng>
+__global__ void __launch_bounds__(kThreads, 3)
+    stream_kernel(const typename Eng::Params prm, const TestArgs a, const uint64_t full_tiles) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  float* sx = reinterpret_cast<float*>(smem);
+  float* sy = sx + kStages * kTile;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sy + kStages * kTile);
+  uint64_t* empty = full + kStages;
+  float4* tab = reinterpret_cast<float4*>(empty + kStages);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kConsumers);
+    }
+    mbar_fence_init();
+  }
+  Eng::stage(prm, tab);
+  __syncthreads();
+
+  if (warp == kConsumers) {  // ---- producer warp: one elected lane drives the TMA ring
+    if (lane == 0) {
+      const uint64_t policy = policy_evict_first();
+      const float* xs = static_cast<const float*>(a.xs);
+      const float* ys = static_cast<const float*>(a.ys);
+      uint32_t it = 0;
+      for (uint64_t tile = blockIdx.x; tile < full_tiles; tile += gridDim.x, ++it) {
+        const uint32_t s = it % kStages, ph = (it / kStages) & 1u;
+        if (it >= kStages) mbar_wait(&empty[s], ph ^ 1u);
+        mbar_arrive_expect_tx(&full[s], 2u * kTile * sizeof(float));
+        bulk_g2s(sx + s * kTile, xs + tile * kTile, kTile * sizeof(float), &full[s], policy);
+        bulk_g2s(sy + s * kTile, ys + tile * kTile, kTile * sizeof(float), &full[s], policy);
+      }
+    }
+    return;
+  }
+
+  // ---- consumer warps
   uint32_t count = 0;
-  for (uint64_t tile = (uint64_t)blockIdx.x * kWarps + warp; tile < tiles;
-       tile += (uint64_t)gridDim.x * kWarps) {
-    const uint64_t base = tile * 32u * P;
+  uint32_t it = 0;
+  for (uint64_t tile = blockIdx.x; tile < full_tiles; tile += gridDim.x, ++it) {
+    const uint32_t s = it % kStages, ph = (it / kStages) & 1u;
+    mbar_wait(&full[s], ph);
+    const float* px = sx + s * kTile + warp * kWarpPts + lane;
+    const float* py = sy + s * kTile + warp * kWarpPts + lane;
     float x[P], y[P];
     bool in[P];
 #pragma unroll
     for (int p = 0; p < P; ++p) {
-      const uint64_t idx = base + 32u * p + lane;
-      const bool ok = idx < a.m;
-      x[p] = (ok ? ld_stream(xs + idx) : 0.f) - ox;
-      y[p] = (ok ? ld_stream(ys + idx) : 0.f) - oy;
+      x[p] = px[32 * p] - prm.ox;
+      y[p] = py[32 * p] - prm.oy;
     }
-    float lo[P], hi[P];
-#pragma unroll
-    for (int p = 0; p < P; ++p) { lo[p] = -INFINITY; hi[p] = INFINITY; }
-    // x' >= B y' + C  (max over XLO), x' <= B y' + C (min over XHI)
-    for (uint32_t i = 0; i < n0; ++i) {
-      const float4 c = s_coef4[g0 + i];
-#pragma unroll
-      for (int p = 0; p < P; ++p) lo[p] = fmax3(lo[p], fmaf(c.x, y[p], c.y), fmaf(c.z, y[p], c.w));
-    }
-    for (uint32_t i = 0; i < n1; ++i) {
-      const float4 c = s_coef4[g1 + i];
-#pragma unroll
-      for (int p = 0; p < P; ++p) hi[p] = fmin3(hi[p], fmaf(c.x, y[p], c.y), fmaf(c.z, y[p], c.w));
-    }
-#pragma unroll
-    for (int p = 0; p < P; ++p) {
-      in[p] = (x[p] >= lo[p]) & (x[p] <= hi[p]);
-      lo[p] = -INFINITY;
-      hi[p] = INFINITY;
-    }
-    // y' >= B x' + C (max over YLO), y' <= B x' + C (min over YHI)
-    for (uint32_t i = 0; i < n2; ++i) {
-      const float4 c = s_coef4[g2 + i];
-#pragma unroll
-      for (int p = 0; p < P; ++p) lo[p] = fmax3(lo[p], fmaf(c.x, x[p], c.y), fmaf(c.z, x[p], c.w));
-    }
-    for (uint32_t i = 0; i < n3; ++i) {
-      const float4 c = s_coef4[g3 + i];
-#pragma unroll
-      for (int p = 0; p < P; ++p) hi[p] = fmin3(hi[p], fmaf(c.x, x[p], c.y), fmaf(c.z, x[p], c.w));
-    }
-#pragma unroll
-    for (int p = 0; p < P; ++p) {
-      const uint64_t idx = base + 32u * p + lane;
-      in[p] = in[p] & (y[p] >= lo[p]) & (y[p] <= hi[p]) & (idx < a.m);
-    }
-    count += emit_words<P>(in, base, a.m, a, lane);
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+    Eng::eval(prm, tab, x, y, in);
+    count += emit<false>(in, tile * kTile + warp * kWarpPts, a, lane);
+  }
+  // tail (< one tile): the CTA next in round-robin order, guarded loads
+  if (blockIdx.x == full_tiles % gridDim.x) {
+    for (uint64_t base = full_tiles * kTile + (uint64_t)warp * kWarpPts; base < a.m;
+         base += (uint64_t)kConsumers * kWarpPts)
+      count += guarded_tile<Eng>(prm, tab, a, base, lane);
   }
   flush_count(count, a);
 }
 
-// ---------------------------------------------------------------------------
-// Crossing kernel (engines.cpp:165-204). For edge w = v[k-1] -> u = v[k]:
-//   in_range  <=>  (u.y > qy) != (w.y > qy)  <=>  sign(h_k) ^ sign(h_{k-1}),
-//                  h = qy - v.y (never -0.0: see prep.cu)
-//   on_left   <=>  qx < x-of-edge-at-qy  <=>  d = (w.x - qx) + h_{k-1} * dvx/dvy > 0
-// crossing bit = (H_k ^ H_{k-1}) & ~D, parity accumulated by XOR in bit 31.
-// Points exactly on an edge line are inside the 1e-5 parity band, so the
-// reference's closed-boundary latch (engines.cpp:194-196) is not repeated in
-// fp32; the f64 kernel repeats it exactly.
-template <int P>
-__global__ void __launch_bounds__(kThreads) cross_kernel(const CrossTable tab, const float ox,
-                                                         const float oy, const TestArgs a) {
-  extern __shared__ float4 s_vert[];
-  for (uint32_t i = threadIdx.x; i < tab.n; i += kThreads) s_vert[i] = tab.vert[i];
+template <class Eng>
+__global__ void __launch_bounds__(kThreads) generic_kernel(const typename Eng::Params prm,
+                                                          const TestArgs a) {
+  extern __shared__ __align__(16) float4 gtab[];
+  Eng::stage(prm, gtab);
   __syncthreads();
   const int lane = threadIdx.x & 31;
-  const int warp = threadIdx.x >> 5;
-  const float* xs = static_cast<const float*>(a.xs);
-  const float* ys = static_cast<const float*>(a.ys);
-  const uint64_t tiles = (a.m + 32u * P - 1) / (32u * P);
-  const uint32_t n = tab.n;
+  const uint64_t gwarp = (uint64_t)blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5);
   uint32_t count = 0;
-  for (uint64_t tile = (uint64_t)blockIdx.x * kWarps + warp; tile < tiles;
-       tile += (uint64_t)gridDim.x * kWarps) {
-    const uint64_t base = tile * 32u * P;
-    float x[P], y[P];
-#pragma unroll
-    for (int p = 0; p < P; ++p) {
-      const uint64_t idx = base + 32u * p + lane;
-      const bool ok = idx < a.m;
-      x[p] = (ok ? ld_stream(xs + idx) : 0.f) - ox;
-      y[p] = (ok ? ld_stream(ys + idx) : 0.f) - oy;
-    }
-    uint32_t par[P];
-    bool in[P];
-    if (n > 0) {
-      const float4 last = s_vert[n - 1];
-      float hp[P], gp[P];
-#pragma unroll
-      for (int p = 0; p < P; ++p) {
-        hp[p] = y[p] - last.y;
-        gp[p] = last.x - x[p];
-        par[p] = 0;
-      }
-      for (uint32_t k = 0; k < n; ++k) {
-        const float4 v = s_vert[k];
-#pragma unroll
-        for (int p = 0; p < P; ++p) {
-          const float h = y[p] - v.y;
-          const float d = fmaf(hp[p], v.z, gp[p]);
-          par[p] ^= (__float_as_uint(h) ^ __float_as_uint(hp[p])) & ~__float_as_uint(d);
-          hp[p] = h;
-          gp[p] = v.x - x[p];
-        }
-      }
-    } else {
-#pragma unroll
-      for (int p = 0; p < P; ++p) par[p] = 0;
-    }
-#pragma unroll
-    for (int p = 0; p < P; ++p) {
-      const uint64_t idx = base + 32u * p + lane;
-      in[p] = (par[p] >> 31) & (idx < a.m);
-    }
-    count += emit_words<P>(in, base, a.m, a, lane);
-  }
+  for (uint64_t base = gwarp * kWarpPts; base < a.m;
+       base += (uint64_t)gridDim.x * (kThreads / 32) * kWarpPts)
+    count += guarded_tile<Eng>(prm, gtab, a, base, lane);
   flush_count(count, a);
 }
 
-template <class K>
-int grid_for(K kernel, size_t smem, uint64_t m, int pts_per_block) {
-  int dev = 0, sms = 0, per_sm = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kThreads, smem);
+int sm_count() {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  return sms;
+}
+
+template <class Eng>
+cudaError_t launch(const typename Eng::Params& prm, const TestArgs& a, cudaStream_t stream) {
+  const size_t tab = Eng::table_bytes(prm);
+  const bool aligned = ((reinterpret_cast<uintptr_t>(a.xs) | reinterpret_cast<uintptr_t>(a.ys)) & 15) == 0;
+  const uint64_t full_tiles = aligned ? a.m / kTile : 0;
+  if (full_tiles == 0) {
+    auto k = generic_kernel<Eng>;
+    if (tab > 48 * 1024) {
+      cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tab);
+      if (e != cudaSuccess) return e;
+    }
+    const uint64_t warps = (a.m + kWarpPts - 1) / kWarpPts;
+    const uint64_t blocks = (warps + kThreads / 32 - 1) / (kThreads / 32);
+    const uint64_t cap = (uint64_t)sm_count() * 4;
+    k<<<(int)(blocks < cap ? blocks : cap), kThreads, tab, stream>>>(prm, a);
+    return cudaGetLastError();
+  }
+  auto k = stream_kernel<Eng>;
+  const size_t smem = 2 * kStages * kTile * sizeof(float) + 2 * kStages * sizeof(uint64_t) + tab;
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  int per_sm = 0;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kThreads, smem);
+  if (e != cudaSuccess) return e;
   if (per_sm < 1) per_sm = 1;
-  const uint64_t need = (m + pts_per_block - 1) / pts_per_block;
-  const uint64_t cap = (uint64_t)sms * per_sm;
-  return static_cast<int>(need < cap ? (need ? need : 1) : cap);
+  const uint64_t cap = (uint64_t)sm_count() * per_sm;
+  const int grid = (int)(full_tiles < cap ? full_tiles : cap);
+  k<<<grid, kThreads, smem, stream>>>(prm, a, full_tiles);
+  return cudaGetLastError();
 }
 
 }  // namespace
 
 cudaError_t launch_test_f32(const DevTables& t, int engine, const TestArgs& a,
                             cudaStream_t stream) {
-  constexpr int P = 8;
   if (engine == 0 || engine == 1) {
-    const SlabTable& tab = t.slab[engine];
-    const size_t smem = (size_t)tab.total * sizeof(float2);
-    auto k = slab_kernel<P>;
-    if (smem > 48 * 1024) {
-      cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      if (e != cudaSuccess) return e;
-    }
-    const int grid = grid_for(k, smem, a.m, kThreads * P);
-    k<<<grid, kThreads, smem, stream>>>(tab, t.ox, t.oy, a);
-    return cudaGetLastError();
+    SlabEngine::Params prm{t.slab[engine], t.ox, t.oy};
+    return launch<SlabEngine>(prm, a, stream);
   }
-  const size_t smem = (size_t)t.cross.n * sizeof(float4);
-  auto k = cross_kernel<P>;
-  if (smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-  }
-  const int grid = grid_for(k, smem, a.m, kThreads * P);
-  k<<<grid, kThreads, smem, stream>>>(t.cross, t.ox, t.oy, a);
-  return cudaGetLastError();
+  CrossEngine::Params prm{t.cross, t.ox, t.oy};
+  return launch<CrossEngine>(prm, a, stream);
 }
 
 }  // namespace vpipg

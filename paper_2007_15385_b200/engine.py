@@ -133,6 +133,35 @@ class PreparedPolygon:
         return w, b, cnt.value
 
 
+    def test_host_multi(self, xs: np.ndarray, ys: np.ndarray, engines=(0, 1, 2),
+                        words=None, counts_only: bool = False):
+        """All requested engines over one host batch (vpipg_test_host_multi).
+
+        `words`: optional list of 3 preallocated uint32 arrays (e.g. pinned
+        buffers); returns (words list, counts list)."""
+        is_np = isinstance(xs, np.ndarray)
+        dtype = F32 if str(xs.dtype).endswith("float32") else F64
+        m = xs.size if is_np else xs.numel()
+        mask = 0
+        for e in engines:
+            mask |= 1 << _engine_id(e)
+        if words is None and not counts_only:
+            words = [np.zeros((m + 31) // 32, dtype=np.uint32) if (mask >> e) & 1 else None
+                     for e in range(3)]
+        wp = (C.c_void_p * 3)(*[C.c_void_p(w.ctypes.data if isinstance(w, np.ndarray) else
+                                           (w.data_ptr() if w is not None else None))
+                                for w in (words or [None] * 3)])
+        cnt = (C.c_uint64 * 3)()
+        check(load().vpipg_test_host_multi(self._h, mask, dtype, C.c_void_p(_host_ptr(xs)),
+                                           C.c_void_p(_host_ptr(ys)), m, wp, None, cnt),
+              "vpipg_test_host_multi")
+        return words, [cnt[i] for i in range(3)]
+
+
+def _host_ptr(a) -> int:
+    return a.ctypes.data if isinstance(a, np.ndarray) else a.data_ptr()
+
+
 def fill_uniform_points(seed: int, first: int, xs, ys, box, stream=None) -> None:
     """Counter-based device point stream (vpipg_fill_uniform_points)."""
     import torch

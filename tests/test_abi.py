@@ -46,8 +46,13 @@ def test_kernels_use_fma_and_3way_minmax():
     """The slab kernel's inner loop is FFMA + FMNMX3 (two edges per FMNMX3)."""
     sass = subprocess.run(["cuobjdump", "-sass", str(_lib.LIB_PATH)], capture_output=True,
                           text=True, check=True).stdout
-    body = sass.split("slab_kernel")[1].split("Function :")[0]
-    assert "FMNMX3" in body and "FFMA" in body
+    blocks = [b for b in sass.split("Function :") if "SlabEngine" in b.split("\n")[0]]
+    assert blocks
+    for body in blocks:
+        assert "FMNMX3" in body and "FFMA" in body
+    # the streaming kernel moves points with the bulk-copy (TMA) engine
+    stream = [b for b in sass.split("Function :") if "stream_kernel" in b.split("\n")[0]]
+    assert stream and all("UBLKCP" in b for b in stream)
 
 
 def test_strerror_and_version():
