@@ -50,8 +50,8 @@ __device__ int slab_classify(double a, double b, double c, float2* bc) {
 }
 
 // Block-wide deterministic scatter of per-edge (class, coef) into the four
-// groups of one slab table, each padded to an even length with a neutral
-// entry. Edge order is preserved inside a group.
+// groups of one slab table, each padded with neutral entries to an even,
+// non-zero length. Edge order is preserved inside a group.
 __device__ void slab_scatter(int n, int (*cls_of)(int, const void*, float2*), const void* ctx,
                              float2* out, uint32_t* cnt_out) {
   __shared__ uint32_t s_base[kGroups];
@@ -71,11 +71,13 @@ __device__ void slab_scatter(int n, int (*cls_of)(int, const void*, float2*), co
     uint32_t acc = 0;
     for (int g = 0; g < kGroups; ++g) {
       s_base[g] = acc;
-      const uint32_t padded = (s_count[g] + 1u) & ~1u;
+      // even length (two edges per 16-byte load) and at least one pair, so
+      // the kernels can seed their running max / min from the first pair
+      uint32_t padded = (s_count[g] + 1u) & ~1u;
+      if (padded == 0) padded = 2;
       cnt_out[g] = padded;
-      if (padded != s_count[g]) {  // neutral pad entry at the group's end
-        out[acc + padded - 1] = make_float2(0.f, (g == kXlo || g == kYlo) ? -INFINITY : INFINITY);
-      }
+      for (uint32_t q = s_count[g]; q < padded; ++q)  // neutral pad entries
+        out[acc + q] = make_float2(0.f, (g == kXlo || g == kYlo) ? -INFINITY : INFINITY);
       acc += padded;
     }
   }
@@ -172,10 +174,10 @@ __global__ void __launch_bounds__(kPrepThreads) prep_kernel(PrepArgs a) {
     }
     s_inner[0] = cx;
     s_inner[1] = cy;
-    float ox = static_cast<float>(cx), oy = static_cast<float>(cy);
-    // a zero origin is stored as -0.0f so that x - ox never yields -0.0
-    if (ox == 0.f) ox = -0.f;
-    if (oy == 0.f) oy = -0.f;
+    // The fp32 tables use the absolute frame (origin 0): the parity band is
+    // relative to max(1, |x|, |y|, extent), and one FFMA with |B| <= 1 keeps the
+    // rounding error ~2^-24 of that scale, so no per-point shift is needed.
+    const float ox = 0.f, oy = 0.f;
     a.meta->inner_x = cx;
     a.meta->inner_y = cy;
     a.meta->ox = ox;
@@ -258,9 +260,8 @@ __global__ void __launch_bounds__(kPrepThreads) prep_kernel(PrepArgs a) {
       r.pad_ = 0;
       a.ray[e] = r;
       // fp32 crossing record for vertex i (edge j -> i)
-      // (+0.0 turns a -0.0 difference into +0.0: sign bits are tested directly)
-      const float xl = static_cast<float>((ux - ox) + 0.0);
-      const float yl = static_cast<float>((uy - oy) + 0.0);
+      const float xl = static_cast<float>(ux - ox);
+      const float yl = static_cast<float>(uy - oy);
       const float bk = (dvy != 0.0) ? static_cast<float>(dvx / dvy) : 0.f;
       a.cross_vert[i] = make_float4(xl, yl, bk, 0.f);
     }

@@ -6,17 +6,18 @@
 //   ray_kernel       (engines.cpp:165-204) -> CrossEngine
 //   count_inside     (engines.cpp:215-217) -> fused popc + one atomic per warp
 //
-// Streaming structure (stream_kernel): a persistent grid of CTAs, each with one
-// producer warp and kConsumers consumer warps. The producer's elected lane
-// moves 2048-point tiles of xs and ys into a kStages-deep shared-memory ring
-// with cp.async.bulk (TMA, evict-first) and arms a "full" mbarrier per stage;
-// consumer warps copy their 256-point slice into registers, release the stage
-// on its "empty" mbarrier and evaluate while the next tiles are in flight.
-// Lane l of a consumer warp owns points 32*p + l (p < P) of its slice, so the
-// ballot of sub-tile p is exactly one PIPM mask word (io.cpp:272-279, bit j =
-// point j) and word stores are coalesced. The polygon table is staged once per
-// CTA in shared memory and read with warp-uniform 16-byte broadcasts.
-// generic_kernel handles unaligned inputs with guarded direct loads.
+// Streaming structure (stream_kernel): a persistent grid; every warp owns a
+// private kStages-deep shared-memory ring and streams its own 512-point slices
+// (slice g goes to warp g mod W) with cp.async.bulk (the 1-D TMA path,
+// evict-first). Lane 0 arms the stage's "full" mbarrier with the expected
+// bytes; after the warp copied a stage into registers, all 32 lanes arrive on
+// its "empty" mbarrier (release) and lane 0 refills it with slice g + S*W, so
+// loads run kStages slices ahead of the math with no cross-warp coupling.
+// Lane l owns points 32*p + l (p < P) of a slice, so the ballot of sub-tile p
+// is exactly one PIPM mask word (io.cpp:272-279, bit j = point j) and word
+// stores are coalesced. The polygon table is staged once per CTA in shared
+// memory and read with warp-uniform 16-byte broadcasts. generic_kernel handles
+// unaligned inputs with guarded direct loads.
 #include <cstdint>
 
 #include "tma_pipe.cuh"
@@ -27,12 +28,11 @@ namespace vpipg {
 
 namespace {
 
-constexpr int P = 8;                          // points per lane per tile
-constexpr int kConsumers = 8;                 // consumer warps per CTA
-constexpr int kThreads = (kConsumers + 1) * 32;
-constexpr int kWarpPts = 32 * P;              // 256 points per warp slice
-constexpr int kTile = kConsumers * kWarpPts;  // 2048 points per stage
-constexpr int kStages = 4;
+constexpr int P = 16;                 // points per lane per slice
+constexpr int kWarps = 8;             // warps per CTA
+constexpr int kThreads = kWarps * 32;
+constexpr int kWarpPts = 32 * P;      // 512 points per warp slice
+constexpr int kStages = 2;            // per-warp ring depth
 
 __device__ __forceinline__ float fmax3(float a, float b, float c) {
   float r;
@@ -63,11 +63,20 @@ struct SlabEngine {
 
   // Two groups that bound the same coordinate (lo: max-reduced, hi: min-reduced),
   // consumed in lockstep so each iteration carries 4 edges x P points of work.
+  // Both groups hold >= 1 pair (prep.cu pads), so the first pair seeds lo / hi.
   __device__ __forceinline__ static void section(const float4* A, uint32_t na, const float4* B,
                                                  uint32_t nb, const float (&v)[P], float (&lo)[P],
                                                  float (&hi)[P]) {
+    {
+      const float4 a = A[0], b = B[0];
+#pragma unroll
+      for (int p = 0; p < P; ++p) {
+        lo[p] = fmaxf(fmaf(a.x, v[p], a.y), fmaf(a.z, v[p], a.w));
+        hi[p] = fminf(fmaf(b.x, v[p], b.y), fmaf(b.z, v[p], b.w));
+      }
+    }
     const uint32_t nc = na < nb ? na : nb;
-    uint32_t i = 0;
+    uint32_t i = 1;
     for (; i < nc; ++i) {
       const float4 a = A[i], b = B[i];
 #pragma unroll
@@ -88,30 +97,27 @@ struct SlabEngine {
     }
   }
 
+  // slack[p] >= 0 <=> point p is inside: the smallest of x' - max(XLO),
+  // min(XHI) - x', y' - max(YLO), min(YHI) - y' (an exact zero is +0.0).
   __device__ __forceinline__ static void eval(const Params& prm, const float4* s,
                                               const float (&x)[P], const float (&y)[P],
-                                              bool (&in)[P]) {
+                                              float (&slack)[P]) {
     const SlabTable& t = prm.tab;
     float lo[P], hi[P];
-#pragma unroll
-    for (int p = 0; p < P; ++p) { lo[p] = -INFINITY; hi[p] = INFINITY; }
     section(s + t.off[0] / 2, t.cnt[0] / 2, s + t.off[1] / 2, t.cnt[1] / 2, y, lo, hi);
 #pragma unroll
-    for (int p = 0; p < P; ++p) {
-      in[p] = (x[p] >= lo[p]) & (x[p] <= hi[p]);
-      lo[p] = -INFINITY;
-      hi[p] = INFINITY;
-    }
+    for (int p = 0; p < P; ++p) slack[p] = fminf(x[p] - lo[p], hi[p] - x[p]);
     section(s + t.off[2] / 2, t.cnt[2] / 2, s + t.off[3] / 2, t.cnt[3] / 2, x, lo, hi);
 #pragma unroll
-    for (int p = 0; p < P; ++p) in[p] = in[p] & (y[p] >= lo[p]) & (y[p] <= hi[p]);
+    for (int p = 0; p < P; ++p) slack[p] = fmin3(slack[p], y[p] - lo[p], hi[p] - y[p]);
   }
 };
 
 // ---------------------------------------------------------------------------
 // Crossing engine (engines.cpp:165-204). For edge w = v[k-1] -> u = v[k]:
 //   in_range <=> (u.y > qy) != (w.y > qy) <=> sign(h_k) ^ sign(h_{k-1}),
-//                h = qy - v.y (never -0.0, see prep.cu)
+//                h = qy - v.y (a -0.0 from qy = -0.0 merely moves vertex k to
+//                "above" for both of its edges at once, which keeps the parity)
 //   on_left  <=> qx < x-of-edge-at-qy <=> d = (w.x - qx) + h_{k-1} * dvx/dvy > 0
 // crossing bit = (H_k ^ H_{k-1}) & ~D; parity accumulated by XOR in bit 31.
 // Points exactly on an edge line lie inside the 1e-5 parity band, so the
@@ -128,9 +134,10 @@ struct CrossEngine {
     for (uint32_t i = threadIdx.x; i < p.tab.n; i += blockDim.x) s[i] = p.tab.vert[i];
   }
 
+  // slack[p] = +1 (odd crossing parity: inside) or -1 (even: outside)
   __device__ __forceinline__ static void eval(const Params& prm, const float4* s,
                                               const float (&x)[P], const float (&y)[P],
-                                              bool (&in)[P]) {
+                                              float (&slack)[P]) {
     const uint32_t n = prm.tab.n;
     uint32_t par[P];
 #pragma unroll
@@ -144,6 +151,23 @@ struct CrossEngine {
         gp[p] = last.x - x[p];
       }
       uint32_t k = 0;
+      for (; k + 3 < n; k += 4) {
+        const float4 v0 = s[k], v1 = s[k + 1], v2 = s[k + 2], v3 = s[k + 3];
+#pragma unroll
+        for (int p = 0; p < P; ++p) {
+          const float h0 = y[p] - v0.y, g0 = v0.x - x[p];
+          const float h1 = y[p] - v1.y, g1 = v1.x - x[p];
+          const float h2 = y[p] - v2.y, g2 = v2.x - x[p];
+          const float h3 = y[p] - v3.y;
+          const uint32_t t0 = (__float_as_uint(h0) ^ __float_as_uint(hp[p])) & ~__float_as_uint(fmaf(hp[p], v0.z, gp[p]));
+          const uint32_t t1 = (__float_as_uint(h1) ^ __float_as_uint(h0)) & ~__float_as_uint(fmaf(h0, v1.z, g0));
+          const uint32_t t2 = (__float_as_uint(h2) ^ __float_as_uint(h1)) & ~__float_as_uint(fmaf(h1, v2.z, g1));
+          const uint32_t t3 = (__float_as_uint(h3) ^ __float_as_uint(h2)) & ~__float_as_uint(fmaf(h2, v3.z, g2));
+          par[p] ^= t0 ^ t1 ^ t2 ^ t3;
+          hp[p] = h3;
+          gp[p] = v3.x - x[p];
+        }
+      }
       for (; k + 1 < n; k += 2) {
         const float4 v0 = s[k], v1 = s[k + 1];
 #pragma unroll
@@ -171,31 +195,46 @@ struct CrossEngine {
       }
     }
 #pragma unroll
-    for (int p = 0; p < P; ++p) in[p] = (par[p] >> 31) != 0;
+    for (int p = 0; p < P; ++p) slack[p] = __uint_as_float((~par[p] & 0x80000000u) | 0x3f800000u);
   }
 };
 
 // ---------------------------------------------------------------------------
-// Output: ballot words (PIPM order), optional byte mask, per-lane bit counts.
+// Output: ballot words (PIPM order), optional byte mask, per-lane inside count.
+// The P words of a slice are warp-uniform; lane 0 writes them with 16-byte
+// streaming stores (a slice's words are 64 contiguous, 64-byte aligned bytes).
 template <bool kGuard>
-__device__ __forceinline__ uint32_t emit(const bool (&in)[P], uint64_t base, const TestArgs& a,
-                                         int lane) {
-  uint32_t mine = 0;
+__device__ __forceinline__ uint32_t emit(const float (&slack)[P], uint64_t base,
+                                         const TestArgs& a, int lane) {
+  uint32_t w[P];
+  uint32_t cnt = 0;
 #pragma unroll
   for (int p = 0; p < P; ++p) {
-    const uint32_t w = __ballot_sync(0xffffffffu, in[p]);
-    if (lane == p) mine = w;
+    const bool ok = (slack[p] >= 0.f) & (!kGuard || base + 32u * p + lane < a.m);
+    w[p] = __ballot_sync(0xffffffffu, ok);
+    cnt += ok;
   }
-  const uint64_t w0 = base >> 5;
-  if (a.words && lane < P && (!kGuard || w0 + lane < ((a.m + 31) >> 5))) __stcs(a.words + w0 + lane, mine);
+  if (a.words && lane == 0) {
+    const uint64_t w0 = base >> 5;
+    if (!kGuard && (reinterpret_cast<uintptr_t>(a.words) & 15) == 0) {
+      uint4* dst = reinterpret_cast<uint4*>(a.words + w0);
+#pragma unroll
+      for (int q = 0; q < P / 4; ++q) __stcs(dst + q, make_uint4(w[4 * q], w[4 * q + 1], w[4 * q + 2], w[4 * q + 3]));
+    } else {
+      const uint64_t nwords = (a.m + 31) >> 5;
+#pragma unroll
+      for (int p = 0; p < P; ++p)
+        if (!kGuard || w0 + p < nwords) a.words[w0 + p] = w[p];
+    }
+  }
   if (a.bytes) {
 #pragma unroll
     for (int p = 0; p < P; ++p) {
       const uint64_t idx = base + 32u * p + lane;
-      if (!kGuard || idx < a.m) a.bytes[idx] = in[p] ? 1 : 0;
+      if (!kGuard || idx < a.m) a.bytes[idx] = (w[p] >> lane) & 1u;
     }
   }
-  return lane < P ? __popc(mine) : 0u;
+  return cnt;
 }
 
 __device__ __forceinline__ void flush_count(uint32_t cnt, const TestArgs& a) {
@@ -210,82 +249,83 @@ __device__ __forceinline__ uint32_t guarded_tile(const typename Eng::Params& prm
                                                  const TestArgs& a, uint64_t base, int lane) {
   const float* xs = static_cast<const float*>(a.xs);
   const float* ys = static_cast<const float*>(a.ys);
-  float x[P], y[P];
-  bool in[P];
+  float x[P], y[P], slack[P];
 #pragma unroll
   for (int p = 0; p < P; ++p) {
     const uint64_t idx = base + 32u * p + lane;
     const bool ok = idx < a.m;
-    x[p] = (ok ? __ldcs(xs + idx) : 0.f) - prm.ox;
-    y[p] = (ok ? __ldcs(ys + idx) : 0.f) - prm.oy;
+    x[p] = ok ? __ldcs(xs + idx) : 0.f;
+    y[p] = ok ? __ldcs(ys + idx) : 0.f;
   }
-  Eng::eval(prm, tab, x, y, in);
-#pragma unroll
-  for (int p = 0; p < P; ++p) in[p] = in[p] & (base + 32u * p + lane < a.m);
-  return emit<true>(in, base, a, lane);
+  Eng::eval(prm, tab, x, y, slack);
+  return emit<true>(slack, base, a, lane);
 }
 
 template <class Eng>
-__global__ void __launch_bounds__(kThreads, 3)
-    stream_kernel(const typename Eng::Params prm, const TestArgs a, const uint64_t full_tiles) {
+__global__ void __launch_bounds__(kThreads, 2)
+    stream_kernel(const typename Eng::Params prm, const TestArgs a, const uint64_t full_slices) {
   extern __shared__ __align__(128) unsigned char smem[];
-  float* sx = reinterpret_cast<float*>(smem);
-  float* sy = sx + kStages * kTile;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sy + kStages * kTile);
-  uint64_t* empty = full + kStages;
-  float4* tab = reinterpret_cast<float4*>(empty + kStages);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (threadIdx.x == 0) {
+  // per-warp ring: [stage][x | y][kWarpPts] floats, then the barriers, then the table
+  float* ring = reinterpret_cast<float*>(smem) + (size_t)warp * kStages * 2 * kWarpPts;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<float*>(smem) +
+                                               (size_t)kWarps * kStages * 2 * kWarpPts);
+  uint64_t* full = bars + warp * 2 * kStages;
+  uint64_t* empty = full + kStages;
+  float4* tab = reinterpret_cast<float4*>(bars + kWarps * 2 * kStages);
+  if (lane == 0) {
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], kConsumers);
+      mbar_init(&empty[s], 32);
     }
     mbar_fence_init();
   }
   Eng::stage(prm, tab);
   __syncthreads();
 
-  if (warp == kConsumers) {  // ---- producer warp: one elected lane drives the TMA ring
-    if (lane == 0) {
-      const uint64_t policy = policy_evict_first();
-      const float* xs = static_cast<const float*>(a.xs);
-      const float* ys = static_cast<const float*>(a.ys);
-      uint32_t it = 0;
-      for (uint64_t tile = blockIdx.x; tile < full_tiles; tile += gridDim.x, ++it) {
-        const uint32_t s = it % kStages, ph = (it / kStages) & 1u;
-        if (it >= kStages) mbar_wait(&empty[s], ph ^ 1u);
-        mbar_arrive_expect_tx(&full[s], 2u * kTile * sizeof(float));
-        bulk_g2s(sx + s * kTile, xs + tile * kTile, kTile * sizeof(float), &full[s], policy);
-        bulk_g2s(sy + s * kTile, ys + tile * kTile, kTile * sizeof(float), &full[s], policy);
-      }
+  const uint64_t W = (uint64_t)gridDim.x * kWarps;
+  const uint64_t g0 = (uint64_t)blockIdx.x * kWarps + warp;
+  const float* xs = static_cast<const float*>(a.xs);
+  const float* ys = static_cast<const float*>(a.ys);
+  uint64_t policy = 0;
+  if (lane == 0) {
+    policy = policy_evict_first();
+    for (int s = 0; s < kStages; ++s) {
+      const uint64_t g = g0 + s * W;
+      if (g >= full_slices) break;
+      mbar_arrive_expect_tx(&full[s], 2u * kWarpPts * sizeof(float));
+      bulk_g2s(ring + s * 2 * kWarpPts, xs + g * kWarpPts, kWarpPts * sizeof(float), &full[s], policy);
+      bulk_g2s(ring + s * 2 * kWarpPts + kWarpPts, ys + g * kWarpPts, kWarpPts * sizeof(float),
+               &full[s], policy);
     }
-    return;
   }
-
-  // ---- consumer warps
   uint32_t count = 0;
   uint32_t it = 0;
-  for (uint64_t tile = blockIdx.x; tile < full_tiles; tile += gridDim.x, ++it) {
+  for (uint64_t g = g0; g < full_slices; g += W, ++it) {
     const uint32_t s = it % kStages, ph = (it / kStages) & 1u;
     mbar_wait(&full[s], ph);
-    const float* px = sx + s * kTile + warp * kWarpPts + lane;
-    const float* py = sy + s * kTile + warp * kWarpPts + lane;
-    float x[P], y[P];
-    bool in[P];
+    const float* px = ring + s * 2 * kWarpPts + lane;
+    float x[P], y[P], slack[P];
 #pragma unroll
     for (int p = 0; p < P; ++p) {
-      x[p] = px[32 * p] - prm.ox;
-      y[p] = py[32 * p] - prm.oy;
+      x[p] = px[32 * p];
+      y[p] = px[kWarpPts + 32 * p];
     }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[s]);
-    Eng::eval(prm, tab, x, y, in);
-    count += emit<false>(in, tile * kTile + warp * kWarpPts, a, lane);
+    mbar_arrive(&empty[s]);  // release: this lane's reads of stage s are done
+    const uint64_t gn = g + kStages * W;
+    if (lane == 0 && gn < full_slices) {
+      mbar_wait(&empty[s], ph);
+      mbar_arrive_expect_tx(&full[s], 2u * kWarpPts * sizeof(float));
+      bulk_g2s(ring + s * 2 * kWarpPts, xs + gn * kWarpPts, kWarpPts * sizeof(float), &full[s], policy);
+      bulk_g2s(ring + s * 2 * kWarpPts + kWarpPts, ys + gn * kWarpPts, kWarpPts * sizeof(float),
+               &full[s], policy);
+    }
+    Eng::eval(prm, tab, x, y, slack);
+    count += emit<false>(slack, g * kWarpPts, a, lane);
   }
-  // tail (< one tile): the CTA next in round-robin order, guarded loads
-  if (blockIdx.x == full_tiles % gridDim.x) {
-    for (uint64_t base = full_tiles * kTile + (uint64_t)warp * kWarpPts; base < a.m;
-         base += (uint64_t)kConsumers * kWarpPts)
+  // partial last slice: the warp next in round-robin order, guarded loads
+  if (g0 == full_slices % W) {
+    for (uint64_t base = full_slices * kWarpPts; base < a.m; base += kWarpPts)
       count += guarded_tile<Eng>(prm, tab, a, base, lane);
   }
   flush_count(count, a);
@@ -320,8 +360,8 @@ template <class Eng>
 cudaError_t launch(const typename Eng::Params& prm, const TestArgs& a, cudaStream_t stream) {
   const size_t tab = Eng::table_bytes(prm);
   const bool aligned = ((reinterpret_cast<uintptr_t>(a.xs) | reinterpret_cast<uintptr_t>(a.ys)) & 15) == 0;
-  const uint64_t full_tiles = aligned ? a.m / kTile : 0;
-  if (full_tiles == 0) {
+  const uint64_t full_slices = aligned ? a.m / kWarpPts : 0;
+  if (full_slices < kWarps) {
     auto k = generic_kernel<Eng>;
     if (tab > 48 * 1024) {
       cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tab);
@@ -334,7 +374,8 @@ cudaError_t launch(const typename Eng::Params& prm, const TestArgs& a, cudaStrea
     return cudaGetLastError();
   }
   auto k = stream_kernel<Eng>;
-  const size_t smem = 2 * kStages * kTile * sizeof(float) + 2 * kStages * sizeof(uint64_t) + tab;
+  const size_t smem = (size_t)kWarps * kStages * 2 * kWarpPts * sizeof(float) +
+                      (size_t)kWarps * 2 * kStages * sizeof(uint64_t) + tab;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   int per_sm = 0;
@@ -342,8 +383,9 @@ cudaError_t launch(const typename Eng::Params& prm, const TestArgs& a, cudaStrea
   if (e != cudaSuccess) return e;
   if (per_sm < 1) per_sm = 1;
   const uint64_t cap = (uint64_t)sm_count() * per_sm;
-  const int grid = (int)(full_tiles < cap ? full_tiles : cap);
-  k<<<grid, kThreads, smem, stream>>>(prm, a, full_tiles);
+  const uint64_t want = (full_slices + kWarps - 1) / kWarps;
+  const int grid = (int)(want < cap ? want : cap);
+  k<<<grid, kThreads, smem, stream>>>(prm, a, full_slices);
   return cudaGetLastError();
 }
 
