@@ -42,6 +42,11 @@ METRIC = "point-polygon tests/sec"
 UNIT = "tests/s"
 PEAKS_FILE = ROOT / "MEASURED_PEAKS.json"
 PIPE_PEAKS_FILE = ROOT / "profiles" / "pipe_peaks_r01.json"
+TRAFFIC_FILE = ROOT / "profiles" / "traffic_r01.json"
+# dispatch cycles per point-edge per warp lane-slot (tools/pipe_peaks.cu model:
+# FFMA/FADD 1 cycle, FMNMX3/LOP3 2): slab = FFMA + FMNMX3/2, crossing =
+# 2 FADD + FFMA + 1.5 LOP3
+ISSUE_CYCLES_PER_PE = {"voronoi": 2.0, "sign_of_offset": 2.0, "ray_crossing": 6.0}
 HBM_FALLBACK_GBS = 6650.0
 # FFMA lane-ops per SM per clock on sm_100a (tools/pipe_peaks.cu: 3.79 warp-inst/clk/SM)
 FFMA_PER_SM_CLK = 128
@@ -270,6 +275,7 @@ def main():
     import torch
     import torch.distributed as dist
     import paper_2007_15385_b200 as vp
+    from paper_2007_15385_b200.multi import reduce_counts
 
     torch.cuda.set_device(local)
     if world > 1:
@@ -302,8 +308,7 @@ def main():
             if record:
                 b.record(stream)
                 pairs.append((a, b))
-        if world > 1:
-            dist.all_reduce(counts)
+        reduce_counts(counts)  # NCCL all-reduce of the 3 inside counts (no-op at N=1)
         if record:
             kevents.append(pairs)
 
@@ -393,23 +398,38 @@ def main():
                         "GB_per_s": bytes_per_launch / t / 1e9,
                         "point_edge_per_s": pe / t,
                         "tflops_alg": 4 * pe / t / 1e12})
+    clk_hz = ((clocks or {}).get("sm_mhz") or 1965.0) * 1e6
+    sms = torch.cuda.get_device_properties(local).multi_processor_count
+    for k in kernels:
+        peak_pe = sms * 4 * 32 * clk_hz / ISSUE_CYCLES_PER_PE[k["engine"]]
+        k["issue_model_frac"] = k["point_edge_per_s"] / peak_pe
     dom = max(range(3), key=lambda e: per_kernel_ms[e])
     dk = kernels[dom]
     hbm_frac = dk["GB_per_s"] / hbm_peak
     fma_tflops = 2 * fma_peak / 1e12 if fma_peak else 2 * FFMA_PER_SM_CLK * 148 * 1.965e9 / 1e12
     fma_frac = dk["tflops_alg"] / fma_tflops
     compute_bound = (4 * pe / (fma_tflops * 1e12)) > (bytes_per_launch / (hbm_peak * 1e9))
+    traffic = None
+    try:  # DRAM bytes per launch from the committed ncu --set full capture (same kernel/config)
+        tj = json.loads(TRAFFIC_FILE.read_text())
+        if tj["workload"] == args.workload:
+            traffic = tj["dram_bytes_per_launch"][dk["engine"]] * m / tj["points"]
+    except Exception:
+        pass
     if compute_bound:
         roof = {"bound": "fp32-fma", "achieved": dk["tflops_alg"], "peak": fma_tflops,
-                "unit": "TFLOP/s", "frac": fma_frac, "traffic": None}
+                "unit": "TFLOP/s", "frac": fma_frac, "traffic": traffic}
     else:
         roof = {"bound": "hbm", "achieved": dk["GB_per_s"], "peak": hbm_peak, "unit": "GB/s",
-                "frac": hbm_frac, "traffic": None}
+                "frac": hbm_frac, "traffic": traffic}
     roof.update({"kernel": dk["engine"], "hbm_GB_per_s": dk["GB_per_s"], "hbm_frac": hbm_frac,
                  "hbm_peak_source": hbm_src, "fma_frac": fma_frac,
                  "fma_peak_source": "tools/pipe_peaks.cu FFMA lane-ops/s x2 (profiles/pipe_peaks_r01.json)",
                  "per_unit": f"{bytes_per_launch / m:.3f} B and {4 * n_edges} flops per test "
-                             f"(n={n_edges} edges, 4 flops per point-edge)"})
+                             f"(n={n_edges} edges, 4 flops per point-edge)",
+                 "algorithmic_bytes_per_launch": bytes_per_launch,
+                 "traffic_source": "profiles/traffic_r01.json (ncu dram__bytes_read+write)",
+                 "issue_model_frac": dk["issue_model_frac"]})
 
     step_s = ms_max * 1e-3 / args.steps
     total_tests = 3 * M

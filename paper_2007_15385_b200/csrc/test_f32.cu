@@ -61,18 +61,22 @@ struct SlabEngine {
     for (uint32_t i = threadIdx.x; i < p.tab.total / 2; i += blockDim.x) s[i] = src[i];
   }
 
-  // Two groups that bound the same coordinate (lo: max-reduced, hi: min-reduced),
-  // consumed in lockstep so each iteration carries 4 edges x P points of work.
-  // Both groups hold >= 1 pair (prep.cu pads), so the first pair seeds lo / hi.
+  // Two groups that bound the coordinate w as a function of the other one, v
+  // (lo: max-reduced, hi: min-reduced), consumed in lockstep so each iteration
+  // carries 4 edges x P points of work. w itself seeds both reductions (a
+  // free third operand of the first FMNMX3; prep.cu guarantees >= 1 pair per
+  // group), so afterwards lo >= w >= hi and the point satisfies the section
+  // iff lo == hi, i.e. hi - lo >= 0.
   __device__ __forceinline__ static void section(const float4* A, uint32_t na, const float4* B,
-                                                 uint32_t nb, const float (&v)[P], float (&lo)[P],
+                                                 uint32_t nb, const float (&v)[P],
+                                                 const float (&w)[P], float (&lo)[P],
                                                  float (&hi)[P]) {
     {
       const float4 a = A[0], b = B[0];
 #pragma unroll
       for (int p = 0; p < P; ++p) {
-        lo[p] = fmaxf(fmaf(a.x, v[p], a.y), fmaf(a.z, v[p], a.w));
-        hi[p] = fminf(fmaf(b.x, v[p], b.y), fmaf(b.z, v[p], b.w));
+        lo[p] = fmax3(w[p], fmaf(a.x, v[p], a.y), fmaf(a.z, v[p], a.w));
+        hi[p] = fmin3(w[p], fmaf(b.x, v[p], b.y), fmaf(b.z, v[p], b.w));
       }
     }
     const uint32_t nc = na < nb ? na : nb;
@@ -97,19 +101,18 @@ struct SlabEngine {
     }
   }
 
-  // slack[p] >= 0 <=> point p is inside: the smallest of x' - max(XLO),
-  // min(XHI) - x', y' - max(YLO), min(YHI) - y' (an exact zero is +0.0).
+  // slack[p] >= 0 <=> point p is inside (every half-plane holds; ties inside)
   __device__ __forceinline__ static void eval(const Params& prm, const float4* s,
                                               const float (&x)[P], const float (&y)[P],
                                               float (&slack)[P]) {
     const SlabTable& t = prm.tab;
     float lo[P], hi[P];
-    section(s + t.off[0] / 2, t.cnt[0] / 2, s + t.off[1] / 2, t.cnt[1] / 2, y, lo, hi);
+    section(s + t.off[0] / 2, t.cnt[0] / 2, s + t.off[1] / 2, t.cnt[1] / 2, y, x, lo, hi);
 #pragma unroll
-    for (int p = 0; p < P; ++p) slack[p] = fminf(x[p] - lo[p], hi[p] - x[p]);
-    section(s + t.off[2] / 2, t.cnt[2] / 2, s + t.off[3] / 2, t.cnt[3] / 2, x, lo, hi);
+    for (int p = 0; p < P; ++p) slack[p] = hi[p] - lo[p];
+    section(s + t.off[2] / 2, t.cnt[2] / 2, s + t.off[3] / 2, t.cnt[3] / 2, x, y, lo, hi);
 #pragma unroll
-    for (int p = 0; p < P; ++p) slack[p] = fmin3(slack[p], y[p] - lo[p], hi[p] - y[p]);
+    for (int p = 0; p < P; ++p) slack[p] = fminf(slack[p], hi[p] - lo[p]);
   }
 };
 

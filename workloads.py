@@ -161,7 +161,5 @@ def c5_point_seed() -> int:
 
 def shard(m: int, rank: int, world: int, align: int = 1024):
     """Contiguous, `align`-aligned point range of one rank (masks concatenate)."""
-    per = -(-m // world)
-    per = -(-per // align) * align
-    lo = min(m, rank * per)
-    return lo, min(m, lo + per)
+    from paper_2007_15385_b200.multi import shard as _shard
+    return _shard(m, rank, world, align)
