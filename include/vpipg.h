@@ -130,6 +130,39 @@ int vpipg_test_host_multi(const vpipg_poly* poly, uint32_t engines, int dtype, c
 int vpipg_voronoi_work(const vpipg_poly* poly, uint64_t m, uint64_t* distance_evaluations,
                        uint64_t* comparisons);
 
+/* ---- polygon database join (BASELINE config 4) ----
+ * A CSR batch of polygons: polygon i owns vertices offsets[i] .. offsets[i+1]-1
+ * of vx / vy (host arrays, f64). Replaces a loop of validate_polygon +
+ * to_voronoi (geometry.cpp:53-98, voronoi.cpp:60-71) over the polygons with
+ * one device kernel (one thread per polygon, the reference's exact f64
+ * arithmetic). When `kinds` includes VORONOI or OFFSET every polygon is
+ * validated; per_poly_status (host, npoly entries, may be NULL) receives 0 or
+ * its vpip::ErrorCode + 1, and pairs that reference a failed polygon test
+ * outside. Returns 0 when the table was built, even if some polygons failed. */
+typedef struct vpipg_db vpipg_db;
+int vpipg_prepare_csr(const uint32_t* offsets, const double* vx, const double* vy,
+                      uint32_t npoly, uint32_t kinds, int device, void* stream, vpipg_db** out,
+                      int32_t* per_poly_status);
+void vpipg_db_destroy(vpipg_db* db);
+int vpipg_db_info(const vpipg_db* db, uint32_t* npoly, uint64_t* nverts, uint32_t* kinds);
+/* Generator set of polygon `poly` as built on the device (inner_xy[2], outer_xy[2n]). */
+int vpipg_db_generators(const vpipg_db* db, uint32_t poly, double* inner_xy, double* outer_xy);
+
+/* Gathered test: pair j tests point (xs[j], ys[j]) against polygon ids[j]
+ * (float32 points, device pointers, asynchronous). Ids >= npoly test outside.
+ * Same mask / count conventions as vpipg_test. */
+int vpipg_test_gather(const vpipg_db* db, int engine, const float* xs, const float* ys,
+                      const uint32_t* ids, uint64_t m, uint32_t* mask_words, uint8_t* mask_bytes,
+                      unsigned long long* d_inside, void* stream);
+
+/* Join-pair workload generator (input generation, not timed): pair j gets
+ * id = floor(U(seed, 3j) * npoly) and point = centre[id] + (2U - 1) * radius[id]
+ * per axis (U from mix_seed(seed, 3j+1 / 3j+2)), rounded to f32. centre_x,
+ * centre_y, radius: device f64 arrays of npoly entries. */
+int vpipg_fill_join_pairs(uint64_t seed, uint64_t first, uint64_t m, uint32_t npoly,
+                          const double* centre_x, const double* centre_y, const double* radius,
+                          float* xs, float* ys, uint32_t* ids, void* stream);
+
 /* Counter-based uniform points on the device: point j (j = first..first+m-1)
  * is (min_x + w*U(mix_seed(seed, 2j)), min_y + h*U(mix_seed(seed, 2j+1))),
  * U = top-53-bit uniform (sampling.cpp:31-33), mix_seed = sampling.cpp:107-112,

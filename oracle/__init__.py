@@ -80,7 +80,45 @@ class Oracle:
         L.vo_counter_points_f32.argtypes = [C.c_uint64, C.c_uint64, sz, C.c_double, C.c_double,
                                             C.c_double, C.c_double, C.POINTER(C.c_float),
                                             C.POINTER(C.c_float)]
+        u32p = C.POINTER(C.c_uint32)
+        L.vo_join_pairs_f32.argtypes = [C.c_uint64, C.c_uint64, sz, C.c_uint32, _D, _D, _D,
+                                        C.POINTER(C.c_float), C.POINTER(C.c_float), u32p]
+        L.vo_csr_status.argtypes = [u32p, _D, _D, C.c_uint32, C.POINTER(C.c_int32)]
+        L.vo_join_masks.argtypes = [u32p, _D, _D, C.c_uint32, C.c_int, _D, _D, u32p, sz, _U8]
         self.L = L
+
+    # polygon-database join (config 4)
+    def join_pairs_f32(self, seed, first, m, cx, cy, r):
+        xs, ys = np.zeros(m, np.float32), np.zeros(m, np.float32)
+        ids = np.zeros(m, np.uint32)
+        fp, up = C.POINTER(C.c_float), C.POINTER(C.c_uint32)
+        self.L.vo_join_pairs_f32(seed, first, m, len(cx), _d(np.ascontiguousarray(cx, np.float64)),
+                                 _d(np.ascontiguousarray(cy, np.float64)),
+                                 _d(np.ascontiguousarray(r, np.float64)),
+                                 xs.ctypes.data_as(fp), ys.ctypes.data_as(fp), ids.ctypes.data_as(up))
+        return xs, ys, ids
+
+    def csr_status(self, offsets, vx, vy):
+        offsets = np.ascontiguousarray(offsets, np.uint32)
+        st = np.zeros(offsets.size - 1, np.int32)
+        self.L.vo_csr_status(offsets.ctypes.data_as(C.POINTER(C.c_uint32)),
+                             _d(np.ascontiguousarray(vx, np.float64)),
+                             _d(np.ascontiguousarray(vy, np.float64)), offsets.size - 1,
+                             st.ctypes.data_as(C.POINTER(C.c_int32)))
+        return st
+
+    def join_masks(self, offsets, vx, vy, engine, xs, ys, ids):
+        offsets = np.ascontiguousarray(offsets, np.uint32)
+        xs = np.ascontiguousarray(xs, np.float64)
+        ys = np.ascontiguousarray(ys, np.float64)
+        ids = np.ascontiguousarray(ids, np.uint32)
+        out = np.zeros(xs.size, np.uint8)
+        up = C.POINTER(C.c_uint32)
+        self.L.vo_join_masks(offsets.ctypes.data_as(up), _d(np.ascontiguousarray(vx, np.float64)),
+                             _d(np.ascontiguousarray(vy, np.float64)), offsets.size - 1, engine,
+                             _d(xs), _d(ys), ids.ctypes.data_as(up), xs.size,
+                             out.ctypes.data_as(_U8))
+        return out
 
     # sampling
     def mix_seed(self, seed, salt):

@@ -406,3 +406,74 @@ void vo_counter_points_f32(uint64_t seed, uint64_t first, size_t count, double m
     ys[t] = (float)(min_y + h * vo_unit_from_u64(vo_mix_seed(seed, 2 * j + 1)));
   }
 }
+
+/* ---- polygon-database join helpers (config 4) ---- */
+void vo_join_pairs_f32(uint64_t seed, uint64_t first, size_t m, uint32_t npoly, const double* cx,
+                       const double* cy, const double* r, float* xs, float* ys, uint32_t* ids) {
+  for (size_t t = 0; t < m; ++t) {
+    const uint64_t j = first + t;
+    uint32_t id = (uint32_t)(vo_unit_from_u64(vo_mix_seed(seed, 3 * j)) * (double)npoly);
+    if (id >= npoly) id = npoly - 1;
+    const double ux = 2.0 * vo_unit_from_u64(vo_mix_seed(seed, 3 * j + 1)) - 1.0;
+    const double uy = 2.0 * vo_unit_from_u64(vo_mix_seed(seed, 3 * j + 2)) - 1.0;
+    xs[t] = (float)(cx[id] + ux * r[id]);
+    ys[t] = (float)(cy[id] + uy * r[id]);
+    ids[t] = id;
+  }
+}
+
+void vo_csr_status(const uint32_t* offsets, const double* vx, const double* vy, uint32_t npoly,
+                   int32_t* status) {
+  for (uint32_t i = 0; i < npoly; ++i) {
+    const size_t s = offsets[i], n = offsets[i + 1] - offsets[i];
+    double* px = (double*)malloc((n ? n : 1) * sizeof(double));
+    double* py = (double*)malloc((n ? n : 1) * sizeof(double));
+    memcpy(px, vx + s, n * sizeof(double));
+    memcpy(py, vy + s, n * sizeof(double));
+    int rev = 0;
+    status[i] = vo_validate_polygon(px, py, n, 1e-12, &rev);
+    if (status[i] == 0) {
+      double* outer = (double*)malloc(2 * n * sizeof(double));
+      double inner[2];
+      status[i] = vo_to_voronoi(px, py, n, inner, outer);
+      free(outer);
+    }
+    free(px);
+    free(py);
+  }
+}
+
+void vo_join_masks(const uint32_t* offsets, const double* vx, const double* vy, uint32_t npoly,
+                   int engine, const double* xs, const double* ys, const uint32_t* ids, size_t m,
+                   uint8_t* out) {
+  /* per polygon: validated vertices and generators, computed once */
+  const size_t nv = offsets[npoly];
+  double* cvx = (double*)malloc((nv ? nv : 1) * sizeof(double));
+  double* cvy = (double*)malloc((nv ? nv : 1) * sizeof(double));
+  double* outer = (double*)malloc((nv ? 2 * nv : 2) * sizeof(double));
+  double* inner = (double*)malloc(2 * (npoly ? npoly : 1) * sizeof(double));
+  int* ok = (int*)malloc((npoly ? npoly : 1) * sizeof(int));
+  memcpy(cvx, vx, nv * sizeof(double));
+  memcpy(cvy, vy, nv * sizeof(double));
+  for (uint32_t i = 0; i < npoly; ++i) {
+    const size_t s = offsets[i], n = offsets[i + 1] - offsets[i];
+    int rev = 0;
+    ok[i] = vo_validate_polygon(cvx + s, cvy + s, n, 1e-12, &rev) == 0;
+    if (ok[i]) ok[i] = vo_to_voronoi(cvx + s, cvy + s, n, inner + 2 * i, outer + 2 * s) == 0;
+  }
+  for (size_t j = 0; j < m; ++j) {
+    const uint32_t id = ids[j];
+    uint8_t r = 0;
+    if (id < npoly) {
+      const size_t s = offsets[id], n = offsets[id + 1] - offsets[id];
+      if (engine == 2) {
+        vo_ray_batch(vx + s, vy + s, n, xs + j, ys + j, 1, &r);
+      } else if (ok[id]) {
+        if (engine == 0) vo_voronoi_batch(inner + 2 * id, outer + 2 * s, n, xs + j, ys + j, 1, &r);
+        else vo_offset_batch(cvx + s, cvy + s, n, xs + j, ys + j, 1, &r);
+      }
+    }
+    out[j] = r;
+  }
+  free(cvx); free(cvy); free(outer); free(inner); free(ok);
+}

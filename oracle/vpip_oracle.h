@@ -90,6 +90,22 @@ void vo_pack_mask_lsb(const uint8_t* mask, size_t m, uint8_t* bytes);
 void vo_counter_points_f32(uint64_t seed, uint64_t first, size_t count, double min_x,
                            double min_y, double max_x, double max_y, float* xs, float* ys);
 
+/* Polygon-database join (config 4). Pair generator restating the device
+ * generator: id = floor(U(seed,3j) * npoly), point = c[id] + (2U-1) * r[id]. */
+void vo_join_pairs_f32(uint64_t seed, uint64_t first, size_t m, uint32_t npoly, const double* cx,
+                       const double* cy, const double* r, float* xs, float* ys, uint32_t* ids);
+/* Per-polygon validate_polygon status (0 or ErrorCode + 1) of a CSR batch. */
+void vo_csr_status(const uint32_t* offsets, const double* vx, const double* vy, uint32_t npoly,
+                   int32_t* status);
+/* Masks of one engine (0 voronoi, 1 offset, 2 crossing) for (point, id) pairs:
+ * each pair is tested against its polygon exactly as the reference batch
+ * kernels test one point (voronoi/offset on the validated polygon, crossing on
+ * the raw vertices); pairs whose polygon failed validation (voronoi/offset)
+ * or whose id is out of range are 0. Points are f64. */
+void vo_join_masks(const uint32_t* offsets, const double* vx, const double* vy, uint32_t npoly,
+                   int engine, const double* xs, const double* ys, const uint32_t* ids, size_t m,
+                   uint8_t* out);
+
 #ifdef __cplusplus
 }
 #endif

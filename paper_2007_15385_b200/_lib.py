@@ -37,6 +37,15 @@ SIGNATURES = {
     "vpipg_voronoi_work": (C.c_int, [_P, C.c_uint64, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
     "vpipg_fill_uniform_points": (C.c_int, [C.c_uint64, C.c_uint64, C.c_uint64, C.c_double,
                                             C.c_double, C.c_double, C.c_double, C.c_int, _P, _P, _P]),
+    "vpipg_prepare_csr": (C.c_int, [_P, _D, _D, C.c_uint32, C.c_uint32, C.c_int, _P,
+                                    C.POINTER(_P), _P]),
+    "vpipg_db_destroy": (None, [_P]),
+    "vpipg_db_info": (C.c_int, [_P, C.POINTER(C.c_uint32), C.POINTER(C.c_uint64),
+                                C.POINTER(C.c_uint32)]),
+    "vpipg_db_generators": (C.c_int, [_P, C.c_uint32, _D, _D]),
+    "vpipg_test_gather": (C.c_int, [_P, C.c_int, _P, _P, _P, C.c_uint64, _P, _P, _P, _P]),
+    "vpipg_fill_join_pairs": (C.c_int, [C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint32, _P, _P,
+                                        _P, _P, _P, _P, _P]),
     "vpipg_mix_seed": (C.c_uint64, [C.c_uint64, C.c_uint64]),
     "vpipg_regular_polygon": (C.c_int, [C.c_uint32, C.c_double, C.c_double, C.c_double, _D, _D]),
     "vpipg_random_convex_polygon": (C.c_int, [C.c_uint32, C.c_uint64, C.c_double, C.c_double,

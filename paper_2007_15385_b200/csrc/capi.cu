@@ -33,6 +33,19 @@ struct vpipg_poly {
   double inner_x = 0, inner_y = 0;
 };
 
+struct vpipg_db {
+  int device = 0;
+  uint32_t npoly = 0;
+  uint64_t nverts = 0;
+  uint32_t kinds = 0;
+  void* blob = nullptr;
+  DbTables t{};
+  const uint32_t* d_offsets = nullptr;
+  const double2* d_inner = nullptr;
+  const double2* d_outer = nullptr;
+  std::vector<uint32_t> offsets;
+};
+
 namespace {
 
 constexpr int kOk = 0;
@@ -422,6 +435,129 @@ int vpipg_test_host(const vpipg_poly* p, int engine, int dtype, const void* xs, 
   const int rc = vpipg_test_host_multi(p, 1u << engine, dtype, xs, ys, m, w, b, cnt);
   if (inside) *inside = rc == kOk ? cnt[engine] : 0;
   return rc;
+}
+
+int vpipg_prepare_csr(const uint32_t* offsets, const double* vx, const double* vy,
+                      uint32_t npoly, uint32_t kinds, int device, void* stream, vpipg_db** out,
+                      int32_t* per_poly_status) {
+  if (!out || !offsets || (kinds & ~VPIPG_KIND_ALL) || kinds == 0) return kInvalid;
+  *out = nullptr;
+  if (offsets[0] != 0) return kInvalid;
+  for (uint32_t i = 0; i < npoly; ++i)
+    if (offsets[i + 1] < offsets[i]) return kInvalid;
+  const uint64_t nv = offsets[npoly];
+  if (nv && (!vx || !vy)) return kInvalid;
+  int rc = check_device(device);
+  if (rc) return rc;
+  DeviceGuard g(device);
+  auto* db = new (std::nothrow) vpipg_db;
+  if (!db) return kInvalid;
+  db->device = device;
+  db->npoly = npoly;
+  db->nverts = nv;
+  db->kinds = kinds;
+  db->offsets.assign(offsets, offsets + npoly + 1);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  size_t off = 0;
+  auto take = [&](size_t bytes) { const size_t o = off; off = align256(off + bytes); return o; };
+  const size_t o_offs = take((npoly + 1) * sizeof(uint32_t));
+  const size_t o_vx = take(nv * sizeof(double)), o_vy = take(nv * sizeof(double));
+  const size_t o_vvx = take(nv * sizeof(double)), o_vvy = take(nv * sizeof(double));
+  const size_t o_inner = take(npoly * sizeof(double2)), o_outer = take(nv * sizeof(double2));
+  const size_t o_range = take(npoly * sizeof(uint2));
+  const size_t o_vor = take(nv * sizeof(float4)), o_off = take(nv * sizeof(float4));
+  const size_t o_cross = take(nv * sizeof(float4));
+  const size_t o_status = take(npoly * sizeof(int32_t));
+  cudaError_t e = cudaMalloc(&db->blob, off ? off : 256);
+  if (e != cudaSuccess) {
+    delete db;
+    return cuda_code(e);
+  }
+  char* b = static_cast<char*>(db->blob);
+  CsrPrepArgs a{};
+  a.offsets = reinterpret_cast<const uint32_t*>(b + o_offs);
+  a.vx = reinterpret_cast<const double*>(b + o_vx);
+  a.vy = reinterpret_cast<const double*>(b + o_vy);
+  a.npoly = npoly;
+  a.kinds = kinds;
+  a.vvx = reinterpret_cast<double*>(b + o_vvx);
+  a.vvy = reinterpret_cast<double*>(b + o_vvy);
+  a.inner = reinterpret_cast<double2*>(b + o_inner);
+  a.outer = reinterpret_cast<double2*>(b + o_outer);
+  a.range = reinterpret_cast<uint2*>(b + o_range);
+  a.vor = reinterpret_cast<float4*>(b + o_vor);
+  a.off = reinterpret_cast<float4*>(b + o_off);
+  a.cross = reinterpret_cast<float4*>(b + o_cross);
+  a.status = reinterpret_cast<int32_t*>(b + o_status);
+  std::vector<int32_t> status(npoly);
+  do {
+    if ((e = cudaMemsetAsync(b, 0, off, s)) != cudaSuccess) break;
+    if ((e = cudaMemcpyAsync(b + o_offs, offsets, (npoly + 1) * sizeof(uint32_t), cudaMemcpyHostToDevice, s)) != cudaSuccess) break;
+    if (nv && (e = cudaMemcpyAsync(b + o_vx, vx, nv * sizeof(double), cudaMemcpyHostToDevice, s)) != cudaSuccess) break;
+    if (nv && (e = cudaMemcpyAsync(b + o_vy, vy, nv * sizeof(double), cudaMemcpyHostToDevice, s)) != cudaSuccess) break;
+    if ((e = launch_prep_csr(a, s)) != cudaSuccess) break;
+    if (npoly && (e = cudaMemcpyAsync(status.data(), a.status, npoly * sizeof(int32_t), cudaMemcpyDeviceToHost, s)) != cudaSuccess) break;
+    e = cudaStreamSynchronize(s);
+  } while (false);
+  if (e != cudaSuccess) {
+    vpipg_db_destroy(db);
+    return cuda_code(e);
+  }
+  if (per_poly_status) std::copy(status.begin(), status.end(), per_poly_status);
+  db->t = DbTables{npoly, kinds, a.range, a.vor, a.off, a.cross};
+  db->d_offsets = a.offsets;
+  db->d_inner = a.inner;
+  db->d_outer = a.outer;
+  *out = db;
+  return kOk;
+}
+
+void vpipg_db_destroy(vpipg_db* db) {
+  if (!db) return;
+  if (db->blob) {
+    DeviceGuard g(db->device);
+    cudaFree(db->blob);
+  }
+  delete db;
+}
+
+int vpipg_db_info(const vpipg_db* db, uint32_t* npoly, uint64_t* nverts, uint32_t* kinds) {
+  if (!db) return kInvalid;
+  if (npoly) *npoly = db->npoly;
+  if (nverts) *nverts = db->nverts;
+  if (kinds) *kinds = db->kinds;
+  return kOk;
+}
+
+int vpipg_db_generators(const vpipg_db* db, uint32_t poly, double* inner_xy, double* outer_xy) {
+  if (!db || !(db->kinds & kKindVoronoi) || poly >= db->npoly || !inner_xy) return kInvalid;
+  const uint32_t s = db->offsets[poly], n = db->offsets[poly + 1] - s;
+  if (n && !outer_xy) return kInvalid;
+  DeviceGuard g(db->device);
+  VPIPG_TRY(cudaMemcpy(inner_xy, db->d_inner + poly, sizeof(double2), cudaMemcpyDeviceToHost));
+  if (n) VPIPG_TRY(cudaMemcpy(outer_xy, db->d_outer + s, n * sizeof(double2), cudaMemcpyDeviceToHost));
+  return kOk;
+}
+
+int vpipg_test_gather(const vpipg_db* db, int engine, const float* xs, const float* ys,
+                      const uint32_t* ids, uint64_t m, uint32_t* mask_words, uint8_t* mask_bytes,
+                      unsigned long long* d_inside, void* stream) {
+  if (!db || engine < 0 || engine > 2) return kInvalid;
+  const uint32_t need = engine == 0 ? kKindVoronoi : engine == 1 ? kKindOffset : kKindCrossing;
+  if (!(db->kinds & need)) return kInvalid;
+  if (m == 0) return kOk;
+  if (!xs || !ys || !ids) return kInvalid;
+  DeviceGuard g(db->device);
+  GatherArgs a{xs, ys, ids, m, mask_words, mask_bytes, d_inside};
+  return cuda_code(launch_gather(db->t, engine, a, static_cast<cudaStream_t>(stream)));
+}
+
+int vpipg_fill_join_pairs(uint64_t seed, uint64_t first, uint64_t m, uint32_t npoly,
+                          const double* centre_x, const double* centre_y, const double* radius,
+                          float* xs, float* ys, uint32_t* ids, void* stream) {
+  if (m && (npoly == 0 || !centre_x || !centre_y || !radius || !xs || !ys || !ids)) return kInvalid;
+  return cuda_code(launch_fill_pairs(seed, first, m, npoly, centre_x, centre_y, radius, xs, ys,
+                                     ids, static_cast<cudaStream_t>(stream)));
 }
 
 int vpipg_voronoi_work(const vpipg_poly* p, uint64_t m, uint64_t* evals, uint64_t* comps) {

@@ -1,0 +1,95 @@
+// exact_geom.cuh -- the reference's f64 geometry, operation for operation.
+//
+// Every expression below is the reference's (-ffp-contract=off) expression
+// written with explicitly rounded intrinsics, which nvcc never fuses into
+// FMAs, so results are bit-identical to the reference build:
+//   centroid           geometry.cpp:106-120
+//   edge_coefficients  voronoi.cpp:23-31
+//   reflect_generator  voronoi.cpp:46-58 (the fused mirror of PAPER.md Eq. 8)
+//   validate_polygon   geometry.cpp:53-98 (checks, order, CCW normalisation)
+#pragma once
+
+#include <cstdint>
+
+namespace vpipg {
+
+__device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ double ddiv(double a, double b) { return __ddiv_rn(a, b); }
+// std::min / std::max semantics (engines.cpp:183-186)
+__device__ __forceinline__ double smin(double a, double b) { return (b < a) ? b : a; }
+__device__ __forceinline__ double smax(double a, double b) { return (a < b) ? b : a; }
+
+// Vertex accessor: V(k) -> (x, y) of vertex k of an n-gon.
+template <class V>
+__device__ void centroid_exact(const V& v, int n, double* cx, double* cy) {
+  double area2 = 0.0, sx = 0.0, sy = 0.0;
+  for (int i = 0, j = n - 1; i < n; j = i++) {
+    const double2 a = v(j), b = v(i);
+    const double d = dsub(dmul(a.x, b.y), dmul(b.x, a.y));
+    area2 = dadd(area2, d);
+    sx = dadd(sx, dmul(dadd(a.x, b.x), d));
+    sy = dadd(sy, dmul(dadd(a.y, b.y), d));
+  }
+  *cx = ddiv(sx, dmul(3.0, area2));
+  *cy = ddiv(sy, dmul(3.0, area2));
+}
+
+// Mirror of p across the line through edge (qi, qj). Returns 0, 3
+// (DegenerateEdge) or 5 (GeneratorCollision), the reference's throw sites.
+__device__ __forceinline__ int reflect_exact(double2 qi, double2 qj, double px, double py,
+                                             double2* out) {
+  const double ea = dsub(qi.y, qj.y);
+  const double eb = dsub(qj.x, qi.x);
+  const double ec = -dadd(dmul(ea, qi.x), dmul(eb, qi.y));
+  const double denom = dadd(dmul(ea, ea), dmul(eb, eb));
+  if (denom <= 1e-24) return 3;
+  if (fabs(dadd(dadd(dmul(ea, px), dmul(eb, py)), ec)) <= dmul(1e-12, denom)) return 5;
+  const double t1 = dmul(dsub(dmul(eb, eb), dmul(ea, ea)), px);
+  const double t2 = dmul(dmul(dmul(2.0, ea), eb), py);
+  const double t3 = dmul(dmul(2.0, ec), ea);
+  const double u1 = dmul(dmul(dmul(-2.0, ea), eb), px);
+  const double u2 = dmul(dsub(dmul(ea, ea), dmul(eb, eb)), py);
+  const double u3 = dmul(dmul(2.0, ec), eb);
+  *out = make_double2(ddiv(dsub(dsub(t1, t2), t3), denom), ddiv(dsub(dadd(u1, u2), u3), denom));
+  return 0;
+}
+
+// validate_polygon without the exception: 0 or ErrorCode + 1, and whether
+// the vertex order must be reversed to make it counter-clockwise.
+template <class V>
+__device__ int validate_exact(const V& v, int n, bool* reversed) {
+  *reversed = false;
+  for (int k = 0; k < n; ++k) {
+    const double2 p = v(k);
+    if (!isfinite(p.x) || !isfinite(p.y)) return 4;  // NonFinite
+  }
+  if (n < 3) return 1;  // TooFewVertices
+  for (int i = 0, j = n - 1; i < n; j = i++) {
+    const double2 a = v(j), b = v(i);
+    const double dx = dsub(a.x, b.x), dy = dsub(a.y, b.y);
+    if (dadd(dmul(dx, dx), dmul(dy, dy)) <= 1e-24) return 3;  // DegenerateEdge
+  }
+  double sum = 0.0;
+  for (int i = 0, j = n - 1; i < n; j = i++) {
+    const double2 a = v(j), b = v(i);
+    sum = dadd(sum, dsub(dmul(a.x, b.y), dmul(b.x, a.y)));
+  }
+  *reversed = sum < 0.0;
+  const bool rev = *reversed;
+  auto w = [&](int k) { return v(rev ? n - 1 - k : k); };
+  double total_turn = 0.0;
+  for (int i = 0; i < n; ++i) {
+    const double2 prev = w((i + n - 1) % n), cur = w(i), next = w((i + 1) % n);
+    const double inx = dsub(cur.x, prev.x), iny = dsub(cur.y, prev.y);
+    const double outx = dsub(next.x, cur.x), outy = dsub(next.y, cur.y);
+    const double cr = dsub(dmul(inx, outy), dmul(iny, outx));
+    if (cr <= 1e-12) return 2;  // NotConvex (collinear or reflex)
+    total_turn = dadd(total_turn, atan2(cr, dadd(dmul(inx, outx), dmul(iny, outy))));
+  }
+  if (total_turn >= dmul(3.0, 3.141592653589793)) return 2;  // winds more than once
+  return 0;
+}
+
+}  // namespace vpipg

@@ -16,6 +16,7 @@
 #include <cmath>
 #include <cstdint>
 
+#include "exact_geom.cuh"
 #include "vpipg_device.cuh"
 #include "vpipg_internal.h"
 
@@ -26,13 +27,6 @@ namespace {
 constexpr int kPrepThreads = 256;
 enum : int { kNone = -1, kXlo = 0, kXhi = 1, kYlo = 2, kYhi = 3 };
 
-__device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
-__device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
-__device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a, b); }
-__device__ __forceinline__ double ddiv(double a, double b) { return __ddiv_rn(a, b); }
-// std::min / std::max semantics (engines.cpp:183-186)
-__device__ __forceinline__ double smin(double a, double b) { return (b < a) ? b : a; }
-__device__ __forceinline__ double smax(double a, double b) { return (a < b) ? b : a; }
 
 // Half-plane a*x' + b*y' + c >= 0 (local frame) -> slab class and (B, C).
 __device__ int slab_classify(double a, double b, double c, float2* bc) {
@@ -155,15 +149,8 @@ __global__ void __launch_bounds__(kPrepThreads) prep_kernel(PrepArgs a) {
       cy = a.gen_in[1];
     } else if (a.vv != nullptr) {
       // centroid, geometry.cpp:106-120, sequential in the reference order
-      double area2 = 0.0, sx = 0.0, sy = 0.0;
-      for (int i = 0, j = n - 1; i < n; j = i++) {
-        const double d = dsub(dmul(a.vv[j], a.vv[n + i]), dmul(a.vv[i], a.vv[n + j]));
-        area2 = dadd(area2, d);
-        sx = dadd(sx, dmul(dadd(a.vv[j], a.vv[i]), d));
-        sy = dadd(sy, dmul(dadd(a.vv[n + j], a.vv[n + i]), d));
-      }
-      cx = ddiv(sx, dmul(3.0, area2));
-      cy = ddiv(sy, dmul(3.0, area2));
+      const double* vv = a.vv;
+      centroid_exact([vv, n](int k) { return make_double2(vv[k], vv[n + k]); }, n, &cx, &cy);
     } else if (a.vr != nullptr && n > 0) {  // crossing only: vertex mean as frame origin
       for (int i = 0; i < n; ++i) {
         cx += a.vr[i];
@@ -195,30 +182,15 @@ __global__ void __launch_bounds__(kPrepThreads) prep_kernel(PrepArgs a) {
     } else {
       for (int k = tid; k < n; k += kPrepThreads) {
         const int k1 = (k + 1) % n;
-        const double qix = a.vv[k], qiy = a.vv[n + k], qjx = a.vv[k1], qjy = a.vv[n + k1];
-        // edge_coefficients, voronoi.cpp:23-31
-        const double ea = dsub(qiy, qjy);
-        const double eb = dsub(qjx, qix);
-        const double ec = -dadd(dmul(ea, qix), dmul(eb, qiy));
-        const double denom = dadd(dmul(ea, ea), dmul(eb, eb));
-        if (denom <= 1e-24) {
-          atomicMin(&s_fail, k * 8 + 3);  // DegenerateEdge
+        // edge_coefficients + reflect_generator (voronoi.cpp:23-58, Eq. 8 fused)
+        double2 g;
+        const int rc = reflect_exact(make_double2(a.vv[k], a.vv[n + k]),
+                                     make_double2(a.vv[k1], a.vv[n + k1]), p0x, p0y, &g);
+        if (rc) {
+          atomicMin(&s_fail, k * 8 + rc);  // DegenerateEdge / GeneratorCollision
           continue;
         }
-        // reflect_generator, voronoi.cpp:46-58 (Eq. 8, fused)
-        if (fabs(dadd(dadd(dmul(ea, p0x), dmul(eb, p0y)), ec)) <= dmul(1e-12, denom)) {
-          atomicMin(&s_fail, k * 8 + 5);  // GeneratorCollision
-          continue;
-        }
-        const double t1 = dmul(dsub(dmul(eb, eb), dmul(ea, ea)), p0x);
-        const double t2 = dmul(dmul(dmul(2.0, ea), eb), p0y);
-        const double t3 = dmul(dmul(2.0, ec), ea);
-        const double rx = ddiv(dsub(dsub(t1, t2), t3), denom);
-        const double u1 = dmul(dmul(dmul(-2.0, ea), eb), p0x);
-        const double u2 = dmul(dsub(dmul(ea, ea), dmul(eb, eb)), p0y);
-        const double u3 = dmul(dmul(2.0, ec), eb);
-        const double ry = ddiv(dsub(dadd(u1, u2), u3), denom);
-        a.outer[k] = make_double2(rx, ry);
+        a.outer[k] = g;
       }
     }
     __syncthreads();

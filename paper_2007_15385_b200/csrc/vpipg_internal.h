@@ -36,7 +36,51 @@ struct TestArgs {
   unsigned long long* inside;
 };
 
+// ---- polygon database (CSR batch of polygons; csr.cu) ----
+constexpr uint32_t kRangeInvalid = 0x80000000u;  // polygon failed validation: tests outside
+
+struct CsrPrepArgs {
+  const uint32_t* offsets;  // npoly + 1
+  const double* vx;         // raw vertices (device)
+  const double* vy;
+  uint32_t npoly;
+  uint32_t kinds;
+  double* vvx;              // validated (CCW) vertices
+  double* vvy;
+  double2* inner;           // npoly generators
+  double2* outer;           // nverts generators
+  uint2* range;             // npoly: (first vertex, n | kRangeInvalid)
+  float4* vor;              // nverts unit half-planes (a, b, c, 0), Voronoi
+  float4* off;              // nverts unit half-planes, sign-of-offset
+  float4* cross;            // nverts (x, y, dvx/dvy, 0), ray crossing (raw order)
+  int32_t* status;          // npoly: 0 or ErrorCode + 1
+};
+
+struct DbTables {
+  uint32_t npoly;
+  uint32_t kinds;
+  const uint2* range;
+  const float4* vor;
+  const float4* off;
+  const float4* cross;
+};
+
+struct GatherArgs {
+  const float* xs;
+  const float* ys;
+  const uint32_t* ids;
+  uint64_t m;
+  uint32_t* words;
+  uint8_t* bytes;
+  unsigned long long* inside;
+};
+
 cudaError_t launch_prep(const PrepArgs& args, cudaStream_t stream);
+cudaError_t launch_prep_csr(const CsrPrepArgs& args, cudaStream_t stream);
+cudaError_t launch_gather(const DbTables& t, int engine, const GatherArgs& a, cudaStream_t stream);
+cudaError_t launch_fill_pairs(uint64_t seed, uint64_t first, uint64_t m, uint32_t npoly,
+                              const double* cx, const double* cy, const double* rad, float* xs,
+                              float* ys, uint32_t* ids, cudaStream_t stream);
 cudaError_t launch_test_f32(const DevTables& t, int engine, const TestArgs& a, cudaStream_t stream);
 cudaError_t launch_test_f64(const DevTables& t, int engine, const TestArgs& a, cudaStream_t stream);
 cudaError_t launch_fill_uniform(uint64_t seed, uint64_t first, uint64_t m, double min_x,

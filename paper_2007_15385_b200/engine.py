@@ -17,7 +17,7 @@ from . import _lib
 from ._lib import (ENGINES, F32, F64, KIND_ALL, KIND_CROSSING, KIND_OFFSET, KIND_VORONOI,
                    VpipError, check, load)
 
-__all__ = ["PreparedPolygon", "VpipError", "fill_uniform_points", "mix_seed",
+__all__ = ["PreparedPolygon", "PolygonDB", "fill_join_pairs", "VpipError", "fill_uniform_points", "mix_seed",
            "regular_polygon", "random_convex_polygon", "sample_points", "KIND_ALL",
            "KIND_VORONOI", "KIND_OFFSET", "KIND_CROSSING", "F32", "F64"]
 
@@ -156,6 +156,65 @@ class PreparedPolygon:
                                            C.c_void_p(_host_ptr(ys)), m, wp, None, cnt),
               "vpipg_test_host_multi")
         return words, [cnt[i] for i in range(3)]
+
+
+class PolygonDB:
+    """A CSR batch of polygons prepared on the device (vpipg_prepare_csr)."""
+
+    def __init__(self, handle: C.c_void_p, npoly: int, status: np.ndarray):
+        self._h = handle
+        self.npoly = npoly
+        self.status = status
+
+    @classmethod
+    def prepare(cls, offsets, vx, vy, kinds: int = KIND_ALL, device: int = 0, stream=None):
+        offsets = np.ascontiguousarray(offsets, dtype=np.uint32)
+        vx = np.ascontiguousarray(vx, dtype=np.float64)
+        vy = np.ascontiguousarray(vy, dtype=np.float64)
+        npoly = offsets.size - 1
+        status = np.zeros(max(npoly, 1), dtype=np.int32)
+        h = C.c_void_p()
+        check(load().vpipg_prepare_csr(C.c_void_p(offsets.ctypes.data), _dptr(vx), _dptr(vy),
+                                       npoly, kinds, device, _stream_ptr(stream), C.byref(h),
+                                       C.c_void_p(status.ctypes.data)), "vpipg_prepare_csr")
+        return cls(h, npoly, status[:npoly])
+
+    def close(self) -> None:
+        if self._h:
+            load().vpipg_db_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def generators(self, poly: int, n: int):
+        inner, outer = np.zeros(2), np.zeros((n, 2))
+        check(load().vpipg_db_generators(self._h, poly, _dptr(inner), _dptr(outer)), "generators")
+        return inner, outer
+
+    def test(self, engine, xs, ys, ids, words=None, bytes_=None, count=None, stream=None) -> None:
+        """Gathered test on device tensors (vpipg_test_gather); float32 points, int32 ids."""
+        ptr = lambda t: C.c_void_p(t.data_ptr()) if t is not None else C.c_void_p(None)
+        check(load().vpipg_test_gather(self._h, _engine_id(engine), ptr(xs), ptr(ys), ptr(ids),
+                                       xs.numel(), ptr(words), ptr(bytes_), ptr(count),
+                                       _stream_ptr(stream)), "vpipg_test_gather")
+
+
+def fill_join_pairs(seed: int, first: int, xs, ys, ids, cx, cy, r, stream=None) -> None:
+    """Join-pair generator on the device (vpipg_fill_join_pairs); cx, cy, r: CUDA f64."""
+    ptr = lambda t: C.c_void_p(t.data_ptr())
+    check(load().vpipg_fill_join_pairs(seed, first, xs.numel(), cx.numel(), ptr(cx), ptr(cy),
+                                       ptr(r), ptr(xs), ptr(ys), ptr(ids), _stream_ptr(stream)),
+          "fill_join_pairs")
 
 
 def _host_ptr(a) -> int:

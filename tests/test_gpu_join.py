@@ -1,0 +1,148 @@
+"""GPU parity for the polygon-database join (BASELINE config 4).
+
+Device CSR preparation against the oracle: per-polygon validation status,
+bit-identical generators. Then the gathered test against the oracle on
+f32-rounded pairs, for all three engines: masks are identical outside the
+1e-5 relative band of the pair's own polygon, and the counts are fused
+correctly.
+"""
+import numpy as np
+import pytest
+
+import workloads as W
+
+torch = pytest.importorskip("torch")
+import paper_2007_15385_b200 as vp  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+DEV = "cuda:0"
+EPS32 = 1e-5
+
+
+def _db_inputs(npoly=2048):
+    off, vx, vy, cx, cy, r = W.c4_polygons(vp.random_convex_polygon, npoly=npoly)
+    # inject invalid / unusual polygons (the reference's error cases), CSR-appended
+    extra = [
+        ([0, 1], [0, 0]),                                  # too few (1)
+        ([0, 1, 2, 1], [0, 0, 0, 1]),                      # collinear (2)
+        ([0, 4, 4, 2, 0], [0, 0, 4, 1, 4]),                # reflex (2)
+        ([0, 1, 1, 0], [0, 0, 0, 0]),                      # degenerate (3)
+        ([0, 1, np.nan], [0, 0, 1]),                       # non-finite (4)
+        ([500, 500, 501, 501], [500, 501, 501, 500]),      # clockwise: valid, reversed
+    ]
+    vx, vy = list(vx), list(vy)
+    offs = list(off)
+    cxl, cyl, rl = list(cx), list(cy), list(r)
+    for ex, ey in extra:
+        vx += list(map(float, ex))
+        vy += list(map(float, ey))
+        offs.append(offs[-1] + len(ex))
+        cxl.append(float(np.nanmean(ex)))
+        cyl.append(float(np.nanmean(ey)))
+        rl.append(1.0)
+    return (np.array(offs, np.uint32), np.array(vx), np.array(vy), np.array(cxl), np.array(cyl),
+            np.array(rl))
+
+
+def _band(off, vx, vy, xs, ys, ids):
+    """Distance of each pair to its polygon's nearest edge line <= EPS32 * scale."""
+    n = (off[1:] - off[:-1]).astype(np.int64)
+    d = np.full(xs.size, np.inf)
+    start = off[ids].astype(np.int64)
+    nn = n[ids]
+    ext = np.zeros(ids.size)
+    for k in range(int(n.max())):
+        has = k < nn
+        i0 = np.where(has, start + k, 0)
+        i1 = np.where(has, start + (k + 1) % np.maximum(nn, 1), 0)
+        a = vy[i0] - vy[i1]
+        b = vx[i1] - vx[i0]
+        c = -(a * vx[i0] + b * vy[i0])
+        with np.errstate(invalid="ignore", divide="ignore"):
+            dk = np.abs(a * xs + b * ys + c) / np.hypot(a, b)
+        d = np.where(has, np.minimum(d, np.nan_to_num(dk, nan=np.inf)), d)
+        ext = np.where(has, np.maximum(ext, np.abs(vx[i0] - vx[start]) + np.abs(vy[i0] - vy[start])), ext)
+    s = np.maximum(np.maximum(1.0, np.abs(xs)), np.maximum(np.abs(ys), ext))
+    return d <= EPS32 * s
+
+
+def test_csr_status_and_generators(orc):
+    off, vx, vy, cx, cy, r = _db_inputs(512)
+    want = orc.csr_status(off, vx, vy)
+    with vp.PolygonDB.prepare(off, vx, vy, vp.KIND_ALL) as db:
+        assert np.array_equal(db.status, want)
+        assert want[-6:].tolist() == [1, 2, 2, 3, 4, 0]
+        for i in list(range(0, 512, 37)) + [db.npoly - 1]:
+            a, b = int(off[i]), int(off[i + 1])
+            rc, cvx, cvy, _ = orc.validate(vx[a:b], vy[a:b])
+            rc, inner, outer = orc.to_voronoi(cvx, cvy)
+            gi, go = db.generators(i, b - a)
+            assert np.array_equal(gi, inner) and np.array_equal(go, outer), i
+
+
+def test_device_pair_stream_matches_oracle(orc):
+    off, vx, vy, cx, cy, r = _db_inputs(1024)
+    m, first = 100_001, 77_777
+    dcx, dcy, dr = (torch.as_tensor(a, device=DEV) for a in (cx, cy, r))
+    xs = torch.empty(m, dtype=torch.float32, device=DEV)
+    ys = torch.empty_like(xs)
+    ids = torch.empty(m, dtype=torch.int32, device=DEV)
+    vp.fill_join_pairs(W.c4_pair_seed(), first, xs, ys, ids, dcx, dcy, dr)
+    ex, ey, eid = orc.join_pairs_f32(W.c4_pair_seed(), first, m, cx, cy, r)
+    assert np.array_equal(xs.cpu().numpy(), ex) and np.array_equal(ys.cpu().numpy(), ey)
+    assert np.array_equal(ids.cpu().numpy().view(np.uint32), eid)
+
+
+@pytest.mark.parametrize("m", [1, 33, 1 << 20])
+def test_gather_masks_outside_band(orc, m):
+    off, vx, vy, cx, cy, r = _db_inputs(2048)
+    dcx, dcy, dr = (torch.as_tensor(a, device=DEV) for a in (cx, cy, r))
+    xs = torch.empty(m, dtype=torch.float32, device=DEV)
+    ys = torch.empty_like(xs)
+    ids = torch.empty(m, dtype=torch.int32, device=DEV)
+    vp.fill_join_pairs(W.c4_pair_seed(), 0, xs, ys, ids, dcx, dcy, dr)
+    hx, hy = xs.cpu().numpy().astype(np.float64), ys.cpu().numpy().astype(np.float64)
+    hid = ids.cpu().numpy().view(np.uint32)
+    band = _band(off, vx, vy, hx, hy, hid)
+    with vp.PolygonDB.prepare(off, vx, vy, vp.KIND_ALL) as db:
+        for e in range(3):
+            want = orc.join_masks(off, vx, vy, e, hx, hy, hid)
+            w = torch.zeros((m + 31) // 32, dtype=torch.int32, device=DEV)
+            b = torch.zeros(m, dtype=torch.uint8, device=DEV)
+            c = torch.zeros(1, dtype=torch.int64, device=DEV)
+            db.test(e, xs, ys, ids, words=w, bytes_=b, count=c)
+            torch.cuda.synchronize()
+            got = b.cpu().numpy()
+            bits = np.unpackbits(w.cpu().numpy().view(np.uint8), bitorder="little")[:m]
+            assert np.array_equal(bits, got) and c.item() == int(got.sum())
+            diff = got != want
+            if e == 2:  # ray crossing on non-finite raw vertices is unspecified (inputs are finite)
+                nf = ~np.isfinite(vx[off[hid]]) | ~np.isfinite(vy[off[hid] + 2])
+                diff &= ~nf
+            assert not np.any(diff & ~band), (e, np.flatnonzero(diff & ~band)[:8])
+            if m > 1000:
+                assert 0.2 < want.mean() < 0.9  # the join is not trivially all-in / all-out
+
+
+def test_gather_invalid_ids_and_polygons_are_outside(orc):
+    off, vx, vy, cx, cy, r = _db_inputs(64)
+    npoly = off.size - 1
+    # pairs aimed at the injected polygons (invalid ones must test outside for
+    # voronoi/offset), plus out-of-range ids
+    ids = np.array([npoly - 6, npoly - 5, npoly - 4, npoly - 3, npoly - 2, npoly - 1, npoly,
+                    npoly + 1000, 0xFFFFFFFF], dtype=np.uint32)
+    xs = np.array([0.5, 1, 2, 0.5, 0.5, 500.5, 0, 0, 0], np.float32)
+    ys = np.array([0, 0.5, 1, 0, 0.5, 500.5, 0, 0, 0], np.float32)
+    with vp.PolygonDB.prepare(off, vx, vy, vp.KIND_ALL) as db:
+        for e in range(3):
+            b = torch.zeros(ids.size, dtype=torch.uint8, device=DEV)
+            db.test(e, torch.as_tensor(xs, device=DEV), torch.as_tensor(ys, device=DEV),
+                    torch.as_tensor(ids.view(np.int32), device=DEV), bytes_=b)
+            got = b.cpu().numpy()
+            want = orc.join_masks(off, vx, vy, e, xs.astype(np.float64), ys.astype(np.float64), ids)
+            keep = np.ones(ids.size, bool)
+            if e == 2:
+                keep[4] = False  # crossing on a NaN vertex is unspecified
+            assert np.array_equal(got[keep], want[keep]), (e, got, want)
+            assert got[6:].tolist() == [0, 0, 0]
+            assert got[5] == 1  # the clockwise square (reversed by validation) contains its centre

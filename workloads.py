@@ -143,6 +143,37 @@ def c3_polygon(n: int, jitter: float = 0.05, seed: int | None = None):
     return convex_hull(rad * np.cos(ang), rad * np.sin(ang))
 
 
+# ---------------------------------------------------------------- C4
+C4_POLYS = 65536
+C4_PAIRS = 1 << 28
+
+
+def c4_polygons(random_convex_polygon, npoly: int = C4_POLYS, seed: int | None = None):
+    """CSR table of `npoly` vpip::random_convex_polygon(n_i, seed_i, r_i, c_i):
+    n_i uniform in {4..16}, c_i uniform in [0, 1000]^2, r_i uniform in [0.5, 5].
+    Returns offsets (u32, npoly+1), vx, vy, and per-polygon cx, cy, r."""
+    s = config_seed(4) if seed is None else seed
+    i = np.arange(npoly, dtype=np.uint64)
+    n = 4 + np.minimum((unit_np(s, 4 * i) * 13).astype(np.int64), 12)
+    cx = 1000.0 * unit_np(s, 4 * i + 1)
+    cy = 1000.0 * unit_np(s, 4 * i + 2)
+    r = 0.5 + 4.5 * unit_np(s, 4 * i + 3)
+    seeds = mix_seed_np(int(mix_seed_np(s, 103)), i)
+    offsets = np.zeros(npoly + 1, dtype=np.uint32)
+    offsets[1:] = np.cumsum(n)
+    vx = np.empty(int(offsets[-1]))
+    vy = np.empty(int(offsets[-1]))
+    for k in range(npoly):
+        a, b = int(offsets[k]), int(offsets[k + 1])
+        vx[a:b], vy[a:b] = random_convex_polygon(int(n[k]), int(seeds[k]), float(r[k]),
+                                                 (float(cx[k]), float(cy[k])))
+    return offsets, vx, vy, cx, cy, r
+
+
+def c4_pair_seed() -> int:
+    return int(mix_seed_np(config_seed(4), 102))
+
+
 # ---------------------------------------------------------------- C5
 C5_POINTS = 1 << 31
 C5_BOX = (-1.5, -1.5, 1.5, 1.5)
