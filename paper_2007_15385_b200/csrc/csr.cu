@@ -86,7 +86,8 @@ __global__ void prep_csr_kernel(CsrPrepArgs a) {
     }
   }
   a.status[i] = status;
-  // crossing alone accepts any polygon; otherwise a failed polygon tests outside
+  // a failed polygon tests outside under Voronoi / sign-of-offset (crossing
+  // ignores the flag: it accepts any polygon)
   const bool bad = convex && status != 0;
   a.range[i] = make_uint2(s, static_cast<uint32_t>(n) | (bad ? kRangeInvalid : 0u));
 }
@@ -115,7 +116,9 @@ __global__ void __launch_bounds__(kGThreads) gather_kernel(const DbTables t, con
       y[p] = ok[p] ? __ldcs(a.ys + j) : 0.f;
       ok[p] = ok[p] && id < t.npoly;
       const uint2 r = ok[p] ? __ldg(t.range + id) : make_uint2(0u, 0u);
-      ok[p] = ok[p] && !(r.y & kRangeInvalid);
+      // a polygon that failed validation only disables the convex engines: ray
+      // crossing takes the raw vertices of any polygon (vpip.cpp:120-128)
+      if (kEngine != 2) ok[p] = ok[p] && !(r.y & kRangeInvalid);
       start[p] = r.x;
       n[p] = ok[p] ? (r.y & ~kRangeInvalid) : 0u;
       nmax = n[p] > nmax ? n[p] : nmax;
