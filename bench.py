@@ -163,15 +163,17 @@ def build_workload(name: str, lo: int, hi: int, torch, vp, stream):
 
 
 def workload_size(name: str) -> int:
-    return {"c5": W.C5_POINTS, "c2": W.C2_CLUSTERS * W.C2_PER_CLUSTER, "c1": W.C1_POINTS}.get(
-        name.split(":")[0], W.C3_POINTS)
+    return {"c5": W.C5_POINTS, "c2": W.C2_CLUSTERS * W.C2_PER_CLUSTER, "c1": W.C1_POINTS,
+            "c4": W.C4_PAIRS}.get(name.split(":")[0], W.C3_POINTS)
 
 
 def workload_desc(name: str) -> str:
     return {"c5": "C5 multi-GPU scaling: random convex 32-gon, 2^31 f32 points U[-1.5,1.5]^2, "
                   "3 engines + NCCL all-reduce of inside counts",
             "c2": "C2 vehicle footprint 12-gon, 2^24 f32 lidar-like clustered points",
-            "c1": "C1 random 8-angle hull, 2^20 points (f32 copy of the f64 oracle config)"}.get(
+            "c1": "C1 random 8-angle hull, 2^20 points (f32 copy of the f64 oracle config)",
+            "c4": "C4 polygon-database join: 65536 random convex 4..16-gons (CSR), 2^28 f32 "
+                  "(point, polygon id) pairs, gathered test"}.get(
         name.split(":")[0], f"C3 n-sweep regular {name} jittered hull, 2^28 f32 points")
 
 
@@ -201,8 +203,32 @@ def cpu_reference_sample(name: str, sample: int):
 def time_cpu_reference(name: str, sample: int, reps: int, warmup: int):
     """Times the three reference engines on the sample; returns (tests/s, kind, cores, s/rep)."""
     import oracle
-    vx, vy, xs, ys = cpu_reference_sample(name, sample)
     cores = os.cpu_count() or 1
+    if name == "c4":  # one reference batch call per polygon over its id-grouped pairs
+        import paper_2007_15385_b200 as vp
+        orc = oracle.Oracle()
+        off, vx, vy, cx, cy, r = W.c4_polygons(vp.random_convex_polygon)
+        sample = min(sample, 1 << 24)
+        xs, ys, ids = orc.join_pairs_f32(W.c4_pair_seed(), 0, sample, cx, cy, r)
+        try:
+            ref, kind = oracle.Reference(), "reference"
+        except FileNotFoundError:
+            ref, kind, cores = None, "port", 1
+        per_rep = []
+        for rr in range(warmup + reps):
+            if ref is not None:
+                _, ns = ref.join(off, vx, vy, xs, ys, ids, threads=cores)
+                t = sum(ns) * 1e-9
+            else:
+                t0 = time.perf_counter()
+                for e in range(3):
+                    orc.join_masks(off, vx, vy, e, xs.astype(np.float64), ys.astype(np.float64), ids)
+                t = time.perf_counter() - t0
+            if rr >= warmup:
+                per_rep.append(t)
+        t = statistics.median(per_rep)
+        return 3 * xs.size / t, kind, cores, t
+    vx, vy, xs, ys = cpu_reference_sample(name, sample)
     try:
         ref = oracle.Reference()
         kind = "reference"
@@ -251,6 +277,90 @@ def config_block(args, world):
                    else "L2 flushed between steps (256 MB write)")}
 
 
+# ----------------------------------------------------------------- GPU jobs
+class PolygonJob:
+    """One polygon against a device-resident point stream (C1, C2, C3, C5)."""
+
+    issue_cycles = ISSUE_CYCLES_PER_PE
+    bytes_per_unit = 8  # f32 x + y per test
+    e2e_path = ("vpipg_test_host_multi (C-ABI, pinned host buffers, 4 Mi-point chunks "
+                "double-buffered over 2 streams; one H2D per chunk feeds all 3 engines)")
+
+    def __init__(self, workload, lo, hi, device, torch, vp, stream):
+        self.torch = torch
+        vx, vy, self.xs, self.ys = build_workload(workload, lo, hi, torch, vp, stream)
+        t0 = time.perf_counter()
+        self.poly = vp.PreparedPolygon.prepare(vx, vy, vp.KIND_ALL, device=device, stream=stream)
+        self.prep_ms = (time.perf_counter() - t0) * 1e3
+        self.n_edges = self.poly.n
+
+    def launch(self, e, words, count, stream):
+        self.poly.test(e, self.xs, self.ys, words=words, count=count, stream=stream)
+
+    def prepare_host(self):
+        t = self.torch
+        self.hx = t.empty(self.xs.numel(), dtype=t.float32, pin_memory=True)
+        self.hy = t.empty(self.ys.numel(), dtype=t.float32, pin_memory=True)
+        self.hx.copy_(self.xs)
+        self.hy.copy_(self.ys)
+
+    def run_host(self, hw, stream):
+        _, cnt = self.poly.test_host_multi(self.hx, self.hy, (0, 1, 2), words=hw)
+        return cnt
+
+
+class JoinJob:
+    """C4: a CSR polygon database and (point, polygon id) pairs, gathered test."""
+
+    # affine gather: 2 FFMA + LOP3/2 per point-edge; crossing as in the stream kernel
+    issue_cycles = {"voronoi": 3.0, "sign_of_offset": 3.0, "ray_crossing": 6.0}
+    bytes_per_unit = 12  # f32 x + y + u32 id per test
+    e2e_path = ("pinned host pairs -> H2D (cudaMemcpyAsync) -> vpipg_test_gather x 3 engines -> "
+                "D2H mask words, all on one stream")
+
+    def __init__(self, workload, lo, hi, device, torch, vp, stream):
+        self.torch = torch
+        off, vx, vy, cx, cy, r = W.c4_polygons(vp.random_convex_polygon)
+        t0 = time.perf_counter()
+        self.db = vp.PolygonDB.prepare(off, vx, vy, vp.KIND_ALL, device=device, stream=stream)
+        self.prep_ms = (time.perf_counter() - t0) * 1e3
+        nv = (off[1:] - off[:-1]).astype(np.float64)
+        self.n_edges = float(nv.mean())  # ids are uniform over the polygons
+        m = hi - lo
+        dev = torch.device("cuda", device)
+        self.xs = torch.empty(m, dtype=torch.float32, device=dev)
+        self.ys = torch.empty(m, dtype=torch.float32, device=dev)
+        self.ids = torch.empty(m, dtype=torch.int32, device=dev)
+        c = [torch.as_tensor(a, device=dev) for a in (cx, cy, r)]
+        vp.fill_join_pairs(W.c4_pair_seed(), lo, self.xs, self.ys, self.ids, *c, stream=stream)
+
+    def launch(self, e, words, count, stream):
+        self.db.test(e, self.xs, self.ys, self.ids, words=words, count=count, stream=stream)
+
+    def prepare_host(self):
+        t = self.torch
+        self.h = [t.empty(a.numel(), dtype=a.dtype, pin_memory=True) for a in (self.xs, self.ys, self.ids)]
+        for hbuf, d in zip(self.h, (self.xs, self.ys, self.ids)):
+            hbuf.copy_(d)
+        self.d = [t.empty_like(a) for a in (self.xs, self.ys, self.ids)]
+        self.dw = [t.empty((self.xs.numel() + 31) // 32, dtype=t.int32, device=self.xs.device)
+                   for _ in range(3)]
+        self.dc = t.zeros(3, dtype=t.int64, device=self.xs.device)
+
+    def run_host(self, hw, stream):
+        t = self.torch
+        with t.cuda.stream(stream):
+            for dbuf, hbuf in zip(self.d, self.h):
+                dbuf.copy_(hbuf, non_blocking=True)
+            self.dc.zero_()
+            for e in range(3):
+                self.db.test(e, *self.d, words=self.dw[e], count=self.dc[e:e + 1], stream=stream)
+                hw[e].copy_(self.dw[e], non_blocking=True)
+            cnt = self.dc.to("cpu", non_blocking=True)
+        stream.synchronize()
+        return cnt.tolist()
+
+
 # ----------------------------------------------------------------- GPU arm
 def main():
     ap = argparse.ArgumentParser()
@@ -285,13 +395,13 @@ def main():
     lo, hi = W.shard(M, rank, world)
     m = hi - lo
     with torch.cuda.stream(stream):
-        vx, vy, xs, ys = build_workload(args.workload, lo, hi, torch, vp, stream)
-        poly = vp.PreparedPolygon.prepare(vx, vy, vp.KIND_ALL, device=local, stream=stream)
+        job = (JoinJob if args.workload == "c4" else PolygonJob)(args.workload, lo, hi, local,
+                                                                 torch, vp, stream)
         words = [torch.zeros((m + 31) // 32, dtype=torch.int32, device="cuda") for _ in range(3)]
         counts = torch.zeros(3, dtype=torch.int64, device="cuda")
         flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda") if M * 8 <= 4 * 126e6 else None
     stream.synchronize()
-    n_edges = poly.n
+    n_edges = job.n_edges
 
     kevents = []  # per step, per engine: (start, end) on the launch stream
 
@@ -304,7 +414,7 @@ def main():
             if record:
                 a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 a.record(stream)
-            poly.test(e, xs, ys, words=words[e], count=counts[e:e + 1], stream=stream)
+            job.launch(e, words[e], counts[e:e + 1], stream)
             if record:
                 b.record(stream)
                 pairs.append((a, b))
@@ -343,13 +453,10 @@ def main():
                      for e in range(3)]
     final_counts = counts.tolist()
 
-    # ---- end-to-end through the host-buffer C-ABI (pinned host memory) ----
+    # ---- end-to-end through the public API with pinned host buffers ----
     e2e = None
     if not args.no_e2e:
-        hx = torch.empty(m, dtype=torch.float32, pin_memory=True)
-        hy = torch.empty(m, dtype=torch.float32, pin_memory=True)
-        hx.copy_(xs)
-        hy.copy_(ys)
+        job.prepare_host()
         hw = [torch.empty((m + 31) // 32, dtype=torch.int32, pin_memory=True) for _ in range(3)]
         torch.cuda.synchronize()
         times = []
@@ -357,7 +464,7 @@ def main():
             if world > 1:
                 dist.barrier()
             t0 = time.perf_counter()
-            _, cnt = poly.test_host_multi(hx, hy, (0, 1, 2), words=hw)
+            cnt = job.run_host(hw, stream)
             if world > 1:
                 ct = torch.tensor(cnt, dtype=torch.int64, device="cuda")
                 dist.all_reduce(ct)
@@ -369,10 +476,9 @@ def main():
         if world > 1:
             dist.all_reduce(t_e2e, op=dist.ReduceOp.MAX)
         e2e = {"value": 3 * M / float(t_e2e.item()), "unit": UNIT,
-               "h2d_bytes_per_step": 2 * 4 * m, "d2h_bytes_per_step": 3 * 4 * ((m + 31) // 32),
-               "steps": args.e2e_steps,
-               "path": "vpipg_test_host_multi (C-ABI, pinned host buffers, 4 Mi-point chunks "
-                       "double-buffered over 2 streams, counts read back + NCCL all-reduce)"}
+               "h2d_bytes_per_step": job.bytes_per_unit * m,
+               "d2h_bytes_per_step": 3 * 4 * ((m + 31) // 32),
+               "steps": args.e2e_steps, "path": job.e2e_path}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -389,8 +495,8 @@ def main():
         return
 
     hbm_peak, hbm_src, fma_peak = load_peaks()
-    bytes_per_launch = m * 8 + 4 * ((m + 31) // 32)
-    pe = m * n_edges
+    bytes_per_launch = m * job.bytes_per_unit + 4 * ((m + 31) // 32)
+    pe = int(m * n_edges)
     kernels = []
     for e, name in enumerate(("voronoi", "sign_of_offset", "ray_crossing")):
         t = per_kernel_ms[e] * 1e-3
@@ -401,7 +507,7 @@ def main():
     clk_hz = ((clocks or {}).get("sm_mhz") or 1965.0) * 1e6
     sms = torch.cuda.get_device_properties(local).multi_processor_count
     for k in kernels:
-        peak_pe = sms * 4 * 32 * clk_hz / ISSUE_CYCLES_PER_PE[k["engine"]]
+        peak_pe = sms * 4 * 32 * clk_hz / job.issue_cycles[k["engine"]]
         k["issue_model_frac"] = k["point_edge_per_s"] / peak_pe
     dom = max(range(3), key=lambda e: per_kernel_ms[e])
     dk = kernels[dom]
@@ -441,6 +547,7 @@ def main():
         "config": config_block(args, world),
         "gpu_launches": 3 * args.steps,
         "roofline": roof, "kernels": kernels, "inside_counts": final_counts,
+        "prepare_ms": job.prep_ms,
         "clocks": clocks, "e2e": e2e, "cpu_baseline": cpu,
     }
     print(json.dumps(line), flush=True)

@@ -279,7 +279,33 @@ class Reference:
         L.vr_voronoi_batch_gens.argtypes = [_D, _D, sz, C.c_void_p, C.c_int, _U8,
                                             C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]
         L.vr_scalar.argtypes = [C.c_void_p, C.c_int, C.c_double, C.c_double]
+        u32p = C.POINTER(C.c_uint32)
+        L.vr_join_new.restype = C.c_void_p
+        L.vr_join_new.argtypes = [u32p, _D, _D, C.c_uint32, _D, _D, u32p, sz]
+        L.vr_join_free.argtypes = [C.c_void_p]
+        L.vr_join_run.restype = C.c_uint64
+        L.vr_join_run.argtypes = [C.c_void_p, C.c_int, C.c_int, _U8]
         self.L = L
+
+    def join(self, offsets, vx, vy, xs, ys, ids, threads=1, engines=(0, 1, 2)):
+        """Per-polygon batch calls over id-grouped pairs (grouping untimed).
+        Returns (masks, ns per engine)."""
+        offsets = np.ascontiguousarray(offsets, np.uint32)
+        xs, ys = np.ascontiguousarray(xs, np.float64), np.ascontiguousarray(ys, np.float64)
+        ids = np.ascontiguousarray(ids, np.uint32)
+        up = C.POINTER(C.c_uint32)
+        h = self.L.vr_join_new(offsets.ctypes.data_as(up), _d(np.ascontiguousarray(vx, np.float64)),
+                               _d(np.ascontiguousarray(vy, np.float64)), offsets.size - 1,
+                               _d(xs), _d(ys), ids.ctypes.data_as(up), xs.size)
+        out, times = [], []
+        try:
+            for e in engines:
+                m = np.zeros(xs.size, np.uint8)
+                times.append(self.L.vr_join_run(h, e, threads, m.ctypes.data_as(_U8)))
+                out.append(m)
+        finally:
+            self.L.vr_join_free(h)
+        return out, times
 
     def validate(self, vx, vy):
         vx, vy = np.ascontiguousarray(vx, np.float64), np.ascontiguousarray(vy, np.float64)

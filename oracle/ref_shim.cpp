@@ -11,6 +11,7 @@
 #include <cstdint>
 #include <cstring>
 #include <optional>
+#include <thread>
 #include <vector>
 
 #include "vpip/engines.hpp"
@@ -208,6 +209,71 @@ void vr_voronoi_batch_gens(const double* inner_xy, const double* outer_xy, std::
   std::memcpy(out, mask.data(), mask.size());
   if (evals) *evals = stats.distance_evaluations;
   if (comps) *comps = stats.comparisons;
+}
+
+// ---- polygon-database join baseline (config 4) ----
+// The reference has no gather API; its natural use is one batch call per
+// polygon over that polygon's points. vr_join_new groups the
+// pairs by id and validates / converts every polygon (untimed preparation);
+// vr_join_run times the per-polygon *_contains_batch calls, polygons split
+// over `threads` std::threads, each call single-threaded.
+struct Join {
+  std::vector<Poly> polys;
+  std::vector<vpip::PointBatch> batches;
+  std::vector<std::vector<std::uint64_t>> index;
+};
+
+void* vr_join_new(const uint32_t* offsets, const double* vx, const double* vy, uint32_t npoly,
+                  const double* xs, const double* ys, const uint32_t* ids, std::size_t m) {
+  auto* j = new Join;
+  j->polys.resize(npoly);
+  j->batches.resize(npoly);
+  j->index.resize(npoly);
+  for (uint32_t i = 0; i < npoly; ++i) {
+    Poly& p = j->polys[i];
+    p.raw = to_points(vx + offsets[i], vy + offsets[i], offsets[i + 1] - offsets[i]);
+    try {
+      p.convex.emplace(vpip::validate_polygon(p.raw));
+      p.gens.emplace(vpip::to_voronoi(*p.convex));
+    } catch (const vpip::Error&) {
+    }
+  }
+  for (std::size_t k = 0; k < m; ++k) {
+    if (ids[k] >= npoly) continue;
+    j->batches[ids[k]].push_back({xs[k], ys[k]});
+    j->index[ids[k]].push_back(k);
+  }
+  return j;
+}
+
+void vr_join_free(void* j) { delete static_cast<Join*>(j); }
+
+uint64_t vr_join_run(void* jp, int engine, int threads, uint8_t* out) {
+  Join& j = *static_cast<Join*>(jp);
+  const std::size_t np = j.polys.size();
+  std::vector<vpip::InclusionMask> masks(np);
+  auto work = [&](std::size_t lo, std::size_t hi) {
+    for (std::size_t i = lo; i < hi; ++i) {
+      const Poly& p = j.polys[i];
+      const vpip::PointBatch& b = j.batches[i];
+      if (b.empty()) continue;
+      if (engine == 2) masks[i] = vpip::ray_crossing_contains_batch(p.raw, b, 1);
+      else if (!p.convex) masks[i].assign(b.size(), 0);
+      else if (engine == 0) masks[i] = vpip::voronoi_contains_batch(*p.gens, b, 1);
+      else masks[i] = vpip::sign_of_offset_contains_batch(*p.convex, b, 1);
+    }
+  };
+  const auto t0 = std::chrono::steady_clock::now();
+  {
+    std::vector<std::jthread> pool;
+    const int t = std::max(threads, 1);
+    for (int c = 0; c < t; ++c) pool.emplace_back(work, np * c / t, np * (c + 1) / t);
+  }
+  const auto t1 = std::chrono::steady_clock::now();
+  if (out)
+    for (std::size_t i = 0; i < np; ++i)
+      for (std::size_t k = 0; k < masks[i].size(); ++k) out[j.index[i][k]] = masks[i][k];
+  return static_cast<uint64_t>(std::chrono::duration_cast<std::chrono::nanoseconds>(t1 - t0).count());
 }
 
 int vr_scalar(void* poly, int engine, double px, double py) {

@@ -8,7 +8,11 @@ from __future__ import annotations
 import ctypes as C
 from pathlib import Path
 
-LIB_PATH = Path(__file__).resolve().parent / "lib" / "libvpipg.so"
+import os
+
+# VPIPG_LIBRARY overrides the in-tree library (kernel-variant experiments only)
+LIB_PATH = Path(os.environ.get("VPIPG_LIBRARY") or
+                Path(__file__).resolve().parent / "lib" / "libvpipg.so")
 
 ENGINE_VORONOI, ENGINE_OFFSET, ENGINE_CROSSING = 0, 1, 2
 ENGINES = {"voronoi": 0, "sign_of_offset": 1, "offset": 1, "ray_crossing": 2, "crossing": 2}

@@ -53,6 +53,21 @@ def _run(cmd: list[str]) -> None:
         sys.stderr.write(r.stderr)
 
 
+def build_variant(tag: str, defines: list[str]) -> Path:
+    """Experimental kernel variant (e.g. -DVPIPG_P=8) as lib/variants/libvpipg_<tag>.so."""
+    out = PKG / "lib" / "variants" / f"libvpipg_{tag}.so"
+    vdir = OBJ / f"v_{tag}"
+    vdir.mkdir(parents=True, exist_ok=True)
+    out.parent.mkdir(parents=True, exist_ok=True)
+    build()
+    objs = [OBJ / (s + ".o") for s in CU_SOURCES + CXX_SOURCES if s != "test_f32.cu"]
+    vobj = vdir / "test_f32.cu.o"
+    _run([NVCC, *NVCC_FLAGS, *defines, "-c", str(CSRC / "test_f32.cu"), "-o", str(vobj)])
+    _run([NVCC, *ARCH, "-shared", "-o", str(out), str(vobj), *map(str, objs), "-cudart", "static",
+          "-Xlinker", "--no-undefined", "-lrt", "-lpthread", "-ldl"])
+    return out
+
+
 def build(verbose: bool = False) -> Path:
     OBJ.mkdir(exist_ok=True)
     LIB.parent.mkdir(exist_ok=True)

@@ -24,14 +24,22 @@
 #include "vpipg_device.cuh"
 #include "vpipg_internal.h"
 
+// points per lane per slice (tuned on C5, profiles/round1_summary.md): the
+// slab kernel amortises its per-slice work best at 16, the crossing kernel
+// (more live registers per point) at 12; both run 2 CTAs of 8 warps per SM
+#ifndef VPIPG_SLAB_P
+#define VPIPG_SLAB_P 16
+#endif
+#ifndef VPIPG_CROSS_P
+#define VPIPG_CROSS_P 12
+#endif
+
 namespace vpipg {
 
 namespace {
 
-constexpr int P = 16;                 // points per lane per slice
 constexpr int kWarps = 8;             // warps per CTA
 constexpr int kThreads = kWarps * 32;
-constexpr int kWarpPts = 32 * P;      // 512 points per warp slice
 constexpr int kStages = 2;            // per-warp ring depth
 
 __device__ __forceinline__ float fmax3(float a, float b, float c) {
@@ -49,7 +57,9 @@ __device__ __forceinline__ float fmin3(float a, float b, float c) {
 // Slab engine (Voronoi and sign-of-offset): inside iff
 //   max(XLO) <= x' <= min(XHI)  and  max(YLO) <= y' <= min(YHI)
 // where each group entry is t = B * (other coordinate) + C (see prep.cu).
+template <int P>
 struct SlabEngine {
+  static constexpr int kP = P;
   struct Params {
     SlabTable tab;
     float ox, oy;
@@ -126,7 +136,9 @@ struct SlabEngine {
 // Points exactly on an edge line lie inside the 1e-5 parity band, so the
 // reference's closed-boundary latch (engines.cpp:194-196) is repeated only by
 // the exact f64 kernel.
+template <int P>
 struct CrossEngine {
+  static constexpr int kP = P;
   struct Params {
     CrossTable tab;
     float ox, oy;
@@ -206,7 +218,7 @@ struct CrossEngine {
 // Output: ballot words (PIPM order), optional byte mask, per-lane inside count.
 // The P words of a slice are warp-uniform; lane 0 writes them with 16-byte
 // streaming stores (a slice's words are 64 contiguous, 64-byte aligned bytes).
-template <bool kGuard>
+template <bool kGuard, int P>
 __device__ __forceinline__ uint32_t emit(const float (&slack)[P], uint64_t base,
                                          const TestArgs& a, int lane) {
   uint32_t w[P];
@@ -250,6 +262,7 @@ __device__ __forceinline__ void flush_count(uint32_t cnt, const TestArgs& a) {
 template <class Eng>
 __device__ __forceinline__ uint32_t guarded_tile(const typename Eng::Params& prm, const float4* tab,
                                                  const TestArgs& a, uint64_t base, int lane) {
+  constexpr int P = Eng::kP;
   const float* xs = static_cast<const float*>(a.xs);
   const float* ys = static_cast<const float*>(a.ys);
   float x[P], y[P], slack[P];
@@ -261,12 +274,14 @@ __device__ __forceinline__ uint32_t guarded_tile(const typename Eng::Params& prm
     y[p] = ok ? __ldcs(ys + idx) : 0.f;
   }
   Eng::eval(prm, tab, x, y, slack);
-  return emit<true>(slack, base, a, lane);
+  return emit<true, P>(slack, base, a, lane);
 }
 
 template <class Eng>
 __global__ void __launch_bounds__(kThreads, 2)
     stream_kernel(const typename Eng::Params prm, const TestArgs a, const uint64_t full_slices) {
+  constexpr int P = Eng::kP;
+  constexpr int kWarpPts = 32 * P;
   extern __shared__ __align__(128) unsigned char smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // per-warp ring: [stage][x | y][kWarpPts] floats, then the barriers, then the table
@@ -324,7 +339,7 @@ __global__ void __launch_bounds__(kThreads, 2)
                &full[s], policy);
     }
     Eng::eval(prm, tab, x, y, slack);
-    count += emit<false>(slack, g * kWarpPts, a, lane);
+    count += emit<false, P>(slack, g * kWarpPts, a, lane);
   }
   // partial last slice: the warp next in round-robin order, guarded loads
   if (g0 == full_slices % W) {
@@ -337,6 +352,7 @@ __global__ void __launch_bounds__(kThreads, 2)
 template <class Eng>
 __global__ void __launch_bounds__(kThreads) generic_kernel(const typename Eng::Params prm,
                                                           const TestArgs a) {
+  constexpr int kWarpPts = 32 * Eng::kP;
   extern __shared__ __align__(16) float4 gtab[];
   Eng::stage(prm, gtab);
   __syncthreads();
@@ -361,6 +377,7 @@ int sm_count() {
 
 template <class Eng>
 cudaError_t launch(const typename Eng::Params& prm, const TestArgs& a, cudaStream_t stream) {
+  constexpr int kWarpPts = 32 * Eng::kP;
   const size_t tab = Eng::table_bytes(prm);
   const bool aligned = ((reinterpret_cast<uintptr_t>(a.xs) | reinterpret_cast<uintptr_t>(a.ys)) & 15) == 0;
   const uint64_t full_slices = aligned ? a.m / kWarpPts : 0;
@@ -397,11 +414,13 @@ cudaError_t launch(const typename Eng::Params& prm, const TestArgs& a, cudaStrea
 cudaError_t launch_test_f32(const DevTables& t, int engine, const TestArgs& a,
                             cudaStream_t stream) {
   if (engine == 0 || engine == 1) {
-    SlabEngine::Params prm{t.slab[engine], t.ox, t.oy};
-    return launch<SlabEngine>(prm, a, stream);
+    using E = SlabEngine<VPIPG_SLAB_P>;
+    typename E::Params prm{t.slab[engine], t.ox, t.oy};
+    return launch<E>(prm, a, stream);
   }
-  CrossEngine::Params prm{t.cross, t.ox, t.oy};
-  return launch<CrossEngine>(prm, a, stream);
+  using E = CrossEngine<VPIPG_CROSS_P>;
+  typename E::Params prm{t.cross, t.ox, t.oy};
+  return launch<E>(prm, a, stream);
 }
 
 }  // namespace vpipg

@@ -153,3 +153,32 @@ def test_reference_acceptance_suite_if_present():
     r = subprocess.run([str(oracle.REF_ACCEPTANCE)], capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stdout
     assert "all 8 criteria passed" in r.stdout
+
+
+def test_join_oracle_matches_reference_batches(orc):
+    """vo_join_masks (per-pair restatement) == the reference's per-polygon batch
+    calls over id-grouped pairs (the C4 CPU baseline), bit for bit."""
+    import oracle
+    import paper_2007_15385_b200 as vp
+    if not oracle.REF_SO.exists():
+        pytest.skip("oracle/_ref not built")
+    ref = oracle.Reference()
+    off, vx, vy, cx, cy, r = W.c4_polygons(vp.random_convex_polygon, npoly=512)
+    xs, ys, ids = orc.join_pairs_f32(W.c4_pair_seed(), 0, 50_000, cx, cy, r)
+    masks, _ = ref.join(off, vx, vy, xs, ys, ids, threads=2)
+    for e in range(3):
+        want = orc.join_masks(off, vx, vy, e, xs.astype(np.float64), ys.astype(np.float64), ids)
+        assert np.array_equal(masks[e], want), e
+    assert 0.3 < masks[0].mean() < 0.8
+
+
+def test_c4_workload_polygons_are_valid_and_deterministic(orc):
+    import paper_2007_15385_b200 as vp
+    a = W.c4_polygons(vp.random_convex_polygon, npoly=300)
+    b = W.c4_polygons(orc.random_convex_polygon, npoly=300)
+    for x, y in zip(a, b):
+        assert np.array_equal(x, y)
+    off = a[0]
+    n = off[1:] - off[:-1]
+    assert n.min() >= 4 and n.max() <= 16
+    assert (orc.csr_status(*a[:3]) == 0).all()
