@@ -130,6 +130,37 @@ int vpipg_test_host_multi(const vpipg_poly* poly, uint32_t engines, int dtype, c
 int vpipg_voronoi_work(const vpipg_poly* poly, uint64_t m, uint64_t* distance_evaluations,
                        uint64_t* comparisons);
 
+/* ---- engine cross-validation on the device (run_validation, bench.cpp:279-308) ---- */
+#define VPIPG_REPORT_SAMPLES 100
+typedef struct {
+  uint64_t point_count;
+  /* {voronoi/offset, voronoi/crossing, offset/crossing} (bench.hpp:91-92); for
+   * vpipg_compare_masks: {a/b, a/b, 0} */
+  uint64_t pair_disagreements[3];
+  uint64_t disagreeing_points;
+  /* disagreeing points farther than the band from every edge supporting line */
+  uint64_t outside_band;
+  int pass; /* outside_band == 0 */
+  uint32_t n_samples;                           /* first disagreements by index */
+  uint64_t sample_index[VPIPG_REPORT_SAMPLES];
+  double sample_dist[VPIPG_REPORT_SAMPLES];     /* edge_line_distance (voronoi.cpp:73-82) */
+  uint32_t sample_engines[VPIPG_REPORT_SAMPLES];/* bit0 voronoi, bit1 offset, bit2 crossing, bit3 outside band */
+} vpipg_report;
+
+/* All three engines on one batch (device pointers, f32 or f64), then every
+ * disagreeing point's distance to the nearest edge line against `band`
+ * (absolute, like tol::kAgreementBand, or relative: band * max(1, |x|, |y|,
+ * polygon extent) when band_relative != 0). Needs a handle prepared with all
+ * three kinds. Synchronous on `stream`. */
+int vpipg_validate(const vpipg_poly* poly, int dtype, const void* xs, const void* ys, uint64_t m,
+                   double band, int band_relative, vpipg_report* out, void* stream);
+
+/* The same classification for two existing masks (device word arrays) of one
+ * batch, e.g. the reference-exact f64 engine against the fp32 engine. */
+int vpipg_compare_masks(const vpipg_poly* poly, int dtype, const void* xs, const void* ys,
+                        uint64_t m, const uint32_t* words_a, const uint32_t* words_b, double band,
+                        int band_relative, vpipg_report* out, void* stream);
+
 /* ---- polygon database join (BASELINE config 4) ----
  * A CSR batch of polygons: polygon i owns vertices offsets[i] .. offsets[i+1]-1
  * of vx / vy (host arrays, f64). Replaces a loop of validate_polygon +

@@ -279,6 +279,8 @@ class Reference:
         L.vr_voronoi_batch_gens.argtypes = [_D, _D, sz, C.c_void_p, C.c_int, _U8,
                                             C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]
         L.vr_scalar.argtypes = [C.c_void_p, C.c_int, C.c_double, C.c_double]
+        L.vr_run_validation.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_double,
+                                        C.POINTER(C.c_uint64)]
         u32p = C.POINTER(C.c_uint32)
         L.vr_join_new.restype = C.c_void_p
         L.vr_join_new.argtypes = [u32p, _D, _D, C.c_uint32, _D, _D, u32p, sz]
@@ -286,6 +288,23 @@ class Reference:
         L.vr_join_run.restype = C.c_uint64
         L.vr_join_run.argtypes = [C.c_void_p, C.c_int, C.c_int, _U8]
         self.L = L
+
+    def run_validation(self, vx, vy, xs, ys, band=1e-9, threads=1):
+        """The reference's run_validation: ({pair counts}, disagreeing, pass)."""
+        vx, vy = np.ascontiguousarray(vx, np.float64), np.ascontiguousarray(vy, np.float64)
+        xs, ys = np.ascontiguousarray(xs, np.float64), np.ascontiguousarray(ys, np.float64)
+        code = C.c_int()
+        p = self.L.vr_poly_new(_d(vx), _d(vy), vx.size, 1, C.byref(code))
+        if not p:
+            raise ValueError(code.value)
+        b = self.L.vr_batch_new(_d(xs), _d(ys), xs.size)
+        out = (C.c_uint64 * 5)()
+        try:
+            self.L.vr_run_validation(p, b, threads, band, out)
+        finally:
+            self.L.vr_batch_free(b)
+            self.L.vr_poly_free(p)
+        return list(out[:3]), out[3], bool(out[4])
 
     def join(self, offsets, vx, vy, xs, ys, ids, threads=1, engines=(0, 1, 2)):
         """Per-polygon batch calls over id-grouped pairs (grouping untimed).

@@ -14,6 +14,7 @@
 #include <thread>
 #include <vector>
 
+#include "vpip/bench.hpp"
 #include "vpip/engines.hpp"
 #include "vpip/geometry.hpp"
 #include "vpip/sampling.hpp"
@@ -274,6 +275,19 @@ uint64_t vr_join_run(void* jp, int engine, int threads, uint8_t* out) {
     for (std::size_t i = 0; i < np; ++i)
       for (std::size_t k = 0; k < masks[i].size(); ++k) out[j.index[i][k]] = masks[i][k];
   return static_cast<uint64_t>(std::chrono::duration_cast<std::chrono::nanoseconds>(t1 - t0).count());
+}
+
+// run_validation (bench.cpp:279-308) on a convex polygon handle: fills
+// counts[0..4] = {v/o, v/c, o/c pair disagreements, disagreeing points, pass}.
+int vr_run_validation(void* poly, void* batch, int threads, double band, uint64_t* counts) {
+  const Poly& p = *static_cast<Poly*>(poly);
+  if (!p.convex) return 6;
+  const vpip::ValidationReport r = vpip::run_validation(
+      *p.convex, *p.gens, *static_cast<vpip::PointBatch*>(batch), threads, band);
+  for (int i = 0; i < 3; ++i) counts[i] = r.pair_disagreements[i];
+  counts[3] = r.disagreeing_points;
+  counts[4] = r.pass ? 1 : 0;
+  return 0;
 }
 
 int vr_scalar(void* poly, int engine, double px, double py) {

@@ -21,6 +21,19 @@ KIND_VORONOI, KIND_OFFSET, KIND_CROSSING, KIND_ALL = 1, 2, 4, 7
 F64, F32 = 0, 1
 ERR_CUDA, ERR_ARCH = 100, 300
 
+REPORT_SAMPLES = 100
+
+
+class Report(C.Structure):
+    """vpipg_report (include/vpipg.h): run_validation's ValidationReport (bench.hpp:84-102)."""
+    _fields_ = [("point_count", C.c_uint64), ("pair_disagreements", C.c_uint64 * 3),
+                ("disagreeing_points", C.c_uint64), ("outside_band", C.c_uint64),
+                ("pass_", C.c_int), ("n_samples", C.c_uint32),
+                ("sample_index", C.c_uint64 * REPORT_SAMPLES),
+                ("sample_dist", C.c_double * REPORT_SAMPLES),
+                ("sample_engines", C.c_uint32 * REPORT_SAMPLES)]
+
+
 # name -> (restype, argtypes); every symbol include/vpipg.h declares.
 _P = C.c_void_p
 _D = C.POINTER(C.c_double)
@@ -41,6 +54,9 @@ SIGNATURES = {
     "vpipg_voronoi_work": (C.c_int, [_P, C.c_uint64, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
     "vpipg_fill_uniform_points": (C.c_int, [C.c_uint64, C.c_uint64, C.c_uint64, C.c_double,
                                             C.c_double, C.c_double, C.c_double, C.c_int, _P, _P, _P]),
+    "vpipg_validate": (C.c_int, [_P, C.c_int, _P, _P, C.c_uint64, C.c_double, C.c_int, _P, _P]),
+    "vpipg_compare_masks": (C.c_int, [_P, C.c_int, _P, _P, C.c_uint64, _P, _P, C.c_double, C.c_int,
+                                      _P, _P]),
     "vpipg_prepare_csr": (C.c_int, [_P, _D, _D, C.c_uint32, C.c_uint32, C.c_int, _P,
                                     C.POINTER(_P), _P]),
     "vpipg_db_destroy": (None, [_P]),

@@ -123,6 +123,7 @@ int build(vpipg_poly* p, const double* vv, const double* vr, const double* gen, 
   const size_t o_s0 = take((n + 4) * sizeof(float2));
   const size_t o_s1 = take((n + 4) * sizeof(float2));
   const size_t o_cross = take(n * sizeof(float4));
+  const size_t o_lines = take(n * sizeof(double4));
   const size_t o_meta = take(sizeof(PrepMeta));
   VPIPG_TRY(cudaMalloc(&p->blob, off));
   char* b = static_cast<char*>(p->blob);
@@ -148,6 +149,7 @@ int build(vpipg_poly* p, const double* vv, const double* vr, const double* gen, 
   a.slab_coef[0] = reinterpret_cast<float2*>(b + o_s0);
   a.slab_coef[1] = reinterpret_cast<float2*>(b + o_s1);
   a.cross_vert = reinterpret_cast<float4*>(b + o_cross);
+  a.lines = reinterpret_cast<double4*>(b + o_lines);
   a.meta = reinterpret_cast<PrepMeta*>(b + o_meta);
   VPIPG_TRY(launch_prep(a, s));
   PrepMeta meta;
@@ -178,6 +180,7 @@ int build(vpipg_poly* p, const double* vv, const double* vr, const double* gen, 
   }
   t.cross.vert = a.cross_vert;
   t.cross.n = p->n;
+  t.lines = a.lines;
   p->inner_x = meta.inner_x;
   p->inner_y = meta.inner_y;
   return kOk;
@@ -558,6 +561,103 @@ int vpipg_fill_join_pairs(uint64_t seed, uint64_t first, uint64_t m, uint32_t np
   if (m && (npoly == 0 || !centre_x || !centre_y || !radius || !xs || !ys || !ids)) return kInvalid;
   return cuda_code(launch_fill_pairs(seed, first, m, npoly, centre_x, centre_y, radius, xs, ys,
                                      ids, static_cast<cudaStream_t>(stream)));
+}
+
+namespace {
+
+double poly_extent(const vpipg_poly* p) {
+  if (p->vx.empty()) return 0.0;
+  const auto [x0, x1] = std::minmax_element(p->vx.begin(), p->vx.end());
+  const auto [y0, y1] = std::minmax_element(p->vy.begin(), p->vy.end());
+  return std::max(*x1 - *x0, *y1 - *y0);
+}
+
+int classify(const vpipg_poly* p, int dtype, const void* xs, const void* ys, uint64_t m,
+             const uint32_t* w0, const uint32_t* w1, const uint32_t* w2, double band,
+             int relative, vpipg_report* out, cudaStream_t s) {
+  ReportDev* rep = nullptr;
+  VPIPG_TRY(cudaMallocAsync(reinterpret_cast<void**>(&rep), sizeof(ReportDev), s));
+  int rc = kOk;
+  auto fail = [&](cudaError_t e) {
+    if (e != cudaSuccess && rc == kOk) rc = cuda_code(e);
+    return rc != kOk;
+  };
+  ClassifyArgs a{{w0, w1, w2}, xs, ys, dtype, m, band, relative, poly_extent(p), p->t.lines,
+                 p->n, rep};
+  // counters only (the sample arrays are written before they are read)
+  struct Head {
+    unsigned long long pair[3], dis, out, rec;
+  } head{};
+  std::vector<unsigned long long> idx;
+  std::vector<double> dist;
+  std::vector<uint32_t> bits;
+  if (!fail(cudaMemsetAsync(rep, 0, sizeof(Head), s)) && !fail(launch_classify(a, s)) &&
+      !fail(cudaMemcpyAsync(&head, rep, sizeof(Head), cudaMemcpyDeviceToHost, s)) &&
+      !fail(cudaStreamSynchronize(s))) {
+    const size_t k = std::min<unsigned long long>(head.rec, kSampleCapacity);
+    idx.resize(k);
+    dist.resize(k);
+    bits.resize(k);
+    if (k) {
+      fail(cudaMemcpyAsync(idx.data(), rep->sample_index, k * 8, cudaMemcpyDeviceToHost, s));
+      fail(cudaMemcpyAsync(dist.data(), rep->sample_dist, k * 8, cudaMemcpyDeviceToHost, s));
+      fail(cudaMemcpyAsync(bits.data(), rep->sample_bits, k * 4, cudaMemcpyDeviceToHost, s));
+      fail(cudaStreamSynchronize(s));
+    }
+  }
+  cudaFreeAsync(rep, s);
+  if (rc) return rc;
+  std::memset(out, 0, sizeof(*out));
+  out->point_count = m;
+  for (int i = 0; i < 3; ++i) out->pair_disagreements[i] = head.pair[i];
+  if (!w2) out->pair_disagreements[2] = 0;
+  out->disagreeing_points = head.dis;
+  out->outside_band = head.out;
+  out->pass = head.out == 0;
+  // the first disagreements by index (exact while fewer than kSampleCapacity occurred)
+  std::vector<size_t> order(idx.size());
+  for (size_t i = 0; i < order.size(); ++i) order[i] = i;
+  std::sort(order.begin(), order.end(), [&](size_t a1, size_t b1) { return idx[a1] < idx[b1]; });
+  out->n_samples = static_cast<uint32_t>(std::min<size_t>(order.size(), VPIPG_REPORT_SAMPLES));
+  for (uint32_t i = 0; i < out->n_samples; ++i) {
+    out->sample_index[i] = idx[order[i]];
+    out->sample_dist[i] = dist[order[i]];
+    out->sample_engines[i] = bits[order[i]];
+  }
+  return kOk;
+}
+
+}  // namespace
+
+int vpipg_validate(const vpipg_poly* p, int dtype, const void* xs, const void* ys, uint64_t m,
+                   double band, int band_relative, vpipg_report* out, void* stream) {
+  if (!p || !out || (p->kinds & VPIPG_KIND_ALL) != VPIPG_KIND_ALL) return kInvalid;
+  if (dtype != VPIPG_F32 && dtype != VPIPG_F64) return kInvalid;
+  if (m && (!xs || !ys)) return kInvalid;
+  DeviceGuard g(p->device);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const uint64_t nw = (m + 31) / 32;
+  uint32_t* w = nullptr;
+  VPIPG_TRY(cudaMallocAsync(reinterpret_cast<void**>(&w), 3 * std::max<uint64_t>(nw, 1) * 4, s));
+  int rc = kOk;
+  for (int e = 0; e < 3 && rc == kOk; ++e) {
+    TestArgs a{xs, ys, m, w + e * nw, nullptr, nullptr};
+    rc = dispatch(p, e, dtype, a, s);
+  }
+  if (rc == kOk) rc = classify(p, dtype, xs, ys, m, w, w + nw, w + 2 * nw, band, band_relative, out, s);
+  cudaFreeAsync(w, s);
+  cudaStreamSynchronize(s);
+  return rc;
+}
+
+int vpipg_compare_masks(const vpipg_poly* p, int dtype, const void* xs, const void* ys,
+                        uint64_t m, const uint32_t* words_a, const uint32_t* words_b, double band,
+                        int band_relative, vpipg_report* out, void* stream) {
+  if (!p || !out || (m && (!xs || !ys || !words_a || !words_b))) return kInvalid;
+  if (dtype != VPIPG_F32 && dtype != VPIPG_F64) return kInvalid;
+  DeviceGuard g(p->device);
+  return classify(p, dtype, xs, ys, m, words_a, words_b, nullptr, band, band_relative, out,
+                  static_cast<cudaStream_t>(stream));
 }
 
 int vpipg_voronoi_work(const vpipg_poly* p, uint64_t m, uint64_t* evals, uint64_t* comps) {

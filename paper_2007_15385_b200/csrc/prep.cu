@@ -238,6 +238,28 @@ __global__ void __launch_bounds__(kPrepThreads) prep_kernel(PrepArgs a) {
       a.cross_vert[i] = make_float4(xl, yl, bk, 0.f);
     }
   }
+  // ---- band metric lines: edge k (v[k] -> v[k+1]) of the validated vertices,
+  // else the raw ones, else the generator bisectors (voronoi.cpp:23-35, 73-82)
+  {
+    const double* vv = a.vv ? a.vv : a.vr;
+    for (int k = tid; k < n; k += kPrepThreads) {
+      double la, lb, lc;
+      if (vv) {
+        const int k1 = (k + 1) % n;
+        la = vv[n + k] - vv[n + k1];
+        lb = vv[k1] - vv[k];
+        lc = -(la * vv[k] + lb * vv[n + k]);
+      } else {  // bisector of p0 and outer[k]
+        const double2 g = a.outer[k];
+        la = g.x - p0x;
+        lb = g.y - p0y;
+        lc = -(la * 0.5 * (p0x + g.x) + lb * 0.5 * (p0y + g.y));
+      }
+      const double h = hypot(la, lb);
+      const double s = h > 0.0 ? 1.0 / h : 0.0;
+      a.lines[k] = make_double4(la * s, lb * s, lc * s, 0.0);
+    }
+  }
   __syncthreads();
   if (tid == 0) a.meta->status = (s_fail == INT_MAX) ? 0 : (s_fail & 7);
 }

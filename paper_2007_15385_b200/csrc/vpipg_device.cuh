@@ -69,6 +69,9 @@ struct DevTables {
   float ox, oy;              // local-frame origin (f32; zero stored as -0.0f)
   SlabTable slab[2];         // [0] Voronoi (from generators), [1] sign-of-offset
   CrossTable cross;
+  // unit-normal supporting lines (a, b, c, 0) of the n edges, f64: the band
+  // metric edge_line_distance (voronoi.cpp:73-82) of the validation kernels
+  const double4* lines;
 };
 
 // Written by the prep kernel, read back by the (synchronous) prepare call.

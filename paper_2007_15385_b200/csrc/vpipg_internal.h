@@ -24,6 +24,7 @@ struct PrepArgs {
   RayEdgeF64* ray;
   float2* slab_coef[2];  // capacity n + 4 entries each
   float4* cross_vert;
+  double4* lines;        // n unit-normal edge lines (band metric)
   PrepMeta* meta;
 };
 
@@ -83,6 +84,32 @@ cudaError_t launch_fill_pairs(uint64_t seed, uint64_t first, uint64_t m, uint32_
                               float* ys, uint32_t* ids, cudaStream_t stream);
 cudaError_t launch_test_f32(const DevTables& t, int engine, const TestArgs& a, cudaStream_t stream);
 cudaError_t launch_test_f64(const DevTables& t, int engine, const TestArgs& a, cudaStream_t stream);
+// ---- validation (validate.cu): run_validation (bench.cpp:279-308) on the device ----
+constexpr int kReportSamples = 100;
+constexpr uint32_t kSampleCapacity = 1u << 16;
+struct ReportDev {                    // device-side accumulators
+  unsigned long long pair[3];         // voronoi/offset, voronoi/crossing, offset/crossing
+  unsigned long long disagreeing;
+  unsigned long long outside_band;
+  unsigned long long n_recorded;
+  unsigned long long sample_index[kSampleCapacity];
+  double sample_dist[kSampleCapacity];
+  uint32_t sample_bits[kSampleCapacity];  // engine mask bits v | s << 1 | c << 2
+};
+struct ClassifyArgs {
+  const uint32_t* w[3];  // mask words per engine (w[2] may be null: two-mask compare)
+  const void* xs;
+  const void* ys;
+  int dtype;
+  uint64_t m;
+  double band;
+  int relative;          // band * max(1, |x|, |y|, extent) when set
+  double extent;
+  const double4* lines;
+  uint32_t n;
+  ReportDev* rep;
+};
+cudaError_t launch_classify(const ClassifyArgs& a, cudaStream_t stream);
 cudaError_t launch_fill_uniform(uint64_t seed, uint64_t first, uint64_t m, double min_x,
                                 double min_y, double max_x, double max_y, int dtype, void* xs,
                                 void* ys, cudaStream_t stream);

@@ -133,6 +133,29 @@ class PreparedPolygon:
         return w, b, cnt.value
 
 
+    def validate(self, xs, ys, band: float = 1e-9, relative: bool = False, stream=None):
+        """run_validation on the device (vpipg_validate): returns a dict report."""
+        import torch
+        rep = _lib.Report()
+        dtype = F32 if xs.dtype == torch.float32 else F64
+        check(load().vpipg_validate(self._h, dtype, C.c_void_p(xs.data_ptr()),
+                                    C.c_void_p(ys.data_ptr()), xs.numel(), band, int(relative),
+                                    C.byref(rep), _stream_ptr(stream)), "vpipg_validate")
+        return _report_dict(rep)
+
+    def compare_masks(self, xs, ys, words_a, words_b, band: float, relative: bool = True,
+                      stream=None):
+        """Band classification of two masks of one batch (vpipg_compare_masks)."""
+        import torch
+        rep = _lib.Report()
+        dtype = F32 if xs.dtype == torch.float32 else F64
+        check(load().vpipg_compare_masks(self._h, dtype, C.c_void_p(xs.data_ptr()),
+                                         C.c_void_p(ys.data_ptr()), xs.numel(),
+                                         C.c_void_p(words_a.data_ptr()),
+                                         C.c_void_p(words_b.data_ptr()), band, int(relative),
+                                         C.byref(rep), _stream_ptr(stream)), "vpipg_compare_masks")
+        return _report_dict(rep)
+
     def test_host_multi(self, xs: np.ndarray, ys: np.ndarray, engines=(0, 1, 2),
                         words=None, counts_only: bool = False):
         """All requested engines over one host batch (vpipg_test_host_multi).
@@ -215,6 +238,14 @@ def fill_join_pairs(seed: int, first: int, xs, ys, ids, cx, cy, r, stream=None) 
     check(load().vpipg_fill_join_pairs(seed, first, xs.numel(), cx.numel(), ptr(cx), ptr(cy),
                                        ptr(r), ptr(xs), ptr(ys), ptr(ids), _stream_ptr(stream)),
           "fill_join_pairs")
+
+
+def _report_dict(rep) -> dict:
+    k = rep.n_samples
+    return {"point_count": rep.point_count, "pair_disagreements": list(rep.pair_disagreements),
+            "disagreeing_points": rep.disagreeing_points, "outside_band": rep.outside_band,
+            "pass": bool(rep.pass_), "sample_index": list(rep.sample_index[:k]),
+            "sample_dist": list(rep.sample_dist[:k]), "sample_engines": list(rep.sample_engines[:k])}
 
 
 def _host_ptr(a) -> int:

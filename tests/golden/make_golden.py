@@ -116,6 +116,8 @@ def main() -> None:
             vx, vy = vx.astype(np.float32).astype(np.float64), vy.astype(np.float32).astype(np.float64)
             xs, ys = xs.astype(np.float32).astype(np.float64), ys.astype(np.float32).astype(np.float64)
         (mv, mo, mr), _ = R.masks(vx, vy, xs, ys)
+        pairs, dis, ok = R.run_validation(vx, vy, xs, ys, band=1e-9)  # bench.cpp:279-308
+        fx[f"case_{name}_validation"] = np.array(pairs + [dis, int(ok)], np.int64)
         cases.append(name)
         p = f"case_{name}_"
         fx[p + "v"] = np.array([vx, vy])

@@ -1,0 +1,79 @@
+"""Device-side engine cross-validation (run_validation, bench.cpp:279-308) and
+the full-size parity property at BASELINE.json's 2^31-point C5 config."""
+import numpy as np
+import pytest
+
+from conftest import case_names
+import workloads as W
+
+torch = pytest.importorskip("torch")
+import paper_2007_15385_b200 as vp  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+DEV = "cuda:0"
+
+
+def test_device_validation_equals_reference_run_validation(golden, orc):
+    """f64 engines + band classification on the device reproduce the reference's
+    ValidationReport (pair counts, disagreeing points, verdict) on every golden case."""
+    for name in case_names(golden):
+        pre = f"case_{name}_"
+        vx, vy = golden[pre + "v"]
+        rc, cvx, cvy, _ = orc.validate(vx, vy)  # run_validation uses polygon.vertices()
+        assert rc == 0
+        xs, ys = golden[pre + "pts"].astype(np.float64)
+        want = golden[pre + "validation"]
+        with vp.PreparedPolygon.prepare(cvx, cvy, vp.KIND_ALL) as p:
+            rep = p.validate(torch.as_tensor(xs, device=DEV), torch.as_tensor(ys, device=DEV),
+                             band=1e-9)
+        assert rep["pair_disagreements"] == want[:3].tolist(), name
+        assert rep["disagreeing_points"] == want[3], name
+        assert rep["pass"] == bool(want[4]), name
+        assert rep["point_count"] == xs.size
+
+
+def test_validation_samples_and_failures():
+    # a square with points exactly on and far off its boundary: the f32 crossing
+    # kernel (no on-segment latch) disagrees with the others exactly on edges
+    vx, vy = np.array([0., 1, 1, 0]), np.array([0., 0, 1, 1])
+    xs = torch.tensor([0.5, 1.0, 0.25, 2.0, 1.0], dtype=torch.float32, device=DEV)
+    ys = torch.tensor([0.5, 0.5, 0.0, 2.0, 1.0], dtype=torch.float32, device=DEV)
+    with vp.PreparedPolygon.prepare(vx, vy, vp.KIND_ALL) as p:
+        rep = p.validate(xs, ys, band=1e-9)
+        assert rep["pass"] and rep["outside_band"] == 0
+        for i, d in zip(rep["sample_index"], rep["sample_dist"]):
+            assert d <= 1e-9 and i in (1, 2, 4)
+        # two different masks: disagreements far from any edge line fail the check
+        w_a = torch.tensor([0b00001], dtype=torch.int32, device=DEV)
+        w_b = torch.tensor([0b01000], dtype=torch.int32, device=DEV)  # point 3 (2, 2) is far outside
+        rep = p.compare_masks(xs, ys, w_a, w_b, band=1e-5)
+        assert not rep["pass"] and rep["outside_band"] == 2 and rep["disagreeing_points"] == 2
+        assert rep["sample_index"] == [0, 3]
+
+
+def test_c5_full_scale_parity():
+    """BASELINE.json config 5 at full size (2^31 points): the three fp32 engines
+    agree outside the 1e-5 relative band, and the fp32 Voronoi mask equals the
+    reference-exact fp64 Voronoi mask (same points, widened) outside the band."""
+    vx, vy = W.c5_polygon(vp.random_convex_polygon)
+    m = W.C5_POINTS
+    xs = torch.empty(m, dtype=torch.float32, device=DEV)
+    ys = torch.empty(m, dtype=torch.float32, device=DEV)
+    vp.fill_uniform_points(W.c5_point_seed(), 0, xs, ys, W.C5_BOX)
+    with vp.PreparedPolygon.prepare(vx, vy, vp.KIND_ALL) as p:
+        rep = p.validate(xs, ys, band=1e-5, relative=True)
+        assert rep["pass"], rep
+        assert rep["disagreeing_points"] < m * 1e-6
+        w32 = torch.empty(m // 32, dtype=torch.int32, device=DEV)
+        c32 = torch.zeros(1, dtype=torch.int64, device=DEV)
+        p.test(0, xs, ys, words=w32, count=c32)
+        xd, yd = xs.double(), ys.double()
+        w64 = torch.empty(m // 32, dtype=torch.int32, device=DEV)
+        c64 = torch.zeros(1, dtype=torch.int64, device=DEV)
+        p.test(0, xd, yd, words=w64, count=c64)
+        torch.cuda.synchronize()
+        cmp = p.compare_masks(xd, yd, w64, w32, band=1e-5, relative=True)
+        assert cmp["pass"], cmp
+        assert abs(c32.item() - c64.item()) <= cmp["disagreeing_points"]
+        print("C5 2^31: f32/f64 voronoi disagreements (all in band):", cmp["disagreeing_points"],
+              "three-engine disagreements:", rep["disagreeing_points"])
