@@ -91,6 +91,7 @@ struct SlabEngine {
     }
     const uint32_t nc = na < nb ? na : nb;
     uint32_t i = 1;
+#pragma unroll 1
     for (; i < nc; ++i) {
       const float4 a = A[i], b = B[i];
 #pragma unroll
@@ -99,11 +100,13 @@ struct SlabEngine {
         hi[p] = fmin3(hi[p], fmaf(b.x, v[p], b.y), fmaf(b.z, v[p], b.w));
       }
     }
+#pragma unroll 1
     for (uint32_t j = i; j < na; ++j) {
       const float4 a = A[j];
 #pragma unroll
       for (int p = 0; p < P; ++p) lo[p] = fmax3(lo[p], fmaf(a.x, v[p], a.y), fmaf(a.z, v[p], a.w));
     }
+#pragma unroll 1
     for (uint32_t j = i; j < nb; ++j) {
       const float4 b = B[j];
 #pragma unroll
@@ -166,6 +169,7 @@ struct CrossEngine {
         gp[p] = last.x - x[p];
       }
       uint32_t k = 0;
+#pragma unroll 1
       for (; k + 3 < n; k += 4) {
         const float4 v0 = s[k], v1 = s[k + 1], v2 = s[k + 2], v3 = s[k + 3];
 #pragma unroll
@@ -183,6 +187,7 @@ struct CrossEngine {
           gp[p] = v3.x - x[p];
         }
       }
+#pragma unroll 1
       for (; k + 1 < n; k += 2) {
         const float4 v0 = s[k], v1 = s[k + 1];
 #pragma unroll
