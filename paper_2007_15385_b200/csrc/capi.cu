@@ -461,15 +461,19 @@ int vpipg_prepare_csr(const uint32_t* offsets, const double* vx, const double* v
   db->kinds = kinds;
   db->offsets.assign(offsets, offsets + npoly + 1);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
+  // fixed-stride 32-byte-aligned blocks: header (2 slots) + n_max + 1 rows
+  uint32_t nmax = 0;
+  for (uint32_t i = 0; i < npoly; ++i) nmax = std::max(nmax, offsets[i + 1] - offsets[i]);
+  const uint32_t stride = (nmax + 3 + 3) & ~3u;
+  const uint64_t slots = uint64_t(npoly) * stride;
   size_t off = 0;
   auto take = [&](size_t bytes) { const size_t o = off; off = align256(off + bytes); return o; };
   const size_t o_offs = take((npoly + 1) * sizeof(uint32_t));
   const size_t o_vx = take(nv * sizeof(double)), o_vy = take(nv * sizeof(double));
   const size_t o_vvx = take(nv * sizeof(double)), o_vvy = take(nv * sizeof(double));
   const size_t o_inner = take(npoly * sizeof(double2)), o_outer = take(nv * sizeof(double2));
-  const size_t o_range = take(npoly * sizeof(uint2));
-  const size_t o_vor = take(nv * sizeof(float4)), o_off = take(nv * sizeof(float4));
-  const size_t o_cross = take(nv * sizeof(float4));
+  const size_t o_gen = take(slots * sizeof(float2)), o_ccw = take(slots * sizeof(float2));
+  const size_t o_raw = take(slots * sizeof(float2));
   const size_t o_status = take(npoly * sizeof(int32_t));
   cudaError_t e = cudaMalloc(&db->blob, off ? off : 256);
   if (e != cudaSuccess) {
@@ -479,6 +483,7 @@ int vpipg_prepare_csr(const uint32_t* offsets, const double* vx, const double* v
   char* b = static_cast<char*>(db->blob);
   CsrPrepArgs a{};
   a.offsets = reinterpret_cast<const uint32_t*>(b + o_offs);
+  a.stride = stride;
   a.vx = reinterpret_cast<const double*>(b + o_vx);
   a.vy = reinterpret_cast<const double*>(b + o_vy);
   a.npoly = npoly;
@@ -487,10 +492,9 @@ int vpipg_prepare_csr(const uint32_t* offsets, const double* vx, const double* v
   a.vvy = reinterpret_cast<double*>(b + o_vvy);
   a.inner = reinterpret_cast<double2*>(b + o_inner);
   a.outer = reinterpret_cast<double2*>(b + o_outer);
-  a.range = reinterpret_cast<uint2*>(b + o_range);
-  a.vor = reinterpret_cast<float4*>(b + o_vor);
-  a.off = reinterpret_cast<float4*>(b + o_off);
-  a.cross = reinterpret_cast<float4*>(b + o_cross);
+  a.gen = reinterpret_cast<float2*>(b + o_gen);
+  a.ccw = reinterpret_cast<float2*>(b + o_ccw);
+  a.raw = reinterpret_cast<float2*>(b + o_raw);
   a.status = reinterpret_cast<int32_t*>(b + o_status);
   std::vector<int32_t> status(npoly);
   do {
@@ -507,7 +511,7 @@ int vpipg_prepare_csr(const uint32_t* offsets, const double* vx, const double* v
     return cuda_code(e);
   }
   if (per_poly_status) std::copy(status.begin(), status.end(), per_poly_status);
-  db->t = DbTables{npoly, kinds, a.range, a.vor, a.off, a.cross};
+  db->t = DbTables{npoly, kinds, stride, a.gen, a.ccw, a.raw};
   db->d_offsets = a.offsets;
   db->d_inner = a.inner;
   db->d_outer = a.outer;

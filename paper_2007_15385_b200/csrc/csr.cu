@@ -4,15 +4,20 @@
 // prep_csr_kernel, one thread per polygon:
 //   validate_polygon (geometry.cpp:53-98) -> per-polygon status, CCW order,
 //   to_voronoi (voronoi.cpp:60-71) with the reference's exact f64 arithmetic,
-//   then fp32 half-plane tables in affine form a*x + b*y + c >= 0 (unit
-//   normal, so the value is a signed distance) for the Voronoi engine (from
-//   the generators: perpendicular bisector of inner and outer[k]) and the
-//   sign-of-offset engine (from the edges, engines.cpp:146-152), and the
-//   crossing table (x, y, dvx/dvy) from the RAW vertices (vpip.cpp:120-128).
-// gather_kernel: every (point, polygon id) pair fetches its own polygon's
-//   rows from the L2-resident tables (per-lane loops of divergent length),
-//   2 FFMA + 1/2 LOP3 per point-edge for the affine engines, the test_f32.cu
-//   crossing arithmetic for ray crossing; ballot words, fused counts.
+//   then compact fp32 rows in a polygon-local frame (centre c = f32 bounding
+//   box centre): the generators [inner, outer_k] (Voronoi), the validated
+//   vertices (sign-of-offset) and the RAW vertices (ray crossing,
+//   vpip.cpp:120-128), 8 bytes per row, each polygon starting on an even row.
+// gather_kernel: every (point, polygon id) pair reads its polygon's 16-byte
+//   header and streams its rows two at a time (16-byte loads) from the
+//   L2-resident tables; q' = q - c is exact in f32 (Sterbenz) for points near
+//   their polygon. Per point-edge:
+//     Voronoi    |q'-pk'|^2 - |q'-p0'|^2 >= 0 (the reference's squared
+//                distances, engines.cpp:85-98): 5 FP ops
+//     offset     a_j*b_i - a_i*b_j >= 0 with (a, b) = q' - v': the cross
+//                product (q - v_j) x (v_i - v_j) of engines.cpp:150-152
+//     crossing   in_range = H_i ^ H_j, on_left = sign(s) ^ H_i (H = [v.y > qy],
+//                s the same cross product), parity by XOR (engines.cpp:187-196)
 #include <climits>
 #include <cmath>
 #include <cstdint>
@@ -31,10 +36,8 @@ struct CsrView {
   __device__ double2 operator()(int k) const { return make_double2(x[k], y[k]); }
 };
 
-__device__ float4 unit_halfplane(double a, double b, double c) {
-  const double s = 1.0 / hypot(a, b);
-  return make_float4(static_cast<float>(a * s), static_cast<float>(b * s),
-                     static_cast<float>(c * s), 0.f);
+__device__ __forceinline__ float2 local(double2 p, double cx, double cy) {
+  return make_float2(static_cast<float>(p.x - cx), static_cast<float>(p.y - cy));
 }
 
 __global__ void prep_csr_kernel(CsrPrepArgs a) {
@@ -42,6 +45,7 @@ __global__ void prep_csr_kernel(CsrPrepArgs a) {
   if (i >= a.npoly) return;
   const uint32_t s = a.offsets[i];
   const int n = static_cast<int>(a.offsets[i + 1] - s);
+  const uint64_t blk = (uint64_t)i * a.stride;
   const CsrView raw{a.vx + s, a.vy + s};
   int status = 0;
   bool rev = false;
@@ -49,122 +53,150 @@ __global__ void prep_csr_kernel(CsrPrepArgs a) {
   if (convex) status = validate_exact(raw, n, &rev);
   double* vvx = a.vvx + s;
   double* vvy = a.vvy + s;
+  double x0 = INFINITY, x1 = -INFINITY, y0 = INFINITY, y1 = -INFINITY;
   for (int k = 0; k < n; ++k) {
     const double2 p = raw(rev ? n - 1 - k : k);
     vvx[k] = p.x;
     vvy[k] = p.y;
+    if (isfinite(p.x) && isfinite(p.y)) {
+      x0 = fmin(x0, p.x); x1 = fmax(x1, p.x);
+      y0 = fmin(y0, p.y); y1 = fmax(y1, p.y);
+    }
   }
+  // polygon-local frame: f32 centre of the bounding box (exactly representable)
+  const float fcx = (x0 <= x1) ? static_cast<float>(0.5 * (x0 + x1)) : 0.f;
+  const float fcy = (y0 <= y1) ? static_cast<float>(0.5 * (y0 + y1)) : 0.f;
+  const double cx = fcx, cy = fcy;
   const CsrView val{vvx, vvy};
   if (status == 0 && (a.kinds & kKindVoronoi)) {
-    double cx, cy;
-    centroid_exact(val, n, &cx, &cy);
-    a.inner[i] = make_double2(cx, cy);
+    double px, py;
+    centroid_exact(val, n, &px, &py);
+    a.inner[i] = make_double2(px, py);
+    a.gen[blk + 2] = local(make_double2(px, py), cx, cy);
     for (int k = 0; k < n && status == 0; ++k) {
       double2 g;
-      status = reflect_exact(val(k), val((k + 1) % n), cx, cy, &g);
+      status = reflect_exact(val(k), val((k + 1) % n), px, py, &g);
       if (status) break;
       a.outer[s + k] = g;
-      // |x - p0|^2 <= |x - pk|^2  <=>  d.(m - x) >= 0, d = pk - p0, m = midpoint
-      const double dx = g.x - cx, dy = g.y - cy;
-      const double mx = 0.5 * (cx + g.x), my = 0.5 * (cy + g.y);
-      a.vor[s + k] = unit_halfplane(-dx, -dy, dx * mx + dy * my);
+      a.gen[blk + 3 + k] = local(g, cx, cy);
     }
   }
-  if (status == 0 && (a.kinds & kKindOffset)) {
-    for (int e = 0; e < n; ++e) {
-      const double2 u = val(e), w = val((e + n - 1) % n);
-      const double dvx = u.x - w.x, dvy = u.y - w.y;
-      a.off[s + e] = unit_halfplane(-dvy, dvx, w.x * dvy - w.y * dvx);
-    }
+  if (status == 0 && (a.kinds & kKindOffset) && n > 0) {
+    a.ccw[blk + 2] = local(val(n - 1), cx, cy);
+    for (int k = 0; k < n; ++k) a.ccw[blk + 3 + k] = local(val(k), cx, cy);
   }
-  if (a.kinds & kKindCrossing) {
-    for (int k = 0; k < n; ++k) {
-      const double2 u = raw(k), w = raw((k + n - 1) % n);
-      const double dvy = u.y - w.y;
-      a.cross[s + k] = make_float4(static_cast<float>(u.x), static_cast<float>(u.y),
-                                   dvy != 0.0 ? static_cast<float>((u.x - w.x) / dvy) : 0.f, 0.f);
-    }
+  if ((a.kinds & kKindCrossing) && n > 0) {
+    a.raw[blk + 2] = local(raw(n - 1), cx, cy);
+    for (int k = 0; k < n; ++k) a.raw[blk + 3 + k] = local(raw(k), cx, cy);
   }
   a.status[i] = status;
   // a failed polygon tests outside under Voronoi / sign-of-offset (crossing
   // ignores the flag: it accepts any polygon)
   const bool bad = convex && status != 0;
-  a.range[i] = make_uint2(s, static_cast<uint32_t>(n) | (bad ? kRangeInvalid : 0u));
+  const float nbits = __uint_as_float(static_cast<uint32_t>(n) | (bad ? kRangeInvalid : 0u));
+  for (float2* t : {a.gen, a.ccw, a.raw}) {
+    t[blk] = make_float2(nbits, 0.f);
+    t[blk + 1] = make_float2(fcx, fcy);
+  }
 }
 
 constexpr int kGP = 4;  // pairs per lane
 constexpr int kGThreads = 256;
 
-template <int kEngine>  // 0 voronoi, 1 offset: affine tables; 2 crossing
+// 32-byte (256-bit) read-only load: four rows (or the header + two rows).
+struct Rows4 {
+  float v[8];
+};
+__device__ __forceinline__ Rows4 ld256(const float2* p) {
+  Rows4 r;
+  asm volatile("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=f"(r.v[0]), "=f"(r.v[1]), "=f"(r.v[2]), "=f"(r.v[3]), "=f"(r.v[4]),
+                 "=f"(r.v[5]), "=f"(r.v[6]), "=f"(r.v[7])
+               : "l"(p));
+  return r;
+}
+
+// Per-engine accumulation over consecutive rows.
+template <int kEngine>
+struct RowAcc {
+  uint32_t acc = 0;
+  float pa = 0.f, pb = 0.f;  // previous row relative to q' (offset / crossing), or |q'-p0'|^2
+  __device__ __forceinline__ void first(float qx, float qy, float rx, float ry) {
+    pa = qx - rx;
+    pb = qy - ry;
+    if (kEngine == 0) pa = fmaf(pa, pa, pb * pb);  // inner_sq
+  }
+  __device__ __forceinline__ void next(float qx, float qy, float rx, float ry) {
+    const float a = qx - rx, b = qy - ry;
+    if (kEngine == 0) {  // |q'-pk'|^2 - |q'-p0'|^2 >= 0 for every outer generator
+      acc |= __float_as_uint(fmaf(a, a, b * b) - pa);
+    } else {
+      const float s = fmaf(pa, b, -(a * pb));  // (q - v_j) x (q - v_i)
+      if (kEngine == 1) {
+        acc |= __float_as_uint(s);
+      } else {
+        const uint32_t hi = __float_as_uint(b), hj = __float_as_uint(pb);
+        acc ^= (hi ^ hj) & (__float_as_uint(s) ^ hi);
+      }
+      pa = a;
+      pb = b;
+    }
+  }
+  __device__ __forceinline__ bool inside() const {
+    return kEngine == 2 ? (acc >> 31) != 0 : !(acc >> 31);
+  }
+};
+
+template <int kEngine>  // 0 voronoi, 1 offset, 2 crossing
 __global__ void __launch_bounds__(kGThreads) gather_kernel(const DbTables t, const GatherArgs a) {
   const int lane = threadIdx.x & 31;
   const uint64_t gwarp = (uint64_t)blockIdx.x * (kGThreads / 32) + (threadIdx.x >> 5);
   const uint64_t stride = (uint64_t)gridDim.x * (kGThreads / 32) * 32 * kGP;
-  const float4* rows = kEngine == 0 ? t.vor : kEngine == 1 ? t.off : t.cross;
+  const float2* tab = kEngine == 0 ? t.gen : kEngine == 1 ? t.ccw : t.raw;
   uint32_t count = 0;
   for (uint64_t base = gwarp * 32 * kGP; base < a.m; base += stride) {
-    float x[kGP], y[kGP];
-    uint32_t start[kGP], n[kGP];
+    float qx[kGP], qy[kGP];
+    const float2* blk[kGP];
+    uint32_t rows[kGP];  // n + 1 rows, 0 when the pair tests outside regardless
     bool ok[kGP];
-    uint32_t nmax = 0;
+    RowAcc<kEngine> r[kGP];
+    uint32_t rmax = 0;
 #pragma unroll
     for (int p = 0; p < kGP; ++p) {
       const uint64_t j = base + 32u * p + lane;
       ok[p] = j < a.m;
       const uint32_t id = ok[p] ? __ldcs(a.ids + j) : 0u;
-      x[p] = ok[p] ? __ldcs(a.xs + j) : 0.f;
-      y[p] = ok[p] ? __ldcs(a.ys + j) : 0.f;
+      const float x = ok[p] ? __ldcs(a.xs + j) : 0.f;
+      const float y = ok[p] ? __ldcs(a.ys + j) : 0.f;
       ok[p] = ok[p] && id < t.npoly;
-      const uint2 r = ok[p] ? __ldg(t.range + id) : make_uint2(0u, 0u);
+      blk[p] = tab + (uint64_t)(ok[p] ? id : 0u) * t.stride;
+      const Rows4 h = ok[p] ? ld256(blk[p]) : Rows4{};
+      const uint32_t nf = __float_as_uint(h.v[0]);
       // a polygon that failed validation only disables the convex engines: ray
       // crossing takes the raw vertices of any polygon (vpip.cpp:120-128)
-      if (kEngine != 2) ok[p] = ok[p] && !(r.y & kRangeInvalid);
-      start[p] = r.x;
-      n[p] = ok[p] ? (r.y & ~kRangeInvalid) : 0u;
-      nmax = n[p] > nmax ? n[p] : nmax;
+      if (kEngine != 2) ok[p] = ok[p] && !(nf & kRangeInvalid);
+      const uint32_t n = nf & ~kRangeInvalid;
+      rows[p] = (ok[p] && n > 0) ? n + 1 : 0u;
+      qx[p] = x - h.v[2];  // exact for points near their polygon (Sterbenz)
+      qy[p] = y - h.v[3];
+      r[p].first(qx[p], qy[p], h.v[4], h.v[5]);
+      if (rows[p] > 1) r[p].next(qx[p], qy[p], h.v[6], h.v[7]);
+      rmax = rows[p] > rmax ? rows[p] : rmax;
     }
-    bool in[kGP];
-    if (kEngine != 2) {
-      uint32_t acc[kGP];
-#pragma unroll
-      for (int p = 0; p < kGP; ++p) acc[p] = 0;
-      for (uint32_t e = 0; e < nmax; ++e) {
-#pragma unroll
-        for (int p = 0; p < kGP; ++p) {
-          if (e < n[p]) {
-            const float4 c = __ldg(rows + start[p] + e);
-            acc[p] |= __float_as_uint(fmaf(c.x, x[p], fmaf(c.y, y[p], c.z)));
-          }
-        }
-      }
-#pragma unroll
-      for (int p = 0; p < kGP; ++p) in[p] = ok[p] && !(acc[p] >> 31);
-    } else {
-      uint32_t par[kGP];
-      float hp[kGP], gp[kGP];
+    for (uint32_t k = 2; k < rmax; k += 4) {  // rows k .. k+3 = slots k+2 .. k+5
 #pragma unroll
       for (int p = 0; p < kGP; ++p) {
-        par[p] = 0;
-        const float4 last = n[p] ? __ldg(rows + start[p] + n[p] - 1) : make_float4(0.f, 0.f, 0.f, 0.f);
-        hp[p] = y[p] - last.y;
-        gp[p] = last.x - x[p];
-      }
-      for (uint32_t k = 0; k < nmax; ++k) {
+        if (k < rows[p]) {
+          const Rows4 q4 = ld256(blk[p] + k + 2);
 #pragma unroll
-        for (int p = 0; p < kGP; ++p) {
-          if (k < n[p]) {
-            const float4 v = __ldg(rows + start[p] + k);
-            const float h = y[p] - v.y;
-            const float d = fmaf(hp[p], v.z, gp[p]);
-            par[p] ^= (__float_as_uint(h) ^ __float_as_uint(hp[p])) & ~__float_as_uint(d);
-            hp[p] = h;
-            gp[p] = v.x - x[p];
-          }
+          for (int u = 0; u < 4; ++u)
+            if (k + u < rows[p]) r[p].next(qx[p], qy[p], q4.v[2 * u], q4.v[2 * u + 1]);
         }
       }
-#pragma unroll
-      for (int p = 0; p < kGP; ++p) in[p] = ok[p] && (par[p] >> 31);
     }
+    bool in[kGP];
+#pragma unroll
+    for (int p = 0; p < kGP; ++p) in[p] = ok[p] && rows[p] > 0 && r[p].inside();
     uint32_t w[kGP];
 #pragma unroll
     for (int p = 0; p < kGP; ++p) {

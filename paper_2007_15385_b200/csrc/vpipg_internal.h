@@ -40,30 +40,39 @@ struct TestArgs {
 // ---- polygon database (CSR batch of polygons; csr.cu) ----
 constexpr uint32_t kRangeInvalid = 0x80000000u;  // polygon failed validation: tests outside
 
+// Gather tables are compact, polygon-local, fixed-stride blocks: polygon i
+// owns `stride` float2 slots starting at slot i * stride (32-byte aligned):
+//   slots 0-1  header (n | kRangeInvalid as u32 bits, unused, f32 centre cx, cy)
+//   slots 2..  n + 1 rows relative to the centre:
+//              Voronoi  [inner, outer_0 .. outer_{n-1}]
+//              offset   [v_{n-1}, v_0 .. v_{n-1}] (validated, CCW)
+//              crossing [v_{n-1}, v_0 .. v_{n-1}] (raw order)
+// so one 32-byte load brings the header with the first two rows and every
+// further load four rows; consecutive rows are the engine's edges.
 struct CsrPrepArgs {
-  const uint32_t* offsets;  // npoly + 1
+  const uint32_t* offsets;  // npoly + 1 (input CSR)
   const double* vx;         // raw vertices (device)
   const double* vy;
   uint32_t npoly;
   uint32_t kinds;
-  double* vvx;              // validated (CCW) vertices
+  uint32_t stride;          // slots per polygon block (multiple of 4)
+  double* vvx;              // validated (CCW) vertices, input CSR layout
   double* vvy;
-  double2* inner;           // npoly generators
-  double2* outer;           // nverts generators
-  uint2* range;             // npoly: (first vertex, n | kRangeInvalid)
-  float4* vor;              // nverts unit half-planes (a, b, c, 0), Voronoi
-  float4* off;              // nverts unit half-planes, sign-of-offset
-  float4* cross;            // nverts (x, y, dvx/dvy, 0), ray crossing (raw order)
+  double2* inner;           // npoly generators (f64, exact)
+  double2* outer;           // nverts generators (f64, exact), input CSR layout
+  float2* gen;              // npoly * stride slots (Voronoi)
+  float2* ccw;              // npoly * stride slots (sign-of-offset)
+  float2* raw;              // npoly * stride slots (ray crossing)
   int32_t* status;          // npoly: 0 or ErrorCode + 1
 };
 
 struct DbTables {
   uint32_t npoly;
   uint32_t kinds;
-  const uint2* range;
-  const float4* vor;
-  const float4* off;
-  const float4* cross;
+  uint32_t stride;
+  const float2* gen;
+  const float2* ccw;
+  const float2* raw;
 };
 
 struct GatherArgs {
