@@ -283,8 +283,8 @@ class PolygonJob:
 
     issue_cycles = ISSUE_CYCLES_PER_PE
     bytes_per_unit = 8  # f32 x + y per test
-    e2e_path = ("vpipg_test_host_multi (C-ABI, pinned host buffers, 4 Mi-point chunks "
-                "double-buffered over 2 streams; one H2D per chunk feeds all 3 engines)")
+    e2e_path = ("vpipg_test_host_multi (C-ABI, pinned host buffers, 16 Mi-point chunks on 3 "
+                "streams; one H2D per chunk feeds all 3 engines)")
 
     def __init__(self, workload, lo, hi, device, torch, vp, stream):
         self.torch = torch
@@ -315,8 +315,8 @@ class JoinJob:
     # affine gather: 2 FFMA + LOP3/2 per point-edge; crossing as in the stream kernel
     issue_cycles = {"voronoi": 3.0, "sign_of_offset": 3.0, "ray_crossing": 6.0}
     bytes_per_unit = 12  # f32 x + y + u32 id per test
-    e2e_path = ("pinned host pairs -> H2D (cudaMemcpyAsync) -> vpipg_test_gather x 3 engines -> "
-                "D2H mask words, all on one stream")
+    e2e_path = ("pinned host pairs -> H2D in 16 Mi-pair chunks over 2 streams -> "
+                "vpipg_test_gather x 3 engines -> D2H mask words")
 
     def __init__(self, workload, lo, hi, device, torch, vp, stream):
         self.torch = torch
@@ -348,17 +348,29 @@ class JoinJob:
         self.dc = t.zeros(3, dtype=t.int64, device=self.xs.device)
 
     def run_host(self, hw, stream):
+        """Chunked pipeline over two streams: H2D of chunk k+1 overlaps the
+        gathers of chunk k (the join has no host-buffer C-ABI entry of its own)."""
         t = self.torch
-        with t.cuda.stream(stream):
-            for dbuf, hbuf in zip(self.d, self.h):
-                dbuf.copy_(hbuf, non_blocking=True)
-            self.dc.zero_()
-            for e in range(3):
-                self.db.test(e, *self.d, words=self.dw[e], count=self.dc[e:e + 1], stream=stream)
-                hw[e].copy_(self.dw[e], non_blocking=True)
-            cnt = self.dc.to("cpu", non_blocking=True)
-        stream.synchronize()
-        return cnt.tolist()
+        m = self.xs.numel()
+        chunk = 1 << 24
+        if not hasattr(self, "streams"):
+            self.streams = [t.cuda.Stream(), t.cuda.Stream()]
+        self.dc.zero_()
+        t.cuda.synchronize()
+        for c, lo in enumerate(range(0, m, chunk)):
+            hi = min(m, lo + chunk)
+            s = self.streams[c % 2]
+            with t.cuda.stream(s):
+                d = [dbuf[lo:hi] for dbuf in self.d]
+                for dst, hbuf in zip(d, self.h):
+                    dst.copy_(hbuf[lo:hi], non_blocking=True)
+                for e in range(3):
+                    w = self.dw[e][lo // 32:(hi + 31) // 32]
+                    self.db.test(e, *d, words=w, count=self.dc[e:e + 1], stream=s)
+                    hw[e][lo // 32:(hi + 31) // 32].copy_(w, non_blocking=True)
+        for s in self.streams:
+            s.synchronize()
+        return self.dc.tolist()
 
 
 # ----------------------------------------------------------------- GPU arm

@@ -359,11 +359,13 @@ int vpipg_test_host_multi(const vpipg_poly* p, uint32_t engines, int dtype, cons
   if (!xs || !ys) return kInvalid;
   DeviceGuard g(p->device);
   const size_t elt = dtype == VPIPG_F64 ? sizeof(double) : sizeof(float);
-  // chunks of 4 Mi points (32-aligned so mask words line up), two in flight:
-  // the points cross PCIe once and every requested engine tests them
-  const uint64_t chunk = std::min<uint64_t>(m, uint64_t(1) << 22);
+  // chunks of 16 Mi points (32-aligned so mask words line up), kSlots in
+  // flight on their own streams: the points cross PCIe once, every requested
+  // engine tests them, and the copy engines stay busy in both directions
+  constexpr int kSlots = 3;
+  const uint64_t chunk = std::min<uint64_t>(m, uint64_t(1) << 24);
   const uint64_t chunk_words = (chunk + 31) / 32;
-  cudaStream_t st[2];
+  cudaStream_t st[kSlots];
   for (auto& s : st) VPIPG_TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
   struct Slot {
     void* x = nullptr;
@@ -371,13 +373,13 @@ int vpipg_test_host_multi(const vpipg_poly* p, uint32_t engines, int dtype, cons
     uint32_t* w[3] = {nullptr, nullptr, nullptr};
     uint8_t* b[3] = {nullptr, nullptr, nullptr};
     unsigned long long* c = nullptr;
-  } slot[2];
+  } slot[kSlots];
   int rc = kOk;
   auto fail = [&](cudaError_t e) {
     if (e != cudaSuccess && rc == kOk) rc = cuda_code(e);
     return rc != kOk;
   };
-  for (int i = 0; i < 2 && rc == kOk; ++i) {
+  for (int i = 0; i < kSlots && rc == kOk; ++i) {
     if (fail(cudaMallocAsync(&slot[i].x, chunk * elt, st[i]))) break;
     if (fail(cudaMallocAsync(&slot[i].y, chunk * elt, st[i]))) break;
     for (int k = 0; k < ne && rc == kOk; ++k) {
@@ -393,7 +395,7 @@ int vpipg_test_host_multi(const vpipg_poly* p, uint32_t engines, int dtype, cons
   const char* hx = static_cast<const char*>(xs);
   const char* hy = static_cast<const char*>(ys);
   for (uint64_t base = 0, c = 0; rc == kOk && base < m; base += chunk, ++c) {
-    const int i = static_cast<int>(c & 1);
+    const int i = static_cast<int>(c % kSlots);
     const uint64_t len = std::min<uint64_t>(chunk, m - base);
     if (fail(cudaMemcpyAsync(slot[i].x, hx + base * elt, len * elt, cudaMemcpyHostToDevice, st[i]))) break;
     if (fail(cudaMemcpyAsync(slot[i].y, hy + base * elt, len * elt, cudaMemcpyHostToDevice, st[i]))) break;
@@ -410,8 +412,8 @@ int vpipg_test_host_multi(const vpipg_poly* p, uint32_t engines, int dtype, cons
         break;
     }
   }
-  unsigned long long cnt[2][3] = {{0, 0, 0}, {0, 0, 0}};
-  for (int i = 0; i < 2; ++i) {
+  unsigned long long cnt[kSlots][3] = {};
+  for (int i = 0; i < kSlots; ++i) {
     if (rc == kOk && slot[i].c) fail(cudaMemcpyAsync(cnt[i], slot[i].c, 24, cudaMemcpyDeviceToHost, st[i]));
     void* ptrs[] = {slot[i].x, slot[i].y, slot[i].w[0], slot[i].w[1], slot[i].w[2],
                     slot[i].b[0], slot[i].b[1], slot[i].b[2], slot[i].c};
@@ -423,7 +425,10 @@ int vpipg_test_host_multi(const vpipg_poly* p, uint32_t engines, int dtype, cons
     cudaStreamDestroy(s);
   }
   if (rc == kOk && inside)
-    for (int k = 0; k < ne; ++k) inside[eng[k]] = cnt[0][eng[k]] + cnt[1][eng[k]];
+    for (int k = 0; k < ne; ++k) {
+      inside[eng[k]] = 0;
+      for (int i = 0; i < kSlots; ++i) inside[eng[k]] += cnt[i][eng[k]];
+    }
   return rc;
 }
 
