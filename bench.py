@@ -227,7 +227,10 @@ def time_cpu_reference(name: str, sample: int, reps: int, warmup: int):
             if rr >= warmup:
                 per_rep.append(t)
         t = statistics.median(per_rep)
-        return 3 * xs.size / t, kind, cores, t
+        desc = (f"first {xs.size} pairs of the C4 stream (f32 widened to f64), pairs grouped by "
+                f"polygon id (untimed), one reference *_contains_batch call per polygon, "
+                f"polygons split over {cores} threads, 3 engines")
+        return 3 * xs.size / t, kind, cores, t, desc
     vx, vy, xs, ys = cpu_reference_sample(name, sample)
     try:
         ref = oracle.Reference()
@@ -247,23 +250,23 @@ def time_cpu_reference(name: str, sample: int, reps: int, warmup: int):
         if r >= warmup:
             per_rep.append(t)
     t = statistics.median(per_rep)
-    return 3 * xs.size / t, kind, cores, t
+    desc = (f"first {xs.size} points of the workload stream (f32 rounded, widened to f64), "
+            f"3 engines, *_contains_batch(threads={cores}) timed like bench.cpp:196-199")
+    return 3 * xs.size / t, kind, cores, t, desc
 
 
 def run_reference_arm(args, rank: int, world: int):
     if rank != 0:
         return
     steps, warmup = args.steps, args.warmup
-    value, kind, cores, t = time_cpu_reference(args.workload, args.cpu_sample, steps, warmup)
+    value, kind, cores, t, desc = time_cpu_reference(args.workload, args.cpu_sample, steps, warmup)
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": steps, "warmup": warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": config_block(args, world),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind,
-                         "sample": f"first {args.cpu_sample} points of the workload stream "
-                                   "(f32 rounded, widened to f64), 3 engines per step, "
-                                   "*_contains_batch(threads=cores) timed like bench.cpp:196-199"},
+                         "sample": desc + f"; median of {steps} steps after {warmup} warm-up"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -494,11 +497,10 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        v, kind, cores, t = time_cpu_reference(args.workload, args.cpu_sample, reps=3, warmup=1)
+        v, kind, cores, t, desc = time_cpu_reference(args.workload, args.cpu_sample, reps=3,
+                                                     warmup=1)
         cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": kind,
-               "sample": f"first {args.cpu_sample} points of the same stream (f32 widened to "
-                         f"f64), 3 engines, threads={cores}, median of 3 after 1 warm-up; "
-                         f"{t * 1e3:.1f} ms per 3-engine pass"}
+               "sample": f"{desc}; median of 3 after 1 warm-up, {t * 1e3:.1f} ms per pass"}
 
     if world > 1:
         dist.barrier()
@@ -529,9 +531,8 @@ def main():
     compute_bound = (4 * pe / (fma_tflops * 1e12)) > (bytes_per_launch / (hbm_peak * 1e9))
     traffic = None
     try:  # DRAM bytes per launch from the committed ncu --set full capture (same kernel/config)
-        tj = json.loads(TRAFFIC_FILE.read_text())
-        if tj["workload"] == args.workload:
-            traffic = tj["dram_bytes_per_launch"][dk["engine"]] * m / tj["points"]
+        tj = json.loads(TRAFFIC_FILE.read_text())[args.workload]
+        traffic = tj["dram_bytes_per_launch"][dk["engine"]] * m / tj["points"]
     except Exception:
         pass
     if compute_bound:
@@ -546,7 +547,8 @@ def main():
                  "per_unit": f"{bytes_per_launch / m:.3f} B and {4 * n_edges} flops per test "
                              f"(n={n_edges} edges, 4 flops per point-edge)",
                  "algorithmic_bytes_per_launch": bytes_per_launch,
-                 "traffic_source": "profiles/traffic_r01.json (ncu dram__bytes_read+write)",
+                 "traffic_source": "profiles/traffic_r01.json (ncu --set full dram__bytes_read+write "
+                                   "of this kernel on this workload, scaled to this launch)",
                  "issue_model_frac": dk["issue_model_frac"]})
 
     step_s = ms_max * 1e-3 / args.steps
