@@ -281,6 +281,8 @@ class Reference:
         L.vr_scalar.argtypes = [C.c_void_p, C.c_int, C.c_double, C.c_double]
         L.vr_run_validation.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_double,
                                         C.POINTER(C.c_uint64)]
+        L.vr_read_bench_csv.restype = C.c_long
+        L.vr_read_bench_csv.argtypes = [C.c_char_p, _D]
         u32p = C.POINTER(C.c_uint32)
         L.vr_join_new.restype = C.c_void_p
         L.vr_join_new.argtypes = [u32p, _D, _D, C.c_uint32, _D, _D, u32p, sz]
@@ -288,6 +290,12 @@ class Reference:
         L.vr_join_run.restype = C.c_uint64
         L.vr_join_run.argtypes = [C.c_void_p, C.c_int, C.c_int, _U8]
         self.L = L
+
+    def read_bench_csv(self, text: str):
+        """The reference's read_bench_csv + median: (#records, medians[3][13] for n=3..15)."""
+        med = np.zeros(39)
+        n = self.L.vr_read_bench_csv(text.encode(), _d(med))
+        return n, med.reshape(3, 13)
 
     def run_validation(self, vx, vy, xs, ys, band=1e-9, threads=1):
         """The reference's run_validation: ({pair counts}, disagreeing, pass)."""

@@ -11,6 +11,7 @@
 #include <cstdint>
 #include <cstring>
 #include <optional>
+#include <sstream>
 #include <thread>
 #include <vector>
 
@@ -288,6 +289,25 @@ int vr_run_validation(void* poly, void* batch, int threads, double band, uint64_
   counts[3] = r.disagreeing_points;
   counts[4] = r.pass ? 1 : 0;
   return 0;
+}
+
+// read_bench_csv (bench.cpp:177-208) on a CSV text; returns the record count
+// (or -1 on a parse error) and the median Query wall time per (engine, n) in
+// `medians` laid out [engine][n - 3] for n = 3..15 (0 when absent).
+long vr_read_bench_csv(const char* text, double* medians) {
+  try {
+    std::istringstream in(text);
+    const std::vector<vpip::BenchRecord> recs = vpip::read_bench_csv(in);
+    std::vector<double> t[3][13];
+    for (const vpip::BenchRecord& r : recs)
+      if (r.phase == vpip::BenchPhase::Query && r.n_edges >= 3 && r.n_edges <= 15)
+        t[static_cast<int>(r.engine)][r.n_edges - 3].push_back(static_cast<double>(r.wall_time_ns));
+    for (int e = 0; e < 3; ++e)
+      for (int i = 0; i < 13; ++i) medians[e * 13 + i] = t[e][i].empty() ? 0.0 : vpip::median(t[e][i]);
+    return static_cast<long>(recs.size());
+  } catch (const vpip::Error&) {
+    return -1;
+  }
 }
 
 int vr_scalar(void* poly, int engine, double px, double py) {

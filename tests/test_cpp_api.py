@@ -3,6 +3,7 @@ import importlib.util
 import subprocess
 from pathlib import Path
 
+import numpy as np
 import pytest
 
 HERE = Path(__file__).resolve().parent
@@ -25,3 +26,30 @@ def test_cpp_api_on_gpu():
     r = subprocess.run([str(binary)], capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "0 failed" in r.stdout
+
+
+@pytest.mark.gpu
+def test_gpu_bench_records_in_reference_csv_schema():
+    """§8(f)4: run_benchmark on the GPU drop-in writes the reference CSV schema;
+    the reference's own read_bench_csv parses it, and acceptance criterion 6's
+    shape checks (acceptance.cpp:211-255) hold on the GPU medians."""
+    import sys
+    sys.path.insert(0, str(HERE.parent / "tools"))
+    import gpu_run_benchmark as gb
+    import oracle
+    recs = gb.run_benchmark(batch=200_000, reps=5)
+    csv = gb.to_csv(recs)
+    assert csv.splitlines()[0] == gb.HEADER
+    assert len(recs) == 13 + 3 * 13 * 5
+    if not oracle.REF_SO.exists():
+        pytest.skip("oracle/_ref not built")
+    n, med = oracle.Reference().read_bench_csv(csv)
+    assert n == len(recs)
+    for e in range(3):
+        for i in range(1, 13):
+            # monotone within 10 % (the GPU drop-in is transfer-bound and flat in
+            # n, so a drop under a 50 us noise floor is also accepted)
+            assert med[e, i] >= 0.9 * med[e, i - 1] or med[e, i - 1] - med[e, i] < 5e4, (e, i)
+    # voronoi within 4x of sign-of-offset at every n
+    assert (np.maximum(med[0] / med[1], med[1] / med[0]) <= 4.0).all()
+    assert med[0, 12] / med[0, 0] <= 6.0
