@@ -90,6 +90,13 @@ def build(verbose: bool = False) -> Path:
     if jobs or _stale(LIB, objs):
         _run([NVCC, *ARCH, "-shared", "-o", str(LIB), *map(str, objs), "-cudart", "static",
               "-Xlinker", "--no-undefined", "-lrt", "-lpthread", "-ldl"])
+    cli = PKG / "bin" / "vpipg"
+    cli_src = CSRC / "cli" / "vpipg_cli.cpp"
+    if _stale(cli, [cli_src, LIB] + hdrs):
+        cli.parent.mkdir(exist_ok=True)
+        _run(["g++", *CXX_FLAGS, str(cli_src), "-o", str(cli), f"-L{LIB.parent}", "-lvpipg",
+              f"-L{CUDA_HOME / 'lib64'}", "-lcudart", "-Wl,-rpath,$ORIGIN/../lib",
+              f"-Wl,-rpath,{CUDA_HOME / 'lib64'}"])
     if verbose:
         print(f"built {LIB}")
     return LIB

@@ -1,0 +1,82 @@
+"""`vpipg` CLI: the GPU drop-in for `vpip test|convert|validate`, mirroring the
+reference's own CLI smoke test (proj/tests/cli_smoke.sh:11-66), plus PIPB in /
+PIPM out against the reference masks (§8(f)3)."""
+import struct
+import subprocess
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+from conftest import unpack
+
+ROOT = Path(__file__).resolve().parents[1]
+BIN = ROOT / "paper_2007_15385_b200" / "bin" / "vpipg"
+
+
+def run(*args, cwd):
+    return subprocess.run([str(BIN), *map(str, args)], cwd=cwd, capture_output=True, text=False)
+
+
+@pytest.fixture
+def files(tmp_path):
+    (tmp_path / "square.json").write_text('{"vertices": [[0,0],[1,0],[1,1],[0,1]]}\n')
+    (tmp_path / "square.csv").write_text("0,0\n1,0\n1,1\n0,1\n")
+    (tmp_path / "pts.csv").write_text("0.5,0.5\n2,2\n1,0.5\n")
+    (tmp_path / "arrow.csv").write_text("0,0\n4,0\n4,4\n2,1\n0,4\n")
+    (tmp_path / "notch.csv").write_text("2,2\n")
+    (tmp_path / "bad.json").write_text('{"vertices": [[0,0],[1,0]]}\n')
+    return tmp_path
+
+
+def test_input_errors_exit_2_without_a_device(files):
+    assert run("convert", "--polygon", "missing.json", cwd=files).returncode == 2
+    assert run("test", "--polygon", "square.json", cwd=files).returncode == 2  # usage
+    assert run("frobnicate", cwd=files).returncode == 2
+    (files / "junk.csv").write_text("0,0\n1,x\n")
+    assert run("test", "--polygon", "junk.csv", "--points", "pts.csv", "--engine", "voronoi",
+               cwd=files).returncode == 2
+
+
+@pytest.mark.gpu
+def test_cli_smoke(files):
+    for poly, e in [("square.json", "voronoi"), ("square.csv", "offset"), ("square.csv", "crossing")]:
+        r = run("test", "--polygon", poly, "--points", "pts.csv", "--engine", e, "--out",
+                f"mask_{e}.csv", cwd=files)
+        assert r.returncode == 0, r.stderr
+        assert (files / f"mask_{e}.csv").read_text() == "1\n0\n1\n"
+        assert b"2 of 3 points inside" in r.stderr
+    r = run("test", "--polygon", "square.csv", "--points", "pts.csv", "--engine", "voronoi",
+            "--format", "binary", "--out", "mask.bin", cwd=files)
+    data = (files / "mask.bin").read_bytes()
+    assert r.returncode == 0 and len(data) == 17 and data[:4] == b"PIPM" and data[16] == 0b101
+    r = run("test", "--polygon", "arrow.csv", "--points", "notch.csv", "--engine", "crossing",
+            "--out", "mask_n.csv", cwd=files)
+    assert r.returncode == 0 and (files / "mask_n.csv").read_text() == "0\n"
+    assert run("test", "--polygon", "arrow.csv", "--points", "notch.csv", "--engine", "offset",
+               cwd=files).returncode == 2
+    r = run("validate", "--polygon", "square.json", "--count", "20000", "--seed", "7", cwd=files)
+    assert r.returncode == 0 and b"PASS" in r.stdout
+    r = run("convert", "--polygon", "square.json", "--out", "gens.json", cwd=files)
+    text = (files / "gens.json").read_text()
+    assert r.returncode == 0 and '"inner": [0.5, 0.5]' in text and '"outer"' in text
+    assert run("convert", "--polygon", "bad.json", cwd=files).returncode == 2
+
+
+@pytest.mark.gpu
+def test_pipb_in_pipm_out_equals_reference(files, golden, orc):
+    name = "c1_sample"
+    vx, vy = golden[f"case_{name}_v"]
+    xs, ys = golden[f"case_{name}_pts"].astype(np.float64)
+    (files / "poly.csv").write_text("".join(f"{x!r},{y!r}\n" for x, y in zip(vx, vy)))
+    inter = np.empty(2 * xs.size)
+    inter[0::2], inter[1::2] = xs, ys
+    (files / "pts.pipb").write_bytes(b"PIPB" + struct.pack("<IQ", 1, xs.size) + inter.tobytes())
+    for e, eng in enumerate(("voronoi", "offset", "crossing")):
+        r = run("test", "--polygon", "poly.csv", "--points", "pts.pipb", "--engine", eng,
+                "--format", "binary", "--out", f"m{e}.pipm", cwd=files)
+        assert r.returncode == 0, r.stderr
+        data = (files / f"m{e}.pipm").read_bytes()
+        assert data[:4] == b"PIPM" and struct.unpack("<IQ", data[4:16]) == (1, xs.size)
+        want = unpack(golden[f"case_{name}_masks"][e], xs.size)
+        assert data[16:] == orc.pack(want).tobytes(), eng  # bit-exact PIPM payload
