@@ -68,7 +68,7 @@ def test_pipb_in_pipm_out_equals_reference(files, golden, orc):
     name = "c1_sample"
     vx, vy = golden[f"case_{name}_v"]
     xs, ys = golden[f"case_{name}_pts"].astype(np.float64)
-    (files / "poly.csv").write_text("".join(f"{x!r},{y!r}\n" for x, y in zip(vx, vy)))
+    (files / "poly.csv").write_text("".join(f"{float(x)!r},{float(y)!r}\n" for x, y in zip(vx, vy)))
     inter = np.empty(2 * xs.size)
     inter[0::2], inter[1::2] = xs, ys
     (files / "pts.pipb").write_bytes(b"PIPB" + struct.pack("<IQ", 1, xs.size) + inter.tobytes())
