@@ -65,6 +65,9 @@ struct SlabEngine {
     float ox, oy;
   };
   static size_t table_bytes(const Params& p) { return (size_t)p.tab.total * sizeof(float2); }
+  __device__ static const float4* global_table(const Params& p) {
+    return reinterpret_cast<const float4*>(p.tab.coef);
+  }
 
   __device__ static void stage(const Params& p, float4* s) {
     const float4* src = reinterpret_cast<const float4*>(p.tab.coef);
@@ -147,6 +150,7 @@ struct CrossEngine {
     float ox, oy;
   };
   static size_t table_bytes(const Params& p) { return (size_t)p.tab.n * sizeof(float4); }
+  __device__ static const float4* global_table(const Params& p) { return p.tab.vert; }
 
   __device__ static void stage(const Params& p, float4* s) {
     for (uint32_t i = threadIdx.x; i < p.tab.n; i += blockDim.x) s[i] = p.tab.vert[i];
@@ -282,7 +286,10 @@ __device__ __forceinline__ uint32_t guarded_tile(const typename Eng::Params& prm
   return emit<true, P>(slack, base, a, lane);
 }
 
-template <class Eng>
+// kSmemTab: the polygon table is staged in shared memory once per CTA (the
+// normal case); polygons whose table exceeds kSmemTableMax read it from global
+// memory with warp-uniform loads instead.
+template <class Eng, bool kSmemTab>
 __global__ void __launch_bounds__(kThreads, 2)
     stream_kernel(const typename Eng::Params prm, const TestArgs a, const uint64_t full_slices) {
   constexpr int P = Eng::kP;
@@ -295,7 +302,7 @@ __global__ void __launch_bounds__(kThreads, 2)
                                                (size_t)kWarps * kStages * 2 * kWarpPts);
   uint64_t* full = bars + warp * 2 * kStages;
   uint64_t* empty = full + kStages;
-  float4* tab = reinterpret_cast<float4*>(bars + kWarps * 2 * kStages);
+  float4* s_tab = reinterpret_cast<float4*>(bars + kWarps * 2 * kStages);
   if (lane == 0) {
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&full[s], 1);
@@ -303,7 +310,8 @@ __global__ void __launch_bounds__(kThreads, 2)
     }
     mbar_fence_init();
   }
-  Eng::stage(prm, tab);
+  if (kSmemTab) Eng::stage(prm, s_tab);
+  const float4* tab = kSmemTab ? s_tab : Eng::global_table(prm);
   __syncthreads();
 
   const uint64_t W = (uint64_t)gridDim.x * kWarps;
@@ -354,13 +362,16 @@ __global__ void __launch_bounds__(kThreads, 2)
   flush_count(count, a);
 }
 
-template <class Eng>
+template <class Eng, bool kSmemTab>
 __global__ void __launch_bounds__(kThreads) generic_kernel(const typename Eng::Params prm,
                                                           const TestArgs a) {
   constexpr int kWarpPts = 32 * Eng::kP;
-  extern __shared__ __align__(16) float4 gtab[];
-  Eng::stage(prm, gtab);
-  __syncthreads();
+  extern __shared__ __align__(16) float4 s_gtab[];
+  if (kSmemTab) {
+    Eng::stage(prm, s_gtab);
+    __syncthreads();
+  }
+  const float4* gtab = kSmemTab ? s_gtab : Eng::global_table(prm);
   const int lane = threadIdx.x & 31;
   const uint64_t gwarp = (uint64_t)blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5);
   uint32_t count = 0;
@@ -380,14 +391,17 @@ int sm_count() {
   return sms;
 }
 
+constexpr size_t kSmemTableMax = 96 * 1024;
+
 template <class Eng>
 cudaError_t launch(const typename Eng::Params& prm, const TestArgs& a, cudaStream_t stream) {
   constexpr int kWarpPts = 32 * Eng::kP;
-  const size_t tab = Eng::table_bytes(prm);
+  const bool staged = Eng::table_bytes(prm) <= kSmemTableMax;
+  const size_t tab = staged ? Eng::table_bytes(prm) : 0;
   const bool aligned = ((reinterpret_cast<uintptr_t>(a.xs) | reinterpret_cast<uintptr_t>(a.ys)) & 15) == 0;
   const uint64_t full_slices = aligned ? a.m / kWarpPts : 0;
   if (full_slices < kWarps) {
-    auto k = generic_kernel<Eng>;
+    auto k = staged ? generic_kernel<Eng, true> : generic_kernel<Eng, false>;
     if (tab > 48 * 1024) {
       cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tab);
       if (e != cudaSuccess) return e;
@@ -398,7 +412,7 @@ cudaError_t launch(const typename Eng::Params& prm, const TestArgs& a, cudaStrea
     k<<<(int)(blocks < cap ? blocks : cap), kThreads, tab, stream>>>(prm, a);
     return cudaGetLastError();
   }
-  auto k = stream_kernel<Eng>;
+  auto k = staged ? stream_kernel<Eng, true> : stream_kernel<Eng, false>;
   const size_t smem = (size_t)kWarps * kStages * 2 * kWarpPts * sizeof(float) +
                       (size_t)kWarps * 2 * kStages * sizeof(uint64_t) + tab;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

@@ -54,22 +54,30 @@ __device__ __forceinline__ void flush_count(uint32_t cnt, const TestArgs& a) {
   if ((threadIdx.x & 31) == 0 && a.inside && cnt) atomicAdd(a.inside, (unsigned long long)cnt);
 }
 
-template <int kEngine, int P>
+// kSmem: per-edge records staged in shared memory (small polygons) or read
+// straight from global memory with warp-uniform addresses (any n).
+template <int kEngine, int P, bool kSmem>
 __global__ void __launch_bounds__(kThreads) exact_kernel(const DevTables t, const TestArgs a) {
-  extern __shared__ double4 s_tab[];
+  extern __shared__ double4 s_dyn[];
   const uint32_t n = t.n;
-  // stage the per-edge records
+  const void* s_tab;
   if (kEngine == 0) {
-    double2* s = reinterpret_cast<double2*>(s_tab);
-    for (uint32_t i = threadIdx.x; i < n; i += kThreads) s[i] = t.outer[i];
+    double2* s = reinterpret_cast<double2*>(s_dyn);
+    if (kSmem)
+      for (uint32_t i = threadIdx.x; i < n; i += kThreads) s[i] = t.outer[i];
+    s_tab = kSmem ? static_cast<const void*>(s) : t.outer;
   } else if (kEngine == 1) {
-    OffsetEdgeF64* s = reinterpret_cast<OffsetEdgeF64*>(s_tab);
-    for (uint32_t i = threadIdx.x; i < n; i += kThreads) s[i] = t.off[i];
+    OffsetEdgeF64* s = reinterpret_cast<OffsetEdgeF64*>(s_dyn);
+    if (kSmem)
+      for (uint32_t i = threadIdx.x; i < n; i += kThreads) s[i] = t.off[i];
+    s_tab = kSmem ? static_cast<const void*>(s) : t.off;
   } else {
-    RayEdgeF64* s = reinterpret_cast<RayEdgeF64*>(s_tab);
-    for (uint32_t i = threadIdx.x; i < n; i += kThreads) s[i] = t.ray[i];
+    RayEdgeF64* s = reinterpret_cast<RayEdgeF64*>(s_dyn);
+    if (kSmem)
+      for (uint32_t i = threadIdx.x; i < n; i += kThreads) s[i] = t.ray[i];
+    s_tab = kSmem ? static_cast<const void*>(s) : t.ray;
   }
-  __syncthreads();
+  if (kSmem) __syncthreads();
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   const double* xs = static_cast<const double*>(a.xs);
@@ -89,7 +97,7 @@ __global__ void __launch_bounds__(kThreads) exact_kernel(const DevTables t, cons
       y[p] = ok ? __ldcs(ys + idx) : 0.0;
     }
     if (kEngine == 0) {
-      const double2* s = reinterpret_cast<const double2*>(s_tab);
+      const double2* s = static_cast<const double2*>(s_tab);
       double inner_sq[P];
 #pragma unroll
       for (int p = 0; p < P; ++p) {
@@ -107,7 +115,7 @@ __global__ void __launch_bounds__(kThreads) exact_kernel(const DevTables t, cons
         }
       }
     } else if (kEngine == 1) {
-      const OffsetEdgeF64* s = reinterpret_cast<const OffsetEdgeF64*>(s_tab);
+      const OffsetEdgeF64* s = static_cast<const OffsetEdgeF64*>(s_tab);
       uint32_t flags[P];
 #pragma unroll
       for (int p = 0; p < P; ++p) flags[p] = 0;
@@ -122,7 +130,7 @@ __global__ void __launch_bounds__(kThreads) exact_kernel(const DevTables t, cons
 #pragma unroll
       for (int p = 0; p < P; ++p) in[p] = (flags[p] == 0u) | (flags[p] == n);
     } else {
-      const RayEdgeF64* s = reinterpret_cast<const RayEdgeF64*>(s_tab);
+      const RayEdgeF64* s = static_cast<const RayEdgeF64*>(s_tab);
       bool parity[P], on_edge[P];
 #pragma unroll
       for (int p = 0; p < P; ++p) { parity[p] = false; on_edge[p] = false; }
@@ -152,8 +160,9 @@ template <int kEngine>
 cudaError_t launch_one(const DevTables& t, const TestArgs& a, size_t rec_bytes,
                        cudaStream_t stream) {
   constexpr int P = 4;
-  auto k = exact_kernel<kEngine, P>;
-  const size_t smem = (size_t)t.n * rec_bytes;
+  const bool staged = (size_t)t.n * rec_bytes <= 96 * 1024;
+  auto k = staged ? exact_kernel<kEngine, P, true> : exact_kernel<kEngine, P, false>;
+  const size_t smem = staged ? (size_t)t.n * rec_bytes : 0;
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;

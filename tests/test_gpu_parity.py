@@ -262,3 +262,27 @@ def test_generator_set_handle(golden):
         assert np.array_equal(b, want)
         with pytest.raises(vp.VpipError):  # offset tables were not prepared
             run_device(p, 1, xs, ys)
+
+
+@pytest.mark.parametrize("n", [1024, 10000])
+def test_many_edge_polygons_use_global_tables(orc, n):
+    """Polygons whose edge tables exceed the shared-memory staging budget (the
+    f64 ray records at n=1024 already do) read them from global memory;
+    results stay exact (f64) / band-exact (f32)."""
+    vx, vy = orc.regular_polygon(n, 1.0)
+    xs, ys = orc.sample_points(20_000, (-1.2, -1.2, 1.2, 1.2), 31 + n)
+    # add points hugging the boundary: the interesting region for many edges
+    t = np.linspace(0, 2 * np.pi, 5000, endpoint=False)
+    xs = np.concatenate([xs, 0.99999 * np.cos(t), 1.00001 * np.cos(t)])
+    ys = np.concatenate([ys, 0.99999 * np.sin(t), 1.00001 * np.sin(t)])
+    want = orc.masks(vx, vy, xs, ys)
+    with vp.PreparedPolygon.prepare(vx, vy, vp.KIND_ALL) as p:
+        for e in range(3):
+            _, b, c = run_device(p, e, xs, ys)
+            assert np.array_equal(b, want[e]), (n, e)
+            _, b32, _ = run_device(p, e, xs.astype(np.float32), ys.astype(np.float32))
+            want32 = orc.masks(vx, vy, xs.astype(np.float32).astype(np.float64),
+                               ys.astype(np.float32).astype(np.float64))[e]
+            band = band_mask(orc, vx, vy, xs.astype(np.float32).astype(np.float64),
+                             ys.astype(np.float32).astype(np.float64))
+            assert not np.any((b32 != want32) & ~band), (n, e)
