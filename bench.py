@@ -493,7 +493,8 @@ def main():
         e2e = {"value": 3 * M / float(t_e2e.item()), "unit": UNIT,
                "h2d_bytes_per_step": job.bytes_per_unit * m,
                "d2h_bytes_per_step": 3 * 4 * ((m + 31) // 32),
-               "steps": args.e2e_steps, "path": job.e2e_path}
+               "steps": args.e2e_steps, "step_ms": [round(t * 1e3, 2) for t in times],
+               "path": job.e2e_path}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

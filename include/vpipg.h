@@ -109,8 +109,9 @@ int vpipg_test(const vpipg_poly* poly, int engine, int dtype, const void* xs, co
                unsigned long long* d_inside, void* stream);
 
 /* Same with HOST buffers (pageable or pinned): chunked host->device copies,
- * the test kernel and device->host mask copies are pipelined over two
- * streams on `device`. Synchronous; *inside receives the count (may be NULL).
+ * the test kernel and device->host mask copies are pipelined over three
+ * streams on `device`, through a per-device staging area kept between
+ * calls. Synchronous; *inside receives the count (may be NULL).
  * This is the path the vpip:: C++ shim uses. */
 int vpipg_test_host(const vpipg_poly* poly, int engine, int dtype, const void* xs,
                     const void* ys, uint64_t m, uint32_t* mask_words, uint8_t* mask_bytes,
@@ -123,6 +124,10 @@ int vpipg_test_host(const vpipg_poly* poly, int engine, int dtype, const void* x
 int vpipg_test_host_multi(const vpipg_poly* poly, uint32_t engines, int dtype, const void* xs,
                           const void* ys, uint64_t m, uint32_t* const* mask_words,
                           uint8_t* const* mask_bytes, uint64_t* inside);
+
+/* Frees the per-device staging (chunk buffers and streams) the host-buffer
+ * calls keep between calls; the next host call re-creates it. */
+int vpipg_release_staging(int device);
 
 /* Instrumented work counters of voronoi_contains_batch(..., BatchStats&)
  * (engines.cpp:256-273): the branch-free kernels perform exactly

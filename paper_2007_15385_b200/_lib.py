@@ -51,6 +51,7 @@ SIGNATURES = {
                                   C.POINTER(C.c_uint64)]),
     "vpipg_test_host_multi": (C.c_int, [_P, C.c_uint32, C.c_int, _P, _P, C.c_uint64, _P, _P,
                                         C.POINTER(C.c_uint64)]),
+    "vpipg_release_staging": (C.c_int, [C.c_int]),
     "vpipg_voronoi_work": (C.c_int, [_P, C.c_uint64, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
     "vpipg_fill_uniform_points": (C.c_int, [C.c_uint64, C.c_uint64, C.c_uint64, C.c_double,
                                             C.c_double, C.c_double, C.c_double, C.c_int, _P, _P, _P]),

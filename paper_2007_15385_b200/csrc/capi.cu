@@ -346,6 +346,93 @@ int vpipg_test(const vpipg_poly* p, int engine, int dtype, const void* xs, const
   return dispatch(p, engine, dtype, a, static_cast<cudaStream_t>(stream));
 }
 
+namespace {
+
+// Per-device staging for the host-buffer path: kSlots chunk slots (points,
+// mask words, mask bytes, counts) and their streams, allocated on first use,
+// grown on demand and kept for the life of the process (vpipg_release_staging
+// frees them), so a steady stream of host batches pays no allocation, stream
+// creation or pool trimming per call. Calls on one device serialise on its
+// mutex -- they share the PCIe link anyway.
+constexpr int kSlots = 3;
+constexpr uint64_t kChunk = uint64_t(1) << 24;  // 16 Mi points, 32-aligned
+
+struct Staging {
+  std::mutex mu;
+  cudaStream_t st[kSlots] = {};
+  char* buf[kSlots] = {};
+  size_t cap = 0;  // bytes per slot
+};
+
+Staging& staging(int device) {
+  static Staging s[64];
+  return s[device];
+}
+
+struct SlotView {
+  void* x;
+  void* y;
+  uint32_t* w[3];
+  uint8_t* b[3];
+  unsigned long long* c;
+};
+
+size_t slot_bytes(uint64_t chunk, size_t elt, bool bytes) {
+  const uint64_t words = (chunk + 31) / 32;
+  return 2 * align256(chunk * elt) + 3 * align256(words * 4) + (bytes ? 3 * align256(chunk) : 0) + 256;
+}
+
+SlotView slot_view(char* b, uint64_t chunk, size_t elt, bool bytes) {
+  SlotView v{};
+  size_t off = 0;
+  auto take = [&](size_t n) { char* q = b + off; off += align256(n); return q; };
+  v.x = take(chunk * elt);
+  v.y = take(chunk * elt);
+  for (auto& w : v.w) w = reinterpret_cast<uint32_t*>(take((chunk + 31) / 32 * 4));
+  for (auto& q : v.b) q = bytes ? reinterpret_cast<uint8_t*>(take(chunk)) : nullptr;
+  v.c = reinterpret_cast<unsigned long long*>(take(24));
+  return v;
+}
+
+// Caller holds st.mu and the device guard.
+int staging_reserve(Staging& st, size_t need) {
+  if (!st.st[0])
+    for (auto& s : st.st) VPIPG_TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  if (need <= st.cap) return kOk;
+  for (auto& b : st.buf) {
+    if (b) cudaFree(b);
+    b = nullptr;
+  }
+  st.cap = 0;
+  for (auto& b : st.buf) VPIPG_TRY(cudaMalloc(&b, need));
+  st.cap = need;
+  return kOk;
+}
+
+}  // namespace
+
+int vpipg_release_staging(int device) {
+  if (device < 0 || device >= 64) return kInvalid;
+  Staging& st = staging(device);
+  std::lock_guard<std::mutex> lock(st.mu);
+  if (!st.st[0] && !st.cap) return kOk;
+  DeviceGuard g(device);
+  int rc = kOk;
+  for (auto& s : st.st) {
+    if (!s) continue;
+    const cudaError_t e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess && rc == kOk) rc = cuda_code(e);
+    cudaStreamDestroy(s);
+    s = nullptr;
+  }
+  for (auto& b : st.buf) {
+    if (b) cudaFree(b);
+    b = nullptr;
+  }
+  st.cap = 0;
+  return rc;
+}
+
 int vpipg_test_host_multi(const vpipg_poly* p, uint32_t engines, int dtype, const void* xs,
                           const void* ys, uint64_t m, uint32_t* const* mask_words,
                           uint8_t* const* mask_bytes, uint64_t* inside) {
@@ -359,71 +446,49 @@ int vpipg_test_host_multi(const vpipg_poly* p, uint32_t engines, int dtype, cons
   if (!xs || !ys) return kInvalid;
   DeviceGuard g(p->device);
   const size_t elt = dtype == VPIPG_F64 ? sizeof(double) : sizeof(float);
-  // chunks of 16 Mi points (32-aligned so mask words line up), kSlots in
-  // flight on their own streams: the points cross PCIe once, every requested
-  // engine tests them, and the copy engines stay busy in both directions
-  constexpr int kSlots = 3;
-  const uint64_t chunk = std::min<uint64_t>(m, uint64_t(1) << 24);
-  const uint64_t chunk_words = (chunk + 31) / 32;
-  cudaStream_t st[kSlots];
-  for (auto& s : st) VPIPG_TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
-  struct Slot {
-    void* x = nullptr;
-    void* y = nullptr;
-    uint32_t* w[3] = {nullptr, nullptr, nullptr};
-    uint8_t* b[3] = {nullptr, nullptr, nullptr};
-    unsigned long long* c = nullptr;
-  } slot[kSlots];
-  int rc = kOk;
+  bool want_bytes = false;
+  for (int k = 0; k < ne; ++k) want_bytes |= mask_bytes && mask_bytes[eng[k]];
+  // chunks of 16 Mi points, kSlots in flight on their own streams: the points
+  // cross PCIe once, every requested engine tests them, and the copy engines
+  // stay busy in both directions
+  const uint64_t chunk = std::min<uint64_t>(m, kChunk);
+  Staging& st = staging(p->device);
+  std::lock_guard<std::mutex> lock(st.mu);
+  int rc = staging_reserve(st, slot_bytes(chunk, elt, want_bytes));
+  if (rc) return rc;
+  SlotView slot[kSlots];
+  for (int i = 0; i < kSlots; ++i) slot[i] = slot_view(st.buf[i], chunk, elt, want_bytes);
   auto fail = [&](cudaError_t e) {
     if (e != cudaSuccess && rc == kOk) rc = cuda_code(e);
     return rc != kOk;
   };
-  for (int i = 0; i < kSlots && rc == kOk; ++i) {
-    if (fail(cudaMallocAsync(&slot[i].x, chunk * elt, st[i]))) break;
-    if (fail(cudaMallocAsync(&slot[i].y, chunk * elt, st[i]))) break;
-    for (int k = 0; k < ne && rc == kOk; ++k) {
-      const int e = eng[k];
-      if (mask_words && mask_words[e])
-        fail(cudaMallocAsync(reinterpret_cast<void**>(&slot[i].w[e]), chunk_words * 4, st[i]));
-      if (mask_bytes && mask_bytes[e] && rc == kOk)
-        fail(cudaMallocAsync(reinterpret_cast<void**>(&slot[i].b[e]), chunk, st[i]));
-    }
-    if (rc == kOk && !fail(cudaMallocAsync(reinterpret_cast<void**>(&slot[i].c), 24, st[i])))
-      fail(cudaMemsetAsync(slot[i].c, 0, 24, st[i]));
-  }
+  for (int i = 0; i < kSlots && rc == kOk; ++i) fail(cudaMemsetAsync(slot[i].c, 0, 24, st.st[i]));
   const char* hx = static_cast<const char*>(xs);
   const char* hy = static_cast<const char*>(ys);
   for (uint64_t base = 0, c = 0; rc == kOk && base < m; base += chunk, ++c) {
     const int i = static_cast<int>(c % kSlots);
+    cudaStream_t s = st.st[i];
     const uint64_t len = std::min<uint64_t>(chunk, m - base);
-    if (fail(cudaMemcpyAsync(slot[i].x, hx + base * elt, len * elt, cudaMemcpyHostToDevice, st[i]))) break;
-    if (fail(cudaMemcpyAsync(slot[i].y, hy + base * elt, len * elt, cudaMemcpyHostToDevice, st[i]))) break;
+    if (fail(cudaMemcpyAsync(slot[i].x, hx + base * elt, len * elt, cudaMemcpyHostToDevice, s))) break;
+    if (fail(cudaMemcpyAsync(slot[i].y, hy + base * elt, len * elt, cudaMemcpyHostToDevice, s))) break;
     for (int k = 0; k < ne && rc == kOk; ++k) {
       const int e = eng[k];
-      TestArgs a{slot[i].x, slot[i].y, len, slot[i].w[e], slot[i].b[e], slot[i].c + e};
-      rc = dispatch(p, e, dtype, a, st[i]);
+      uint32_t* dw = mask_words && mask_words[e] ? slot[i].w[e] : nullptr;
+      uint8_t* db = mask_bytes && mask_bytes[e] ? slot[i].b[e] : nullptr;
+      TestArgs a{slot[i].x, slot[i].y, len, dw, db, slot[i].c + e};
+      rc = dispatch(p, e, dtype, a, s);
       if (rc) break;
-      if (slot[i].w[e] && fail(cudaMemcpyAsync(mask_words[e] + base / 32, slot[i].w[e],
-                                               ((len + 31) / 32) * 4, cudaMemcpyDeviceToHost, st[i])))
+      if (dw && fail(cudaMemcpyAsync(mask_words[e] + base / 32, dw, ((len + 31) / 32) * 4,
+                                     cudaMemcpyDeviceToHost, s)))
         break;
-      if (slot[i].b[e] && fail(cudaMemcpyAsync(mask_bytes[e] + base, slot[i].b[e], len,
-                                               cudaMemcpyDeviceToHost, st[i])))
+      if (db && fail(cudaMemcpyAsync(mask_bytes[e] + base, db, len, cudaMemcpyDeviceToHost, s)))
         break;
     }
   }
   unsigned long long cnt[kSlots][3] = {};
-  for (int i = 0; i < kSlots; ++i) {
-    if (rc == kOk && slot[i].c) fail(cudaMemcpyAsync(cnt[i], slot[i].c, 24, cudaMemcpyDeviceToHost, st[i]));
-    void* ptrs[] = {slot[i].x, slot[i].y, slot[i].w[0], slot[i].w[1], slot[i].w[2],
-                    slot[i].b[0], slot[i].b[1], slot[i].b[2], slot[i].c};
-    for (void* ptr : ptrs)
-      if (ptr) cudaFreeAsync(ptr, st[i]);
-  }
-  for (auto& s : st) {
-    fail(cudaStreamSynchronize(s));
-    cudaStreamDestroy(s);
-  }
+  for (int i = 0; i < kSlots; ++i)
+    if (rc == kOk) fail(cudaMemcpyAsync(cnt[i], slot[i].c, 24, cudaMemcpyDeviceToHost, st.st[i]));
+  for (auto& s : st.st) fail(cudaStreamSynchronize(s));
   if (rc == kOk && inside)
     for (int k = 0; k < ne; ++k) {
       inside[eng[k]] = 0;

@@ -252,6 +252,11 @@ def _host_ptr(a) -> int:
     return a.ctypes.data if isinstance(a, np.ndarray) else a.data_ptr()
 
 
+def release_staging(device: int = 0) -> None:
+    """Free the per-device staging the host-buffer calls keep (vpipg_release_staging)."""
+    check(load().vpipg_release_staging(device), "vpipg_release_staging")
+
+
 def fill_uniform_points(seed: int, first: int, xs, ys, box, stream=None) -> None:
     """Counter-based device point stream (vpipg_fill_uniform_points)."""
     import torch

@@ -231,6 +231,43 @@ def test_host_buffer_path_equals_device_path(orc):
             assert np.array_equal(wd32, wh32) and cd32 == ch32
 
 
+def test_host_multi_and_staging_reuse(orc):
+    """vpipg_test_host_multi over several 16 Mi-point chunks equals the device
+    path per engine; the per-device staging survives growth (f32 -> f64 ->
+    bytes), release, and concurrent host callers on two handles."""
+    import threading
+    vx, vy = W.c1_polygon()
+    m = (1 << 24) * 2 + 12345
+    xs, ys = orc.sample_points(m, W.C1_BOX, 7)
+    x32, y32 = xs.astype(np.float32), ys.astype(np.float32)
+    with vp.PreparedPolygon.prepare(vx, vy, vp.KIND_ALL) as p:
+        ref = [run_device(p, e, x32, y32, bytes_=False) for e in range(3)]
+        for _ in range(2):
+            words, cnt = p.test_host_multi(x32, y32, (0, 1, 2))
+            for e in range(3):
+                assert np.array_equal(words[e], ref[e][0]) and cnt[e] == ref[e][2]
+            vp.release_staging(0)
+        # growth to f64 with byte masks, then back to a small f32 batch
+        wh, bh, ch = p.test_host(2, xs[:3_000_001], ys[:3_000_001], words=True, bytes_=True)
+        wd, bd, cd = run_device(p, 2, xs[:3_000_001], ys[:3_000_001])
+        assert np.array_equal(wh, wd) and np.array_equal(bh, bd) and ch == cd
+        out = {}
+
+        def worker(k):
+            with vp.PreparedPolygon.prepare(vx, vy, vp.KIND_ALL) as q:
+                out[k] = q.test_host_multi(x32[: 1 << 22], y32[: 1 << 22], (0, 1, 2))
+
+        ts = [threading.Thread(target=worker, args=(k,)) for k in range(3)]
+        for t in ts:
+            t.start()
+        for t in ts:
+            t.join()
+        for k in range(3):
+            for e in range(3):
+                assert np.array_equal(out[k][0][e], ref[e][0][: (1 << 22) // 32])
+    vp.release_staging(0)
+
+
 def test_concurrent_streams_share_one_handle(orc):
     # test_engines.cpp:243-257: one generator set serves concurrent callers
     vx, vy = W.c1_polygon()
