@@ -76,20 +76,20 @@ struct SlabEngine {
 
   // Two groups that bound the coordinate w as a function of the other one, v
   // (lo: max-reduced, hi: min-reduced), consumed in lockstep so each iteration
-  // carries 4 edges x P points of work. w itself seeds both reductions (a
-  // free third operand of the first FMNMX3; prep.cu guarantees >= 1 pair per
-  // group), so afterwards lo >= w >= hi and the point satisfies the section
-  // iff lo == hi, i.e. hi - lo >= 0.
+  // carries 4 edges x P points of work. The seeds wlo / whi enter as the free
+  // third operand of the first FMNMX3 (prep.cu guarantees >= 1 pair per
+  // group). With wlo = whi = w, afterwards lo >= w >= hi and the point
+  // satisfies the section iff lo <= hi.
   __device__ __forceinline__ static void section(const float4* A, uint32_t na, const float4* B,
                                                  uint32_t nb, const float (&v)[P],
-                                                 const float (&w)[P], float (&lo)[P],
-                                                 float (&hi)[P]) {
+                                                 const float (&wlo)[P], const float (&whi)[P],
+                                                 float (&lo)[P], float (&hi)[P]) {
     {
       const float4 a = A[0], b = B[0];
 #pragma unroll
       for (int p = 0; p < P; ++p) {
-        lo[p] = fmax3(w[p], fmaf(a.x, v[p], a.y), fmaf(a.z, v[p], a.w));
-        hi[p] = fmin3(w[p], fmaf(b.x, v[p], b.y), fmaf(b.z, v[p], b.w));
+        lo[p] = fmax3(wlo[p], fmaf(a.x, v[p], a.y), fmaf(a.z, v[p], a.w));
+        hi[p] = fmin3(whi[p], fmaf(b.x, v[p], b.y), fmaf(b.z, v[p], b.w));
       }
     }
     const uint32_t nc = na < nb ? na : nb;
@@ -117,18 +117,28 @@ struct SlabEngine {
     }
   }
 
-  // slack[p] >= 0 <=> point p is inside (every half-plane holds; ties inside)
+  // Point p is inside iff a[p] >= b[p] (every half-plane holds; ties inside).
+  // Section 1 (x bounded by lines in y) leaves lo1 >= x >= hi1 with the
+  // violation f1 = lo1 - hi1 >= 0, zero iff the point satisfies it. Section 2
+  // is seeded with lo = y + f1, hi = y, so its lo <= hi test also fails when
+  // section 1 did: y + f1 > y for every f1 that survives rounding against y,
+  // and an f1 below half an ulp of y is a violation of < 6e-8 |y|, inside the
+  // 1e-5 band. One compare per point decides both sections.
   __device__ __forceinline__ static void eval(const Params& prm, const float4* s,
                                               const float (&x)[P], const float (&y)[P],
-                                              float (&slack)[P]) {
+                                              float (&a)[P], float (&b)[P]) {
     const SlabTable& t = prm.tab;
     float lo[P], hi[P];
-    section(s + t.off[0] / 2, t.cnt[0] / 2, s + t.off[1] / 2, t.cnt[1] / 2, y, x, lo, hi);
+    section(s + t.off[0] / 2, t.cnt[0] / 2, s + t.off[1] / 2, t.cnt[1] / 2, y, x, x, lo, hi);
+    float seed[P];
 #pragma unroll
-    for (int p = 0; p < P; ++p) slack[p] = hi[p] - lo[p];
-    section(s + t.off[2] / 2, t.cnt[2] / 2, s + t.off[3] / 2, t.cnt[3] / 2, x, y, lo, hi);
+    for (int p = 0; p < P; ++p) seed[p] = y[p] + (lo[p] - hi[p]);
+    section(s + t.off[2] / 2, t.cnt[2] / 2, s + t.off[3] / 2, t.cnt[3] / 2, x, seed, y, lo, hi);
 #pragma unroll
-    for (int p = 0; p < P; ++p) slack[p] = fminf(slack[p], hi[p] - lo[p]);
+    for (int p = 0; p < P; ++p) {
+      a[p] = hi[p];
+      b[p] = lo[p];
+    }
   }
 };
 
@@ -156,10 +166,10 @@ struct CrossEngine {
     for (uint32_t i = threadIdx.x; i < p.tab.n; i += blockDim.x) s[i] = p.tab.vert[i];
   }
 
-  // slack[p] = +1 (odd crossing parity: inside) or -1 (even: outside)
+  // a[p] = +1 (odd crossing parity: inside) or -1 (even: outside), b[p] = 0
   __device__ __forceinline__ static void eval(const Params& prm, const float4* s,
                                               const float (&x)[P], const float (&y)[P],
-                                              float (&slack)[P]) {
+                                              float (&a)[P], float (&b)[P]) {
     const uint32_t n = prm.tab.n;
     uint32_t par[P];
 #pragma unroll
@@ -219,7 +229,10 @@ struct CrossEngine {
       }
     }
 #pragma unroll
-    for (int p = 0; p < P; ++p) slack[p] = __uint_as_float((~par[p] & 0x80000000u) | 0x3f800000u);
+    for (int p = 0; p < P; ++p) {
+      a[p] = __uint_as_float((~par[p] & 0x80000000u) | 0x3f800000u);
+      b[p] = 0.f;
+    }
   }
 };
 
@@ -227,16 +240,28 @@ struct CrossEngine {
 // Output: ballot words (PIPM order), optional byte mask, per-lane inside count.
 // The P words of a slice are warp-uniform; lane 0 writes them with 16-byte
 // streaming stores (a slice's words are 64 contiguous, 64-byte aligned bytes).
+// inside = (a >= b): one FSETP feeds both the ballot and a predicated count
+__device__ __forceinline__ uint32_t vote_ge(float a, float b, uint32_t& cnt) {
+  uint32_t w;
+  asm volatile(
+      "{\n\t.reg .pred q;\n\t"
+      "setp.ge.f32 q, %2, %3;\n\t"
+      "vote.sync.ballot.b32 %0, q, 0xffffffff;\n\t"
+      "@q add.u32 %1, %1, 1;\n\t}"
+      : "=r"(w), "+r"(cnt)
+      : "f"(a), "f"(b));
+  return w;
+}
+
 template <bool kGuard, int P>
-__device__ __forceinline__ uint32_t emit(const float (&slack)[P], uint64_t base,
+__device__ __forceinline__ uint32_t emit(float (&av)[P], const float (&bv)[P], uint64_t base,
                                          const TestArgs& a, int lane) {
   uint32_t w[P];
   uint32_t cnt = 0;
 #pragma unroll
   for (int p = 0; p < P; ++p) {
-    const bool ok = (slack[p] >= 0.f) & (!kGuard || base + 32u * p + lane < a.m);
-    w[p] = __ballot_sync(0xffffffffu, ok);
-    cnt += ok;
+    if (kGuard && base + 32u * p + lane >= a.m) av[p] = -INFINITY;
+    w[p] = vote_ge(av[p], bv[p], cnt);
   }
   if (a.words && lane == 0) {
     const uint64_t w0 = base >> 5;
@@ -274,7 +299,7 @@ __device__ __forceinline__ uint32_t guarded_tile(const typename Eng::Params& prm
   constexpr int P = Eng::kP;
   const float* xs = static_cast<const float*>(a.xs);
   const float* ys = static_cast<const float*>(a.ys);
-  float x[P], y[P], slack[P];
+  float x[P], y[P], va[P], vb[P];
 #pragma unroll
   for (int p = 0; p < P; ++p) {
     const uint64_t idx = base + 32u * p + lane;
@@ -282,8 +307,8 @@ __device__ __forceinline__ uint32_t guarded_tile(const typename Eng::Params& prm
     x[p] = ok ? __ldcs(xs + idx) : 0.f;
     y[p] = ok ? __ldcs(ys + idx) : 0.f;
   }
-  Eng::eval(prm, tab, x, y, slack);
-  return emit<true, P>(slack, base, a, lane);
+  Eng::eval(prm, tab, x, y, va, vb);
+  return emit<true, P>(va, vb, base, a, lane);
 }
 
 // kSmemTab: the polygon table is staged in shared memory once per CTA (the
@@ -336,7 +361,7 @@ __global__ void __launch_bounds__(kThreads, 2)
     const uint32_t s = it % kStages, ph = (it / kStages) & 1u;
     mbar_wait(&full[s], ph);
     const float* px = ring + s * 2 * kWarpPts + lane;
-    float x[P], y[P], slack[P];
+    float x[P], y[P], va[P], vb[P];
 #pragma unroll
     for (int p = 0; p < P; ++p) {
       x[p] = px[32 * p];
@@ -351,8 +376,8 @@ __global__ void __launch_bounds__(kThreads, 2)
       bulk_g2s(ring + s * 2 * kWarpPts + kWarpPts, ys + gn * kWarpPts, kWarpPts * sizeof(float),
                &full[s], policy);
     }
-    Eng::eval(prm, tab, x, y, slack);
-    count += emit<false, P>(slack, g * kWarpPts, a, lane);
+    Eng::eval(prm, tab, x, y, va, vb);
+    count += emit<false, P>(va, vb, g * kWarpPts, a, lane);
   }
   // partial last slice: the warp next in round-robin order, guarded loads
   if (g0 == full_slices % W) {
