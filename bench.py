@@ -377,6 +377,19 @@ class JoinJob:
 
 
 # ----------------------------------------------------------------- GPU arm
+def stdout_to_stderr(fn, *a):
+    """Run fn with fd 1 pointed at stderr: NCCL prints its version banner on
+    stdout at communicator init, and stdout must carry exactly one JSON line."""
+    sys.stdout.flush()
+    saved = os.dup(1)
+    os.dup2(2, 1)
+    try:
+        return fn(*a)
+    finally:
+        os.dup2(saved, 1)
+        os.close(saved)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -400,12 +413,15 @@ def main():
     import torch
     import torch.distributed as dist
     import paper_2007_15385_b200 as vp
-    from paper_2007_15385_b200.multi import reduce_counts
+    from paper_2007_15385_b200.multi import CountComm
 
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     stream = torch.cuda.Stream()
+    # the count all-reduce: libvpipg's own NCCL communicator on the launch
+    # stream (a 1-rank communicator at N=1, so the step is the same at every N)
+    comm = stdout_to_stderr(CountComm.from_process_group, local)
     M = args.points or workload_size(args.workload)
     lo, hi = W.shard(M, rank, world)
     m = hi - lo
@@ -433,7 +449,7 @@ def main():
             if record:
                 b.record(stream)
                 pairs.append((a, b))
-        reduce_counts(counts)  # NCCL all-reduce of the 3 inside counts (no-op at N=1)
+        comm.allreduce(counts, stream)  # NCCL sum of the 3 inside counts
         if record:
             kevents.append(pairs)
 

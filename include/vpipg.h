@@ -13,8 +13,9 @@
  *  - Return 0 on success. 1..7 are vpip::ErrorCode in declaration order
  *    (proj/include/vpip/error.hpp:23-31): 1 TooFewVertices, 2 NotConvex,
  *    3 DegenerateEdge, 4 NonFinite, 5 GeneratorCollision, 6 InvalidParameter,
- *    7 ParseError. 100 + cudaError_t for CUDA failures, 300 when the device
- *    is not an sm_100 part. No exception crosses the ABI.
+ *    7 ParseError. 100 when the device is not an sm_100 part, 101 when
+ *    libnccl.so.2 cannot be loaded, 200 + ncclResult_t for NCCL failures,
+ *    1000 + cudaError_t for CUDA failures. No exception crosses the ABI.
  *  - `stream` is a cudaStream_t passed as void* (NULL = legacy default).
  *    Device-pointer calls are asynchronous on that stream; the caller owns
  *    point, mask and count buffers; the library owns a handle's tables.
@@ -43,7 +44,7 @@
 extern "C" {
 #endif
 
-#define VPIPG_ABI_VERSION 1
+#define VPIPG_ABI_VERSION 2
 
 /* engines: vpip::EngineKind order (engines.hpp:64-73) */
 #define VPIPG_ENGINE_VORONOI 0
@@ -60,8 +61,10 @@ extern "C" {
 #define VPIPG_F64 0
 #define VPIPG_F32 1
 
-#define VPIPG_ERR_CUDA 100
-#define VPIPG_ERR_ARCH 300
+#define VPIPG_ERR_ARCH 100
+#define VPIPG_ERR_NCCL_MISSING 101
+#define VPIPG_ERR_NCCL 200
+#define VPIPG_ERR_CUDA 1000
 
 typedef struct vpipg_poly vpipg_poly;
 
@@ -206,6 +209,34 @@ int vpipg_fill_join_pairs(uint64_t seed, uint64_t first, uint64_t m, uint32_t np
 int vpipg_fill_uniform_points(uint64_t seed, uint64_t first, uint64_t m, double min_x,
                               double min_y, double max_x, double max_y, int dtype, void* xs,
                               void* ys, void* stream);
+
+/* ---- Multi-GPU: the inside-count all-reduce -------------
+ * Points shard across GPUs with no data exchange; the one collective of the
+ * path is a sum of the per-GPU inside counts (3 u64 for the three engines),
+ * launched on the test kernels' stream right after them (graph-capturable).
+ * NCCL is loaded at run time (dlopen "libnccl.so.2", or $VPIPG_NCCL_LIBRARY),
+ * so the library itself has no link-time NCCL dependency.
+ *
+ * One process per GPU: rank 0 calls vpipg_comm_unique_id, ships the 128 bytes
+ * to the other ranks out of band (torch.distributed, MPI, a file), and every
+ * rank calls vpipg_comm_init. One process driving several GPUs:
+ * vpipg_comm_init_all, then vpipg_allreduce_counts_group from one thread. */
+typedef struct vpipg_comm vpipg_comm;
+
+/* NCCL_VERSION_CODE of the loaded libnccl (e.g. 22809 for 2.28.9). */
+int vpipg_nccl_version(int* version);
+int vpipg_comm_unique_id(uint8_t id[128]);
+int vpipg_comm_init(const uint8_t id[128], int nranks, int rank, int device, vpipg_comm** out);
+int vpipg_comm_init_all(int ndev, const int* devices, vpipg_comm** comms);
+int vpipg_comm_info(const vpipg_comm* comm, int* nranks, int* rank, int* device);
+/* In-place sum of n device u64 counters over all ranks, on `stream`. */
+int vpipg_allreduce_counts(vpipg_comm* comm, unsigned long long* d_counts, int n, void* stream);
+/* The same for several communicators driven by one thread (vpipg_comm_init_all):
+ * comms[i], d_counts[i], streams[i] belong to the same device. */
+int vpipg_allreduce_counts_group(int ncomms, vpipg_comm* const* comms,
+                                 unsigned long long* const* d_counts, int n,
+                                 void* const* streams);
+int vpipg_comm_destroy(vpipg_comm* comm);
 
 /* Host-side seeded polygon and point samplers with the reference's exact
  * semantics (sampling.cpp:50-105), for building workloads. Vertices come

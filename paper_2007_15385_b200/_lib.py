@@ -19,7 +19,7 @@ ENGINES = {"voronoi": 0, "sign_of_offset": 1, "offset": 1, "ray_crossing": 2, "c
 ENGINE_NAMES = ("voronoi", "sign_of_offset", "ray_crossing")
 KIND_VORONOI, KIND_OFFSET, KIND_CROSSING, KIND_ALL = 1, 2, 4, 7
 F64, F32 = 0, 1
-ERR_CUDA, ERR_ARCH = 100, 300
+ERR_ARCH, ERR_NCCL_MISSING, ERR_NCCL, ERR_CUDA = 100, 101, 200, 1000
 
 REPORT_SAMPLES = 100
 
@@ -52,6 +52,14 @@ SIGNATURES = {
     "vpipg_test_host_multi": (C.c_int, [_P, C.c_uint32, C.c_int, _P, _P, C.c_uint64, _P, _P,
                                         C.POINTER(C.c_uint64)]),
     "vpipg_release_staging": (C.c_int, [C.c_int]),
+    "vpipg_nccl_version": (C.c_int, [C.POINTER(C.c_int)]),
+    "vpipg_comm_unique_id": (C.c_int, [C.c_char_p]),
+    "vpipg_comm_init": (C.c_int, [C.c_char_p, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_void_p)]),
+    "vpipg_comm_init_all": (C.c_int, [C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_void_p)]),
+    "vpipg_comm_info": (C.c_int, [_P, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int)]),
+    "vpipg_allreduce_counts": (C.c_int, [_P, _P, C.c_int, _P]),
+    "vpipg_allreduce_counts_group": (C.c_int, [C.c_int, _P, _P, C.c_int, _P]),
+    "vpipg_comm_destroy": (C.c_int, [_P]),
     "vpipg_voronoi_work": (C.c_int, [_P, C.c_uint64, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
     "vpipg_fill_uniform_points": (C.c_int, [C.c_uint64, C.c_uint64, C.c_uint64, C.c_double,
                                             C.c_double, C.c_double, C.c_double, C.c_int, _P, _P, _P]),
@@ -108,7 +116,13 @@ class VpipError(RuntimeError):
 
     @property
     def name(self) -> str:
-        return self.NAMES.get(self.code, "CudaError" if self.code < ERR_ARCH else "ArchError")
+        if self.code in self.NAMES:
+            return self.NAMES[self.code]
+        if self.code >= ERR_CUDA:
+            return "CudaError"
+        if self.code >= ERR_NCCL:
+            return "NcclError"
+        return "NcclMissing" if self.code == ERR_NCCL_MISSING else "ArchError"
 
 
 def check(rc: int, where: str = "") -> None:

@@ -228,9 +228,11 @@ const char* vpipg_strerror(int code) {
     case 6: return "invalid parameter";
     case 7: return "parse error";
     case VPIPG_ERR_ARCH: return "device is not an sm_100 (B200) GPU";
+    case VPIPG_ERR_NCCL_MISSING: return "libnccl.so.2 could not be loaded";
     default: break;
   }
-  if (code >= VPIPG_ERR_CUDA && code < VPIPG_ERR_ARCH)
+  if (code > VPIPG_ERR_NCCL && code < VPIPG_ERR_NCCL + 100) return vpipg_nccl_error_string(code);
+  if (code > VPIPG_ERR_CUDA)
     return cudaGetErrorString(static_cast<cudaError_t>(code - VPIPG_ERR_CUDA));
   return "unknown error";
 }

@@ -124,3 +124,6 @@ cudaError_t launch_fill_uniform(uint64_t seed, uint64_t first, uint64_t m, doubl
                                 void* ys, cudaStream_t stream);
 
 }  // namespace vpipg
+
+// comm.cpp: text for a VPIPG_ERR_NCCL + ncclResult_t code
+const char* vpipg_nccl_error_string(int code);

@@ -57,11 +57,12 @@ def test_kernels_use_fma_and_3way_minmax():
 
 def test_strerror_and_version():
     lib = _lib.load()
-    assert lib.vpipg_abi_version() == 1
+    assert lib.vpipg_abi_version() == 2
     assert lib.vpipg_strerror(0) == b"ok"
     assert lib.vpipg_strerror(2) == b"not convex"
     assert lib.vpipg_strerror(5) == b"generator collision"
-    assert b"sm_100" in lib.vpipg_strerror(300)
+    assert b"sm_100" in lib.vpipg_strerror(100)
+    assert b"nccl" in lib.vpipg_strerror(101)
 
 
 def test_no_gpu_fails_loudly():
@@ -70,7 +71,7 @@ def test_no_gpu_fails_loudly():
         pytest.skip("a GPU is present")
     with pytest.raises(vp.VpipError) as e:
         vp.PreparedPolygon.prepare([0, 1, 1, 0], [0, 0, 1, 1])
-    assert e.value.code >= 100  # CUDA error, never a silent CPU path
+    assert e.value.code >= 1000  # CUDA error, never a silent CPU path
 
 
 def test_invalid_arguments_rejected_before_device():
@@ -99,3 +100,20 @@ def test_sampler_errors():
     assert e.value.code == 6
     with pytest.raises(vp.VpipError):
         vp.sample_points(4, (0, 0, 0, 1), 1)
+
+
+def test_nccl_loads_at_run_time_without_a_gpu():
+    """The count all-reduce's NCCL is dlopen'ed: version and unique id work on a
+    CPU host; bad arguments are rejected before any device call."""
+    import ctypes as C
+    lib = _lib.load()
+    v = C.c_int()
+    assert lib.vpipg_nccl_version(C.byref(v)) == 0 and v.value >= 21800
+    buf = C.create_string_buffer(128)
+    assert lib.vpipg_comm_unique_id(buf) == 0 and any(buf.raw)
+    h = C.c_void_p()
+    assert lib.vpipg_comm_init(buf, 2, 2, 0, C.byref(h)) == 6  # rank out of range
+    assert lib.vpipg_comm_init(None, 1, 0, 0, C.byref(h)) == 6
+    assert lib.vpipg_allreduce_counts(None, None, 3, None) == 6
+    assert lib.vpipg_comm_destroy(None) == 0
+    assert b"nccl" in lib.vpipg_strerror(101).lower()

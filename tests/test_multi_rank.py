@@ -17,7 +17,7 @@ import torch.distributed as dist
 import torch.multiprocessing as mp
 
 import workloads as W
-from paper_2007_15385_b200.multi import reduce_counts, shard
+from paper_2007_15385_b200.multi import reduce_counts, shard, shared_unique_id
 
 
 def _free_port():
@@ -38,8 +38,11 @@ def _rank(rank, world, port, m, out):
     words = [np.packbits(mk, bitorder="little") for mk in masks]
     counts = torch.tensor([int(mk.sum()) for mk in masks], dtype=torch.int64)
     reduce_counts(counts)
+    # the NCCL unique id of the library's count communicator travels over the
+    # process group; every rank must hold rank 0's bytes
+    uid = shared_unique_id()
     gathered = [None] * world
-    dist.all_gather_object(gathered, (lo, hi, words))
+    dist.all_gather_object(gathered, (lo, hi, words, uid))
     if rank == 0:
         out.put((counts.tolist(), gathered))
     dist.barrier()
@@ -64,7 +67,8 @@ def test_two_rank_shards_and_count_allreduce(m):
     xs, ys = orc.counter_points_f32(W.c5_point_seed(), 0, m, W.C5_BOX)
     full = orc.masks(vx, vy, xs.astype(np.float64), ys.astype(np.float64))
     assert counts == [int(mk.sum()) for mk in full]
-    (lo0, hi0, w0), (lo1, hi1, w1) = gathered
+    (lo0, hi0, w0, u0), (lo1, hi1, w1, u1) = gathered
+    assert len(u0) == 128 and u0 == u1
     assert lo0 == 0 and hi0 == lo1 and hi1 == m and lo1 % 1024 == 0
     for e in range(3):
         # shard boundaries are 32-aligned, so the packed masks simply concatenate
