@@ -178,6 +178,21 @@ def main() -> None:
     fx["arrow_count"] = np.array([L.vr_scalar(p, 3, x, y) for x, y in probes], np.int32)
     L.vr_poly_free(p)
 
+    # --- non-finite and extreme query points (outside the reference's I/O
+    # contract, parse_points_csv rejects NaN, but the batch kernels still give
+    # a defined IEEE answer that the f64 engines must repeat) ---
+    inf, nan = np.inf, np.nan
+    special = [(inf, 0), (-inf, 0), (0, inf), (0, -inf), (inf, inf), (-inf, -inf), (inf, -inf),
+               (nan, 0), (0, nan), (nan, nan), (inf, nan), (nan, -inf), (1e300, 1e300),
+               (-1e308, 5), (5, 1.7e308), (1e-320, 0), (-0.0, -0.0), (0.1, 0.1), (3, 3)]
+    sx, sy = np.array(special, float).T
+    for name, (vx, vy) in (("c1", (c1x, c1y)), ("square", sq)):
+        vx, vy = np.asarray(vx, float), np.asarray(vy, float)
+        (mv, mo, mr), _ = R.masks(vx, vy, sx, sy)
+        fx[f"nonfinite_{name}_v"] = np.array([vx, vy])
+        fx[f"nonfinite_{name}_pts"] = np.array([sx, sy])
+        fx[f"nonfinite_{name}_masks"] = np.array([mv, mo, mr], np.uint8)
+
     # --- C1 at full size: counts + SHA-256 of the packed masks ---
     xs, ys = R.sample_points(W.C1_POINTS, W.C1_BOX, W.mix_seed_np(W.config_seed(1), 100).item())
     (mv, mo, mr), _ = R.masks(c1x, c1y, xs, ys, threads=8)

@@ -92,6 +92,22 @@ def test_f64_engines_bit_exact_on_all_golden_cases(golden):
                 assert c == int(want[e].sum())
 
 
+@pytest.mark.parametrize("name", ["c1", "square"])
+def test_f64_non_finite_points_bit_exact(golden, name):
+    """The f64 kernels repeat the reference's IEEE behaviour on inf / NaN /
+    overflowing points too (Voronoi: inf <= inf is inside, NaN is outside;
+    offset: NaN flags nothing, so inside). f32 kernels promise nothing there:
+    such points have no finite distance to the boundary."""
+    vx, vy = golden[f"nonfinite_{name}_v"]
+    xs, ys = golden[f"nonfinite_{name}_pts"]
+    want = golden[f"nonfinite_{name}_masks"]
+    with vp.PreparedPolygon.prepare(vx, vy, vp.KIND_ALL) as p:
+        for e in range(3):
+            w, b, c = run_device(p, e, xs, ys)
+            assert np.array_equal(b, want[e]), (name, e, b.tolist(), want[e].tolist())
+            assert c == int(want[e].sum())
+
+
 def test_f32_engines_match_outside_band(golden, orc):
     total = {0: 0, 1: 0, 2: 0}
     for name in case_names(golden):

@@ -89,6 +89,16 @@ def test_engine_masks_bit_exact(golden, orc):
         assert np.array_equal(got, want), name
 
 
+@pytest.mark.parametrize("name", ["c1", "square"])
+def test_non_finite_points(golden, orc, name):
+    """inf / NaN / overflowing query points: the reference's IEEE answers."""
+    vx, vy = golden[f"nonfinite_{name}_v"]
+    xs, ys = golden[f"nonfinite_{name}_pts"]
+    got = orc.masks(vx, vy, xs, ys)
+    for e in range(3):
+        assert np.array_equal(got[e], golden[f"nonfinite_{name}_masks"][e]), (name, e)
+
+
 def test_arrow_concave(golden, orc):
     vx, vy = golden["arrow_v"]
     for (x, y), ins, cnt in zip(golden["arrow_pts"].T, golden["arrow_inside"], golden["arrow_count"]):
