@@ -236,79 +236,6 @@ struct CrossEngine {
   }
 };
 
-#ifdef VPIPG_CROSS_FMA
-// Experimental all-FMA-pipe crossing: H = sat(S (u.y - qy)), D = sat(S side),
-// parity of sum D_k (H_k - H_{k-1}); the staged table is (S u.y, S b, S c, 0).
-template <int P>
-struct CrossFmaEngine {
-  static constexpr int kP = P;
-  static constexpr float S = 0x1p40f;
-  struct Params {
-    CrossTable tab;
-    float ox, oy;
-  };
-  static size_t table_bytes(const Params& p) { return (size_t)p.tab.n * sizeof(float4); }
-  __device__ static const float4* global_table(const Params& p) { return p.tab.vert; }
-  __device__ static void stage(const Params& p, float4* s) {
-    const uint32_t n = p.tab.n;
-    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
-      const float4 u = p.tab.vert[i], w = p.tab.vert[i ? i - 1 : n - 1];
-      const float b = fmaxf(-0x1p40f, fminf(0x1p40f, u.z));
-      s[i] = make_float4(u.y * S, b * S, fmaf(-w.y, b, w.x) * S, 0.f);
-    }
-  }
-  __device__ __forceinline__ static void eval(const Params& prm, const float4* s,
-                                              const float (&x)[P], const float (&y)[P],
-                                              float (&a)[P], float (&b)[P]) {
-    const uint32_t n = prm.tab.n;
-    float cnt[P], hp[P];
-    const float4 last = s[n - 1];
-#pragma unroll
-    for (int p = 0; p < P; ++p) {
-      cnt[p] = 0.f;
-      hp[p] = __saturatef(fmaf(y[p], -S, last.x));
-    }
-    uint32_t k = 0;
-#pragma unroll 1
-    for (; k + 3 < n; k += 4) {
-      const float4 v0 = s[k], v1 = s[k + 1], v2 = s[k + 2], v3 = s[k + 3];
-#pragma unroll
-      for (int p = 0; p < P; ++p) {
-        const float h0 = __saturatef(fmaf(y[p], -S, v0.x));
-        const float d0 = __saturatef(fmaf(y[p], v0.y, fmaf(x[p], -S, v0.z)));
-        const float h1 = __saturatef(fmaf(y[p], -S, v1.x));
-        const float d1 = __saturatef(fmaf(y[p], v1.y, fmaf(x[p], -S, v1.z)));
-        const float h2 = __saturatef(fmaf(y[p], -S, v2.x));
-        const float d2 = __saturatef(fmaf(y[p], v2.y, fmaf(x[p], -S, v2.z)));
-        const float h3 = __saturatef(fmaf(y[p], -S, v3.x));
-        const float d3 = __saturatef(fmaf(y[p], v3.y, fmaf(x[p], -S, v3.z)));
-        float c = fmaf(d0, h0 - hp[p], cnt[p]);
-        c = fmaf(d1, h1 - h0, c);
-        c = fmaf(d2, h2 - h1, c);
-        cnt[p] = fmaf(d3, h3 - h2, c);
-        hp[p] = h3;
-      }
-    }
-#pragma unroll 1
-    for (; k < n; ++k) {
-      const float4 v = s[k];
-#pragma unroll
-      for (int p = 0; p < P; ++p) {
-        const float h = __saturatef(fmaf(y[p], -S, v.x));
-        const float d = __saturatef(fmaf(y[p], v.y, fmaf(x[p], -S, v.z)));
-        cnt[p] = fmaf(d, h - hp[p], cnt[p]);
-        hp[p] = h;
-      }
-    }
-#pragma unroll
-    for (int p = 0; p < P; ++p) {
-      a[p] = (__float2int_rn(cnt[p]) & 1) ? 1.f : -1.f;
-      b[p] = 0.f;
-    }
-  }
-};
-#endif
-
 // ---------------------------------------------------------------------------
 // Output: ballot words (PIPM order), optional byte mask, per-lane inside count.
 // The P words of a slice are warp-uniform; lane 0 writes them with 16-byte
@@ -535,11 +462,7 @@ cudaError_t launch_test_f32(const DevTables& t, int engine, const TestArgs& a,
     typename E::Params prm{t.slab[engine], t.ox, t.oy};
     return launch<E>(prm, a, stream);
   }
-#ifdef VPIPG_CROSS_FMA
-  using E = CrossFmaEngine<VPIPG_CROSS_P>;
-#else
   using E = CrossEngine<VPIPG_CROSS_P>;
-#endif
   typename E::Params prm{t.cross, t.ox, t.oy};
   return launch<E>(prm, a, stream);
 }
