@@ -58,3 +58,40 @@ def test_init_all_and_grouped_allreduce():
     torch.cuda.synchronize()
     assert t.tolist() == [5, 7, 1 << 40]
     assert lib.vpipg_comm_destroy(comms[0]) == 0
+
+
+def test_step_is_graph_capturable():
+    """The bench step -- three engine launches plus the count all-reduce on one
+    stream -- captures into a CUDA graph and replays with identical results."""
+    vx, vy = W.c5_polygon(vp.random_convex_polygon)
+    m = (1 << 22) + 777
+    xs = torch.empty(m, dtype=torch.float32, device="cuda")
+    ys = torch.empty_like(xs)
+    vp.fill_uniform_points(W.c5_point_seed(), 0, xs, ys, W.C5_BOX)
+    words = [torch.zeros((m + 31) // 32, dtype=torch.int32, device="cuda") for _ in range(3)]
+    counts = torch.zeros(3, dtype=torch.int64, device="cuda")
+    s = torch.cuda.Stream()
+    with CountComm(CountComm.unique_id(), 1, 0, 0) as comm, \
+            vp.PreparedPolygon.prepare(vx, vy, vp.KIND_ALL) as p:
+        def step():
+            counts.zero_()
+            for e in range(3):
+                p.test(e, xs, ys, words=words[e], count=counts[e:e + 1], stream=s)
+            comm.allreduce(counts, s)
+
+        with torch.cuda.stream(s):
+            step()  # eager reference (also warms the launch path up)
+        s.synchronize()
+        ref_words = [w.clone() for w in words]
+        ref_counts = counts.clone()
+        for w in words:
+            w.zero_()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            step()
+        for _ in range(3):
+            g.replay()
+        torch.cuda.synchronize()
+        assert counts.tolist() == ref_counts.tolist()
+        for w, r in zip(words, ref_words):
+            assert torch.equal(w, r)
