@@ -171,7 +171,7 @@ def workload_desc(name: str) -> str:
     return {"c5": "C5 multi-GPU scaling: random convex 32-gon, 2^31 f32 points U[-1.5,1.5]^2, "
                   "3 engines + NCCL all-reduce of inside counts",
             "c2": "C2 vehicle footprint 12-gon, 2^24 f32 lidar-like clustered points",
-            "c1": "C1 random 8-angle hull, 2^20 points (f32 copy of the f64 oracle config)",
+            "c1": "C1 random 8-angle hull, 2^20 f64 points (the oracle config, exact f64 kernels)",
             "c4": "C4 polygon-database join: 65536 random convex 4..16-gons (CSR), 2^28 f32 "
                   "(point, polygon id) pairs, gathered test"}.get(
         name.split(":")[0], f"C3 n-sweep regular {name} jittered hull, 2^28 f32 points")
@@ -296,14 +296,19 @@ class PolygonJob:
         self.poly = vp.PreparedPolygon.prepare(vx, vy, vp.KIND_ALL, device=device, stream=stream)
         self.prep_ms = (time.perf_counter() - t0) * 1e3
         self.n_edges = self.poly.n
+        # C1 is the f64 oracle config: its points stay f64 and run the exact kernels
+        self.f64 = self.xs.dtype == torch.float64
+        if self.f64:
+            self.bytes_per_unit = 16
+            self.issue_cycles = None
 
     def launch(self, e, words, count, stream):
         self.poly.test(e, self.xs, self.ys, words=words, count=count, stream=stream)
 
     def prepare_host(self):
         t = self.torch
-        self.hx = t.empty(self.xs.numel(), dtype=t.float32, pin_memory=True)
-        self.hy = t.empty(self.ys.numel(), dtype=t.float32, pin_memory=True)
+        self.hx = t.empty(self.xs.numel(), dtype=self.xs.dtype, pin_memory=True)
+        self.hy = t.empty(self.ys.numel(), dtype=self.ys.dtype, pin_memory=True)
         self.hx.copy_(self.xs)
         self.hy.copy_(self.ys)
 
@@ -550,13 +555,17 @@ def main():
                         "tflops_alg": 4 * pe / t / 1e12})
     clk_hz = ((clocks or {}).get("sm_mhz") or 1965.0) * 1e6
     sms = torch.cuda.get_device_properties(local).multi_processor_count
+    f64 = getattr(job, "f64", False)
     for k in kernels:
-        peak_pe = sms * 4 * 32 * clk_hz / job.issue_cycles[k["engine"]]
-        k["issue_model_frac"] = k["point_edge_per_s"] / peak_pe
+        if job.issue_cycles:
+            peak_pe = sms * 4 * 32 * clk_hz / job.issue_cycles[k["engine"]]
+            k["issue_model_frac"] = k["point_edge_per_s"] / peak_pe
     dom = max(range(3), key=lambda e: per_kernel_ms[e])
     dk = kernels[dom]
     hbm_frac = dk["GB_per_s"] / hbm_peak
     fma_tflops = 2 * fma_peak / 1e12 if fma_peak else 2 * FFMA_PER_SM_CLK * 148 * 1.965e9 / 1e12
+    if f64:  # DFMA issues at half the FFMA rate (profiles/pipe_peaks_r01.json)
+        fma_tflops /= 2
     fma_frac = dk["tflops_alg"] / fma_tflops
     compute_bound = (4 * pe / (fma_tflops * 1e12)) > (bytes_per_launch / (hbm_peak * 1e9))
     traffic = None
@@ -566,7 +575,8 @@ def main():
     except Exception:
         pass
     if compute_bound:
-        roof = {"bound": "fp32-fma", "achieved": dk["tflops_alg"], "peak": fma_tflops,
+        roof = {"bound": "fp64-fma" if f64 else "fp32-fma", "achieved": dk["tflops_alg"],
+                "peak": fma_tflops,
                 "unit": "TFLOP/s", "frac": fma_frac, "traffic": traffic}
     else:
         roof = {"bound": "hbm", "achieved": dk["GB_per_s"], "peak": hbm_peak, "unit": "GB/s",
@@ -579,14 +589,15 @@ def main():
                  "algorithmic_bytes_per_launch": bytes_per_launch,
                  "traffic_source": "profiles/traffic_r01.json (ncu --set full dram__bytes_read+write "
                                    "of this kernel on this workload, scaled to this launch)",
-                 "issue_model_frac": dk["issue_model_frac"]})
+                 "issue_model_frac": dk.get("issue_model_frac")})
 
     step_s = ms_max * 1e-3 / args.steps
     total_tests = 3 * M
     line = {
         "metric": METRIC, "value": total_tests / step_s, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_s * 1e3,
-        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "f64" if f64 else "f32",
         "data": "synthetic (seeded counter-based points, reference-sampler polygon)",
         "config": {**config_block(args, world), "n_edges": n_edges},
         "gpu_launches": 3 * args.steps,
