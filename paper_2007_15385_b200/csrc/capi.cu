@@ -8,13 +8,18 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <array>
+#include <atomic>
 #include <cmath>
+#include <condition_variable>
 #include <cstdint>
 #include <cstring>
+#include <functional>
 #include <mutex>
 #include <new>
 #include <numbers>
 #include <random>
+#include <thread>
 #include <vector>
 
 #include "vpipg.h"
@@ -364,7 +369,140 @@ struct Staging {
   cudaStream_t st[kSlots] = {};
   char* buf[kSlots] = {};
   size_t cap = 0;  // bytes per slot
+  // pageable-host path: pinned bounce buffers (points in, mask words out) and
+  // one completion event per slot
+  char* hin[kSlots] = {};
+  char* hout[kSlots] = {};
+  size_t hcap_in = 0, hcap_out = 0;
+  cudaEvent_t ev[kSlots] = {};
 };
+
+}  // namespace
+}  // extern "C"
+
+namespace {
+
+// A small persistent host thread pool for the pageable-buffer copies: one
+// std::thread per hardware thread (at most 16), parallel_for hands out index
+// ranges, the caller works too. One parallel_for at a time.
+class HostPool {
+ public:
+  static HostPool& get() {
+    static HostPool pool;
+    return pool;
+  }
+  template <class F>
+  void parallel_for(int n, F&& fn) {
+    if (n <= 0) return;
+    std::lock_guard<std::mutex> call(call_mu_);
+    if (workers_.empty() || n == 1) {
+      for (int i = 0; i < n; ++i) fn(i);
+      return;
+    }
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      task_ = [&fn](int i) { fn(i); };
+      n_ = n;
+      next_.store(0);
+      busy_ = static_cast<int>(workers_.size());
+      ++gen_;
+    }
+    cv_.notify_all();
+    drain();
+    std::unique_lock<std::mutex> lk(mu_);
+    done_cv_.wait(lk, [&] { return busy_ == 0; });
+    task_ = nullptr;
+  }
+  ~HostPool() {
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      stop_ = true;
+      ++gen_;
+    }
+    cv_.notify_all();
+    for (auto& t : workers_) t.join();
+  }
+
+ private:
+  HostPool() {
+    const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+    const unsigned n = std::min(16u, hw);
+    for (unsigned i = 1; i < n; ++i) workers_.emplace_back([this] { loop(); });
+  }
+  void drain() {
+    for (int i = next_.fetch_add(1); i < n_; i = next_.fetch_add(1)) task_(i);
+  }
+  void loop() {
+    uint64_t seen = 0;
+    for (;;) {
+      {
+        std::unique_lock<std::mutex> lk(mu_);
+        cv_.wait(lk, [&] { return gen_ != seen; });
+        seen = gen_;
+        if (stop_) return;
+      }
+      drain();
+      std::lock_guard<std::mutex> lk(mu_);
+      if (--busy_ == 0) done_cv_.notify_one();
+    }
+  }
+  std::vector<std::thread> workers_;
+  std::mutex call_mu_, mu_;
+  std::condition_variable cv_, done_cv_;
+  std::function<void(int)> task_;
+  std::atomic<int> next_{0};
+  int n_ = 0, busy_ = 0;
+  uint64_t gen_ = 0;
+  bool stop_ = false;
+};
+
+// memcpy split into 256 KiB pieces over the pool
+void pool_memcpy(void* dst, const void* src, size_t bytes) {
+  constexpr size_t kPiece = size_t(1) << 18;
+  const int pieces = static_cast<int>((bytes + kPiece - 1) / kPiece);
+  HostPool::get().parallel_for(pieces, [&](int i) {
+    const size_t o = size_t(i) * kPiece;
+    std::memcpy(static_cast<char*>(dst) + o, static_cast<const char*>(src) + o,
+                std::min(kPiece, bytes - o));
+  });
+}
+
+// mask words (bit j of the stream = point j) -> one byte per point
+void pool_expand_bits(uint8_t* dst, const uint32_t* words, uint64_t m) {
+  static const std::array<uint64_t, 256> lut = [] {
+    std::array<uint64_t, 256> t{};
+    for (int b = 0; b < 256; ++b)
+      for (int k = 0; k < 8; ++k) t[b] |= uint64_t((b >> k) & 1) << (8 * k);
+    return t;
+  }();
+  const uint8_t* src = reinterpret_cast<const uint8_t*>(words);
+  constexpr uint64_t kPiece = uint64_t(1) << 16;  // points per piece (multiple of 8)
+  const int pieces = static_cast<int>((m + kPiece - 1) / kPiece);
+  HostPool::get().parallel_for(pieces, [&](int i) {
+    const uint64_t lo = uint64_t(i) * kPiece, hi = std::min(m, lo + kPiece);
+    uint64_t j = lo;
+    for (; j + 8 <= hi; j += 8) {
+      const uint64_t v = lut[src[j / 8]];
+      std::memcpy(dst + j, &v, 8);
+    }
+    for (; j < hi; ++j) dst[j] = (src[j / 8] >> (j % 8)) & 1u;
+  });
+}
+
+bool host_pinned(const void* p) {
+  if (!p) return true;
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost;
+}
+
+}  // namespace
+
+extern "C" {
+namespace {
 
 Staging& staging(int device) {
   static Staging s[64];
@@ -411,13 +549,127 @@ int staging_reserve(Staging& st, size_t need) {
   return kOk;
 }
 
+// Caller holds st.mu and the device guard.
+int host_reserve(Staging& st, size_t in_bytes, size_t out_bytes) {
+  for (auto& e : st.ev)
+    if (!e) VPIPG_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  if (in_bytes > st.hcap_in) {
+    for (auto& b : st.hin) {
+      if (b) cudaFreeHost(b);
+      b = nullptr;
+    }
+    st.hcap_in = 0;
+    for (auto& b : st.hin) VPIPG_TRY(cudaMallocHost(&b, in_bytes));
+    st.hcap_in = in_bytes;
+  }
+  if (out_bytes > st.hcap_out) {
+    for (auto& b : st.hout) {
+      if (b) cudaFreeHost(b);
+      b = nullptr;
+    }
+    st.hcap_out = 0;
+    for (auto& b : st.hout) VPIPG_TRY(cudaMallocHost(&b, out_bytes));
+    st.hcap_out = out_bytes;
+  }
+  return kOk;
+}
+
+// pageable chunks: about 1/8 of the batch (so even a 1 Mi-point call overlaps
+// its bounce copies with the link), 64 Ki .. 2 Mi points, 32-aligned
+uint64_t host_chunk(uint64_t m) {
+  uint64_t c = (m / 8 + 31) & ~uint64_t(31);
+  return std::min<uint64_t>(std::max<uint64_t>(c, uint64_t(1) << 16), uint64_t(1) << 21);
+}
+
+// The host-buffer path for pageable memory (a std::vector behind the vpip::
+// shim, a numpy array): the pool copies each chunk's points into a pinned
+// bounce slot while the GPU works on the previous chunks, the copy engine
+// moves it at link rate, the engines write mask WORDS (1/8 of the byte mask
+// on the link), and the pool copies / expands them into the caller's words or
+// bytes once that slot's event fires. Pinned inputs skip the bounce copy.
+int host_staged(const vpipg_poly* p, const int* eng, int ne, int dtype, const void* xs,
+                const void* ys, uint64_t m, uint32_t* const* mask_words,
+                uint8_t* const* mask_bytes, uint64_t* inside, Staging& st) {
+  const size_t elt = dtype == VPIPG_F64 ? sizeof(double) : sizeof(float);
+  const uint64_t chunk = std::min<uint64_t>(m, host_chunk(m));
+  const size_t wbytes = align256((chunk + 31) / 32 * 4);
+  int rc = staging_reserve(st, slot_bytes(chunk, elt, false));
+  if (!rc) rc = host_reserve(st, 2 * align256(chunk * elt), 3 * wbytes);
+  if (rc) return rc;
+  SlotView slot[kSlots];
+  for (int i = 0; i < kSlots; ++i) slot[i] = slot_view(st.buf[i], chunk, elt, false);
+  auto fail = [&](cudaError_t e) {
+    if (e != cudaSuccess && rc == kOk) rc = cuda_code(e);
+    return rc != kOk;
+  };
+  auto want = [&](int e) {
+    return (mask_words && mask_words[e]) || (mask_bytes && mask_bytes[e]);
+  };
+  for (int i = 0; i < kSlots && rc == kOk; ++i) fail(cudaMemsetAsync(slot[i].c, 0, 24, st.st[i]));
+  const bool in_pinned = host_pinned(xs) && host_pinned(ys);
+  const char* hx = static_cast<const char*>(xs);
+  const char* hy = static_cast<const char*>(ys);
+  const uint64_t nchunks = (m + chunk - 1) / chunk;
+  auto finish = [&](uint64_t c) {  // chunk c's masks: pinned slot -> caller
+    const int i = static_cast<int>(c % kSlots);
+    if (fail(cudaEventSynchronize(st.ev[i]))) return;
+    const uint64_t base = c * chunk, len = std::min<uint64_t>(chunk, m - base);
+    for (int k = 0; k < ne; ++k) {
+      const int e = eng[k];
+      const uint32_t* hw = reinterpret_cast<const uint32_t*>(st.hout[i] + e * wbytes);
+      if (mask_words && mask_words[e]) pool_memcpy(mask_words[e] + base / 32, hw, (len + 31) / 32 * 4);
+      if (mask_bytes && mask_bytes[e]) pool_expand_bits(mask_bytes[e] + base, hw, len);
+    }
+  };
+  uint64_t c = 0;
+  for (; c < nchunks && rc == kOk; ++c) {
+    const int i = static_cast<int>(c % kSlots);
+    if (c >= kSlots) finish(c - kSlots);
+    if (rc) break;
+    cudaStream_t s = st.st[i];
+    const uint64_t base = c * chunk, len = std::min<uint64_t>(chunk, m - base);
+    const void* sx = hx + base * elt;
+    const void* sy = hy + base * elt;
+    if (!in_pinned) {
+      char* bx = st.hin[i];
+      char* by = st.hin[i] + align256(chunk * elt);
+      pool_memcpy(bx, sx, len * elt);
+      pool_memcpy(by, sy, len * elt);
+      sx = bx;
+      sy = by;
+    }
+    if (fail(cudaMemcpyAsync(slot[i].x, sx, len * elt, cudaMemcpyHostToDevice, s))) break;
+    if (fail(cudaMemcpyAsync(slot[i].y, sy, len * elt, cudaMemcpyHostToDevice, s))) break;
+    for (int k = 0; k < ne && rc == kOk; ++k) {
+      const int e = eng[k];
+      uint32_t* dw = want(e) ? slot[i].w[e] : nullptr;
+      TestArgs a{slot[i].x, slot[i].y, len, dw, nullptr, slot[i].c + e};
+      rc = dispatch(p, e, dtype, a, s);
+      if (!rc && dw)
+        fail(cudaMemcpyAsync(st.hout[i] + e * wbytes, dw, (len + 31) / 32 * 4, cudaMemcpyDeviceToHost, s));
+    }
+    if (rc == kOk) fail(cudaEventRecord(st.ev[i], s));
+  }
+  for (uint64_t f = c > kSlots ? c - kSlots : 0; rc == kOk && f < c; ++f) finish(f);
+  unsigned long long cnt[kSlots][3] = {};
+  for (int i = 0; i < kSlots; ++i)
+    if (rc == kOk) fail(cudaMemcpyAsync(cnt[i], slot[i].c, 24, cudaMemcpyDeviceToHost, st.st[i]));
+  for (auto& s2 : st.st) fail(cudaStreamSynchronize(s2));
+  if (rc == kOk && inside)
+    for (int k = 0; k < ne; ++k) {
+      inside[eng[k]] = 0;
+      for (int i = 0; i < kSlots; ++i) inside[eng[k]] += cnt[i][eng[k]];
+    }
+  return rc;
+}
+
 }  // namespace
 
 int vpipg_release_staging(int device) {
   if (device < 0 || device >= 64) return kInvalid;
   Staging& st = staging(device);
   std::lock_guard<std::mutex> lock(st.mu);
-  if (!st.st[0] && !st.cap) return kOk;
+  if (!st.st[0] && !st.cap && !st.hcap_in) return kOk;
   DeviceGuard g(device);
   int rc = kOk;
   for (auto& s : st.st) {
@@ -432,6 +684,14 @@ int vpipg_release_staging(int device) {
     b = nullptr;
   }
   st.cap = 0;
+  for (int i = 0; i < kSlots; ++i) {
+    if (st.hin[i]) cudaFreeHost(st.hin[i]);
+    if (st.hout[i]) cudaFreeHost(st.hout[i]);
+    if (st.ev[i]) cudaEventDestroy(st.ev[i]);
+    st.hin[i] = st.hout[i] = nullptr;
+    st.ev[i] = nullptr;
+  }
+  st.hcap_in = st.hcap_out = 0;
   return rc;
 }
 
@@ -448,12 +708,25 @@ int vpipg_test_host_multi(const vpipg_poly* p, uint32_t engines, int dtype, cons
   if (!xs || !ys) return kInvalid;
   DeviceGuard g(p->device);
   const size_t elt = dtype == VPIPG_F64 ? sizeof(double) : sizeof(float);
-  bool want_bytes = false;
-  for (int k = 0; k < ne; ++k) want_bytes |= mask_bytes && mask_bytes[eng[k]];
-  // chunks of 16 Mi points, kSlots in flight on their own streams: the points
+  bool want_bytes = false, pinned = host_pinned(xs) && host_pinned(ys);
+  for (int k = 0; k < ne; ++k) {
+    want_bytes |= mask_bytes && mask_bytes[eng[k]];
+    if (mask_words) pinned = pinned && host_pinned(mask_words[eng[k]]);
+    if (mask_bytes) pinned = pinned && host_pinned(mask_bytes[eng[k]]);
+  }
+  if (!pinned) {
+    Staging& st = staging(p->device);
+    std::lock_guard<std::mutex> lock(st.mu);
+    return host_staged(p, eng, ne, dtype, xs, ys, m, mask_words, mask_bytes, inside, st);
+  }
+  // all-pinned buffers: DMA straight from / to the caller's memory in chunks,
+  // kSlots in flight on their own streams: the points
   // cross PCIe once, every requested engine tests them, and the copy engines
   // stay busy in both directions
-  const uint64_t chunk = std::min<uint64_t>(m, kChunk);
+  // about 1/8 of the batch per chunk (1 Mi .. 16 Mi points) so copies in
+  // both directions overlap the kernels even for mid-size batches
+  const uint64_t chunk = std::min<uint64_t>(
+      m, std::min<uint64_t>(kChunk, std::max<uint64_t>(uint64_t(1) << 20, (m / 8 + 31) & ~uint64_t(31))));
   Staging& st = staging(p->device);
   std::lock_guard<std::mutex> lock(st.mu);
   int rc = staging_reserve(st, slot_bytes(chunk, elt, want_bytes));

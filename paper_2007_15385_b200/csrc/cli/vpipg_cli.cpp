@@ -6,6 +6,14 @@
 //                  [--format csv|binary] [--out O] [--dtype f64|f32]
 //   vpipg convert  --polygon P [--out O]
 //   vpipg validate --polygon P [--points F] [--count N] [--seed S] [--band B]
+//   vpipg bench    [--edges 3..15] [--batch N] [--reps R] [--seed S]
+//                  [--engines voronoi,sign_of_offset,ray_crossing] [--threads T] [--out O]
+//
+// `bench` is run_benchmark (bench.cpp:115-222) over the drop-in: the same
+// regular n-gons, batches, discarded warm-ups, seeded shuffled repetition
+// order and CSV schema (bench.cpp:224-234), with every batch call going
+// through the vpip:: API to the B200 (host f64 batch in, byte mask out);
+// `--threads` is accepted and ignored, as in the C++ shim.
 //
 // File formats are the reference's (io.hpp:24-40): polygon JSON
 // {"vertices": [[x, y], ...]} or headerless "x,y" CSV (sniffed); points "x,y"
@@ -15,8 +23,10 @@
 // ballot words: bit j of the payload is point j in both. Exit codes match the
 // reference: 0 ok, 2 on any input / usage / device error. The default dtype is
 // f64, the reference-exact kernels, so masks equal `vpip test` bit for bit.
+#include <algorithm>
 #include <cerrno>
 #include <charconv>
+#include <chrono>
 #include <cmath>
 #include <cstdint>
 #include <cstdio>
@@ -24,6 +34,8 @@
 #include <fstream>
 #include <iostream>
 #include <map>
+#include <optional>
+#include <random>
 #include <sstream>
 #include <stdexcept>
 #include <string>
@@ -33,6 +45,7 @@
 
 #include "vpip/engines.hpp"
 #include "vpip/sampling.hpp"
+#include "vpip/voronoi.hpp"
 #include "vpipg.h"
 
 namespace {
@@ -291,11 +304,155 @@ int cmd_validate(std::map<std::string, std::string>& o) {
   return rep.pass ? 0 : 1;
 }
 
+// "3..15", "7" or "3,5,9" (vpip.cpp:46-77)
+std::vector<int> parse_edge_spec(const std::string& spec) {
+  std::vector<int> counts;
+  std::stringstream ss(spec);
+  std::string tok;
+  auto to_int = [](const std::string& t) {
+    int v = 0;
+    const auto [ptr, ec] = std::from_chars(t.data(), t.data() + t.size(), v);
+    if (ec != std::errc{} || ptr != t.data() + t.size()) throw Fail("bad edge count '" + t + "'");
+    return v;
+  };
+  while (std::getline(ss, tok, ',')) {
+    if (tok.empty()) continue;
+    const size_t dots = tok.find("..");
+    if (dots == std::string::npos) {
+      counts.push_back(to_int(tok));
+    } else {
+      const int lo = to_int(tok.substr(0, dots)), hi = to_int(tok.substr(dots + 2));
+      if (hi < lo) throw Fail("empty edge range '" + tok + "'");
+      for (int n = lo; n <= hi; ++n) counts.push_back(n);
+    }
+  }
+  return counts;
+}
+
+int cmd_bench(std::map<std::string, std::string>& o) {
+  const std::vector<int> edges = parse_edge_spec(o.count("--edges") ? o["--edges"] : "3..15");
+  const size_t batch = o.count("--batch") ? std::stoull(o["--batch"]) : 1000000;
+  const int reps = o.count("--reps") ? std::stoi(o["--reps"]) : 10;
+  const uint64_t seed = o.count("--seed") ? std::stoull(o["--seed"]) : 42;
+  const int threads = o.count("--threads") ? std::stoi(o["--threads"]) : 1;
+  std::vector<vpip::EngineKind> engines;
+  {
+    std::stringstream ss(o.count("--engines") ? o["--engines"]
+                                              : "voronoi,sign_of_offset,ray_crossing");
+    std::string tok;
+    while (std::getline(ss, tok, ',')) {
+      if (tok.empty()) continue;
+      const std::optional<vpip::EngineKind> k = vpip::parse_engine(tok);
+      if (!k) throw Fail("unknown engine '" + tok + "'");
+      engines.push_back(*k);
+    }
+  }
+  // check_config (bench.cpp:48-67)
+  if (edges.empty()) throw Fail("no edge counts configured");
+  for (int n : edges)
+    if (n < 3) throw Fail("edge count " + std::to_string(n) + " is below 3");
+  if (batch < 1 || reps < 1 || threads < 1 || engines.empty()) throw Fail("bad bench configuration");
+
+  using Clock = std::chrono::steady_clock;
+  auto ns_since = [](Clock::time_point t0) {
+    return std::max<uint64_t>(1, std::chrono::duration_cast<std::chrono::nanoseconds>(Clock::now() - t0).count());
+  };
+  struct Work {
+    vpip::ConvexPolygon polygon;
+    vpip::PointBatch batch;
+  };
+  std::vector<Work> work;
+  for (int n : edges) {
+    vpip::ConvexPolygon poly = vpip::regular_polygon(static_cast<size_t>(n), 1.0);
+    const vpip::Box box = vpip::bounding_box(poly.vertices()).scaled(2.0);
+    vpip::PointBatch b = vpip::sample_points(batch, box, vpip::mix_seed(seed, static_cast<uint64_t>(n)));
+    work.push_back({std::move(poly), std::move(b)});
+  }
+  struct Rec {
+    vpip::EngineKind engine;
+    int n;
+    size_t batch;
+    int rep;
+    bool convert;
+    uint64_t ns;
+  };
+  struct Pair {
+    std::optional<Rec> convert;
+    std::vector<Rec> queries;
+    vpip::GeneratorSet gen;
+  };
+  std::vector<std::vector<Pair>> res(engines.size(), std::vector<Pair>(edges.size()));
+  uint64_t sink = 0;
+  auto run_once = [&](vpip::EngineKind e, const Work& w, const vpip::GeneratorSet& g) {
+    switch (e) {
+      case vpip::EngineKind::Voronoi: return vpip::voronoi_contains_batch(g, w.batch, threads);
+      case vpip::EngineKind::SignOfOffset:
+        return vpip::sign_of_offset_contains_batch(w.polygon, w.batch, threads);
+      default: return vpip::ray_crossing_contains_batch(w.polygon.vertices(), w.batch, threads);
+    }
+  };
+  for (size_t e = 0; e < engines.size(); ++e)
+    for (size_t i = 0; i < edges.size(); ++i) {
+      Pair& pr = res[e][i];
+      if (engines[e] == vpip::EngineKind::Voronoi) {
+        const auto t0 = Clock::now();
+        pr.gen = vpip::to_voronoi(work[i].polygon);
+        pr.convert = Rec{engines[e], edges[i], 0, 0, true, ns_since(t0)};
+      }
+      sink += vpip::count_inside(run_once(engines[e], work[i], pr.gen));  // discarded warm-up
+    }
+  std::vector<std::pair<size_t, size_t>> order;
+  for (size_t e = 0; e < engines.size(); ++e)
+    for (size_t i = 0; i < edges.size(); ++i) order.emplace_back(e, i);
+  for (int rep = 0; rep < reps; ++rep) {
+    std::mt19937_64 rng(vpip::mix_seed(seed, 0x0bef0000u + static_cast<unsigned>(rep)));
+    std::shuffle(order.begin(), order.end(), rng);
+    for (const auto& [e, i] : order) {
+      const auto t0 = Clock::now();
+      const vpip::InclusionMask mask = run_once(engines[e], work[i], res[e][i].gen);
+      res[e][i].queries.push_back(Rec{engines[e], edges[i], batch, rep, false, ns_since(t0)});
+      sink += vpip::count_inside(mask);
+    }
+  }
+  std::ostringstream csv;
+  csv << "engine,n_edges,batch_size,repetition,phase,wall_time_ns,throughput_pts_per_s\n";
+  std::map<std::pair<int, int>, std::vector<double>> med;
+  for (size_t e = 0; e < engines.size(); ++e)
+    for (size_t i = 0; i < edges.size(); ++i) {
+      std::vector<Rec> rs;
+      if (res[e][i].convert) rs.push_back(*res[e][i].convert);
+      rs.insert(rs.end(), res[e][i].queries.begin(), res[e][i].queries.end());
+      for (const Rec& r : rs) {
+        const double tp = r.batch ? static_cast<double>(r.batch) / (static_cast<double>(r.ns) * 1e-9) : 0.0;
+        char buf[64];
+        std::snprintf(buf, sizeof buf, "%.17g", tp);
+        csv << vpip::engine_name(r.engine) << ',' << r.n << ',' << r.batch << ',' << r.rep << ','
+            << (r.convert ? "convert" : "query") << ',' << r.ns << ',' << buf << '\n';
+        if (!r.convert) med[{static_cast<int>(e), r.n}].push_back(static_cast<double>(r.ns));
+      }
+    }
+  std::ofstream file;
+  output(o.count("--out") ? o["--out"] : "", file) << csv.str();
+  std::cerr << "engine          n   median ms   median pts/s\n";
+  for (auto& [key, v] : med) {
+    std::sort(v.begin(), v.end());
+    const size_t k = v.size();
+    const double ns = k % 2 ? v[k / 2] : 0.5 * (v[k / 2 - 1] + v[k / 2]);
+    char line[128];
+    std::snprintf(line, sizeof line, "%-14s %3d   %9.3f   %.4g\n",
+                  std::string(vpip::engine_name(engines[key.first])).c_str(), key.second, ns * 1e-6,
+                  static_cast<double>(batch) / (ns * 1e-9));
+    std::cerr << line;
+  }
+  (void)sink;
+  return 0;
+}
+
 }  // namespace
 
 int main(int argc, char** argv) {
   if (argc < 2) {
-    std::cerr << "usage: vpipg test|convert|validate [options]\n";
+    std::cerr << "usage: vpipg test|convert|validate|bench [options]\n";
     return 2;
   }
   const std::string cmd = argv[1];
@@ -312,6 +469,7 @@ int main(int argc, char** argv) {
     if (cmd == "test") return cmd_test(opts);
     if (cmd == "convert") return cmd_convert(opts);
     if (cmd == "validate") return cmd_validate(opts);
+    if (cmd == "bench") return cmd_bench(opts);
     std::cerr << "error: unknown subcommand '" << cmd << "'\n";
   } catch (const std::exception& e) {
     std::cerr << "error: " << e.what() << "\n";

@@ -9,11 +9,15 @@
 #include <algorithm>
 #include <cmath>
 #include <cstring>
+#include <functional>
 #include <limits>
+#include <memory>
+#include <mutex>
 #include <numbers>
 #include <random>
 #include <stdexcept>
 #include <string>
+#include <vector>
 
 #include <cuda_runtime.h>
 
@@ -53,6 +57,47 @@ struct Handle {
   vpipg_poly* p = nullptr;
   ~Handle() { vpipg_destroy(p); }
 };
+
+// The batch functions take the polygon / generator set by value semantics on
+// every call (engines.hpp:90-142), so a caller looping over batches of one
+// polygon would prepare the device tables each time. Prepared handles are
+// therefore cached by their exact input (bitwise, per kind and device), 16
+// entries, least recently used out; handles are immutable and shared, so a
+// cached one may serve concurrent calls (engines.hpp:80-84).
+using HandlePtr = std::shared_ptr<Handle>;
+
+HandlePtr cached_handle(int tag, const std::vector<double>& key,
+                        const std::function<int(int, vpipg_poly**)>& make, const char* what) {
+  struct Entry {
+    int tag, device;
+    std::vector<double> key;
+    HandlePtr h;
+    uint64_t used;
+  };
+  static std::mutex mu;
+  static std::vector<Entry> cache;
+  static uint64_t clock = 0;
+  const int dev = current_device();
+  {
+    std::lock_guard<std::mutex> lock(mu);
+    for (Entry& e : cache)
+      if (e.tag == tag && e.device == dev && e.key.size() == key.size() &&
+          std::memcmp(e.key.data(), key.data(), key.size() * sizeof(double)) == 0) {
+        e.used = ++clock;
+        return e.h;
+      }
+  }
+  auto h = std::make_shared<Handle>();
+  check(make(dev, &h->p), what);  // throws vpip::Error for invalid input
+  std::lock_guard<std::mutex> lock(mu);
+  if (cache.size() >= 16) {
+    auto lru = std::min_element(cache.begin(), cache.end(),
+                                [](const Entry& a, const Entry& b) { return a.used < b.used; });
+    cache.erase(lru);
+  }
+  cache.push_back({tag, dev, key, h, ++clock});
+  return h;
+}
 
 void split(std::span<const Point2> v, std::vector<double>& x, std::vector<double>& y) {
   x.resize(v.size());
@@ -236,11 +281,17 @@ InclusionMask voronoi_contains_batch(const GeneratorSet& g, const PointBatch& po
     outer[2 * k + 1] = g.outer[k].y;
   }
   const double inner[2] = {g.inner.x, g.inner.y};
-  Handle h;
-  check(vpipg_prepare_generators(inner, outer.data(), static_cast<uint32_t>(g.outer.size()),
-                                 current_device(), nullptr, &h.p),
-        "voronoi_contains_batch");
-  return run(h.p, VPIPG_ENGINE_VORONOI, points);
+  std::vector<double> key(outer);
+  key.push_back(inner[0]);
+  key.push_back(inner[1]);
+  const HandlePtr h = cached_handle(
+      VPIPG_ENGINE_VORONOI, key,
+      [&](int dev, vpipg_poly** out) {
+        return vpipg_prepare_generators(inner, outer.data(), static_cast<uint32_t>(g.outer.size()),
+                                        dev, nullptr, out);
+      },
+      "voronoi_contains_batch");
+  return run(h->p, VPIPG_ENGINE_VORONOI, points);
 }
 
 InclusionMask voronoi_contains_batch(const GeneratorSet& g, const PointBatch& points,
@@ -286,11 +337,16 @@ InclusionMask sign_of_offset_contains_batch(const ConvexPolygon& polygon, const 
                                             int) {
   std::vector<double> x, y;
   split(polygon.vertices(), x, y);
-  Handle h;
-  check(vpipg_prepare(x.data(), y.data(), static_cast<uint32_t>(x.size()), VPIPG_KIND_OFFSET,
-                      current_device(), nullptr, &h.p),
-        "sign_of_offset_contains_batch");
-  return run(h.p, VPIPG_ENGINE_OFFSET, points);
+  std::vector<double> key(x);
+  key.insert(key.end(), y.begin(), y.end());
+  const HandlePtr h = cached_handle(
+      VPIPG_ENGINE_OFFSET, key,
+      [&](int dev, vpipg_poly** out) {
+        return vpipg_prepare(x.data(), y.data(), static_cast<uint32_t>(x.size()), VPIPG_KIND_OFFSET, dev,
+                             nullptr, out);
+      },
+      "sign_of_offset_contains_batch");
+  return run(h->p, VPIPG_ENGINE_OFFSET, points);
 }
 
 namespace {
@@ -322,11 +378,16 @@ InclusionMask ray_crossing_contains_batch(std::span<const Point2> vertices, cons
                                           int) {
   std::vector<double> x, y;
   split(vertices, x, y);
-  Handle h;
-  check(vpipg_prepare(x.data(), y.data(), static_cast<uint32_t>(x.size()), VPIPG_KIND_CROSSING,
-                      current_device(), nullptr, &h.p),
-        "ray_crossing_contains_batch");
-  return run(h.p, VPIPG_ENGINE_CROSSING, points);
+  std::vector<double> key(x);
+  key.insert(key.end(), y.begin(), y.end());
+  const HandlePtr h = cached_handle(
+      VPIPG_ENGINE_CROSSING, key,
+      [&](int dev, vpipg_poly** out) {
+        return vpipg_prepare(x.data(), y.data(), static_cast<uint32_t>(x.size()), VPIPG_KIND_CROSSING, dev,
+                             nullptr, out);
+      },
+      "ray_crossing_contains_batch");
+  return run(h->p, VPIPG_ENGINE_CROSSING, points);
 }
 
 // ---------------------------------------------------------------- sampling

@@ -33,6 +33,8 @@ def test_input_errors_exit_2_without_a_device(files):
     assert run("convert", "--polygon", "missing.json", cwd=files).returncode == 2
     assert run("test", "--polygon", "square.json", cwd=files).returncode == 2  # usage
     assert run("frobnicate", cwd=files).returncode == 2
+    assert run("bench", "--edges", "2..4", cwd=files).returncode == 2  # check_config: n >= 3
+    assert run("bench", "--engines", "nope", cwd=files).returncode == 2
     (files / "junk.csv").write_text("0,0\n1,x\n")
     assert run("test", "--polygon", "junk.csv", "--points", "pts.csv", "--engine", "voronoi",
                cwd=files).returncode == 2
@@ -80,3 +82,27 @@ def test_pipb_in_pipm_out_equals_reference(files, golden, orc):
         assert data[:4] == b"PIPM" and struct.unpack("<IQ", data[4:16]) == (1, xs.size)
         want = unpack(golden[f"case_{name}_masks"][e], xs.size)
         assert data[16:] == orc.pack(want).tobytes(), eng  # bit-exact PIPM payload
+
+
+@pytest.mark.gpu
+def test_cli_bench_csv_schema(files, orc):
+    """`vpipg bench` = run_benchmark over the drop-in (bench.cpp:115-234): one
+    convert record per n, R query records per (engine, n), canonical order."""
+    r = run("bench", "--edges", "3,8", "--batch", "100000", "--reps", "3", "--out", "b.csv",
+            cwd=files)
+    assert r.returncode == 0, r.stderr
+    lines = (files / "b.csv").read_text().splitlines()
+    assert lines[0] == "engine,n_edges,batch_size,repetition,phase,wall_time_ns,throughput_pts_per_s"
+    rows = [ln.split(",") for ln in lines[1:]]
+    assert len(rows) == 2 + 3 * 2 * 3
+    assert [x[0] for x in rows[:4]] == ["voronoi"] * 4 and rows[0][4] == "convert"
+    assert rows[0][2] == "0" and float(rows[0][6]) == 0.0
+    q = [x for x in rows if x[4] == "query"]
+    assert all(int(x[2]) == 100000 and int(x[5]) > 0 for x in q)
+    assert {(x[0], x[1]) for x in q} == {(e, n) for e in ("voronoi", "sign_of_offset", "ray_crossing")
+                                         for n in ("3", "8")}
+    assert b"median pts/s" in r.stderr
+    import oracle
+    if oracle.REF_SO.exists():  # the reference's own parser accepts it
+        n, _ = oracle.Reference().read_bench_csv((files / "b.csv").read_text())
+        assert n == len(rows)
