@@ -53,17 +53,23 @@ def _run(cmd: list[str]) -> None:
         sys.stderr.write(r.stderr)
 
 
-def build_variant(tag: str, defines: list[str]) -> Path:
-    """Experimental kernel variant (e.g. -DVPIPG_P=8) as lib/variants/libvpipg_<tag>.so."""
+def build_variant(tag: str, defines: list[str], sources: tuple[str, ...] = ("test_f32.cu",)) -> Path:
+    """Experimental kernel variant (e.g. -DVPIPG_SLAB_P=20) as lib/variants/libvpipg_<tag>.so:
+    `sources` are recompiled with `defines`, everything else is the default build."""
     out = PKG / "lib" / "variants" / f"libvpipg_{tag}.so"
     vdir = OBJ / f"v_{tag}"
     vdir.mkdir(parents=True, exist_ok=True)
     out.parent.mkdir(parents=True, exist_ok=True)
     build()
-    objs = [OBJ / (s + ".o") for s in CU_SOURCES + CXX_SOURCES if s != "test_f32.cu"]
-    vobj = vdir / "test_f32.cu.o"
-    _run([NVCC, *NVCC_FLAGS, *defines, "-c", str(CSRC / "test_f32.cu"), "-o", str(vobj)])
-    _run([NVCC, *ARCH, "-shared", "-o", str(out), str(vobj), *map(str, objs), "-cudart", "static",
+    objs = []
+    for s in CU_SOURCES + CXX_SOURCES:
+        if s in sources:
+            vobj = vdir / (s + ".o")
+            _run([NVCC, *NVCC_FLAGS, *defines, "-c", str(CSRC / s), "-o", str(vobj)])
+            objs.append(vobj)
+        else:
+            objs.append(OBJ / (s + ".o"))
+    _run([NVCC, *ARCH, "-shared", "-o", str(out), *map(str, objs), "-cudart", "static",
           "-Xlinker", "--no-undefined", "-lrt", "-lpthread", "-ldl"])
     return out
 

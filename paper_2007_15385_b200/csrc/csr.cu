@@ -100,7 +100,13 @@ __global__ void prep_csr_kernel(CsrPrepArgs a) {
   }
 }
 
-constexpr int kGP = 4;  // pairs per lane
+#ifndef VPIPG_GP
+#define VPIPG_GP 1
+#endif
+#ifndef VPIPG_GMINB
+#define VPIPG_GMINB 8
+#endif
+constexpr int kGP = VPIPG_GP;  // pairs per lane
 constexpr int kGThreads = 256;
 
 // 32-byte (256-bit) read-only load: four rows (or the header + two rows).
@@ -148,7 +154,8 @@ struct RowAcc {
 };
 
 template <int kEngine>  // 0 voronoi, 1 offset, 2 crossing
-__global__ void __launch_bounds__(kGThreads) gather_kernel(const DbTables t, const GatherArgs a) {
+__global__ void __launch_bounds__(kGThreads, VPIPG_GMINB) gather_kernel(const DbTables t,
+                                                                        const GatherArgs a) {
   const int lane = threadIdx.x & 31;
   const uint64_t gwarp = (uint64_t)blockIdx.x * (kGThreads / 32) + (threadIdx.x >> 5);
   const uint64_t stride = (uint64_t)gridDim.x * (kGThreads / 32) * 32 * kGP;
