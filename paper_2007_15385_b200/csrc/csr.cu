@@ -203,7 +203,13 @@ __global__ void __launch_bounds__(kGThreads, VPIPG_GMINB) gather_kernel(const Db
     }
     bool in[kGP];
 #pragma unroll
-    for (int p = 0; p < kGP; ++p) in[p] = ok[p] && rows[p] > 0 && r[p].inside();
+    for (int p = 0; p < kGP; ++p) {
+      in[p] = ok[p] && rows[p] > 0 && r[p].inside();
+      // a NaN coordinate: the reference's IEEE answer (Voronoi compares are
+      // false -> outside; sign-of-offset raises no flag -> inside)
+      if (kEngine != 2 && ok[p] && rows[p] > 0 && (qx[p] != qx[p] || qy[p] != qy[p]))
+        in[p] = kEngine == 1;
+    }
     uint32_t w[kGP];
 #pragma unroll
     for (int p = 0; p < kGP; ++p) {

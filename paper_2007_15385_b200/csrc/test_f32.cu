@@ -42,14 +42,17 @@ constexpr int kWarps = 8;             // warps per CTA
 constexpr int kThreads = kWarps * 32;
 constexpr int kStages = 2;            // per-warp ring depth
 
+// NaN-propagating three-input max / min (FMNMX3 .NAN, same issue cost): a
+// point with a NaN coordinate turns every bound of its sections into NaN, so
+// the final compare sees NaN and the engine's NaN rule decides (below)
 __device__ __forceinline__ float fmax3(float a, float b, float c) {
   float r;
-  asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+  asm("max.NaN.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
   return r;
 }
 __device__ __forceinline__ float fmin3(float a, float b, float c) {
   float r;
-  asm("min.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+  asm("min.NaN.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
   return r;
 }
 
@@ -57,9 +60,13 @@ __device__ __forceinline__ float fmin3(float a, float b, float c) {
 // Slab engine (Voronoi and sign-of-offset): inside iff
 //   max(XLO) <= x' <= min(XHI)  and  max(YLO) <= y' <= min(YHI)
 // where each group entry is t = B * (other coordinate) + C (see prep.cu).
-template <int P>
+// kNanInside: the answer for a point with a NaN coordinate, the reference's
+// IEEE behaviour -- Voronoi `inner_sq <= outer_sq` is false (outside),
+// sign-of-offset raises no flag, so flags == 0 (inside).
+template <int P, bool kNanIn>
 struct SlabEngine {
   static constexpr int kP = P;
+  static constexpr bool kNanInside = kNanIn;
   struct Params {
     SlabTable tab;
     float ox, oy;
@@ -155,6 +162,7 @@ struct SlabEngine {
 template <int P>
 struct CrossEngine {
   static constexpr int kP = P;
+  static constexpr bool kNanInside = false;  // a = +-1, never NaN
   struct Params {
     CrossTable tab;
     float ox, oy;
@@ -240,20 +248,31 @@ struct CrossEngine {
 // Output: ballot words (PIPM order), optional byte mask, per-lane inside count.
 // The P words of a slice are warp-uniform; lane 0 writes them with 16-byte
 // streaming stores (a slice's words are 64 contiguous, 64-byte aligned bytes).
-// inside = (a >= b): one FSETP feeds both the ballot and a predicated count
+// inside = (a >= b), or (a >= b or unordered) for kNanInside: one FSETP feeds
+// both the ballot and a predicated count
+template <bool kNanInside>
 __device__ __forceinline__ uint32_t vote_ge(float a, float b, uint32_t& cnt) {
   uint32_t w;
-  asm volatile(
-      "{\n\t.reg .pred q;\n\t"
-      "setp.ge.f32 q, %2, %3;\n\t"
-      "vote.sync.ballot.b32 %0, q, 0xffffffff;\n\t"
-      "@q add.u32 %1, %1, 1;\n\t}"
-      : "=r"(w), "+r"(cnt)
-      : "f"(a), "f"(b));
+  if (kNanInside)
+    asm volatile(
+        "{\n\t.reg .pred q;\n\t"
+        "setp.geu.f32 q, %2, %3;\n\t"
+        "vote.sync.ballot.b32 %0, q, 0xffffffff;\n\t"
+        "@q add.u32 %1, %1, 1;\n\t}"
+        : "=r"(w), "+r"(cnt)
+        : "f"(a), "f"(b));
+  else
+    asm volatile(
+        "{\n\t.reg .pred q;\n\t"
+        "setp.ge.f32 q, %2, %3;\n\t"
+        "vote.sync.ballot.b32 %0, q, 0xffffffff;\n\t"
+        "@q add.u32 %1, %1, 1;\n\t}"
+        : "=r"(w), "+r"(cnt)
+        : "f"(a), "f"(b));
   return w;
 }
 
-template <bool kGuard, int P>
+template <bool kGuard, bool kNanInside, int P>
 __device__ __forceinline__ uint32_t emit(float (&av)[P], const float (&bv)[P], uint64_t base,
                                          const TestArgs& a, int lane) {
   uint32_t w[P];
@@ -261,7 +280,7 @@ __device__ __forceinline__ uint32_t emit(float (&av)[P], const float (&bv)[P], u
 #pragma unroll
   for (int p = 0; p < P; ++p) {
     if (kGuard && base + 32u * p + lane >= a.m) av[p] = -INFINITY;
-    w[p] = vote_ge(av[p], bv[p], cnt);
+    w[p] = vote_ge<kNanInside>(av[p], bv[p], cnt);
   }
   if (a.words && lane == 0) {
     const uint64_t w0 = base >> 5;
@@ -308,7 +327,7 @@ __device__ __forceinline__ uint32_t guarded_tile(const typename Eng::Params& prm
     y[p] = ok ? __ldcs(ys + idx) : 0.f;
   }
   Eng::eval(prm, tab, x, y, va, vb);
-  return emit<true, P>(va, vb, base, a, lane);
+  return emit<true, Eng::kNanInside, P>(va, vb, base, a, lane);
 }
 
 // kSmemTab: the polygon table is staged in shared memory once per CTA (the
@@ -377,7 +396,7 @@ __global__ void __launch_bounds__(kThreads, 2)
                &full[s], policy);
     }
     Eng::eval(prm, tab, x, y, va, vb);
-    count += emit<false, P>(va, vb, g * kWarpPts, a, lane);
+    count += emit<false, Eng::kNanInside, P>(va, vb, g * kWarpPts, a, lane);
   }
   // partial last slice: the warp next in round-robin order, guarded loads
   if (g0 == full_slices % W) {
@@ -457,9 +476,14 @@ cudaError_t launch(const typename Eng::Params& prm, const TestArgs& a, cudaStrea
 
 cudaError_t launch_test_f32(const DevTables& t, int engine, const TestArgs& a,
                             cudaStream_t stream) {
-  if (engine == 0 || engine == 1) {
-    using E = SlabEngine<VPIPG_SLAB_P>;
-    typename E::Params prm{t.slab[engine], t.ox, t.oy};
+  if (engine == 0) {
+    using E = SlabEngine<VPIPG_SLAB_P, false>;
+    typename E::Params prm{t.slab[0], t.ox, t.oy};
+    return launch<E>(prm, a, stream);
+  }
+  if (engine == 1) {
+    using E = SlabEngine<VPIPG_SLAB_P, true>;
+    typename E::Params prm{t.slab[1], t.ox, t.oy};
     return launch<E>(prm, a, stream);
   }
   using E = CrossEngine<VPIPG_CROSS_P>;

@@ -151,3 +151,21 @@ def test_gather_invalid_ids_and_polygons_are_outside(orc):
             assert np.array_equal(got[keep], want[keep]), (e, got, want)
             assert got[6:].tolist() == [0, 0, 0]
             assert got[5] == 1  # the clockwise square (reversed by validation) contains its centre
+
+
+def test_gather_nan_points(orc):
+    """NaN query coordinates in the join: Voronoi outside, sign-of-offset inside
+    (the reference's IEEE answers, as in the single-polygon kernels)."""
+    off, vx, vy, cx, cy, r = _db_inputs(64)
+    ids = np.arange(8, dtype=np.uint32)
+    nan = np.float32("nan")
+    xs = np.array([nan, cx[1], nan, cx[3], nan, cx[5], cx[6], cx[7]], np.float32)
+    ys = np.array([cy[0], nan, nan, cy[3], 1e9, cy[5] + 1e4, nan, cy[7]], np.float32)
+    with vp.PolygonDB.prepare(off, vx, vy, vp.KIND_ALL) as db:
+        for e in range(2):
+            b = torch.zeros(ids.size, dtype=torch.uint8, device=DEV)
+            db.test(e, torch.as_tensor(xs, device=DEV), torch.as_tensor(ys, device=DEV),
+                    torch.as_tensor(ids.view(np.int32), device=DEV), bytes_=b)
+            got = b.cpu().numpy()
+            want = orc.join_masks(off, vx, vy, e, xs.astype(np.float64), ys.astype(np.float64), ids)
+            assert np.array_equal(got, want), (e, got.tolist(), want.tolist())

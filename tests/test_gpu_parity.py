@@ -108,6 +108,31 @@ def test_f64_non_finite_points_bit_exact(golden, name):
             assert c == int(want[e].sum())
 
 
+def test_f32_nan_points_follow_the_reference(golden, orc):
+    """f32 kernels on the same points rounded to f32: a NaN coordinate gets the
+    reference's IEEE answer for Voronoi (outside) and sign-of-offset (inside);
+    ray crossing matches when qy is NaN (no edge is in range). A NaN qx with a
+    finite qy makes the reference count only its descending edges -- that case
+    is outside this fp32 kernel's promise, as are points with an infinite
+    coordinate (an infinite distance is inside the relative band)."""
+    for name in ("c1", "square"):
+        vx, vy = golden[f"nonfinite_{name}_v"]
+        with np.errstate(over="ignore"):  # 1e300 -> inf in f32
+            xs, ys = golden[f"nonfinite_{name}_pts"].astype(np.float32)
+        want = orc.masks(vx.astype(np.float32).astype(np.float64),
+                         vy.astype(np.float32).astype(np.float64), xs.astype(np.float64),
+                         ys.astype(np.float64))
+        nan = np.isnan(xs) | np.isnan(ys)
+        fin = np.isfinite(xs) & np.isfinite(ys)
+        band = band_mask(orc, vx, vy, np.where(fin, xs, 0).astype(np.float64),
+                         np.where(fin, ys, 0).astype(np.float64))
+        with vp.PreparedPolygon.prepare(vx, vy, vp.KIND_ALL) as p:
+            for e in range(3):
+                _, b, _ = run_device(p, e, xs, ys)
+                check = (nan if e < 2 else np.isnan(ys)) | (fin & ~band)
+                assert np.array_equal(b[check], want[e][check]), (name, e, b.tolist(), want[e].tolist())
+
+
 def test_f32_engines_match_outside_band(golden, orc):
     total = {0: 0, 1: 0, 2: 0}
     for name in case_names(golden):
