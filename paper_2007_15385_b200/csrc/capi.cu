@@ -15,6 +15,7 @@
 #include <cstdint>
 #include <cstring>
 #include <functional>
+#include <memory>
 #include <mutex>
 #include <new>
 #include <numbers>
@@ -383,8 +384,11 @@ struct Staging {
 namespace {
 
 // A small persistent host thread pool for the pageable-buffer copies: one
-// std::thread per hardware thread (at most 16), parallel_for hands out index
-// ranges, the caller works too. One parallel_for at a time.
+// std::thread per hardware thread (at most 16). parallel_for publishes a job
+// (function, item count, counters); the caller and any worker that wakes in
+// time take items until none are left, and the caller returns as soon as every
+// item is done -- a worker that wakes late finds the job exhausted and goes
+// back to sleep, so no call waits for thread wake-ups.
 class HostPool {
  public:
   static HostPool& get() {
@@ -394,24 +398,22 @@ class HostPool {
   template <class F>
   void parallel_for(int n, F&& fn) {
     if (n <= 0) return;
-    std::lock_guard<std::mutex> call(call_mu_);
     if (workers_.empty() || n == 1) {
       for (int i = 0; i < n; ++i) fn(i);
       return;
     }
+    auto job = std::make_shared<Job>();
+    job->fn = [&fn](int i) { fn(i); };
+    job->n = n;
     {
       std::lock_guard<std::mutex> lk(mu_);
-      task_ = [&fn](int i) { fn(i); };
-      n_ = n;
-      next_.store(0);
-      busy_ = static_cast<int>(workers_.size());
+      job_ = job;
       ++gen_;
     }
     cv_.notify_all();
-    drain();
-    std::unique_lock<std::mutex> lk(mu_);
-    done_cv_.wait(lk, [&] { return busy_ == 0; });
-    task_ = nullptr;
+    run(*job);
+    std::unique_lock<std::mutex> lk(job->mu);
+    job->cv.wait(lk, [&] { return job->done.load() == job->n; });
   }
   ~HostPool() {
     {
@@ -424,34 +426,45 @@ class HostPool {
   }
 
  private:
+  struct Job {
+    std::function<void(int)> fn;
+    int n = 0;
+    std::atomic<int> next{0}, done{0};
+    std::mutex mu;
+    std::condition_variable cv;
+  };
   HostPool() {
     const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
     const unsigned n = std::min(16u, hw);
     for (unsigned i = 1; i < n; ++i) workers_.emplace_back([this] { loop(); });
   }
-  void drain() {
-    for (int i = next_.fetch_add(1); i < n_; i = next_.fetch_add(1)) task_(i);
+  static void run(Job& job) {
+    for (int i = job.next.fetch_add(1); i < job.n; i = job.next.fetch_add(1)) {
+      job.fn(i);
+      if (job.done.fetch_add(1) + 1 == job.n) {
+        std::lock_guard<std::mutex> lk(job.mu);
+        job.cv.notify_all();
+      }
+    }
   }
   void loop() {
     uint64_t seen = 0;
     for (;;) {
+      std::shared_ptr<Job> job;
       {
         std::unique_lock<std::mutex> lk(mu_);
         cv_.wait(lk, [&] { return gen_ != seen; });
         seen = gen_;
         if (stop_) return;
+        job = job_;
       }
-      drain();
-      std::lock_guard<std::mutex> lk(mu_);
-      if (--busy_ == 0) done_cv_.notify_one();
+      if (job) run(*job);
     }
   }
   std::vector<std::thread> workers_;
-  std::mutex call_mu_, mu_;
-  std::condition_variable cv_, done_cv_;
-  std::function<void(int)> task_;
-  std::atomic<int> next_{0};
-  int n_ = 0, busy_ = 0;
+  std::mutex mu_;
+  std::condition_variable cv_;
+  std::shared_ptr<Job> job_;
   uint64_t gen_ = 0;
   bool stop_ = false;
 };
