@@ -77,3 +77,51 @@ def test_c5_full_scale_parity():
         assert abs(c32.item() - c64.item()) <= cmp["disagreeing_points"]
         print("C5 2^31: f32/f64 voronoi disagreements (all in band):", cmp["disagreeing_points"],
               "three-engine disagreements:", rep["disagreeing_points"])
+
+
+def _f32_vs_f64_all_engines(vx, vy, xs, ys):
+    """Every engine: fp32 mask vs the reference-exact fp64 mask of the same
+    (f32) points, classified on the device; disagreements must all lie in the
+    1e-5 relative band. Returns the per-engine disagreement counts."""
+    m = xs.numel()
+    xd, yd = xs.double(), ys.double()
+    out = []
+    with vp.PreparedPolygon.prepare(vx, vy, vp.KIND_ALL) as p:
+        for e in range(3):
+            w32 = torch.empty((m + 31) // 32, dtype=torch.int32, device=DEV)
+            w64 = torch.empty_like(w32)
+            c32 = torch.zeros(1, dtype=torch.int64, device=DEV)
+            c64 = torch.zeros(1, dtype=torch.int64, device=DEV)
+            p.test(e, xs, ys, words=w32, count=c32)
+            p.test(e, xd, yd, words=w64, count=c64)
+            torch.cuda.synchronize()
+            cmp = p.compare_masks(xd, yd, w64, w32, band=1e-5, relative=True)
+            assert cmp["pass"], (e, cmp)
+            assert abs(c32.item() - c64.item()) <= cmp["disagreeing_points"]
+            out.append(cmp["disagreeing_points"])
+    return out
+
+
+@pytest.mark.parametrize("n", W.C3_NS)
+def test_c3_full_scale_f32_vs_f64(n):
+    """BASELINE.json config 3 at full size (2^28 points per n): every fp32 engine
+    equals the reference-exact fp64 engine outside the band."""
+    vx, vy = W.c3_polygon(n)
+    m = W.C3_POINTS
+    xs = torch.empty(m, dtype=torch.float32, device=DEV)
+    ys = torch.empty(m, dtype=torch.float32, device=DEV)
+    vp.fill_uniform_points(int(W.mix_seed_np(W.config_seed(3), 200 + n)), 0, xs, ys, W.C3_BOX)
+    d = _f32_vs_f64_all_engines(vx, vy, xs, ys)
+    assert max(d) < m * 1e-5
+    print(f"C3 n={n}: f32/f64 band disagreements per engine {d}")
+
+
+def test_c2_full_scale_f32_vs_f64():
+    """BASELINE.json config 2 (vehicle 12-gon, 2^24 clustered points)."""
+    vx, vy = W.c2_polygon()
+    px, py = W.c2_points()
+    xs = torch.as_tensor(px, device=DEV)
+    ys = torch.as_tensor(py, device=DEV)
+    assert xs.dtype == torch.float32 and xs.numel() == W.C2_CLUSTERS * W.C2_PER_CLUSTER
+    d = _f32_vs_f64_all_engines(vx, vy, xs, ys)
+    print(f"C2: f32/f64 band disagreements per engine {d}")
