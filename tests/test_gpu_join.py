@@ -95,7 +95,16 @@ def test_device_pair_stream_matches_oracle(orc):
 
 @pytest.mark.parametrize("m", [1, 33, 1 << 20])
 def test_gather_masks_outside_band(orc, m):
-    off, vx, vy, cx, cy, r = _db_inputs(2048)
+    _gather_vs_oracle(orc, m, *_db_inputs(2048))
+
+
+def test_c4_config_gather_vs_oracle(orc):
+    """The real C4 database (65,536 polygons of 4-16 vertices, centres in
+    [0,1000]^2) and 2^22 pairs of its pair stream, every engine vs the oracle."""
+    _gather_vs_oracle(orc, 1 << 22, *W.c4_polygons(vp.random_convex_polygon))
+
+
+def _gather_vs_oracle(orc, m, off, vx, vy, cx, cy, r):
     dcx, dcy, dr = (torch.as_tensor(a, device=DEV) for a in (cx, cy, r))
     xs = torch.empty(m, dtype=torch.float32, device=DEV)
     ys = torch.empty_like(xs)
