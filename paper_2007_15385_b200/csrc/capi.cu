@@ -819,7 +819,7 @@ int vpipg_prepare_csr(const uint32_t* offsets, const double* vx, const double* v
   db->kinds = kinds;
   db->offsets.assign(offsets, offsets + npoly + 1);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  // fixed-stride 32-byte-aligned blocks: header (2 slots) + n_max + 1 rows
+  // fixed-stride 32-byte-aligned blocks: header (2 slots) + up to n_max + 1 rows
   uint32_t nmax = 0;
   for (uint32_t i = 0; i < npoly; ++i) nmax = std::max(nmax, offsets[i + 1] - offsets[i]);
   const uint32_t stride = (nmax + 3 + 3) & ~3u;

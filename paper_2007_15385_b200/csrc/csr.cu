@@ -4,12 +4,15 @@
 // prep_csr_kernel, one thread per polygon:
 //   validate_polygon (geometry.cpp:53-98) -> per-polygon status, CCW order,
 //   to_voronoi (voronoi.cpp:60-71) with the reference's exact f64 arithmetic,
-//   then compact fp32 rows in a polygon-local frame (centre c = f32 bounding
-//   box centre): the generators [inner, outer_k] (Voronoi), the validated
+//   then one fixed-stride, 32-byte-aligned block per polygon and engine: a
+//   16-byte header (n | invalid flag, frame origin c) and fp32 rows in the
+//   polygon-local frame: the n outer generators (Voronoi, c = the centroid
+//   rounded to f32, so the inner generator is the origin), the validated
 //   vertices (sign-of-offset) and the RAW vertices (ray crossing,
-//   vpip.cpp:120-128), 8 bytes per row, each polygon starting on an even row.
-// gather_kernel: every (point, polygon id) pair reads its polygon's 16-byte
-//   header and streams its rows two at a time (16-byte loads) from the
+//   vpip.cpp:120-128), both as v_{n-1}, v_0 .. v_{n-1} with c = the f32
+//   bounding-box centre.
+// gather_kernel: every (point, polygon id) pair reads its polygon's block in
+//   32-byte loads (header + 2 rows, then 4 rows at a time) from the
 //   L2-resident tables; q' = q - c is exact in f32 (Sterbenz) for points near
 //   their polygon. Per point-edge:
 //     Voronoi    |q'-pk'|^2 - |q'-p0'|^2 >= 0 (the reference's squared
@@ -68,19 +71,27 @@ __global__ void prep_csr_kernel(CsrPrepArgs a) {
   const float fcy = (y0 <= y1) ? static_cast<float>(0.5 * (y0 + y1)) : 0.f;
   const double cx = fcx, cy = fcy;
   const CsrView val{vvx, vvy};
+  // Voronoi frame: the centroid rounded to f32, so p0' = p0 - c is below half
+  // an ulp of |p0| (< 6e-8 max(1, |p0|), far inside the 1e-5 band) and is
+  // taken as 0 -- the block carries the n generators only
+  float gcx = fcx, gcy = fcy;
   if (status == 0 && (a.kinds & kKindVoronoi)) {
     double px, py;
     centroid_exact(val, n, &px, &py);
     a.inner[i] = make_double2(px, py);
-    a.gen[blk + 2] = local(make_double2(px, py), cx, cy);
+    gcx = static_cast<float>(px);
+    gcy = static_cast<float>(py);
     for (int k = 0; k < n && status == 0; ++k) {
       double2 g;
       status = reflect_exact(val(k), val((k + 1) % n), px, py, &g);
       if (status) break;
       a.outer[s + k] = g;
-      a.gen[blk + 3 + k] = local(g, cx, cy);
+      a.gen[blk + 2 + k] = local(g, gcx, gcy);
     }
   }
+  // offset / crossing: v_{n-1}, v_0 .. v_{n-1} -- the leading copy of the last
+  // vertex closes the ring without a register pair held across the row loop
+  // (that pair costs the crossing kernel a CTA per SM or a spill)
   if (status == 0 && (a.kinds & kKindOffset) && n > 0) {
     a.ccw[blk + 2] = local(val(n - 1), cx, cy);
     for (int k = 0; k < n; ++k) a.ccw[blk + 3 + k] = local(val(k), cx, cy);
@@ -94,10 +105,10 @@ __global__ void prep_csr_kernel(CsrPrepArgs a) {
   // ignores the flag: it accepts any polygon)
   const bool bad = convex && status != 0;
   const float nbits = __uint_as_float(static_cast<uint32_t>(n) | (bad ? kRangeInvalid : 0u));
-  for (float2* t : {a.gen, a.ccw, a.raw}) {
-    t[blk] = make_float2(nbits, 0.f);
-    t[blk + 1] = make_float2(fcx, fcy);
-  }
+  for (float2* t : {a.gen, a.ccw, a.raw}) t[blk] = make_float2(nbits, 0.f);
+  a.gen[blk + 1] = make_float2(gcx, gcy);
+  a.ccw[blk + 1] = make_float2(fcx, fcy);
+  a.raw[blk + 1] = make_float2(fcx, fcy);
 }
 
 #ifndef VPIPG_GP
@@ -122,15 +133,21 @@ __device__ __forceinline__ Rows4 ld256(const float2* p) {
   return r;
 }
 
-// Per-engine accumulation over consecutive rows.
+// Per-engine accumulation over a polygon's rows (row 0 first): Voronoi rows
+// are the n outer generators (the inner one is the origin); offset / crossing
+// rows are v_{n-1}, v_0 .. v_{n-1}, row 0 only seeding the previous vertex.
 template <int kEngine>
 struct RowAcc {
   uint32_t acc = 0;
   float pa = 0.f, pb = 0.f;  // previous row relative to q' (offset / crossing), or |q'-p0'|^2
   __device__ __forceinline__ void first(float qx, float qy, float rx, float ry) {
-    pa = qx - rx;
-    pb = qy - ry;
-    if (kEngine == 0) pa = fmaf(pa, pa, pb * pb);  // inner_sq
+    if (kEngine == 0) {
+      pa = fmaf(qx, qx, qy * qy);  // inner_sq with p0' = 0
+      next(qx, qy, rx, ry);
+    } else {
+      pa = qx - rx;
+      pb = qy - ry;
+    }
   }
   __device__ __forceinline__ void next(float qx, float qy, float rx, float ry) {
     const float a = qx - rx, b = qy - ry;
@@ -164,7 +181,7 @@ __global__ void __launch_bounds__(kGThreads, VPIPG_GMINB) gather_kernel(const Db
   for (uint64_t base = gwarp * 32 * kGP; base < a.m; base += stride) {
     float qx[kGP], qy[kGP];
     const float2* blk[kGP];
-    uint32_t rows[kGP];  // n + 1 rows, 0 when the pair tests outside regardless
+    uint32_t rows[kGP];  // rows to read (n Voronoi, n + 1 otherwise), 0 = outside regardless
     bool ok[kGP];
     RowAcc<kEngine> r[kGP];
     uint32_t rmax = 0;
@@ -183,10 +200,10 @@ __global__ void __launch_bounds__(kGThreads, VPIPG_GMINB) gather_kernel(const Db
       // crossing takes the raw vertices of any polygon (vpip.cpp:120-128)
       if (kEngine != 2) ok[p] = ok[p] && !(nf & kRangeInvalid);
       const uint32_t n = nf & ~kRangeInvalid;
-      rows[p] = (ok[p] && n > 0) ? n + 1 : 0u;
+      rows[p] = (ok[p] && n > 0) ? (kEngine == 0 ? n : n + 1) : 0u;
       qx[p] = x - h.v[2];  // exact for points near their polygon (Sterbenz)
       qy[p] = y - h.v[3];
-      r[p].first(qx[p], qy[p], h.v[4], h.v[5]);
+      if (rows[p] > 0) r[p].first(qx[p], qy[p], h.v[4], h.v[5]);
       if (rows[p] > 1) r[p].next(qx[p], qy[p], h.v[6], h.v[7]);
       rmax = rows[p] > rmax ? rows[p] : rmax;
     }
