@@ -406,6 +406,8 @@ def main():
     ap.add_argument("--cpu-sample", type=int, default=CPU_SAMPLE)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-graph", action="store_true",
+                    help="time eager launches instead of CUDA-graph replays of the step")
     ap.add_argument("--points", type=int, default=0, help="override the workload size (profiling)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
@@ -471,6 +473,25 @@ def main():
         for _ in range(args.warmup):
             step(False)
     torch.cuda.synchronize()
+    graph = None
+    if not args.no_graph:
+        # the step's work (count reset, 3 engine launches, count all-reduce) as
+        # one CUDA graph; the per-kernel times come from K eager steps run just
+        # before the timed graph replays (events cannot sit inside the graph)
+        with torch.cuda.stream(stream):
+            for _ in range(args.steps):
+                step(True)
+        torch.cuda.synchronize()
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=stream):
+            counts.zero_()
+            for e in range(3):
+                job.launch(e, words[e], counts[e:e + 1], stream)
+            comm.allreduce(counts, stream)
+        with torch.cuda.stream(stream):
+            for _ in range(2):
+                graph.replay()
+        torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     gpus = os.environ.get("CUDA_VISIBLE_DEVICES", ",".join(str(i) for i in range(world)))
@@ -480,15 +501,27 @@ def main():
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
+    gevents = []  # graph mode: per step (start, end) around the replay, flush excluded
     with torch.cuda.stream(stream):
         t_start.record(stream)
         for _ in range(args.steps):
-            step(True)
+            if graph is None:
+                step(True)
+                continue
+            if flush is not None:
+                flush_sink.copy_(flush.view(torch.int64).sum(dtype=torch.int64).view(1))
+            g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            g0.record(stream)
+            graph.replay()
+            g1.record(stream)
+            gevents.append((g0, g1))
         t_end.record(stream)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     clocks = sampler.stop() if sampler else None
+    if graph is not None:
+        sevents = gevents
     # K steps bracketed by t_start / t_end; with an L2 flush between steps the
     # flush kernels sit inside that bracket, so the sum of the per-step events
     # (each starting after its flush) is the timed work instead
@@ -599,7 +632,10 @@ def main():
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "f64" if f64 else "f32",
         "data": "synthetic (seeded counter-based points, reference-sampler polygon)",
-        "config": {**config_block(args, world), "n_edges": n_edges},
+        "config": {**config_block(args, world), "n_edges": n_edges,
+                   "launch": ("eager launches" if args.no_graph else
+                              "one CUDA-graph replay per step (3 engine kernels + count "
+                              "all-reduce); per-kernel times from K eager steps before it")},
         "gpu_launches": 3 * args.steps,
         "roofline": roof, "kernels": kernels, "inside_counts": final_counts,
         "prepare_ms": job.prep_ms,
