@@ -43,6 +43,7 @@ UNIT = "tests/s"
 PEAKS_FILE = ROOT / "MEASURED_PEAKS.json"
 PIPE_PEAKS_FILE = ROOT / "profiles" / "pipe_peaks_r01.json"
 TRAFFIC_FILE = ROOT / "profiles" / "traffic_r01.json"
+NCU_FILE = ROOT / "profiles" / "ncu_full_r01_c5.json"
 # dispatch cycles per point-edge per warp lane-slot (tools/pipe_peaks.cu model:
 # FFMA/FADD 1 cycle, FMNMX3/LOP3 2): slab = FFMA + FMNMX3/2, crossing =
 # 2 FADD + FFMA + 1.5 LOP3
@@ -622,7 +623,18 @@ def main():
                  "algorithmic_bytes_per_launch": bytes_per_launch,
                  "traffic_source": "profiles/traffic_r01.json (ncu --set full dram__bytes_read+write "
                                    "of this kernel on this workload, scaled to this launch)",
-                 "issue_model_frac": dk.get("issue_model_frac")})
+                 "issue_model_frac": dk.get("issue_model_frac"),
+                 "issue_model": "dispatch cycles per point-edge: slab 2 (FFMA + FMNMX3/2), "
+                                "crossing 6 (2 FADD + FFMA + 1.5 LOP3); profiles/round1_summary.md"})
+    try:  # the ncu evidence for the same kernel and workload (issue / pipe utilisation)
+        nk = json.loads(NCU_FILE.with_name(f"ncu_full_r01_{args.workload.split(':')[0]}.json")
+                        .read_text())["kernels"][dk["engine"]]
+        roof["ncu"] = {k.split(".")[0]: nk[k] for k in (
+            "smsp__issue_active.avg.pct_of_peak_sustained_active",
+            "sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active",
+            "sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active") if k in nk}
+    except Exception:
+        pass
 
     step_s = ms_max * 1e-3 / args.steps
     total_tests = 3 * M
