@@ -6,13 +6,17 @@
 //   ray_kernel       (engines.cpp:165-204) -> CrossEngine
 //   count_inside     (engines.cpp:215-217) -> fused popc + one atomic per warp
 //
-// Streaming structure (stream_kernel): a persistent grid; every warp owns a
-// private kStages-deep shared-memory ring and streams its own 512-point slices
-// (slice g goes to warp g mod W) with cp.async.bulk (the 1-D TMA path,
-// evict-first). Lane 0 arms the stage's "full" mbarrier with the expected
-// bytes; after the warp copied a stage into registers, all 32 lanes arrive on
-// its "empty" mbarrier (release) and lane 0 refills it with slice g + S*W, so
-// loads run kStages slices ahead of the math with no cross-warp coupling.
+// Streaming structure: a persistent grid; every warp streams its own slices of
+// 32*P points (slice g goes to warp g mod W), two ways, chosen per engine by
+// measurement:
+//  - stream_kernel (crossing): a private kStages-deep shared-memory ring per
+//    warp filled with cp.async.bulk (the 1-D TMA path, evict-first). Lane 0
+//    arms the stage's "full" mbarrier with the expected bytes; after the warp
+//    copied a stage into registers, all 32 lanes arrive on its "empty"
+//    mbarrier (release) and lane 0 refills it with slice g + S*W, so loads run
+//    kStages slices ahead of the math with no cross-warp coupling.
+//  - ldg_kernel (slab engines): coalesced loads straight into registers after
+//    an L2 prefetch of the slice two rounds ahead.
 // Lane l owns points 32*p + l (p < P) of a slice, so the ballot of sub-tile p
 // is exactly one PIPM mask word (io.cpp:272-279, bit j = point j) and word
 // stores are coalesced. The polygon table is staged once per CTA in shared
@@ -67,6 +71,7 @@ template <int P, bool kNanIn>
 struct SlabEngine {
   static constexpr int kP = P;
   static constexpr bool kNanInside = kNanIn;
+  static constexpr bool kRegStream = true;  // ldg_kernel
   struct Params {
     SlabTable tab;
     float ox, oy;
@@ -163,6 +168,7 @@ template <int P>
 struct CrossEngine {
   static constexpr int kP = P;
   static constexpr bool kNanInside = false;  // a = +-1, never NaN
+  static constexpr bool kRegStream = false;  // stream_kernel (TMA ring)
   struct Params {
     CrossTable tab;
     float ox, oy;
@@ -406,6 +412,60 @@ __global__ void __launch_bounds__(kThreads, 2)
   flush_count(count, a);
 }
 
+// Register-streaming variant (the slab engines): no shared-memory ring -- each
+// warp loads its slice straight into registers (coalesced 128-byte rows,
+// evict-first) after an L2 prefetch of the slice two rounds ahead. Measured
+// against the TMA ring: equal at C5 (compute-bound), 7 % faster at C3 n = 8
+// (memory-bound: 6.6 TB/s), so the slab engines use it; the crossing engine
+// keeps the ring (3 % faster there).
+__device__ __forceinline__ void prefetch_l2(const void* p) {
+  asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(p));
+}
+
+template <class Eng, bool kSmemTab>
+__global__ void __launch_bounds__(kThreads, 2)
+    ldg_kernel(const typename Eng::Params prm, const TestArgs a, const uint64_t full_slices) {
+  constexpr int P = Eng::kP;
+  constexpr int kWarpPts = 32 * P;
+  extern __shared__ __align__(128) unsigned char smem[];
+  float4* s_tab = reinterpret_cast<float4*>(smem);
+  if (kSmemTab) Eng::stage(prm, s_tab);
+  const float4* tab = kSmemTab ? s_tab : Eng::global_table(prm);
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint64_t W = (uint64_t)gridDim.x * kWarps;
+  const uint64_t g0 = (uint64_t)blockIdx.x * kWarps + warp;
+  const float* xs = static_cast<const float*>(a.xs);
+  const float* ys = static_cast<const float*>(a.ys);
+  constexpr int kLines = kWarpPts * 4 / 128;
+  auto prefetch = [&](uint64_t g) {
+    if (g >= full_slices) return;
+    for (int l = lane; l < 2 * kLines; l += 32)
+      prefetch_l2((l < kLines ? xs : ys) + g * kWarpPts + (l % kLines) * 32);
+  };
+  prefetch(g0);
+  prefetch(g0 + W);
+  uint32_t count = 0;
+  for (uint64_t g = g0; g < full_slices; g += W) {
+    prefetch(g + 2 * W);
+    const float* px = xs + g * kWarpPts + lane;
+    const float* py = ys + g * kWarpPts + lane;
+    float x[P], y[P], va[P], vb[P];
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+      x[p] = __ldcs(px + 32 * p);
+      y[p] = __ldcs(py + 32 * p);
+    }
+    Eng::eval(prm, tab, x, y, va, vb);
+    count += emit<false, Eng::kNanInside, P>(va, vb, g * kWarpPts, a, lane);
+  }
+  if (g0 == full_slices % W) {
+    for (uint64_t base = full_slices * kWarpPts; base < a.m; base += kWarpPts)
+      count += guarded_tile<Eng>(prm, tab, a, base, lane);
+  }
+  flush_count(count, a);
+}
+
 template <class Eng, bool kSmemTab>
 __global__ void __launch_bounds__(kThreads) generic_kernel(const typename Eng::Params prm,
                                                           const TestArgs a) {
@@ -456,9 +516,11 @@ cudaError_t launch(const typename Eng::Params& prm, const TestArgs& a, cudaStrea
     k<<<(int)(blocks < cap ? blocks : cap), kThreads, tab, stream>>>(prm, a);
     return cudaGetLastError();
   }
-  auto k = staged ? stream_kernel<Eng, true> : stream_kernel<Eng, false>;
-  const size_t smem = (size_t)kWarps * kStages * 2 * kWarpPts * sizeof(float) +
-                      (size_t)kWarps * 2 * kStages * sizeof(uint64_t) + tab;
+  auto k = Eng::kRegStream ? (staged ? ldg_kernel<Eng, true> : ldg_kernel<Eng, false>)
+                           : (staged ? stream_kernel<Eng, true> : stream_kernel<Eng, false>);
+  const size_t smem = Eng::kRegStream ? tab
+                                      : (size_t)kWarps * kStages * 2 * kWarpPts * sizeof(float) +
+                                            (size_t)kWarps * 2 * kStages * sizeof(uint64_t) + tab;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   int per_sm = 0;

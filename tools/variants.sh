@@ -1,3 +1,4 @@
+shopt -s nullglob
 # A/B kernel variants built by build.build_variant: bash tools/variants.sh [workload]
 w=${1:-c5}
 for v in "" paper_2007_15385_b200/lib/variants/libvpipg_*.so; do
