@@ -516,11 +516,17 @@ cudaError_t launch(const typename Eng::Params& prm, const TestArgs& a, cudaStrea
     k<<<(int)(blocks < cap ? blocks : cap), kThreads, tab, stream>>>(prm, a);
     return cudaGetLastError();
   }
-  auto k = Eng::kRegStream ? (staged ? ldg_kernel<Eng, true> : ldg_kernel<Eng, false>)
-                           : (staged ? stream_kernel<Eng, true> : stream_kernel<Eng, false>);
-  const size_t smem = Eng::kRegStream ? tab
-                                      : (size_t)kWarps * kStages * 2 * kWarpPts * sizeof(float) +
-                                            (size_t)kWarps * 2 * kStages * sizeof(uint64_t) + tab;
+  using Kernel = void (*)(const typename Eng::Params, const TestArgs, const uint64_t);
+  Kernel k;
+  size_t smem;
+  if constexpr (Eng::kRegStream) {
+    k = staged ? ldg_kernel<Eng, true> : ldg_kernel<Eng, false>;
+    smem = tab;
+  } else {
+    k = staged ? stream_kernel<Eng, true> : stream_kernel<Eng, false>;
+    smem = (size_t)kWarps * kStages * 2 * kWarpPts * sizeof(float) +
+           (size_t)kWarps * 2 * kStages * sizeof(uint64_t) + tab;
+  }
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   int per_sm = 0;

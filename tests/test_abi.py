@@ -50,9 +50,14 @@ def test_kernels_use_fma_and_3way_minmax():
     assert blocks
     for body in blocks:
         assert "FMNMX3" in body and "FFMA" in body
-    # the streaming kernel moves points with the bulk-copy (TMA) engine
-    stream = [b for b in sass.split("Function :") if "stream_kernel" in b.split("\n")[0]]
-    assert stream and all("UBLKCP" in b for b in stream)
+    # the crossing engine streams points through the bulk-copy (TMA) ring; the
+    # slab engines load them directly after an L2 prefetch (CCTL.E.PML2)
+    heads = [(b.split("\n")[0], b) for b in sass.split("Function :")]
+    stream = [b for h, b in heads if "stream_kernel" in h]
+    assert stream and all("UBLKCP" in b and "CrossEngine" in h for h, b in heads
+                          if "stream_kernel" in h)
+    ldg = [b for h, b in heads if "ldg_kernel" in h and "SlabEngine" in h]
+    assert ldg and all("CCTL.E.PML2" in b for b in ldg)
 
 
 def test_strerror_and_version():
