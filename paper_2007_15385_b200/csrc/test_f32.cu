@@ -168,7 +168,10 @@ template <int P>
 struct CrossEngine {
   static constexpr int kP = P;
   static constexpr bool kNanInside = false;  // a = +-1, never NaN
-  static constexpr bool kRegStream = false;  // stream_kernel (TMA ring)
+#ifndef VPIPG_CROSS_LDG
+#define VPIPG_CROSS_LDG 0
+#endif
+  static constexpr bool kRegStream = VPIPG_CROSS_LDG;  // 0: stream_kernel (TMA ring)
   struct Params {
     CrossTable tab;
     float ox, oy;
@@ -443,11 +446,13 @@ __global__ void __launch_bounds__(kThreads, 2)
     for (int l = lane; l < 2 * kLines; l += 32)
       prefetch_l2((l < kLines ? xs : ys) + g * kWarpPts + (l % kLines) * 32);
   };
-  prefetch(g0);
-  prefetch(g0 + W);
+#ifndef VPIPG_PF_AHEAD
+#define VPIPG_PF_AHEAD 1
+#endif
+  for (int d = 0; d < VPIPG_PF_AHEAD; ++d) prefetch(g0 + d * W);
   uint32_t count = 0;
   for (uint64_t g = g0; g < full_slices; g += W) {
-    prefetch(g + 2 * W);
+    prefetch(g + VPIPG_PF_AHEAD * W);
     const float* px = xs + g * kWarpPts + lane;
     const float* py = ys + g * kWarpPts + lane;
     float x[P], y[P], va[P], vb[P];
