@@ -309,6 +309,29 @@ def test_host_multi_and_staging_reuse(orc):
     vp.release_staging(0)
 
 
+@pytest.mark.parametrize("m", [4099, 1 << 20])
+def test_unaligned_device_buffers(orc, m):
+    """Point arrays at 4- and 12-byte offsets and a mask-word array that is not
+    16-byte aligned take the guarded paths and give the same words and counts."""
+    vx, vy = W.c1_polygon()
+    xs, ys = orc.sample_points(m + 3, W.C1_BOX, 4242 + m)
+    bx = torch.as_tensor(xs.astype(np.float32), device=DEV)
+    by = torch.as_tensor(ys.astype(np.float32), device=DEV)
+    with vp.PreparedPolygon.prepare(vx, vy, vp.KIND_ALL) as p:
+        for e in range(3):
+            ref_x, ref_y = bx[1:m + 1].clone(), by[3:m + 3].clone()
+            wr = torch.zeros((m + 31) // 32, dtype=torch.int32, device=DEV)
+            cr = torch.zeros(1, dtype=torch.int64, device=DEV)
+            p.test(e, ref_x, ref_y, words=wr, count=cr)
+            wbuf = torch.zeros((m + 31) // 32 + 1, dtype=torch.int32, device=DEV)
+            wu = wbuf[1:]
+            cu = torch.zeros(1, dtype=torch.int64, device=DEV)
+            p.test(e, bx[1:m + 1], by[3:m + 3], words=wu, count=cu)
+            torch.cuda.synchronize()
+            assert torch.equal(wu, wr) and cu.item() == cr.item(), e
+            assert wbuf[0].item() == 0
+
+
 def test_concurrent_streams_share_one_handle(orc):
     # test_engines.cpp:243-257: one generator set serves concurrent callers
     vx, vy = W.c1_polygon()
