@@ -253,6 +253,10 @@ def time_cpu_reference(name: str, sample: int, reps: int, warmup: int):
     t = statistics.median(per_rep)
     desc = (f"first {xs.size} points of the workload stream (f32 rounded, widened to f64), "
             f"3 engines, *_contains_batch(threads={cores}) timed like bench.cpp:196-199")
+    if ref is not None:  # also the single-thread figure, on 1/8 of the sample
+        k = max(1, xs.size // 8)
+        _, ns = ref.masks(vx, vy, xs[:k], ys[:k], threads=1)
+        desc += f"; 1 thread: {3 * k / (sum(ns) * 1e-9):.3e} tests/s on the first {k} points"
     return 3 * xs.size / t, kind, cores, t, desc
 
 
