@@ -11,7 +11,7 @@ ncu --metrics gpu__time_duration.sum --clock-control none -c 200 --csv \
     --log-file gpurun_out/launches_$tag.csv python bench.py --no-e2e --no-cpu-baseline --steps 5 \
     > gpurun_out/launches_$tag.log 2>&1
 $B > gpurun_out/plain_$tag.log 2>&1 && \
-ncu --set full --clock-control none --import-source on -k regex:stream_kernel -s 9 -c 3 \
+ncu --set full --clock-control none --import-source on -k "regex:stream_kernel|ldg_kernel" -s 9 -c 3 \
     -o gpurun_out/full_$tag $B > gpurun_out/full_$tag.log 2>&1 && \
 python tools/ncu_summary.py gpurun_out/full_$tag.ncu-rep \
     --label "ncu --set full --clock-control none, C5 (2^31 f32 points, 32-gon), the three kernels of the first timed step of \`$B\`" \
