@@ -90,6 +90,9 @@ int vpipg_prepare(const double* vx, const double* vy, uint32_t n, uint32_t kinds
 int vpipg_prepare_generators(const double* inner_xy, const double* outer_xy, uint32_t n,
                              int device, void* stream, vpipg_poly** out);
 
+/* Returns the handle's tables to the library's device pool (stream-ordered on
+ * the legacy default stream, no device-wide synchronisation). Work that still
+ * uses the handle on other streams must have completed. */
 void vpipg_destroy(vpipg_poly* poly);
 
 /* n, prepared kinds, and whether validation reversed a clockwise input

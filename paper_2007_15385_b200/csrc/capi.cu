@@ -115,6 +115,26 @@ int validate(std::vector<double>& vx, std::vector<double>& vy, int* reversed) {
 
 size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
+// Per-device pool for polygon blobs: memory stays cached in the pool between
+// prepares (release threshold = max), so prepare / destroy cost no cudaMalloc /
+// cudaFree and no device-wide synchronisation.
+int blob_pool(int device, cudaMemPool_t* out) {
+  static std::mutex mu;
+  static cudaMemPool_t pools[64] = {};
+  std::lock_guard<std::mutex> lock(mu);
+  if (!pools[device]) {
+    cudaMemPoolProps props{};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = device;
+    VPIPG_TRY(cudaMemPoolCreate(&pools[device], &props));
+    uint64_t keep = UINT64_MAX;
+    VPIPG_TRY(cudaMemPoolSetAttribute(pools[device], cudaMemPoolAttrReleaseThreshold, &keep));
+  }
+  *out = pools[device];
+  return kOk;
+}
+
 // Builds the blob, runs the prep kernel, reads back the status.
 int build(vpipg_poly* p, const double* vv, const double* vr, const double* gen, cudaStream_t s) {
   const size_t n = p->n;
@@ -131,24 +151,31 @@ int build(vpipg_poly* p, const double* vv, const double* vr, const double* gen, 
   const size_t o_cross = take(n * sizeof(float4));
   const size_t o_lines = take(n * sizeof(double4));
   const size_t o_meta = take(sizeof(PrepMeta));
-  VPIPG_TRY(cudaMalloc(&p->blob, off));
+  // stream-ordered allocation from the library's per-device pool (no device
+  // synchronisation on prepare / destroy), one packed upload of the inputs
+  cudaMemPool_t pool = nullptr;
+  int rc = blob_pool(p->device, &pool);
+  if (rc) return rc;
+  VPIPG_TRY(cudaMallocFromPoolAsync(&p->blob, off, pool, s));
   char* b = static_cast<char*>(p->blob);
   VPIPG_TRY(cudaMemsetAsync(b, 0, off, s));
+  std::vector<char> up(o_outer, 0);  // [vv | vr | gen] in the blob's own layout
   PrepArgs a{};
   a.n = p->n;
   a.kinds = p->kinds;
   if (vv) {
-    VPIPG_TRY(cudaMemcpyAsync(b + o_vv, vv, 2 * n * sizeof(double), cudaMemcpyHostToDevice, s));
+    std::memcpy(up.data() + o_vv, vv, 2 * n * sizeof(double));
     a.vv = reinterpret_cast<const double*>(b + o_vv);
   }
   if (vr) {
-    VPIPG_TRY(cudaMemcpyAsync(b + o_vr, vr, 2 * n * sizeof(double), cudaMemcpyHostToDevice, s));
+    std::memcpy(up.data() + o_vr, vr, 2 * n * sizeof(double));
     a.vr = reinterpret_cast<const double*>(b + o_vr);
   }
   if (gen) {
-    VPIPG_TRY(cudaMemcpyAsync(b + o_gen, gen, (2 + 2 * n) * sizeof(double), cudaMemcpyHostToDevice, s));
+    std::memcpy(up.data() + o_gen, gen, (2 + 2 * n) * sizeof(double));
     a.gen_in = reinterpret_cast<const double*>(b + o_gen);
   }
+  if (o_outer) VPIPG_TRY(cudaMemcpyAsync(b, up.data(), o_outer, cudaMemcpyHostToDevice, s));
   a.outer = reinterpret_cast<double2*>(b + o_outer);
   a.off = reinterpret_cast<OffsetEdgeF64*>(b + o_off);
   a.ray = reinterpret_cast<RayEdgeF64*>(b + o_ray);
@@ -315,8 +342,11 @@ int vpipg_prepare_generators(const double* inner_xy, const double* outer_xy, uin
 void vpipg_destroy(vpipg_poly* p) {
   if (!p) return;
   if (p->blob) {
+    // back to the pool, ordered after all work on the legacy default stream;
+    // work the caller still has in flight on other streams must be finished
+    // (as with any buffer the caller frees)
     DeviceGuard g(p->device);
-    cudaFree(p->blob);
+    cudaFreeAsync(p->blob, nullptr);
   }
   delete p;
 }
