@@ -207,14 +207,35 @@ __global__ void __launch_bounds__(kGThreads, VPIPG_GMINB) gather_kernel(const Db
       if (rows[p] > 1) r[p].next(qx[p], qy[p], h.v[6], h.v[7]);
       rmax = rows[p] > rmax ? rows[p] : rmax;
     }
-    for (uint32_t k = 2; k < rmax; k += 4) {  // rows k .. k+3 = slots k+2 .. k+5
+    if (kEngine == 1) {
+      // sign-of-offset: per-row predicates (the split loop below spills its
+      // extra live values at 32 registers for this engine)
+      for (uint32_t k = 2; k < rmax; k += 4) {  // rows k .. k+3 = slots k+2 .. k+5
+#pragma unroll
+        for (int p = 0; p < kGP; ++p) {
+          if (k < rows[p]) {
+            const Rows4 q4 = ld256(blk[p] + k + 2);
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+              if (k + u < rows[p]) r[p].next(qx[p], qy[p], q4.v[2 * u], q4.v[2 * u + 1]);
+          }
+        }
+      }
+    } else {
 #pragma unroll
       for (int p = 0; p < kGP; ++p) {
-        if (k < rows[p]) {
+        // full 4-row chunks without per-row predicates, then a tail of <= 3
+        uint32_t k = 2;
+        for (; k + 3 < rows[p]; k += 4) {
           const Rows4 q4 = ld256(blk[p] + k + 2);
 #pragma unroll
-          for (int u = 0; u < 4; ++u)
-            if (k + u < rows[p]) r[p].next(qx[p], qy[p], q4.v[2 * u], q4.v[2 * u + 1]);
+          for (int u = 0; u < 4; ++u) r[p].next(qx[p], qy[p], q4.v[2 * u], q4.v[2 * u + 1]);
+        }
+        if (k < rows[p]) {
+          const Rows4 q4 = ld256(blk[p] + k + 2);
+          r[p].next(qx[p], qy[p], q4.v[0], q4.v[1]);
+          if (k + 1 < rows[p]) r[p].next(qx[p], qy[p], q4.v[2], q4.v[3]);
+          if (k + 2 < rows[p]) r[p].next(qx[p], qy[p], q4.v[4], q4.v[5]);
         }
       }
     }
