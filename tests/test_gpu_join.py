@@ -178,3 +178,27 @@ def test_gather_nan_points(orc):
             got = b.cpu().numpy()
             want = orc.join_masks(off, vx, vy, e, xs.astype(np.float64), ys.astype(np.float64), ids)
             assert np.array_equal(got, want), (e, got.tolist(), want.tolist())
+
+
+@pytest.mark.parametrize("m", [1, 33, 4099, 100003])
+def test_gather_outputs_have_no_stray_writes(m):
+    """Canaries around the join's word / byte outputs stay untouched; bits past
+    m in the last word are zero."""
+    off, vx, vy, cx, cy, r = _db_inputs(256)
+    dcx, dcy, dr = (torch.as_tensor(a, device=DEV) for a in (cx, cy, r))
+    xs = torch.empty(m, dtype=torch.float32, device=DEV)
+    ys = torch.empty_like(xs)
+    ids = torch.empty(m, dtype=torch.int32, device=DEV)
+    vp.fill_join_pairs(W.c4_pair_seed(), 0, xs, ys, ids, dcx, dcy, dr)
+    pad, nw = 64, (m + 31) // 32
+    with vp.PolygonDB.prepare(off, vx, vy, vp.KIND_ALL) as db:
+        for e in range(3):
+            wbuf = torch.full((nw + 2 * pad,), -0x5a5a5a5b, dtype=torch.int32, device=DEV)
+            bbuf = torch.full((m + 2 * pad,), 0xA5, dtype=torch.uint8, device=DEV)
+            db.test(e, xs, ys, ids, words=wbuf[pad:pad + nw], bytes_=bbuf[pad:pad + m])
+            torch.cuda.synchronize()
+            w, b = wbuf.cpu().numpy(), bbuf.cpu().numpy()
+            assert (w[:pad] == -0x5a5a5a5b).all() and (w[pad + nw:] == -0x5a5a5a5b).all()
+            assert (b[:pad] == 0xA5).all() and (b[pad + m:] == 0xA5).all()
+            bits = np.unpackbits(w[pad:pad + nw].view(np.uint8), bitorder="little")
+            assert np.array_equal(bits[:m], b[pad:pad + m]) and not bits[m:].any()

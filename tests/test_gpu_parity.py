@@ -332,6 +332,38 @@ def test_unaligned_device_buffers(orc, m):
             assert wbuf[0].item() == 0
 
 
+@pytest.mark.parametrize("n", [8, 2000])  # 2000: tables past the shared-memory budget
+def test_outputs_have_no_stray_writes(n):
+    """Canary words / bytes before and after every output region stay
+    untouched for ragged sizes, both dtypes, all engines (no sanitizer on this
+    pool: the kernels' bounds are checked by their side effects instead)."""
+    vx, vy = vp.regular_polygon(n, 1.0)
+    rng = np.random.default_rng(n)
+    pad = 64
+    with vp.PreparedPolygon.prepare(vx, vy, vp.KIND_ALL) as p:
+        for m in (1, 31, 33, 4099, 70001):
+            for dt in (torch.float32, torch.float64):
+                xs = torch.as_tensor(rng.uniform(-1.5, 1.5, m), dtype=dt, device=DEV)
+                ys = torch.as_tensor(rng.uniform(-1.5, 1.5, m), dtype=dt, device=DEV)
+                nw = (m + 31) // 32
+                for e in range(3):
+                    wbuf = torch.full((nw + 2 * pad,), -0x5a5a5a5b, dtype=torch.int32, device=DEV)
+                    bbuf = torch.full((m + 2 * pad,), 0xA5, dtype=torch.uint8, device=DEV)
+                    cbuf = torch.zeros(3, dtype=torch.int64, device=DEV)
+                    p.test(e, xs, ys, words=wbuf[pad:pad + nw], bytes_=bbuf[pad:pad + m],
+                           count=cbuf[1:2])
+                    torch.cuda.synchronize()
+                    w, b = wbuf.cpu().numpy(), bbuf.cpu().numpy()
+                    assert (w[:pad] == -0x5a5a5a5b).all() and (w[pad + nw:] == -0x5a5a5a5b).all()
+                    assert (b[:pad] == 0xA5).all() and (b[pad + m:] == 0xA5).all()
+                    assert cbuf[0].item() == 0 and cbuf[2].item() == 0
+                    got = b[pad:pad + m]
+                    assert set(np.unique(got)) <= {0, 1}
+                    bits = np.unpackbits(w[pad:pad + nw].view(np.uint8), bitorder="little")
+                    assert np.array_equal(bits[:m], got) and not bits[m:].any()
+                    assert cbuf[1].item() == int(got.sum())
+
+
 def test_concurrent_streams_share_one_handle(orc):
     # test_engines.cpp:243-257: one generator set serves concurrent callers
     vx, vy = W.c1_polygon()
