@@ -590,6 +590,8 @@ def main():
 
     if world > 1:
         dist.barrier()
+    del graph  # its NCCL node references the communicator: release it first
+    comm.close()  # every rank is past its last count all-reduce
     if rank != 0:
         dist.destroy_process_group() if world > 1 else None
         return
