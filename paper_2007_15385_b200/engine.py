@@ -34,6 +34,23 @@ def _stream_ptr(stream) -> C.c_void_p:
     return C.c_void_p(stream.cuda_stream)  # torch.cuda.Stream
 
 
+def _check_device_batch(xs, ys, dtypes, outs=(), ids=None) -> None:
+    """The C-ABI takes raw pointers; the Python mirror checks what it can see
+    (vpip::Error InvalidParameter, code 6, on a mismatch)."""
+    m = xs.numel()
+    ok = (xs.is_cuda and ys.is_cuda and xs.dtype in dtypes and ys.dtype == xs.dtype
+          and ys.numel() == m and xs.is_contiguous() and ys.is_contiguous())
+    if ids is not None:
+        ok = ok and ids.is_cuda and ids.numel() == m and ids.is_contiguous() and \
+            ids.element_size() == 4
+    for t, need in outs:
+        if t is not None:
+            ok = ok and t.is_cuda and t.is_contiguous() and t.numel() >= need
+    if not ok:
+        raise VpipError(6, "device batch: 1-D contiguous CUDA tensors of matching length "
+                           "and dtype (and large enough outputs) are required")
+
+
 def _engine_id(engine) -> int:
     return ENGINES[engine] if isinstance(engine, str) else int(engine)
 
@@ -112,8 +129,10 @@ class PreparedPolygon:
         uint8 tensor of m; count: int64 tensor of 1 (accumulated).
         """
         import torch
-        dtype = F32 if xs.dtype == torch.float32 else F64
         m = xs.numel()
+        _check_device_batch(xs, ys, (torch.float32, torch.float64),
+                            ((words, (m + 31) // 32), (bytes_, m), (count, 1)))
+        dtype = F32 if xs.dtype == torch.float32 else F64
         ptr = lambda t: C.c_void_p(t.data_ptr()) if t is not None else C.c_void_p(None)
         check(load().vpipg_test(self._h, _engine_id(engine), dtype, ptr(xs), ptr(ys), m,
                                 ptr(words), ptr(bytes_), ptr(count), _stream_ptr(stream)),
@@ -226,6 +245,10 @@ class PolygonDB:
 
     def test(self, engine, xs, ys, ids, words=None, bytes_=None, count=None, stream=None) -> None:
         """Gathered test on device tensors (vpipg_test_gather); float32 points, int32 ids."""
+        import torch
+        m = xs.numel()
+        _check_device_batch(xs, ys, (torch.float32,),
+                            ((words, (m + 31) // 32), (bytes_, m), (count, 1)), ids=ids)
         ptr = lambda t: C.c_void_p(t.data_ptr()) if t is not None else C.c_void_p(None)
         check(load().vpipg_test_gather(self._h, _engine_id(engine), ptr(xs), ptr(ys), ptr(ids),
                                        xs.numel(), ptr(words), ptr(bytes_), ptr(count),

@@ -122,3 +122,20 @@ def test_nccl_loads_at_run_time_without_a_gpu():
     assert lib.vpipg_allreduce_counts(None, None, 3, None) == 6
     assert lib.vpipg_comm_destroy(None) == 0
     assert b"nccl" in lib.vpipg_strerror(101).lower()
+
+
+def test_python_mirror_rejects_bad_device_batches():
+    """The ctypes mirror checks what the raw-pointer ABI cannot: CPU tensors,
+    mismatched lengths / dtypes, short outputs -> InvalidParameter (code 6)."""
+    import torch
+    p = object.__new__(vp.PreparedPolygon)
+    p._h = None
+    x = torch.zeros(64, dtype=torch.float32)
+    with pytest.raises(vp.VpipError) as e:
+        p.test(0, x, x)  # CPU tensors
+    assert e.value.code == 6
+    db = object.__new__(vp.PolygonDB)
+    db._h = None
+    with pytest.raises(vp.VpipError) as e:
+        db.test(0, x, x, torch.zeros(63, dtype=torch.int32))
+    assert e.value.code == 6
