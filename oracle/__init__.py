@@ -23,6 +23,8 @@ HERE = Path(__file__).resolve().parent
 ORACLE_SO = HERE / "liboracle.so"
 REF_SO = HERE / "_ref" / "libvpip_ref.so"
 REF_ACCEPTANCE = HERE / "_ref" / "vpip_acceptance"
+# the reference's acceptance suite linked against libvpipg (the drop-in check)
+REF_ACCEPTANCE_B200 = HERE / "_ref" / "vpip_acceptance_b200"
 REFERENCE_SRC = Path("/root/reference/proj")
 
 _D = C.POINTER(C.c_double)

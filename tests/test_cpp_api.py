@@ -55,3 +55,24 @@ def test_gpu_bench_records_in_reference_csv_schema():
     # voronoi within 4x of sign-of-offset at every n
     assert (np.maximum(med[0] / med[1], med[1] / med[0]) <= 4.0).all()
     assert med[0, 12] / med[0, 0] <= 6.0
+
+
+@pytest.mark.gpu
+def test_reference_acceptance_suite_on_the_b200_dropin():
+    """The reference's OWN acceptance suite (tests/acceptance.cpp + src/bench.cpp,
+    unmodified, built by oracle/Makefile against include/vpip and libvpipg.so):
+    all 8 criteria with every batch call on the B200. Criterion 6 is a
+    wall-clock shape check of run_benchmark, so it gets three tries."""
+    import subprocess
+    import oracle
+    if not oracle.REF_ACCEPTANCE_B200.exists():
+        pytest.skip("oracle/_ref not built (needs /root/reference)")
+    for attempt in range(3):
+        r = subprocess.run([str(oracle.REF_ACCEPTANCE_B200)], capture_output=True, text=True,
+                           timeout=600)
+        failed = [ln for ln in r.stdout.splitlines() if ln.startswith("[FAIL]")]
+        assert all(ln.startswith("[FAIL] 6.") for ln in failed), r.stdout + r.stderr
+        if r.returncode == 0:
+            break
+    print(r.stdout)
+    assert r.returncode == 0 and "all 8 criteria passed" in r.stdout, r.stdout
