@@ -25,6 +25,9 @@ REF_SO = HERE / "_ref" / "libvpip_ref.so"
 REF_ACCEPTANCE = HERE / "_ref" / "vpip_acceptance"
 # the reference's acceptance suite linked against libvpipg (the drop-in check)
 REF_ACCEPTANCE_B200 = HERE / "_ref" / "vpip_acceptance_b200"
+# the reference's unit suites (on oracle/mini_doctest) against the reference / the drop-in
+REF_UNIT = HERE / "_ref" / "vpip_unit_ref"
+REF_UNIT_B200 = HERE / "_ref" / "vpip_unit_b200"
 REFERENCE_SRC = Path("/root/reference/proj")
 
 _D = C.POINTER(C.c_double)

@@ -76,3 +76,17 @@ def test_reference_acceptance_suite_on_the_b200_dropin():
             break
     print(r.stdout)
     assert r.returncode == 0 and "all 8 criteria passed" in r.stdout, r.stdout
+
+
+@pytest.mark.gpu
+def test_reference_unit_suites_on_the_b200_dropin():
+    """The reference's own unit suites (unmodified test_engines / geometry /
+    voronoi / sampling / bench .cpp, 63 test cases) compiled against
+    include/vpip and libvpipg.so: every batch call runs on the B200."""
+    import subprocess
+    import oracle
+    if not oracle.REF_UNIT_B200.exists():
+        pytest.skip("oracle/_ref not built (needs /root/reference)")
+    r = subprocess.run([str(oracle.REF_UNIT_B200)], capture_output=True, text=True, timeout=900)
+    print(r.stdout[-2000:])
+    assert r.returncode == 0 and "| 0 failed" in r.stdout, r.stdout[-4000:]

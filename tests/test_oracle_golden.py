@@ -173,6 +173,19 @@ def test_reference_acceptance_suite_if_present():
     assert "all 8 criteria passed" in r.stdout
 
 
+def test_reference_unit_suites_on_the_reference():
+    """The reference's own unit suites (unmodified test_engines / geometry /
+    voronoi / sampling / bench .cpp) on oracle/mini_doctest against the
+    reference library: all pass, so the harness is faithful."""
+    import subprocess
+    import oracle
+    if not oracle.REF_UNIT.exists():
+        pytest.skip("oracle/_ref not built (needs /root/reference)")
+    r = subprocess.run([str(oracle.REF_UNIT)], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout
+    assert "| 0 failed" in r.stdout
+
+
 def test_join_oracle_matches_reference_batches(orc):
     """vo_join_masks (per-pair restatement) == the reference's per-polygon batch
     calls over id-grouped pairs (the C4 CPU baseline), bit for bit."""
