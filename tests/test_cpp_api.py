@@ -81,7 +81,7 @@ def test_reference_acceptance_suite_on_the_b200_dropin():
 @pytest.mark.gpu
 def test_reference_unit_suites_on_the_b200_dropin():
     """The reference's own unit suites (unmodified test_engines / geometry /
-    voronoi / sampling / bench .cpp, 63 test cases) compiled against
+    voronoi / sampling / bench / io .cpp, 76 test cases) compiled against
     include/vpip and libvpipg.so: every batch call runs on the B200."""
     import subprocess
     import oracle
