@@ -28,6 +28,9 @@ REF_ACCEPTANCE_B200 = HERE / "_ref" / "vpip_acceptance_b200"
 # the reference's unit suites (on oracle/mini_doctest) against the reference / the drop-in
 REF_UNIT = HERE / "_ref" / "vpip_unit_ref"
 REF_UNIT_B200 = HERE / "_ref" / "vpip_unit_b200"
+# the reference CLI (on oracle/mini_cli11) against the reference / the drop-in
+REF_CLI = HERE / "_ref" / "vpip_cli_ref"
+REF_CLI_B200 = HERE / "_ref" / "vpip_cli_b200"
 REFERENCE_SRC = Path("/root/reference/proj")
 
 _D = C.POINTER(C.c_double)

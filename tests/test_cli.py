@@ -106,3 +106,62 @@ def test_cli_bench_csv_schema(files, orc):
     if oracle.REF_SO.exists():  # the reference's own parser accepts it
         n, _ = oracle.Reference().read_bench_csv((files / "b.csv").read_text())
         assert n == len(rows)
+
+
+def _reference_cli_sequence(binary, tmp):
+    """The checks of the reference's tests/cli_smoke.sh, re-expressed: convert,
+    test (all engines, CSV and PIPM), the concave notch under crossing, offset
+    rejecting a concave polygon (exit 2), validate PASS, bench CSV."""
+    (tmp / "square.json").write_text('{"vertices": [[0,0],[1,0],[1,1],[0,1]]}\n')
+    (tmp / "square.csv").write_text("0,0\n1,0\n1,1\n0,1\n")
+    (tmp / "pts.csv").write_text("0.5,0.5\n2,2\n1,0.5\n")
+    (tmp / "arrow.csv").write_text("0,0\n4,0\n4,4\n2,1\n0,4\n")
+    (tmp / "notch.csv").write_text("2,2\n")
+    go = lambda *a: subprocess.run([str(binary), *map(str, a)], cwd=tmp, capture_output=True)
+    assert go("convert", "--polygon", "square.json", "--out", "gens.json").returncode == 0
+    g = (tmp / "gens.json").read_text()
+    assert '"inner"' in g and '"outer"' in g
+    assert go("test", "--polygon", "square.json", "--points", "pts.csv", "--engine", "voronoi",
+              "--out", "mask_v.csv").returncode == 0
+    assert (tmp / "mask_v.csv").read_text() == "1\n0\n1\n"
+    for e in ("offset", "crossing"):
+        assert go("test", "--polygon", "square.csv", "--points", "pts.csv", "--engine", e,
+                  "--out", f"mask_{e}.csv").returncode == 0
+        assert (tmp / f"mask_{e}.csv").read_text() == "1\n0\n1\n"
+    assert go("test", "--polygon", "square.csv", "--points", "pts.csv", "--engine", "voronoi",
+              "--format", "binary", "--out", "mask.bin").returncode == 0
+    assert (tmp / "mask.bin").stat().st_size == 17
+    assert go("test", "--polygon", "arrow.csv", "--points", "notch.csv", "--engine", "crossing",
+              "--out", "mask_n.csv").returncode == 0
+    assert (tmp / "mask_n.csv").read_text() == "0\n"
+    assert go("test", "--polygon", "arrow.csv", "--points", "notch.csv", "--engine",
+              "offset").returncode == 2
+    r = go("validate", "--polygon", "square.json", "--count", "20000", "--seed", "7")
+    assert r.returncode == 0 and b"PASS" in r.stdout
+    assert go("bench", "--edges", "3..4", "--batch", "2000", "--reps", "2", "--out",
+              "bench.csv").returncode == 0
+    assert (tmp / "bench.csv").read_text().startswith("engine,n_edges,batch_size,repetition,")
+
+
+def test_reference_cli_on_the_reference(tmp_path):
+    """The reference's UNMODIFIED CLI (tools/vpip.cpp, on oracle/mini_cli11)
+    linked with the reference library passes the reference's own cli_smoke.sh
+    (and the re-expressed sequence): the harness is faithful."""
+    import oracle
+    if not oracle.REF_CLI.exists():
+        pytest.skip("oracle/_ref not built (needs /root/reference)")
+    smoke = Path("/root/reference/proj/tests/cli_smoke.sh")
+    if smoke.exists():
+        r = subprocess.run(["bash", str(smoke), str(oracle.REF_CLI)], capture_output=True)
+        assert r.returncode == 0 and b"cli smoke ok" in r.stdout, r.stdout + r.stderr
+    _reference_cli_sequence(oracle.REF_CLI, tmp_path)
+
+
+@pytest.mark.gpu
+def test_reference_cli_on_the_b200_dropin(tmp_path):
+    """The reference's unmodified CLI built against include/vpip and libvpipg.so:
+    its smoke sequence passes with every batch call on the B200."""
+    import oracle
+    if not oracle.REF_CLI_B200.exists():
+        pytest.skip("oracle/_ref not built (needs /root/reference)")
+    _reference_cli_sequence(oracle.REF_CLI_B200, tmp_path)
