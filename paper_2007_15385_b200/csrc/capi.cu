@@ -15,12 +15,14 @@
 #include <cstdint>
 #include <cstring>
 #include <functional>
+#include <map>
 #include <memory>
 #include <mutex>
 #include <new>
 #include <numbers>
 #include <random>
 #include <thread>
+#include <tuple>
 #include <vector>
 
 #include "vpipg.h"
@@ -1069,3 +1071,48 @@ int vpipg_fill_uniform_points(uint64_t seed, uint64_t first, uint64_t m, double 
 }
 
 }  // extern "C"
+
+namespace vpipg {
+
+cudaError_t launch_config(const void* kernel, int threads, size_t smem, int* sms, int* per_sm) {
+  struct Key {
+    int dev;
+    const void* k;
+    int threads;
+    size_t smem;
+    bool operator<(const Key& o) const {
+      return std::tie(dev, k, threads, smem) < std::tie(o.dev, o.k, o.threads, o.smem);
+    }
+  };
+  static std::mutex mu;
+  static std::map<Key, std::pair<int, int>> cache;              // -> (sms, blocks per SM)
+  static std::map<std::pair<int, const void*>, size_t> smem_set;  // largest limit set so far
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lock(mu);
+  const Key key{dev, kernel, threads, smem};
+  const auto hit = cache.find(key);
+  if (hit != cache.end()) {
+    *sms = hit->second.first;
+    *per_sm = hit->second.second;
+    return cudaSuccess;
+  }
+  size_t& lim = smem_set[{dev, kernel}];
+  if (smem > 48 * 1024 && smem > lim) {
+    e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    lim = smem;
+  }
+  int n = 0, b = 0;
+  if ((e = cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess) return e;
+  if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kernel, threads, smem)) != cudaSuccess)
+    return e;
+  b = b < 1 ? 1 : b;
+  cache[key] = {n, b};
+  *sms = n;
+  *per_sm = b;
+  return cudaSuccess;
+}
+
+}  // namespace vpipg

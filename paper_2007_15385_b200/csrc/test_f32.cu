@@ -490,15 +490,6 @@ __global__ void __launch_bounds__(kThreads) generic_kernel(const typename Eng::P
   flush_count(count, a);
 }
 
-int sm_count() {
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  }
-  return sms;
-}
 
 constexpr size_t kSmemTableMax = 96 * 1024;
 
@@ -511,13 +502,12 @@ cudaError_t launch(const typename Eng::Params& prm, const TestArgs& a, cudaStrea
   const uint64_t full_slices = aligned ? a.m / kWarpPts : 0;
   if (full_slices < kWarps) {
     auto k = staged ? generic_kernel<Eng, true> : generic_kernel<Eng, false>;
-    if (tab > 48 * 1024) {
-      cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tab);
-      if (e != cudaSuccess) return e;
-    }
+    int sms = 0, per_sm = 0;
+    cudaError_t e = launch_config(reinterpret_cast<const void*>(k), kThreads, tab, &sms, &per_sm);
+    if (e != cudaSuccess) return e;
     const uint64_t warps = (a.m + kWarpPts - 1) / kWarpPts;
     const uint64_t blocks = (warps + kThreads / 32 - 1) / (kThreads / 32);
-    const uint64_t cap = (uint64_t)sm_count() * 4;
+    const uint64_t cap = (uint64_t)sms * 4;
     k<<<(int)(blocks < cap ? blocks : cap), kThreads, tab, stream>>>(prm, a);
     return cudaGetLastError();
   }
@@ -532,13 +522,10 @@ cudaError_t launch(const typename Eng::Params& prm, const TestArgs& a, cudaStrea
     smem = (size_t)kWarps * kStages * 2 * kWarpPts * sizeof(float) +
            (size_t)kWarps * 2 * kStages * sizeof(uint64_t) + tab;
   }
-  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  int sms = 0, per_sm = 0;
+  cudaError_t e = launch_config(reinterpret_cast<const void*>(k), kThreads, smem, &sms, &per_sm);
   if (e != cudaSuccess) return e;
-  int per_sm = 0;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kThreads, smem);
-  if (e != cudaSuccess) return e;
-  if (per_sm < 1) per_sm = 1;
-  const uint64_t cap = (uint64_t)sm_count() * per_sm;
+  const uint64_t cap = (uint64_t)sms * per_sm;
   const uint64_t want = (full_slices + kWarps - 1) / kWarps;
   const int grid = (int)(want < cap ? want : cap);
   k<<<grid, kThreads, smem, stream>>>(prm, a, full_slices);

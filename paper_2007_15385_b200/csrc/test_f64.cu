@@ -163,15 +163,9 @@ cudaError_t launch_one(const DevTables& t, const TestArgs& a, size_t rec_bytes,
   const bool staged = (size_t)t.n * rec_bytes <= 96 * 1024;
   auto k = staged ? exact_kernel<kEngine, P, true> : exact_kernel<kEngine, P, false>;
   const size_t smem = staged ? (size_t)t.n * rec_bytes : 0;
-  if (smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-  }
-  int dev = 0, sms = 0, per_sm = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kThreads, smem);
-  if (per_sm < 1) per_sm = 1;
+  int sms = 0, per_sm = 0;
+  cudaError_t e = launch_config(reinterpret_cast<const void*>(k), kThreads, smem, &sms, &per_sm);
+  if (e != cudaSuccess) return e;
   const uint64_t need = (a.m + kThreads * P - 1) / (kThreads * P);
   const uint64_t cap = (uint64_t)sms * per_sm;
   const int grid = static_cast<int>(need < cap ? (need ? need : 1) : cap);

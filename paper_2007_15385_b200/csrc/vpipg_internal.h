@@ -123,6 +123,12 @@ cudaError_t launch_fill_uniform(uint64_t seed, uint64_t first, uint64_t m, doubl
                                 double min_y, double max_x, double max_y, int dtype, void* xs,
                                 void* ys, cudaStream_t stream);
 
+// Launch configuration cache (capi.cu): for `kernel` on the current device,
+// raises its dynamic shared-memory limit to `smem` if no earlier launch did,
+// and returns the SM count and resident blocks per SM for (threads, smem) --
+// the driver queries run once per (device, kernel, threads, smem).
+cudaError_t launch_config(const void* kernel, int threads, size_t smem, int* sms, int* per_sm);
+
 }  // namespace vpipg
 
 // comm.cpp: text for a VPIPG_ERR_NCCL + ncclResult_t code
