@@ -291,8 +291,8 @@ class PolygonJob:
 
     issue_cycles = ISSUE_CYCLES_PER_PE
     bytes_per_unit = 8  # f32 x + y per test
-    e2e_path = ("vpipg_test_host_multi (C-ABI, pinned host buffers, 16 Mi-point chunks on 3 "
-                "streams; one H2D per chunk feeds all 3 engines)")
+    e2e_path = ("vpipg_test_host_multi (C-ABI, pinned host buffers, chunks of m/8 (1-16 Mi "
+                "points) on 3 streams; one H2D per chunk feeds all 3 engines)")
 
     def __init__(self, workload, lo, hi, device, torch, vp, stream):
         self.torch = torch
@@ -328,8 +328,8 @@ class JoinJob:
     # affine gather: 2 FFMA + LOP3/2 per point-edge; crossing as in the stream kernel
     issue_cycles = {"voronoi": 3.0, "sign_of_offset": 3.0, "ray_crossing": 6.0}
     bytes_per_unit = 12  # f32 x + y + u32 id per test
-    e2e_path = ("pinned host pairs -> H2D in 16 Mi-pair chunks over 2 streams -> "
-                "vpipg_test_gather x 3 engines -> D2H mask words")
+    e2e_path = ("vpipg_test_gather_host (C-ABI, pinned host pairs, chunks of m/8 on 3 streams; "
+                "one H2D per chunk feeds all 3 engines)")
 
     def __init__(self, workload, lo, hi, device, torch, vp, stream):
         self.torch = torch
@@ -355,35 +355,10 @@ class JoinJob:
         self.h = [t.empty(a.numel(), dtype=a.dtype, pin_memory=True) for a in (self.xs, self.ys, self.ids)]
         for hbuf, d in zip(self.h, (self.xs, self.ys, self.ids)):
             hbuf.copy_(d)
-        self.d = [t.empty_like(a) for a in (self.xs, self.ys, self.ids)]
-        self.dw = [t.empty((self.xs.numel() + 31) // 32, dtype=t.int32, device=self.xs.device)
-                   for _ in range(3)]
-        self.dc = t.zeros(3, dtype=t.int64, device=self.xs.device)
 
     def run_host(self, hw, stream):
-        """Chunked pipeline over two streams: H2D of chunk k+1 overlaps the
-        gathers of chunk k (the join has no host-buffer C-ABI entry of its own)."""
-        t = self.torch
-        m = self.xs.numel()
-        chunk = 1 << 24
-        if not hasattr(self, "streams"):
-            self.streams = [t.cuda.Stream(), t.cuda.Stream()]
-        self.dc.zero_()
-        t.cuda.synchronize()
-        for c, lo in enumerate(range(0, m, chunk)):
-            hi = min(m, lo + chunk)
-            s = self.streams[c % 2]
-            with t.cuda.stream(s):
-                d = [dbuf[lo:hi] for dbuf in self.d]
-                for dst, hbuf in zip(d, self.h):
-                    dst.copy_(hbuf[lo:hi], non_blocking=True)
-                for e in range(3):
-                    w = self.dw[e][lo // 32:(hi + 31) // 32]
-                    self.db.test(e, *d, words=w, count=self.dc[e:e + 1], stream=s)
-                    hw[e][lo // 32:(hi + 31) // 32].copy_(w, non_blocking=True)
-        for s in self.streams:
-            s.synchronize()
-        return self.dc.tolist()
+        _, cnt = self.db.test_host(*self.h, (0, 1, 2), words=hw)
+        return cnt
 
 
 # ----------------------------------------------------------------- GPU arm

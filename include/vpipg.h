@@ -197,6 +197,14 @@ int vpipg_test_gather(const vpipg_db* db, int engine, const float* xs, const flo
                       const uint32_t* ids, uint64_t m, uint32_t* mask_words, uint8_t* mask_bytes,
                       unsigned long long* d_inside, void* stream);
 
+/* The join over HOST buffers (pageable or pinned): every engine in the bit set
+ * `engines` over one copy of the pairs, chunked and pipelined like
+ * vpipg_test_host_multi (mask_words / mask_bytes / inside indexed by engine,
+ * arrays of 3, entries may be NULL). Synchronous. */
+int vpipg_test_gather_host(const vpipg_db* db, uint32_t engines, const float* xs, const float* ys,
+                           const uint32_t* ids, uint64_t m, uint32_t* const* mask_words,
+                           uint8_t* const* mask_bytes, uint64_t* inside);
+
 /* Join-pair workload generator (input generation, not timed): pair j gets
  * id = floor(U(seed, 3j) * npoly) and point = centre[id] + (2U - 1) * radius[id]
  * per axis (U from mix_seed(seed, 3j+1 / 3j+2)), rounded to f32. centre_x,

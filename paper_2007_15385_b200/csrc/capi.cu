@@ -626,23 +626,72 @@ uint64_t host_chunk(uint64_t m) {
   return std::min<uint64_t>(std::max<uint64_t>(c, uint64_t(1) << 16), uint64_t(1) << 21);
 }
 
-// The host-buffer path for pageable memory (a std::vector behind the vpip::
-// shim, a numpy array): the pool copies each chunk's points into a pinned
+// Device slot of the generic host pipeline: up to 3 input arrays, the mask
+// words of the 3 engines and the 3 counters.
+struct PipeSlot {
+  void* in[3];
+  uint32_t* w[3];
+  unsigned long long* c;
+};
+
+size_t pipe_slot_bytes(uint64_t chunk, const size_t* elt, int nin) {
+  size_t b = 3 * align256((chunk + 31) / 32 * 4) + 256;
+  for (int k = 0; k < nin; ++k) b += align256(chunk * elt[k]);
+  return b;
+}
+
+PipeSlot pipe_slot_view(char* base, uint64_t chunk, const size_t* elt, int nin) {
+  PipeSlot v{};
+  size_t off = 0;
+  auto take = [&](size_t n) { char* q = base + off; off += align256(n); return q; };
+  for (int k = 0; k < nin; ++k) v.in[k] = take(chunk * elt[k]);
+  for (auto& w : v.w) w = reinterpret_cast<uint32_t*>(take((chunk + 31) / 32 * 4));
+  v.c = reinterpret_cast<unsigned long long*>(take(24));
+  return v;
+}
+
+// Launches engine e on one chunk: device inputs, length, mask words (may be
+// NULL), counter; returns a library code.
+using ChunkLaunch = std::function<int(int e, void* const* din, uint64_t len, uint32_t* dw,
+                                      unsigned long long* dc, cudaStream_t s)>;
+
+// The host-buffer pipeline for pageable memory (a std::vector behind the vpip::
+// shim, a numpy array): the pool copies each chunk's inputs into a pinned
 // bounce slot while the GPU works on the previous chunks, the copy engine
 // moves it at link rate, the engines write mask WORDS (1/8 of the byte mask
 // on the link), and the pool copies / expands them into the caller's words or
 // bytes once that slot's event fires. Pinned inputs skip the bounce copy.
-int host_staged(const vpipg_poly* p, const int* eng, int ne, int dtype, const void* xs,
-                const void* ys, uint64_t m, uint32_t* const* mask_words,
-                uint8_t* const* mask_bytes, uint64_t* inside, Staging& st) {
-  const size_t elt = dtype == VPIPG_F64 ? sizeof(double) : sizeof(float);
-  const uint64_t chunk = std::min<uint64_t>(m, host_chunk(m));
+// Caller holds st.mu and the device guard.
+int host_pipeline(Staging& st, const void* const* hin, const size_t* elt, int nin, uint64_t m,
+                  const int* eng, int ne, uint32_t* const* mask_words, uint8_t* const* mask_bytes,
+                  uint64_t* inside, const ChunkLaunch& launch) {
+  bool in_pinned = true;
+  for (int k = 0; k < nin; ++k) in_pinned = in_pinned && host_pinned(hin[k]);
+  // pinned word outputs and no byte outputs: the D2H lands in the caller's
+  // words directly and, with pinned inputs too, nothing waits until the end
+  bool direct_out = true;
+  for (int k = 0; k < ne; ++k) {
+    const int e = eng[k];
+    if (mask_bytes && mask_bytes[e]) direct_out = false;
+    if (mask_words && mask_words[e] && !host_pinned(mask_words[e])) direct_out = false;
+  }
+  const bool waits = !(in_pinned && direct_out);
+  // nothing to wait for: larger chunks (m/8, 1-16 Mi) straight to the copy
+  // engine; otherwise m/8 in 64 Ki-2 Mi so copy-in / copy-out overlap finely
+  const uint64_t want_chunk =
+      waits ? host_chunk(m)
+            : std::min<uint64_t>(kChunk, std::max<uint64_t>(uint64_t(1) << 20,
+                                                            (m / 8 + 31) & ~uint64_t(31)));
+  const uint64_t chunk = std::min<uint64_t>(m, want_chunk);
   const size_t wbytes = align256((chunk + 31) / 32 * 4);
-  int rc = staging_reserve(st, slot_bytes(chunk, elt, false));
-  if (!rc) rc = host_reserve(st, 2 * align256(chunk * elt), 3 * wbytes);
+  size_t in_bytes = 0;
+  if (!in_pinned)
+    for (int k = 0; k < nin; ++k) in_bytes += align256(chunk * elt[k]);
+  int rc = staging_reserve(st, pipe_slot_bytes(chunk, elt, nin));
+  if (!rc) rc = host_reserve(st, in_bytes, 3 * wbytes);
   if (rc) return rc;
-  SlotView slot[kSlots];
-  for (int i = 0; i < kSlots; ++i) slot[i] = slot_view(st.buf[i], chunk, elt, false);
+  PipeSlot slot[kSlots];
+  for (int i = 0; i < kSlots; ++i) slot[i] = pipe_slot_view(st.buf[i], chunk, elt, nin);
   auto fail = [&](cudaError_t e) {
     if (e != cudaSuccess && rc == kOk) rc = cuda_code(e);
     return rc != kOk;
@@ -651,11 +700,12 @@ int host_staged(const vpipg_poly* p, const int* eng, int ne, int dtype, const vo
     return (mask_words && mask_words[e]) || (mask_bytes && mask_bytes[e]);
   };
   for (int i = 0; i < kSlots && rc == kOk; ++i) fail(cudaMemsetAsync(slot[i].c, 0, 24, st.st[i]));
-  const bool in_pinned = host_pinned(xs) && host_pinned(ys);
-  const char* hx = static_cast<const char*>(xs);
-  const char* hy = static_cast<const char*>(ys);
   const uint64_t nchunks = (m + chunk - 1) / chunk;
   auto finish = [&](uint64_t c) {  // chunk c's masks: pinned slot -> caller
+    if (direct_out) {  // already in place; only the bounce slot's reuse waits
+      if (!in_pinned) fail(cudaEventSynchronize(st.ev[c % kSlots]));
+      return;
+    }
     const int i = static_cast<int>(c % kSlots);
     if (fail(cudaEventSynchronize(st.ev[i]))) return;
     const uint64_t base = c * chunk, len = std::min<uint64_t>(chunk, m - base);
@@ -669,33 +719,33 @@ int host_staged(const vpipg_poly* p, const int* eng, int ne, int dtype, const vo
   uint64_t c = 0;
   for (; c < nchunks && rc == kOk; ++c) {
     const int i = static_cast<int>(c % kSlots);
-    if (c >= kSlots) finish(c - kSlots);
+    if (c >= kSlots && waits) finish(c - kSlots);
     if (rc) break;
     cudaStream_t s = st.st[i];
     const uint64_t base = c * chunk, len = std::min<uint64_t>(chunk, m - base);
-    const void* sx = hx + base * elt;
-    const void* sy = hy + base * elt;
-    if (!in_pinned) {
-      char* bx = st.hin[i];
-      char* by = st.hin[i] + align256(chunk * elt);
-      pool_memcpy(bx, sx, len * elt);
-      pool_memcpy(by, sy, len * elt);
-      sx = bx;
-      sy = by;
+    char* bounce = st.hin[i];
+    for (int k = 0; k < nin && rc == kOk; ++k) {
+      const void* src = static_cast<const char*>(hin[k]) + base * elt[k];
+      if (!in_pinned) {
+        pool_memcpy(bounce, src, len * elt[k]);
+        src = bounce;
+        bounce += align256(chunk * elt[k]);
+      }
+      fail(cudaMemcpyAsync(slot[i].in[k], src, len * elt[k], cudaMemcpyHostToDevice, s));
     }
-    if (fail(cudaMemcpyAsync(slot[i].x, sx, len * elt, cudaMemcpyHostToDevice, s))) break;
-    if (fail(cudaMemcpyAsync(slot[i].y, sy, len * elt, cudaMemcpyHostToDevice, s))) break;
     for (int k = 0; k < ne && rc == kOk; ++k) {
       const int e = eng[k];
       uint32_t* dw = want(e) ? slot[i].w[e] : nullptr;
-      TestArgs a{slot[i].x, slot[i].y, len, dw, nullptr, slot[i].c + e};
-      rc = dispatch(p, e, dtype, a, s);
+      rc = launch(e, slot[i].in, len, dw, slot[i].c + e, s);
       if (!rc && dw)
-        fail(cudaMemcpyAsync(st.hout[i] + e * wbytes, dw, (len + 31) / 32 * 4, cudaMemcpyDeviceToHost, s));
+        fail(cudaMemcpyAsync(direct_out ? static_cast<void*>(mask_words[e] + base / 32)
+                                        : static_cast<void*>(st.hout[i] + e * wbytes),
+                             dw, (len + 31) / 32 * 4, cudaMemcpyDeviceToHost, s));
     }
     if (rc == kOk) fail(cudaEventRecord(st.ev[i], s));
   }
-  for (uint64_t f = c > kSlots ? c - kSlots : 0; rc == kOk && f < c; ++f) finish(f);
+  if (waits)
+    for (uint64_t f = c > kSlots ? c - kSlots : 0; rc == kOk && f < c; ++f) finish(f);
   unsigned long long cnt[kSlots][3] = {};
   for (int i = 0; i < kSlots; ++i)
     if (rc == kOk) fail(cudaMemcpyAsync(cnt[i], slot[i].c, 24, cudaMemcpyDeviceToHost, st.st[i]));
@@ -762,7 +812,14 @@ int vpipg_test_host_multi(const vpipg_poly* p, uint32_t engines, int dtype, cons
   if (!pinned) {
     Staging& st = staging(p->device);
     std::lock_guard<std::mutex> lock(st.mu);
-    return host_staged(p, eng, ne, dtype, xs, ys, m, mask_words, mask_bytes, inside, st);
+    const void* hin[2] = {xs, ys};
+    const size_t el[2] = {elt, elt};
+    return host_pipeline(st, hin, el, 2, m, eng, ne, mask_words, mask_bytes, inside,
+                         [&](int e, void* const* din, uint64_t len, uint32_t* dw,
+                             unsigned long long* dc, cudaStream_t s) {
+                           TestArgs a{din[0], din[1], len, dw, nullptr, dc};
+                           return dispatch(p, e, dtype, a, s);
+                         });
   }
   // all-pinned buffers: DMA straight from / to the caller's memory in chunks,
   // kSlots in flight on their own streams: the points
@@ -947,6 +1004,35 @@ int vpipg_test_gather(const vpipg_db* db, int engine, const float* xs, const flo
   DeviceGuard g(db->device);
   GatherArgs a{xs, ys, ids, m, mask_words, mask_bytes, d_inside};
   return cuda_code(launch_gather(db->t, engine, a, static_cast<cudaStream_t>(stream)));
+}
+
+int vpipg_test_gather_host(const vpipg_db* db, uint32_t engines, const float* xs, const float* ys,
+                           const uint32_t* ids, uint64_t m, uint32_t* const* mask_words,
+                           uint8_t* const* mask_bytes, uint64_t* inside) {
+  if (!db || engines == 0 || (engines & ~7u)) return kInvalid;
+  int eng[3], ne = 0;
+  for (int e = 0; e < 3; ++e) {
+    if (!(engines & (1u << e))) continue;
+    const uint32_t need = e == 0 ? kKindVoronoi : e == 1 ? kKindOffset : kKindCrossing;
+    if (!(db->kinds & need)) return kInvalid;
+    if (inside) inside[e] = 0;
+    eng[ne++] = e;
+  }
+  if (m == 0) return kOk;
+  if (!xs || !ys || !ids) return kInvalid;
+  DeviceGuard g(db->device);
+  Staging& st = staging(db->device);
+  std::lock_guard<std::mutex> lock(st.mu);
+  const void* hin[3] = {xs, ys, ids};
+  const size_t el[3] = {sizeof(float), sizeof(float), sizeof(uint32_t)};
+  return host_pipeline(st, hin, el, 3, m, eng, ne, mask_words, mask_bytes, inside,
+                       [&](int e, void* const* din, uint64_t len, uint32_t* dw,
+                           unsigned long long* dc, cudaStream_t s) {
+                         GatherArgs a{static_cast<const float*>(din[0]),
+                                      static_cast<const float*>(din[1]),
+                                      static_cast<const uint32_t*>(din[2]), len, dw, nullptr, dc};
+                         return cuda_code(launch_gather(db->t, e, a, s));
+                       });
 }
 
 int vpipg_fill_join_pairs(uint64_t seed, uint64_t first, uint64_t m, uint32_t npoly,

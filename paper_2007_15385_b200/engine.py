@@ -254,6 +254,25 @@ class PolygonDB:
                                        xs.numel(), ptr(words), ptr(bytes_), ptr(count),
                                        _stream_ptr(stream)), "vpipg_test_gather")
 
+    def test_host(self, xs, ys, ids, engines=(0, 1, 2), words=None, counts_only: bool = False):
+        """The join over host buffers (vpipg_test_gather_host): float32 xs / ys and
+        uint32 / int32 ids, numpy arrays or (pinned) CPU tensors. Returns
+        (words list, counts list)."""
+        m = xs.size if isinstance(xs, np.ndarray) else xs.numel()
+        mask = 0
+        for e in engines:
+            mask |= 1 << _engine_id(e)
+        if words is None and not counts_only:
+            words = [np.zeros((m + 31) // 32, dtype=np.uint32) if (mask >> e) & 1 else None
+                     for e in range(3)]
+        wp = (C.c_void_p * 3)(*[C.c_void_p(_host_ptr(w) if w is not None else None)
+                                for w in (words or [None] * 3)])
+        cnt = (C.c_uint64 * 3)()
+        check(load().vpipg_test_gather_host(self._h, mask, C.c_void_p(_host_ptr(xs)),
+                                            C.c_void_p(_host_ptr(ys)), C.c_void_p(_host_ptr(ids)),
+                                            m, wp, None, cnt), "vpipg_test_gather_host")
+        return words, [cnt[i] for i in range(3)]
+
 
 def fill_join_pairs(seed: int, first: int, xs, ys, ids, cx, cy, r, stream=None) -> None:
     """Join-pair generator on the device (vpipg_fill_join_pairs); cx, cy, r: CUDA f64."""

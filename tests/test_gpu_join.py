@@ -202,3 +202,28 @@ def test_gather_outputs_have_no_stray_writes(m):
             assert (b[:pad] == 0xA5).all() and (b[pad + m:] == 0xA5).all()
             bits = np.unpackbits(w[pad:pad + nw].view(np.uint8), bitorder="little")
             assert np.array_equal(bits[:m], b[pad:pad + m]) and not bits[m:].any()
+
+
+def test_gather_host_buffers_equal_device_path(orc):
+    """vpipg_test_gather_host (pageable numpy and pinned tensors, several chunks)
+    equals the device gather per engine, words and counts."""
+    off, vx, vy, cx, cy, r = _db_inputs(512)
+    m = (1 << 21) + 4321
+    dcx, dcy, dr = (torch.as_tensor(a, device=DEV) for a in (cx, cy, r))
+    xs = torch.empty(m, dtype=torch.float32, device=DEV)
+    ys = torch.empty_like(xs)
+    ids = torch.empty(m, dtype=torch.int32, device=DEV)
+    vp.fill_join_pairs(W.c4_pair_seed(), 0, xs, ys, ids, dcx, dcy, dr)
+    with vp.PolygonDB.prepare(off, vx, vy, vp.KIND_ALL) as db:
+        ref = []
+        for e in range(3):
+            w = torch.zeros((m + 31) // 32, dtype=torch.int32, device=DEV)
+            c = torch.zeros(1, dtype=torch.int64, device=DEV)
+            db.test(e, xs, ys, ids, words=w, count=c)
+            torch.cuda.synchronize()
+            ref.append((w.cpu().numpy().view(np.uint32), c.item()))
+        hx, hy, hid = xs.cpu().numpy(), ys.cpu().numpy(), ids.cpu().numpy()
+        for args in ((hx, hy, hid), tuple(torch.from_numpy(a).pin_memory() for a in (hx, hy, hid))):
+            words, cnt = db.test_host(*args, (0, 1, 2))
+            for e in range(3):
+                assert np.array_equal(words[e], ref[e][0]) and cnt[e] == ref[e][1], e
