@@ -425,8 +425,11 @@ __device__ __forceinline__ void prefetch_l2(const void* p) {
   asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(p));
 }
 
+#ifndef VPIPG_LDG_MINB
+#define VPIPG_LDG_MINB 2
+#endif
 template <class Eng, bool kSmemTab>
-__global__ void __launch_bounds__(kThreads, 2)
+__global__ void __launch_bounds__(kThreads, VPIPG_LDG_MINB)
     ldg_kernel(const typename Eng::Params prm, const TestArgs a, const uint64_t full_slices) {
   constexpr int P = Eng::kP;
   constexpr int kWarpPts = 32 * P;
