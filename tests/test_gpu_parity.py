@@ -419,3 +419,54 @@ def test_many_edge_polygons_use_global_tables(orc, n):
             band = band_mask(orc, vx, vy, xs.astype(np.float32).astype(np.float64),
                              ys.astype(np.float32).astype(np.float64))
             assert not np.any((b32 != want32) & ~band), (n, e)
+
+
+def test_concurrent_prepare_test_destroy():
+    """8 host threads each prepare their own polygons, test them on their own
+    streams (device and host-buffer paths) and destroy them, concurrently: the
+    blob pool, launch-config cache, staging and thread pool stay consistent
+    (results equal a single-threaded run)."""
+    import threading
+    rng = np.random.default_rng(3)
+    polys = [vp.random_convex_polygon(int(n), int(sd), 1.0)
+             for n, sd in zip(rng.integers(3, 40, 16), rng.integers(0, 1 << 30, 16))]
+    m = 300_001
+    xs = torch.as_tensor(rng.uniform(-1.5, 1.5, m).astype(np.float32), device=DEV)
+    ys = torch.as_tensor(rng.uniform(-1.5, 1.5, m).astype(np.float32), device=DEV)
+    hx, hy = xs.cpu().numpy(), ys.cpu().numpy()
+
+    def run(vx, vy, stream):
+        out = []
+        with vp.PreparedPolygon.prepare(vx, vy, vp.KIND_ALL) as p:
+            for e in range(3):
+                w = torch.zeros((m + 31) // 32, dtype=torch.int32, device=DEV)
+                c = torch.zeros(1, dtype=torch.int64, device=DEV)
+                p.test(e, xs, ys, words=w, count=c, stream=stream)
+                stream.synchronize()
+                out.append((w.cpu().numpy(), c.item()))
+            hw, hc = p.test_host_multi(hx, hy, (0, 1, 2))
+        return out, hw, hc
+
+    ref = [run(vx, vy, torch.cuda.current_stream()) for vx, vy in polys]
+    got, errors = {}, []
+
+    def worker(t):
+        s = torch.cuda.Stream()
+        try:
+            for k in range(t, len(polys), 8):
+                got[k] = run(*polys[k], s)
+        except Exception as ex:  # surfaced below
+            errors.append(ex)
+
+    threads = [threading.Thread(target=worker, args=(t,)) for t in range(8)]
+    for th in threads:
+        th.start()
+    for th in threads:
+        th.join()
+    assert not errors, errors
+    for k in range(len(polys)):
+        (o_ref, hw_ref, hc_ref), (o, hw, hc) = ref[k], got[k]
+        for e in range(3):
+            assert np.array_equal(o[e][0], o_ref[e][0]) and o[e][1] == o_ref[e][1]
+            assert np.array_equal(hw[e], hw_ref[e]) and hc[e] == hc_ref[e]
+            assert hc[e] == o[e][1]
