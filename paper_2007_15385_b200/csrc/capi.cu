@@ -84,7 +84,8 @@ int check_device(int device) {
 }
 
 // validate_polygon (geometry.cpp:53-98): same checks in the same order, same
-// arithmetic (this TU is compiled with -fmad=false on the host side too).
+// arithmetic (host code of this TU is compiled with -ffp-contract=off, as the
+// reference is, so no product is fused into an add).
 int validate(std::vector<double>& vx, std::vector<double>& vy, int* reversed) {
   const size_t n = vx.size();
   for (size_t i = 0; i < n; ++i)
