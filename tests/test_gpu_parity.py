@@ -182,6 +182,43 @@ def test_concave_arrow_crossing(golden):
     assert e.value.code == 2
 
 
+@pytest.mark.parametrize("shape", ["pentagram", "comb", "clockwise_notch"])
+def test_crossing_on_non_convex_polygons(orc, shape):
+    """Ray crossing takes any raw polygon (vpip.cpp:120-128): a self-intersecting
+    pentagram (even-odd rule: the centre is outside), a comb with many
+    concavities, and a clockwise notched polygon. f64 bit-exact against the
+    oracle (boundary probes included), f32 outside the band."""
+    if shape == "pentagram":
+        k = np.arange(5) * 2 % 5
+        vx, vy = np.cos(2 * np.pi * k / 5 + np.pi / 2), np.sin(2 * np.pi * k / 5 + np.pi / 2)
+    elif shape == "comb":
+        teeth = 9
+        xs_top = np.repeat(np.arange(teeth + 1, dtype=float), 2)[1:-1]
+        ys_top = np.tile([3.0, 1.0], teeth)[: xs_top.size]
+        vx = np.concatenate([[0.0, teeth], xs_top[::-1]])
+        vy = np.concatenate([[0.0, 0.0], ys_top[::-1]])
+    else:
+        vx = np.array([0, 0, 2, 2, 3, 3, 5, 5], float)[::-1]
+        vy = np.array([0, 4, 4, 1, 1, 4, 4, 0], float)[::-1]
+    rng = np.random.default_rng(11)
+    x0, x1, y0, y1 = vx.min() - 1, vx.max() + 1, vy.min() - 1, vy.max() + 1
+    xs = np.concatenate([rng.uniform(x0, x1, 20000), vx, (vx + np.roll(vx, 1)) / 2, [0.0]])
+    ys = np.concatenate([rng.uniform(y0, y1, 20000), vy, (vy + np.roll(vy, 1)) / 2, [0.0]])
+    want = orc.ray_batch(vx, vy, xs, ys)
+    with vp.PreparedPolygon.prepare(vx, vy, vp.KIND_CROSSING) as p:
+        _, b, c = run_device(p, 2, xs, ys)
+        assert np.array_equal(b, want) and c == int(want.sum())
+        x32, y32 = xs.astype(np.float32), ys.astype(np.float32)
+        want32 = orc.ray_batch(vx.astype(np.float32).astype(np.float64),
+                               vy.astype(np.float32).astype(np.float64),
+                               x32.astype(np.float64), y32.astype(np.float64))
+        _, b32, _ = run_device(p, 2, x32, y32)
+        band = band_mask(orc, vx, vy, x32.astype(np.float64), y32.astype(np.float64))
+        assert not np.any((b32 != want32) & ~band)
+    if shape == "pentagram":
+        assert want[-1] == 0  # the centre of a pentagram is outside under even-odd
+
+
 @pytest.mark.parametrize("m", [0, 1, 31, 32, 33, 255, 256, 257, 1000, 2049, 4097])
 def test_ragged_sizes(orc, m):
     vx, vy = W.c1_polygon()
