@@ -81,17 +81,18 @@ __device__ void slab_scatter(int n, int (*cls_of)(int, const void*, float2*), co
     const int k = k0 + tid;
     float2 bc = make_float2(0.f, 0.f);
     const int c = (k < n) ? cls_of(k, ctx, &bc) : kNone;
-    uint32_t rank[kGroups];
+    uint32_t rank = 0;  // this edge's rank inside its group, within the warp
+#pragma unroll
     for (int g = 0; g < kGroups; ++g) {
       const unsigned bal = __ballot_sync(0xffffffffu, c == g);
-      rank[g] = __popc(bal & ((1u << lane) - 1u));
+      if (c == g) rank = __popc(bal & ((1u << lane) - 1u));
       if (lane == 0) s_warp[g][warp] = __popc(bal);
     }
     __syncthreads();
     if (c >= 0) {
       uint32_t before = 0;
       for (int w = 0; w < warp; ++w) before += s_warp[c][w];
-      out[s_base[c] + before + rank[c]] = bc;
+      out[s_base[c] + before + rank] = bc;
     }
     __syncthreads();
     if (tid < kGroups) {
