@@ -8,6 +8,7 @@
 // Release build.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <functional>
 #include <limits>
@@ -17,6 +18,7 @@
 #include <random>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include <cuda_runtime.h>
@@ -67,7 +69,8 @@ struct Handle {
 using HandlePtr = std::shared_ptr<Handle>;
 
 HandlePtr cached_handle(int tag, const std::vector<double>& key,
-                        const std::function<int(int, vpipg_poly**)>& make, const char* what) {
+                        const std::function<int(int, vpipg_poly**)>& make, const char* what,
+                        int dev) {
   struct Entry {
     int tag, device;
     std::vector<double> key;
@@ -77,7 +80,6 @@ HandlePtr cached_handle(int tag, const std::vector<double>& key,
   static std::mutex mu;
   static std::vector<Entry> cache;
   static uint64_t clock = 0;
-  const int dev = current_device();
   {
     std::lock_guard<std::mutex> lock(mu);
     for (Entry& e : cache)
@@ -90,7 +92,7 @@ HandlePtr cached_handle(int tag, const std::vector<double>& key,
   auto h = std::make_shared<Handle>();
   check(make(dev, &h->p), what);  // throws vpip::Error for invalid input
   std::lock_guard<std::mutex> lock(mu);
-  if (cache.size() >= 16) {
+  if (cache.size() >= 64) {
     auto lru = std::min_element(cache.begin(), cache.end(),
                                 [](const Entry& a, const Entry& b) { return a.used < b.used; });
     cache.erase(lru);
@@ -108,14 +110,63 @@ void split(std::span<const Point2> v, std::vector<double>& x, std::vector<double
   }
 }
 
-InclusionMask run(const vpipg_poly* p, int engine, const PointBatch& points) {
+using Maker = std::function<int(int, vpipg_poly**)>;
+
+// The batch on the B200(s). `threads` keeps the reference's meaning -- how
+// many parts the batch is split into, the mask never depending on it
+// (test_engines.cpp:227-241) -- and maps to GPUs: with threads > 1 the batch
+// is cut into min(threads, devices, m / 2^20) contiguous shards, shard s runs
+// on device (current + s) mod devices from its own host thread, each through
+// the host-buffer path (one PCIe link per GPU).
+InclusionMask run(int engine, const std::vector<double>& key, const Maker& make, const char* what,
+                  const PointBatch& points, int threads) {
   if (points.xs.size() != points.ys.size())
     throw Error(ErrorCode::InvalidParameter, "xs and ys differ in length");
+  const int dev0 = current_device();
   InclusionMask mask(points.size());
-  if (points.empty()) return mask;
-  check(vpipg_test_host(p, engine, VPIPG_F64, points.xs.data(), points.ys.data(), points.size(),
-                        nullptr, mask.data(), nullptr),
-        "vpipg_test_host");
+  const size_t m = points.size();
+  int ndev = 1;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev < 1) ndev = 1;
+  // VPIPG_SHARDS_PER_GPU (default 1) and VPIPG_MIN_SHARD_POINTS (default
+  // 2^20) let a single-GPU box exercise the sharded path: several shards per
+  // device, run concurrently
+  static const int per_gpu = [] {
+    const char* v = std::getenv("VPIPG_SHARDS_PER_GPU");
+    const int k = v ? std::atoi(v) : 1;
+    return k < 1 ? 1 : k;
+  }();
+  static const size_t min_shard = [] {
+    const char* v = std::getenv("VPIPG_MIN_SHARD_POINTS");
+    const long long k = v ? std::atoll(v) : (1ll << 20);
+    return static_cast<size_t>(k < 1 ? 1 : k);
+  }();
+  const size_t by_size = std::max<size_t>(1, m / min_shard);
+  const int shards = static_cast<int>(std::min<size_t>(
+      std::min<size_t>(static_cast<size_t>(std::max(threads, 1)),
+                       static_cast<size_t>(ndev) * static_cast<size_t>(per_gpu)),
+      by_size));
+  // handles first, on the calling thread: validation errors throw from here
+  std::vector<HandlePtr> h(shards);
+  for (int sh = 0; sh < shards; ++sh) h[sh] = cached_handle(engine, key, make, what, (dev0 + sh) % ndev);
+  if (m == 0) return mask;
+  if (shards == 1) {
+    check(vpipg_test_host(h[0]->p, engine, VPIPG_F64, points.xs.data(), points.ys.data(), m,
+                          nullptr, mask.data(), nullptr),
+          what);
+    return mask;
+  }
+  std::vector<int> rc(shards, 0);
+  std::vector<std::thread> pool;
+  const size_t per = (m + shards - 1) / shards;
+  for (int sh = 0; sh < shards; ++sh)
+    pool.emplace_back([&, sh] {
+      const size_t lo = std::min(m, sh * per), hi = std::min(m, lo + per);
+      if (lo < hi)
+        rc[sh] = vpipg_test_host(h[sh]->p, engine, VPIPG_F64, points.xs.data() + lo,
+                                 points.ys.data() + lo, hi - lo, nullptr, mask.data() + lo, nullptr);
+    });
+  for (auto& t : pool) t.join();
+  for (int r : rc) check(r, what);
   return mask;
 }
 
@@ -274,7 +325,7 @@ bool voronoi_contains(const GeneratorSet& g, Point2 p) {
   return true;
 }
 
-InclusionMask voronoi_contains_batch(const GeneratorSet& g, const PointBatch& points, int) {
+InclusionMask voronoi_contains_batch(const GeneratorSet& g, const PointBatch& points, int threads) {
   std::vector<double> outer(2 * g.outer.size());
   for (std::size_t k = 0; k < g.outer.size(); ++k) {
     outer[2 * k] = g.outer[k].x;
@@ -284,14 +335,13 @@ InclusionMask voronoi_contains_batch(const GeneratorSet& g, const PointBatch& po
   std::vector<double> key(outer);
   key.push_back(inner[0]);
   key.push_back(inner[1]);
-  const HandlePtr h = cached_handle(
+  return run(
       VPIPG_ENGINE_VORONOI, key,
       [&](int dev, vpipg_poly** out) {
         return vpipg_prepare_generators(inner, outer.data(), static_cast<uint32_t>(g.outer.size()),
                                         dev, nullptr, out);
       },
-      "voronoi_contains_batch");
-  return run(h->p, VPIPG_ENGINE_VORONOI, points);
+      "voronoi_contains_batch", points, threads);
 }
 
 InclusionMask voronoi_contains_batch(const GeneratorSet& g, const PointBatch& points,
@@ -334,19 +384,18 @@ bool sign_of_offset_contains(const ConvexPolygon& polygon, Point2 p) {
 }
 
 InclusionMask sign_of_offset_contains_batch(const ConvexPolygon& polygon, const PointBatch& points,
-                                            int) {
+                                            int threads) {
   std::vector<double> x, y;
   split(polygon.vertices(), x, y);
   std::vector<double> key(x);
   key.insert(key.end(), y.begin(), y.end());
-  const HandlePtr h = cached_handle(
+  return run(
       VPIPG_ENGINE_OFFSET, key,
       [&](int dev, vpipg_poly** out) {
         return vpipg_prepare(x.data(), y.data(), static_cast<uint32_t>(x.size()), VPIPG_KIND_OFFSET, dev,
                              nullptr, out);
       },
-      "sign_of_offset_contains_batch");
-  return run(h->p, VPIPG_ENGINE_OFFSET, points);
+      "sign_of_offset_contains_batch", points, threads);
 }
 
 namespace {
@@ -375,19 +424,18 @@ int ray_crossing_count(std::span<const Point2> v, Point2 p) {
 }
 
 InclusionMask ray_crossing_contains_batch(std::span<const Point2> vertices, const PointBatch& points,
-                                          int) {
+                                          int threads) {
   std::vector<double> x, y;
   split(vertices, x, y);
   std::vector<double> key(x);
   key.insert(key.end(), y.begin(), y.end());
-  const HandlePtr h = cached_handle(
+  return run(
       VPIPG_ENGINE_CROSSING, key,
       [&](int dev, vpipg_poly** out) {
         return vpipg_prepare(x.data(), y.data(), static_cast<uint32_t>(x.size()), VPIPG_KIND_CROSSING, dev,
                              nullptr, out);
       },
-      "ray_crossing_contains_batch");
-  return run(h->p, VPIPG_ENGINE_CROSSING, points);
+      "ray_crossing_contains_batch", points, threads);
 }
 
 // ---------------------------------------------------------------- sampling

@@ -90,3 +90,20 @@ def test_reference_unit_suites_on_the_b200_dropin():
     r = subprocess.run([str(oracle.REF_UNIT_B200)], capture_output=True, text=True, timeout=900)
     print(r.stdout[-2000:])
     assert r.returncode == 0 and "| 0 failed" in r.stdout, r.stdout[-4000:]
+
+
+@pytest.mark.gpu
+def test_reference_unit_suites_with_sharded_batches():
+    """The same reference unit suites with every multi-thread batch call sharded
+    (VPIPG_SHARDS_PER_GPU=4: up to 4 concurrent shards per device, so the
+    split / merge path of `threads > 1` runs even on one GPU); the suites'
+    threads-independence cases (test_engines.cpp:227-241) must still hold."""
+    import os
+    import subprocess
+    import oracle
+    if not oracle.REF_UNIT_B200.exists():
+        pytest.skip("oracle/_ref not built (needs /root/reference)")
+    env = dict(os.environ, VPIPG_SHARDS_PER_GPU="4", VPIPG_MIN_SHARD_POINTS="1024")
+    r = subprocess.run([str(oracle.REF_UNIT_B200)], capture_output=True, text=True, timeout=900,
+                       env=env)
+    assert r.returncode == 0 and "| 0 failed" in r.stdout, r.stdout[-4000:]
