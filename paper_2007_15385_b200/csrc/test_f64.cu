@@ -159,7 +159,10 @@ __global__ void __launch_bounds__(kThreads) exact_kernel(const DevTables t, cons
 template <int kEngine>
 cudaError_t launch_one(const DevTables& t, const TestArgs& a, size_t rec_bytes,
                        cudaStream_t stream) {
-  constexpr int P = 4;
+#ifndef VPIPG_F64_P
+#define VPIPG_F64_P 4
+#endif
+  constexpr int P = VPIPG_F64_P;
   const bool staged = (size_t)t.n * rec_bytes <= 96 * 1024;
   auto k = staged ? exact_kernel<kEngine, P, true> : exact_kernel<kEngine, P, false>;
   const size_t smem = staged ? (size_t)t.n * rec_bytes : 0;
