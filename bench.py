@@ -310,6 +310,9 @@ class PolygonJob:
     def launch(self, e, words, count, stream):
         self.poly.test(e, self.xs, self.ys, words=words, count=count, stream=stream)
 
+    def launch_all(self, words, counts, stream):
+        self.poly.test_multi(self.xs, self.ys, (0, 1, 2), words=words, counts=counts, stream=stream)
+
     def prepare_host(self):
         t = self.torch
         self.hx = t.empty(self.xs.numel(), dtype=self.xs.dtype, pin_memory=True)
@@ -350,6 +353,10 @@ class JoinJob:
     def launch(self, e, words, count, stream):
         self.db.test(e, self.xs, self.ys, self.ids, words=words, count=count, stream=stream)
 
+    def launch_all(self, words, counts, stream):
+        for e in range(3):
+            self.launch(e, words[e], counts[e], stream)
+
     def prepare_host(self):
         t = self.torch
         self.h = [t.empty(a.numel(), dtype=a.dtype, pin_memory=True) for a in (self.xs, self.ys, self.ids)]
@@ -386,6 +393,8 @@ def main():
     ap.add_argument("--cpu-sample", type=int, default=CPU_SAMPLE)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--fused", action="store_true",
+                    help="one fused kernel for the three engines (vpipg_test_multi) instead of three")
     ap.add_argument("--no-graph", action="store_true",
                     help="time eager launches instead of CUDA-graph replays of the step")
     ap.add_argument("--points", type=int, default=0, help="override the workload size (profiling)")
@@ -448,7 +457,15 @@ def main():
             s0.record(stream)
         counts.zero_()
         pairs = []
-        for e in range(3):
+        if args.fused:  # one kernel: its time is reported once, for all three engines
+            if record:
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+            job.launch_all(words, [counts[e:e + 1] for e in range(3)], stream)
+            if record:
+                b.record(stream)
+                pairs = [(a, b)] * 3
+        for e in range(0 if args.fused else 3):
             if record:
                 a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 a.record(stream)
@@ -478,8 +495,11 @@ def main():
         graph = torch.cuda.CUDAGraph()
         with torch.cuda.graph(graph, stream=stream):
             counts.zero_()
-            for e in range(3):
-                job.launch(e, words[e], counts[e:e + 1], stream)
+            if args.fused:
+                job.launch_all(words, [counts[e:e + 1] for e in range(3)], stream)
+            else:
+                for e in range(3):
+                    job.launch(e, words[e], counts[e:e + 1], stream)
             comm.allreduce(counts, stream)
         with torch.cuda.stream(stream):
             for _ in range(2):
@@ -575,27 +595,35 @@ def main():
     bytes_per_launch = m * job.bytes_per_unit + 4 * ((m + 31) // 32)
     pe = int(m * n_edges)
     kernels = []
-    for e, name in enumerate(("voronoi", "sign_of_offset", "ray_crossing")):
+    fused = args.fused and isinstance(job, PolygonJob)
+    names = ("voronoi", "sign_of_offset", "ray_crossing")
+    for e, name in enumerate(names[:1] if fused else names):
         t = per_kernel_ms[e] * 1e-3
-        kernels.append({"engine": name, "ms": per_kernel_ms[e],
-                        "GB_per_s": bytes_per_launch / t / 1e9,
-                        "point_edge_per_s": pe / t,
-                        "tflops_alg": 4 * pe / t / 1e12})
+        work = 3 if fused else 1  # the fused kernel tests every point under all three engines
+        nbytes = bytes_per_launch + (2 * 4 * ((m + 31) // 32) if fused else 0)
+        kernels.append({"engine": "fused (voronoi + sign_of_offset + ray_crossing)" if fused else name,
+                        "ms": per_kernel_ms[e],
+                        "GB_per_s": nbytes / t / 1e9,
+                        "point_edge_per_s": work * pe / t,
+                        "tflops_alg": 4 * work * pe / t / 1e12})
     clk_hz = ((clocks or {}).get("sm_mhz") or 1965.0) * 1e6
     sms = torch.cuda.get_device_properties(local).multi_processor_count
     f64 = getattr(job, "f64", False)
     for k in kernels:
         if job.issue_cycles:
-            peak_pe = sms * 4 * 32 * clk_hz / job.issue_cycles[k["engine"]]
+            cyc = (sum(job.issue_cycles.values()) / 3 if fused else job.issue_cycles[k["engine"]])
+            peak_pe = sms * 4 * 32 * clk_hz / cyc
             k["issue_model_frac"] = k["point_edge_per_s"] / peak_pe
-    dom = max(range(3), key=lambda e: per_kernel_ms[e])
+    if fused:
+        per_kernel_ms = per_kernel_ms[:1]
+    dom = max(range(len(kernels)), key=lambda e: per_kernel_ms[e])
     dk = kernels[dom]
     hbm_frac = dk["GB_per_s"] / hbm_peak
     fma_tflops = 2 * fma_peak / 1e12 if fma_peak else 2 * FFMA_PER_SM_CLK * 148 * 1.965e9 / 1e12
     if f64:  # DFMA issues at half the FFMA rate (profiles/pipe_peaks_r01.json)
         fma_tflops /= 2
     fma_frac = dk["tflops_alg"] / fma_tflops
-    compute_bound = (4 * pe / (fma_tflops * 1e12)) > (bytes_per_launch / (hbm_peak * 1e9))
+    compute_bound = (4 * (3 if fused else 1) * pe / (fma_tflops * 1e12)) > (bytes_per_launch / (hbm_peak * 1e9))
     traffic = None
     try:  # DRAM bytes per launch from the committed ncu --set full capture (same kernel/config)
         tj = json.loads(TRAFFIC_FILE.read_text())[args.workload]
@@ -639,10 +667,11 @@ def main():
         "dtype": "f64" if f64 else "f32",
         "data": "synthetic (seeded counter-based points, reference-sampler polygon)",
         "config": {**config_block(args, world), "n_edges": n_edges,
+                   "engines_fused": bool(args.fused),
                    "launch": ("eager launches" if args.no_graph else
                               "one CUDA-graph replay per step (3 engine kernels + count "
                               "all-reduce); per-kernel times from K eager steps before it")},
-        "gpu_launches": 3 * args.steps,
+        "gpu_launches": (1 if args.fused and isinstance(job, PolygonJob) else 3) * args.steps,
         "roofline": roof, "kernels": kernels, "inside_counts": final_counts,
         "prepare_ms": job.prep_ms,
         "clocks": clocks, "e2e": e2e, "cpu_baseline": cpu,

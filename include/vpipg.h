@@ -114,6 +114,16 @@ int vpipg_test(const vpipg_poly* poly, int engine, int dtype, const void* xs, co
                uint64_t m, uint32_t* mask_words, uint8_t* mask_bytes,
                unsigned long long* d_inside, void* stream);
 
+/* Several engines over one device batch: mask_words / mask_bytes / d_inside
+ * indexed by engine (arrays of 3, entries may be NULL). With all three engines
+ * on float32 points this is ONE fused kernel that reads every point once and
+ * tests it under Voronoi, sign-of-offset and crossing in turn (the masks equal
+ * three vpipg_test calls); otherwise the engines run one after another. */
+int vpipg_test_multi(const vpipg_poly* poly, uint32_t engines, int dtype, const void* xs,
+                     const void* ys, uint64_t m, uint32_t* const* mask_words,
+                     uint8_t* const* mask_bytes, unsigned long long* const* d_inside,
+                     void* stream);
+
 /* Same with HOST buffers (pageable or pinned): chunked host->device copies,
  * the test kernel and device->host mask copies are pipelined over three
  * streams on `device`, through a per-device staging area kept between

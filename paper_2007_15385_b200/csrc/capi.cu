@@ -335,6 +335,30 @@ int vpipg_test(const vpipg_poly* p, int engine, int dtype, const void* xs, const
   return dispatch(p, engine, dtype, a, static_cast<cudaStream_t>(stream));
 }
 
+int vpipg_test_multi(const vpipg_poly* p, uint32_t engines, int dtype, const void* xs,
+                     const void* ys, uint64_t m, uint32_t* const* mask_words,
+                     uint8_t* const* mask_bytes, unsigned long long* const* d_inside,
+                     void* stream) {
+  if (!p || engines == 0 || (engines & ~7u)) return kInvalid;
+  DeviceGuard g(p->device);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  TestArgs a[3];
+  for (int e = 0; e < 3; ++e)
+    a[e] = TestArgs{xs, ys, m, mask_words ? mask_words[e] : nullptr,
+                    mask_bytes ? mask_bytes[e] : nullptr, d_inside ? d_inside[e] : nullptr};
+  if (engines == 7u && dtype == VPIPG_F32 && (p->kinds & VPIPG_KIND_ALL) == VPIPG_KIND_ALL && m > 0 &&
+      xs && ys) {
+    const cudaError_t e = launch_test_f32_all(p->t, a, s);
+    if (e != cudaErrorNotSupported) return cuda_code(e);
+  }
+  for (int e = 0; e < 3; ++e)  // one engine at a time
+    if (engines & (1u << e)) {
+      const int rc = dispatch(p, e, dtype, a[e], s);
+      if (rc) return rc;
+    }
+  return kOk;
+}
+
 int vpipg_prepare_csr(const uint32_t* offsets, const double* vx, const double* vy,
                       uint32_t npoly, uint32_t kinds, int device, void* stream, vpipg_db** out,
                       int32_t* per_poly_status) {

@@ -474,6 +474,78 @@ __global__ void __launch_bounds__(kThreads, VPIPG_LDG_MINB)
   flush_count(count, a);
 }
 
+// ---------------------------------------------------------------------------
+// Fused three-engine pass (vpipg_test_multi with all engines, fp32): every
+// point is read once and tested by Voronoi, sign-of-offset and crossing in
+// turn, each writing its own mask words and count. Same slice schedule and
+// loads as ldg_kernel; the three tables sit side by side in shared memory.
+constexpr int kTriP = VPIPG_CROSS_P;  // the crossing engine's register budget sets P
+using TriV = SlabEngine<kTriP, false>;
+using TriO = SlabEngine<kTriP, true>;
+using TriC = CrossEngine<kTriP>;
+struct TriParams {
+  TriV::Params v;
+  TriO::Params o;
+  TriC::Params c;
+  uint32_t off_o, off_c;  // float4 offsets of the offset / crossing tables in shared memory
+};
+
+__global__ void __launch_bounds__(kThreads, 2)
+    tri_kernel(const TriParams prm, const TestArgs av, const TestArgs ao, const TestArgs ac,
+               const uint64_t full_slices) {
+  constexpr int P = kTriP;
+  constexpr int kWarpPts = 32 * P;
+  extern __shared__ __align__(128) unsigned char smem[];
+  float4* s_tab = reinterpret_cast<float4*>(smem);
+  TriV::stage(prm.v, s_tab);
+  TriO::stage(prm.o, s_tab + prm.off_o);
+  TriC::stage(prm.c, s_tab + prm.off_c);
+  const float4* tv = s_tab;
+  const float4* to = s_tab + prm.off_o;
+  const float4* tc = s_tab + prm.off_c;
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint64_t W = (uint64_t)gridDim.x * kWarps;
+  const uint64_t g0 = (uint64_t)blockIdx.x * kWarps + warp;
+  const float* xs = static_cast<const float*>(av.xs);
+  const float* ys = static_cast<const float*>(av.ys);
+  constexpr int kLines = kWarpPts * 4 / 128;
+  auto prefetch = [&](uint64_t g) {
+    if (g >= full_slices) return;
+    for (int l = lane; l < 2 * kLines; l += 32)
+      prefetch_l2((l < kLines ? xs : ys) + g * kWarpPts + (l % kLines) * 32);
+  };
+  prefetch(g0);
+  uint32_t cv = 0, co = 0, cc = 0;
+  for (uint64_t g = g0; g < full_slices; g += W) {
+    prefetch(g + W);
+    const float* px = xs + g * kWarpPts + lane;
+    const float* py = ys + g * kWarpPts + lane;
+    float x[P], y[P], va[P], vb[P];
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+      x[p] = __ldcs(px + 32 * p);
+      y[p] = __ldcs(py + 32 * p);
+    }
+    TriV::eval(prm.v, tv, x, y, va, vb);
+    cv += emit<false, TriV::kNanInside, P>(va, vb, g * kWarpPts, av, lane);
+    TriO::eval(prm.o, to, x, y, va, vb);
+    co += emit<false, TriO::kNanInside, P>(va, vb, g * kWarpPts, ao, lane);
+    TriC::eval(prm.c, tc, x, y, va, vb);
+    cc += emit<false, TriC::kNanInside, P>(va, vb, g * kWarpPts, ac, lane);
+  }
+  if (g0 == full_slices % W) {
+    for (uint64_t base = full_slices * kWarpPts; base < av.m; base += kWarpPts) {
+      cv += guarded_tile<TriV>(prm.v, tv, av, base, lane);
+      co += guarded_tile<TriO>(prm.o, to, ao, base, lane);
+      cc += guarded_tile<TriC>(prm.c, tc, ac, base, lane);
+    }
+  }
+  flush_count(cv, av);
+  flush_count(co, ao);
+  flush_count(cc, ac);
+}
+
 template <class Eng, bool kSmemTab>
 __global__ void __launch_bounds__(kThreads) generic_kernel(const typename Eng::Params prm,
                                                           const TestArgs a) {
@@ -536,6 +608,34 @@ cudaError_t launch(const typename Eng::Params& prm, const TestArgs& a, cudaStrea
 }
 
 }  // namespace
+
+cudaError_t launch_test_f32_all(const DevTables& t, const TestArgs* a, cudaStream_t stream) {
+  // one set of register-streamed loads feeds all three engines
+  static_assert(TriV::kRegStream && TriO::kRegStream, "slab engines stream through registers");
+  constexpr int kWarpPts = 32 * kTriP;
+  TriParams prm{};
+  prm.v = TriV::Params{t.slab[0], t.ox, t.oy};
+  prm.o = TriO::Params{t.slab[1], t.ox, t.oy};
+  prm.c = TriC::Params{t.cross, t.ox, t.oy};
+  const size_t nv = TriV::table_bytes(prm.v) / sizeof(float4);
+  const size_t no = TriO::table_bytes(prm.o) / sizeof(float4);
+  const size_t nc = TriC::table_bytes(prm.c) / sizeof(float4);
+  prm.off_o = static_cast<uint32_t>(nv);
+  prm.off_c = static_cast<uint32_t>(nv + no);
+  const size_t smem = (nv + no + nc) * sizeof(float4);
+  const bool aligned =
+      ((reinterpret_cast<uintptr_t>(a[0].xs) | reinterpret_cast<uintptr_t>(a[0].ys)) & 15) == 0;
+  const uint64_t full_slices = aligned ? a[0].m / kWarpPts : 0;
+  if (smem > kSmemTableMax || full_slices < kWarps) return cudaErrorNotSupported;
+  int sms = 0, per_sm = 0;
+  cudaError_t e = launch_config(reinterpret_cast<const void*>(tri_kernel), kThreads, smem, &sms, &per_sm);
+  if (e != cudaSuccess) return e;
+  const uint64_t cap = (uint64_t)sms * per_sm;
+  const uint64_t want = (full_slices + kWarps - 1) / kWarps;
+  const int grid = (int)(want < cap ? want : cap);
+  tri_kernel<<<grid, kThreads, smem, stream>>>(prm, a[0], a[1], a[2], full_slices);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_test_f32(const DevTables& t, int engine, const TestArgs& a,
                             cudaStream_t stream) {

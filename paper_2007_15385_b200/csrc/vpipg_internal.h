@@ -92,6 +92,9 @@ cudaError_t launch_fill_pairs(uint64_t seed, uint64_t first, uint64_t m, uint32_
                               const double* cx, const double* cy, const double* rad, float* xs,
                               float* ys, uint32_t* ids, cudaStream_t stream);
 cudaError_t launch_test_f32(const DevTables& t, int engine, const TestArgs& a, cudaStream_t stream);
+// all three engines in one fused pass over the points (a[0..2] share xs, ys,
+// m); cudaErrorNotSupported when the tables or the batch do not fit its plan
+cudaError_t launch_test_f32_all(const DevTables& t, const TestArgs* a, cudaStream_t stream);
 cudaError_t launch_test_f64(const DevTables& t, int engine, const TestArgs& a, cudaStream_t stream);
 // ---- validation (validate.cu): run_validation (bench.cpp:279-308) on the device ----
 constexpr int kReportSamples = 100;

@@ -138,6 +138,29 @@ class PreparedPolygon:
                                 ptr(words), ptr(bytes_), ptr(count), _stream_ptr(stream)),
               "vpipg_test")
 
+    def test_multi(self, xs, ys, engines=(0, 1, 2), words=None, bytes_=None, counts=None,
+                   stream=None) -> None:
+        """Several engines over one device batch (vpipg_test_multi): words /
+        bytes_ / counts are lists of 3 (entries may be None; counts entries are
+        int64 tensors of 1, accumulated). All three engines on float32 points
+        run as one fused kernel. Asynchronous."""
+        import torch
+        m = xs.numel()
+        outs = []
+        for lst, need in ((words, (m + 31) // 32), (bytes_, m), (counts, 1)):
+            for t in (lst or []):
+                outs.append((t, need))
+        _check_device_batch(xs, ys, (torch.float32, torch.float64), outs)
+        mask = 0
+        for e in engines:
+            mask |= 1 << _engine_id(e)
+        arr = lambda lst: (C.c_void_p * 3)(*[C.c_void_p(t.data_ptr() if t is not None else None)
+                                             for t in (lst or [None] * 3)])
+        dtype = F32 if xs.dtype == torch.float32 else F64
+        check(load().vpipg_test_multi(self._h, mask, dtype, C.c_void_p(xs.data_ptr()),
+                                      C.c_void_p(ys.data_ptr()), m, arr(words), arr(bytes_),
+                                      arr(counts), _stream_ptr(stream)), "vpipg_test_multi")
+
     def test_host(self, engine, xs: np.ndarray, ys: np.ndarray, words: bool = True,
                   bytes_: bool = False):
         """Host-buffer drop-in (vpipg_test_host): returns (words|None, bytes|None, count)."""

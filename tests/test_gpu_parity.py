@@ -507,3 +507,31 @@ def test_concurrent_prepare_test_destroy():
             assert np.array_equal(o[e][0], o_ref[e][0]) and o[e][1] == o_ref[e][1]
             assert np.array_equal(hw[e], hw_ref[e]) and hc[e] == hc_ref[e]
             assert hc[e] == o[e][1]
+
+
+@pytest.mark.parametrize("m", [5, 4099, 1 << 20, (1 << 22) + 777])
+def test_fused_multi_engine_pass_equals_separate_calls(m):
+    """vpipg_test_multi with all three engines on f32 points (the fused
+    one-read kernel when the batch fits its plan, else one engine at a time)
+    gives exactly the words, bytes and counts of three vpipg_test calls."""
+    vx, vy = W.c5_polygon(vp.random_convex_polygon)
+    xs = torch.empty(m, dtype=torch.float32, device=DEV)
+    ys = torch.empty_like(xs)
+    vp.fill_uniform_points(W.c5_point_seed(), 0, xs, ys, W.C5_BOX)
+    nw = (m + 31) // 32
+    with vp.PreparedPolygon.prepare(vx, vy, vp.KIND_ALL) as p:
+        ref = []
+        for e in range(3):
+            w = torch.zeros(nw, dtype=torch.int32, device=DEV)
+            b = torch.zeros(m, dtype=torch.uint8, device=DEV)
+            c = torch.zeros(1, dtype=torch.int64, device=DEV)
+            p.test(e, xs, ys, words=w, bytes_=b, count=c)
+            ref.append((w, b, c))
+        ws = [torch.zeros(nw, dtype=torch.int32, device=DEV) for _ in range(3)]
+        bs = [torch.zeros(m, dtype=torch.uint8, device=DEV) for _ in range(3)]
+        cs = [torch.zeros(1, dtype=torch.int64, device=DEV) for _ in range(3)]
+        p.test_multi(xs, ys, (0, 1, 2), words=ws, bytes_=bs, counts=cs)
+        torch.cuda.synchronize()
+        for e in range(3):
+            assert torch.equal(ws[e], ref[e][0]) and torch.equal(bs[e], ref[e][1]), e
+            assert cs[e].item() == ref[e][2].item(), e
