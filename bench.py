@@ -141,8 +141,7 @@ def build_workload(name: str, lo: int, hi: int, torch, vp, stream):
         ys = torch.empty(m, dtype=torch.float32, device=dev)
         vp.fill_uniform_points(W.c5_point_seed(), lo, xs, ys, W.C5_BOX, stream=stream)
     elif name.startswith("c3"):
-        n = int(name.split(":")[1]) if ":" in name else 8
-        vx, vy = W.c3_polygon(n)
+        n, (vx, vy) = W.c3_named(name)
         m = hi - lo
         xs = torch.empty(m, dtype=torch.float32, device=dev)
         ys = torch.empty(m, dtype=torch.float32, device=dev)
@@ -175,7 +174,9 @@ def workload_desc(name: str) -> str:
             "c1": "C1 random 8-angle hull, 2^20 f64 points (the oracle config, exact f64 kernels)",
             "c4": "C4 polygon-database join: 65536 random convex 4..16-gons (CSR), 2^28 f32 "
                   "(point, polygon id) pairs, gathered test"}.get(
-        name.split(":")[0], f"C3 n-sweep regular {name} jittered hull, 2^28 f32 points")
+        name.split(":")[0],
+        f"C3 n-sweep regular {name} " + ("unjittered exact-n" if name.startswith("c3x")
+                                         else "jittered hull") + ", 2^28 f32 points")
 
 
 # ----------------------------------------------------------------- CPU reference
@@ -187,8 +188,7 @@ def cpu_reference_sample(name: str, sample: int):
         vx, vy = W.c5_polygon(orc.random_convex_polygon)
         xs, ys = orc.counter_points_f32(W.c5_point_seed(), 0, sample, W.C5_BOX)
     elif name.startswith("c3"):
-        n = int(name.split(":")[1]) if ":" in name else 8
-        vx, vy = W.c3_polygon(n)
+        n, (vx, vy) = W.c3_named(name)
         xs, ys = orc.counter_points_f32(int(W.mix_seed_np(W.config_seed(3), 200 + n)), 0, sample,
                                         W.C3_BOX)
     elif name == "c2":

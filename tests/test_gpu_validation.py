@@ -116,6 +116,21 @@ def test_c3_full_scale_f32_vs_f64(n):
     print(f"C3 n={n}: f32/f64 band disagreements per engine {d}")
 
 
+@pytest.mark.parametrize("n", (64, 256, 1024))
+def test_c3x_exact_n_full_scale_f32_vs_f64(n):
+    """The unjittered exact-n C3 supplement: all n edges live, up to
+    n = 1024, so the tables exceed anything the literal C3 hulls produce."""
+    n_, (vx, vy) = W.c3_named(f"c3x:{n}")
+    assert n_ == n and len(vx) == n
+    m = W.C3_POINTS
+    xs = torch.empty(m, dtype=torch.float32, device=DEV)
+    ys = torch.empty(m, dtype=torch.float32, device=DEV)
+    vp.fill_uniform_points(int(W.mix_seed_np(W.config_seed(3), 200 + n)), 0, xs, ys, W.C3_BOX)
+    d = _f32_vs_f64_all_engines(vx, vy, xs, ys)
+    assert max(d) < m * 1e-5
+    print(f"C3x n={n}: f32/f64 band disagreements per engine {d}")
+
+
 def test_c2_full_scale_f32_vs_f64():
     """BASELINE.json config 2 (vehicle 12-gon, 2^24 clustered points)."""
     vx, vy = W.c2_polygon()

@@ -12,7 +12,7 @@ GPU path and the CPU oracle see identical polygons and points.
       2^24 f32 points in 2048 Gaussian clusters of 8192 (sigma 0.3 m), centre
       angle U[0, 2pi), centre radius U[0, 50] m
   C3  n-sweep: regular n-gons, radii jittered +-5 %, random rotation, convex
-      hull; 2^28 f32 points uniform in [-1.2, 1.2]^2
+      hull; 2^28 f32 points uniform in [-1.2, 1.2]^2 ("c3x": unjittered exact n)
   C5  scaling: vpip::random_convex_polygon(32, seed, 1.0); 2^31 f32 points
       uniform in [-1.5, 1.5]^2 from the counter-based stream
 
@@ -141,6 +141,17 @@ def c3_polygon(n: int, jitter: float = 0.05, seed: int | None = None):
     rad = 1.0 + jitter * (2.0 * unit_np(s, 1 + k) - 1.0)
     ang = rot + 2.0 * math.pi * k / n
     return convex_hull(rad * np.cos(ang), rad * np.sin(ang))
+
+
+def c3_named(name: str):
+    """Polygon of a bench workload name: "c3:<n>" is the literal C3 config (jittered
+    hull, so n_eff < n for large n); "c3x:<n>" is the unjittered exact-n
+    supplement SURVEY §8d recommends (regular n-gon, random rotation, all n
+    vertices strictly convex up to n = 1024) that reaches the compute-bound
+    regime. Both use the C3 point stream of that n."""
+    kind, _, n = name.partition(":")
+    n = int(n) if n else 8
+    return n, c3_polygon(n, jitter=0.0 if kind == "c3x" else 0.05)
 
 
 # ---------------------------------------------------------------- C4
