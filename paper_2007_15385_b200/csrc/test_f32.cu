@@ -37,6 +37,17 @@
 #ifndef VPIPG_CROSS_P
 #define VPIPG_CROSS_P 12
 #endif
+#ifndef VPIPG_CROSS_VOTE
+#define VPIPG_CROSS_VOTE 2
+#endif
+#ifndef VPIPG_SLAB_UNROLL
+#define VPIPG_SLAB_UNROLL 1
+#endif
+#ifndef VPIPG_CROSS_UNROLL
+#define VPIPG_CROSS_UNROLL 1
+#endif
+#define VPIPG_PRAGMA(x) _Pragma(#x)
+#define VPIPG_UNROLL(n) VPIPG_PRAGMA(unroll n)
 
 namespace vpipg {
 
@@ -71,6 +82,7 @@ template <int P, bool kNanIn>
 struct SlabEngine {
   static constexpr int kP = P;
   static constexpr bool kNanInside = kNanIn;
+  static constexpr int kVote = kNanIn ? 1 : 0;  // see vote_in
   static constexpr bool kRegStream = true;  // ldg_kernel
   struct Params {
     SlabTable tab;
@@ -106,7 +118,7 @@ struct SlabEngine {
     }
     const uint32_t nc = na < nb ? na : nb;
     uint32_t i = 1;
-#pragma unroll 1
+    VPIPG_UNROLL(VPIPG_SLAB_UNROLL)
     for (; i < nc; ++i) {
       const float4 a = A[i], b = B[i];
 #pragma unroll
@@ -167,7 +179,8 @@ struct SlabEngine {
 template <int P>
 struct CrossEngine {
   static constexpr int kP = P;
-  static constexpr bool kNanInside = false;  // a = +-1, never NaN
+  static constexpr bool kNanInside = false;
+  static constexpr int kVote = VPIPG_CROSS_VOTE;  // 2: a holds the parity word, sign bit = inside
 #ifndef VPIPG_CROSS_LDG
 #define VPIPG_CROSS_LDG 0
 #endif
@@ -200,7 +213,7 @@ struct CrossEngine {
         gp[p] = last.x - x[p];
       }
       uint32_t k = 0;
-#pragma unroll 1
+      VPIPG_UNROLL(VPIPG_CROSS_UNROLL)
       for (; k + 3 < n; k += 4) {
         const float4 v0 = s[k], v1 = s[k + 1], v2 = s[k + 2], v3 = s[k + 3];
 #pragma unroll
@@ -247,7 +260,11 @@ struct CrossEngine {
     }
 #pragma unroll
     for (int p = 0; p < P; ++p) {
-      a[p] = __uint_as_float((~par[p] & 0x80000000u) | 0x3f800000u);
+      if (kVote == 2) {
+        a[p] = __uint_as_float(par[p]);
+      } else {
+        a[p] = __uint_as_float((~par[p] & 0x80000000u) | 0x3f800000u);
+      }
       b[p] = 0.f;
     }
   }
@@ -257,12 +274,21 @@ struct CrossEngine {
 // Output: ballot words (PIPM order), optional byte mask, per-lane inside count.
 // The P words of a slice are warp-uniform; lane 0 writes them with 16-byte
 // streaming stores (a slice's words are 64 contiguous, 64-byte aligned bytes).
-// inside = (a >= b), or (a >= b or unordered) for kNanInside: one FSETP feeds
-// both the ballot and a predicated count
-template <bool kNanInside>
-__device__ __forceinline__ uint32_t vote_ge(float a, float b, uint32_t& cnt) {
+// kVote 0: inside = (a >= b); 1: (a >= b or unordered), the NaN-inside rule;
+// 2: a's bit pattern is negative as an int (the crossing parity word, no
+// float conversion). One compare feeds both the ballot and a predicated count.
+template <int kVote>
+__device__ __forceinline__ uint32_t vote_in(float a, float b, uint32_t& cnt) {
   uint32_t w;
-  if (kNanInside)
+  if (kVote == 2)
+    asm volatile(
+        "{\n\t.reg .pred q;\n\t"
+        "setp.lt.s32 q, %2, 0;\n\t"
+        "vote.sync.ballot.b32 %0, q, 0xffffffff;\n\t"
+        "@q add.u32 %1, %1, 1;\n\t}"
+        : "=r"(w), "+r"(cnt)
+        : "r"(__float_as_uint(a)));
+  else if (kVote == 1)
     asm volatile(
         "{\n\t.reg .pred q;\n\t"
         "setp.geu.f32 q, %2, %3;\n\t"
@@ -281,15 +307,15 @@ __device__ __forceinline__ uint32_t vote_ge(float a, float b, uint32_t& cnt) {
   return w;
 }
 
-template <bool kGuard, bool kNanInside, int P>
+template <bool kGuard, int kVote, int P>
 __device__ __forceinline__ uint32_t emit(float (&av)[P], const float (&bv)[P], uint64_t base,
                                          const TestArgs& a, int lane) {
   uint32_t w[P];
   uint32_t cnt = 0;
 #pragma unroll
   for (int p = 0; p < P; ++p) {
-    if (kGuard && base + 32u * p + lane >= a.m) av[p] = -INFINITY;
-    w[p] = vote_ge<kNanInside>(av[p], bv[p], cnt);
+    if (kGuard && base + 32u * p + lane >= a.m) av[p] = kVote == 2 ? 0.f : -INFINITY;
+    w[p] = vote_in<kVote>(av[p], bv[p], cnt);
   }
   if (a.words && lane == 0) {
     const uint64_t w0 = base >> 5;
@@ -336,7 +362,7 @@ __device__ __forceinline__ uint32_t guarded_tile(const typename Eng::Params& prm
     y[p] = ok ? __ldcs(ys + idx) : 0.f;
   }
   Eng::eval(prm, tab, x, y, va, vb);
-  return emit<true, Eng::kNanInside, P>(va, vb, base, a, lane);
+  return emit<true, Eng::kVote, P>(va, vb, base, a, lane);
 }
 
 // kSmemTab: the polygon table is staged in shared memory once per CTA (the
@@ -405,7 +431,7 @@ __global__ void __launch_bounds__(kThreads, 2)
                &full[s], policy);
     }
     Eng::eval(prm, tab, x, y, va, vb);
-    count += emit<false, Eng::kNanInside, P>(va, vb, g * kWarpPts, a, lane);
+    count += emit<false, Eng::kVote, P>(va, vb, g * kWarpPts, a, lane);
   }
   // partial last slice: the warp next in round-robin order, guarded loads
   if (g0 == full_slices % W) {
@@ -465,7 +491,7 @@ __global__ void __launch_bounds__(kThreads, VPIPG_LDG_MINB)
       y[p] = __ldcs(py + 32 * p);
     }
     Eng::eval(prm, tab, x, y, va, vb);
-    count += emit<false, Eng::kNanInside, P>(va, vb, g * kWarpPts, a, lane);
+    count += emit<false, Eng::kVote, P>(va, vb, g * kWarpPts, a, lane);
   }
   if (g0 == full_slices % W) {
     for (uint64_t base = full_slices * kWarpPts; base < a.m; base += kWarpPts)
@@ -528,11 +554,11 @@ __global__ void __launch_bounds__(kThreads, 2)
       y[p] = __ldcs(py + 32 * p);
     }
     TriV::eval(prm.v, tv, x, y, va, vb);
-    cv += emit<false, TriV::kNanInside, P>(va, vb, g * kWarpPts, av, lane);
+    cv += emit<false, TriV::kVote, P>(va, vb, g * kWarpPts, av, lane);
     TriO::eval(prm.o, to, x, y, va, vb);
-    co += emit<false, TriO::kNanInside, P>(va, vb, g * kWarpPts, ao, lane);
+    co += emit<false, TriO::kVote, P>(va, vb, g * kWarpPts, ao, lane);
     TriC::eval(prm.c, tc, x, y, va, vb);
-    cc += emit<false, TriC::kNanInside, P>(va, vb, g * kWarpPts, ac, lane);
+    cc += emit<false, TriC::kVote, P>(va, vb, g * kWarpPts, ac, lane);
   }
   if (g0 == full_slices % W) {
     for (uint64_t base = full_slices * kWarpPts; base < av.m; base += kWarpPts) {
