@@ -28,14 +28,36 @@ constexpr int kPrepThreads = 256;
 enum : int { kNone = -1, kXlo = 0, kXhi = 1, kYlo = 2, kYhi = 3 };
 
 
-// Half-plane a*x' + b*y' + c >= 0 (local frame) -> slab class and (B, C).
-__device__ int slab_classify(double a, double b, double c, float2* bc) {
+// Half-plane a*x' + b*y' + c >= 0 (local frame) -> slab class and (B, C),
+// under one of three orientation modes:
+//   kMixed   |a| >= |b| -> x-bound (x' >= / <= B y' + C), else y-bound, so
+//            |B| <= 1 (the general case: two sections, chained seed);
+//   kPreferY every edge is a y-bound unless it is within 2^-VPIPG_SLAB_STEEP
+//            rad of vertical;
+//   kPreferX the transpose.
+// A polygon with no such near-vertical (near-horizontal) edge has empty x (y)
+// groups under kPreferY (kPreferX) and the test kernels run ONE section with
+// no chained seed; slab_scatter picks the cheaper of the two when either
+// applies. Precision: the f32 FFMA and the rounding of B and C misplace the
+// line by about 1.2e-7 (|v'| + |C / B|) in distance whatever |B| is (C / B is
+// the line's intercept, within the polygon's extent of the frame origin for
+// the lines that matter), far inside the 1e-5 band; the cap on |B| keeps
+// B v' finite for any f32 point of interest.
+#ifndef VPIPG_SLAB_STEEP
+#define VPIPG_SLAB_STEEP 16
+#endif
+enum : int { kMixed = 0, kPreferY = 1, kPreferX = 2 };
+__device__ int slab_classify(double a, double b, double c, float2* bc, int mode) {
   if (a == 0.0 && b == 0.0) {
     if (c >= 0.0) return kNone;          // no constraint (e.g. outer == inner)
-    *bc = make_float2(0.f, INFINITY);     // unsatisfiable: x' >= +inf
-    return kXlo;
+    *bc = make_float2(0.f, INFINITY);     // unsatisfiable: x' >= +inf (or y')
+    return mode == kPreferY ? kYlo : kXlo;
   }
-  if (fabs(a) >= fabs(b)) {
+  constexpr double kSteep = static_cast<double>(1ull << VPIPG_SLAB_STEEP);
+  const bool xform = mode == kMixed    ? fabs(a) >= fabs(b)
+                     : mode == kPreferY ? fabs(a) > fabs(b) * kSteep
+                                        : fabs(b) <= fabs(a) * kSteep;
+  if (xform) {
     *bc = make_float2(static_cast<float>(-b / a), static_cast<float>(-c / a));
     return a > 0.0 ? kXlo : kXhi;
   }
@@ -43,44 +65,72 @@ __device__ int slab_classify(double a, double b, double c, float2* bc) {
   return b > 0.0 ? kYlo : kYhi;
 }
 
+__device__ __forceinline__ uint32_t even_len(uint32_t c) { return (c + 1u) & ~1u; }
+
 // Block-wide deterministic scatter of per-edge (class, coef) into the four
-// groups of one slab table, each padded with neutral entries to an even,
-// non-zero length. Edge order is preserved inside a group.
-__device__ void slab_scatter(int n, int (*cls_of)(int, const void*, float2*), const void* ctx,
+// groups of one slab table, each padded with neutral entries to an even
+// length, and to at least one pair unless both groups of its side are empty
+// (single-section table). Edge order is preserved inside a group.
+__device__ void slab_scatter(int n, int (*cls_of)(int, const void*, float2*, int), const void* ctx,
                              float2* out, uint32_t* cnt_out) {
   __shared__ uint32_t s_base[kGroups];
   __shared__ uint32_t s_warp[kGroups][kPrepThreads / 32];
-  __shared__ uint32_t s_count[kGroups];
+  __shared__ uint32_t s_count[3][kGroups];
+  __shared__ int s_mode;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  if (tid < kGroups) s_count[tid] = 0;
+  if (tid < 3 * kGroups) s_count[tid / kGroups][tid % kGroups] = 0;
   __syncthreads();
-  // pass 1: group sizes
+  // pass 1: group sizes under each orientation mode
   for (int k = tid; k < n; k += kPrepThreads) {
     float2 bc;
-    const int c = cls_of(k, ctx, &bc);
-    if (c >= 0) atomicAdd(&s_count[c], 1u);
+    for (int m = 0; m < 3; ++m) {
+      const int c = cls_of(k, ctx, &bc, m);
+      if (c >= 0) atomicAdd(&s_count[m][c], 1u);
+    }
   }
   __syncthreads();
   if (tid == 0) {
+    // single-section candidates, cost = padded edges per point (ties: balance)
+    int mode = kMixed;
+    uint32_t best = UINT32_MAX;
+    for (int m = kPreferY; m <= kPreferX; ++m) {
+      const uint32_t* c = s_count[m];
+      const bool single = m == kPreferY ? (c[kXlo] | c[kXhi]) == 0 : (c[kYlo] | c[kYhi]) == 0;
+      const uint32_t lo = m == kPreferY ? c[kYlo] : c[kXlo];
+      const uint32_t hi = m == kPreferY ? c[kYhi] : c[kXhi];
+      const uint32_t plo = max(even_len(lo), 2u), phi = max(even_len(hi), 2u);
+      const uint32_t cost = 4u * (plo + phi) + (plo > phi ? plo - phi : phi - plo);
+      if (single && cost < best) {
+        best = cost;
+        mode = m;
+      }
+    }
+    s_mode = mode;
+    const uint32_t* cnt = s_count[mode];
+    const bool x_empty = (cnt[kXlo] | cnt[kXhi]) == 0;
+    const bool y_empty = (cnt[kYlo] | cnt[kYhi]) == 0;
     uint32_t acc = 0;
     for (int g = 0; g < kGroups; ++g) {
       s_base[g] = acc;
       // even length (two edges per 16-byte load) and at least one pair, so
-      // the kernels can seed their running max / min from the first pair
-      uint32_t padded = (s_count[g] + 1u) & ~1u;
-      if (padded == 0) padded = 2;
+      // the kernels can seed their running max / min from the first pair --
+      // except that an empty side stays empty (single-section table)
+      uint32_t padded = even_len(cnt[g]);
+      const bool side_empty = g <= kXhi ? x_empty && !y_empty : y_empty;
+      if (padded == 0 && !side_empty) padded = 2;
       cnt_out[g] = padded;
-      for (uint32_t q = s_count[g]; q < padded; ++q)  // neutral pad entries
+      for (uint32_t q = cnt[g]; q < padded; ++q)  // neutral pad entries
         out[acc + q] = make_float2(0.f, (g == kXlo || g == kYlo) ? -INFINITY : INFINITY);
       acc += padded;
     }
   }
   __syncthreads();
+  const int mode = s_mode;
   // pass 2: ordered placement, one 256-edge chunk at a time
   for (int k0 = 0; k0 < n; k0 += kPrepThreads) {
     const int k = k0 + tid;
     float2 bc = make_float2(0.f, 0.f);
-    const int c = (k < n) ? cls_of(k, ctx, &bc) : kNone;
+    const int c = (k < n) ? cls_of(k, ctx, &bc, mode) : kNone;
     uint32_t rank = 0;  // this edge's rank inside its group, within the warp
 #pragma unroll
     for (int g = 0; g < kGroups; ++g) {
@@ -111,13 +161,13 @@ struct VorCtx {
 
 // Voronoi half-plane k: |x - p0|^2 <= |x - pk|^2  <=>  d.(m - x) >= 0 with
 // d = pk - p0 and m the midpoint (the perpendicular bisector, Eq. 9).
-__device__ int vor_class(int k, const void* ctx, float2* bc) {
+__device__ int vor_class(int k, const void* ctx, float2* bc, int mode) {
   const VorCtx& v = *static_cast<const VorCtx*>(ctx);
   const double2 pk = v.outer[k];
   const double dx = pk.x - v.p0x, dy = pk.y - v.p0y;
   const double mx = 0.5 * ((v.p0x - v.ox) + (pk.x - v.ox));
   const double my = 0.5 * ((v.p0y - v.oy) + (pk.y - v.oy));
-  return slab_classify(-dx, -dy, dx * mx + dy * my, bc);
+  return slab_classify(-dx, -dy, dx * mx + dy * my, bc, mode);
 }
 
 struct OffCtx {
@@ -129,12 +179,12 @@ struct OffCtx {
 
 // Sign-of-offset edge e (j = e-1 -> i = e): inside iff lhs >= rhs, i.e.
 // (q - v_j) x dv >= 0 (engines.cpp:150-152 with the flags == 0 branch).
-__device__ int off_class(int e, const void* ctx, float2* bc) {
+__device__ int off_class(int e, const void* ctx, float2* bc, int mode) {
   const OffCtx& o = *static_cast<const OffCtx*>(ctx);
   const int i = e, j = (e + o.n - 1) % o.n;
   const double dvx = o.vx[i] - o.vx[j], dvy = o.vy[i] - o.vy[j];
   const double wx = o.vx[j] - o.ox, wy = o.vy[j] - o.oy;
-  return slab_classify(-dvy, dvx, wx * dvy - wy * dvx, bc);
+  return slab_classify(-dvy, dvx, wx * dvy - wy * dvx, bc, mode);
 }
 
 __global__ void __launch_bounds__(kPrepThreads) prep_kernel(PrepArgs a) {

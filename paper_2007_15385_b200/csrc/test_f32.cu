@@ -78,7 +78,11 @@ __device__ __forceinline__ float fmin3(float a, float b, float c) {
 // kNanInside: the answer for a point with a NaN coordinate, the reference's
 // IEEE behaviour -- Voronoi `inner_sq <= outer_sq` is false (outside),
 // sign-of-offset raises no flag, so flags == 0 (inside).
-template <int P, bool kNanIn>
+// kMode: 0 = two sections (mixed table), 1 = y-only table, 2 = x-only table
+// (prep.cu slab_scatter), -1 = decided per launch from the table counts (the
+// fused kernel); the launcher instantiates the mode the table has, so each
+// streaming kernel carries one code path
+template <int P, bool kNanIn, int kMode = -1>
 struct SlabEngine {
   static constexpr int kP = P;
   static constexpr bool kNanInside = kNanIn;
@@ -142,7 +146,9 @@ struct SlabEngine {
   }
 
   // Point p is inside iff a[p] >= b[p] (every half-plane holds; ties inside).
-  // Section 1 (x bounded by lines in y) leaves lo1 >= x >= hi1 with the
+  // Most tables have one section (prep.cu: every edge expressed as a bound on
+  // y, or every edge on x): lo >= w >= hi, inside iff lo <= hi. Otherwise
+  // section 1 (x bounded by lines in y) leaves lo1 >= x >= hi1 with the
   // violation f1 = lo1 - hi1 >= 0, zero iff the point satisfies it. Section 2
   // is seeded with lo = y + f1, hi = y, so its lo <= hi test also fails when
   // section 1 did: y + f1 > y for every f1 that survives rounding against y,
@@ -153,11 +159,32 @@ struct SlabEngine {
                                               float (&a)[P], float (&b)[P]) {
     const SlabTable& t = prm.tab;
     float lo[P], hi[P];
-    section(s + t.off[0] / 2, t.cnt[0] / 2, s + t.off[1] / 2, t.cnt[1] / 2, y, x, x, lo, hi);
-    float seed[P];
+    // single-section tables: y alone, bounded by lines in x (mode 1), or x
+    // alone, bounded by lines in y (mode 2)
+    auto y_only = [&] {
+      section(s + t.off[2] / 2, t.cnt[2] / 2, s + t.off[3] / 2, t.cnt[3] / 2, x, y, y, lo, hi);
+    };
+    auto x_only = [&] {
+      section(s + t.off[0] / 2, t.cnt[0] / 2, s + t.off[1] / 2, t.cnt[1] / 2, y, x, x, lo, hi);
+    };
+    auto mixed = [&] {
+      section(s + t.off[0] / 2, t.cnt[0] / 2, s + t.off[1] / 2, t.cnt[1] / 2, y, x, x, lo, hi);
+      float seed[P];
 #pragma unroll
-    for (int p = 0; p < P; ++p) seed[p] = y[p] + (lo[p] - hi[p]);
-    section(s + t.off[2] / 2, t.cnt[2] / 2, s + t.off[3] / 2, t.cnt[3] / 2, x, seed, y, lo, hi);
+      for (int p = 0; p < P; ++p) seed[p] = y[p] + (lo[p] - hi[p]);
+      section(s + t.off[2] / 2, t.cnt[2] / 2, s + t.off[3] / 2, t.cnt[3] / 2, x, seed, y, lo, hi);
+    };
+    if constexpr (kMode == 0) {
+      mixed();
+    } else if constexpr (kMode == 1) {
+      y_only();
+    } else if constexpr (kMode == 2) {
+      x_only();
+    } else {
+      if (t.cnt[0] == 0) y_only();
+      else if (t.cnt[2] == 0) x_only();
+      else mixed();
+    }
 #pragma unroll
     for (int p = 0; p < P; ++p) {
       a[p] = hi[p];
@@ -663,18 +690,25 @@ cudaError_t launch_test_f32_all(const DevTables& t, const TestArgs* a, cudaStrea
   return cudaGetLastError();
 }
 
+template <bool kNanIn, int kMode>
+cudaError_t launch_slab_mode(const DevTables& t, int engine, const TestArgs& a, cudaStream_t stream) {
+  using E = SlabEngine<VPIPG_SLAB_P, kNanIn, kMode>;
+  typename E::Params prm{t.slab[engine], t.ox, t.oy};
+  return launch<E>(prm, a, stream);
+}
+
+template <bool kNanIn>
+cudaError_t launch_slab(const DevTables& t, int engine, const TestArgs& a, cudaStream_t stream) {
+  const SlabTable& tab = t.slab[engine];
+  if (tab.cnt[0] == 0) return launch_slab_mode<kNanIn, 1>(t, engine, a, stream);
+  if (tab.cnt[2] == 0) return launch_slab_mode<kNanIn, 2>(t, engine, a, stream);
+  return launch_slab_mode<kNanIn, 0>(t, engine, a, stream);
+}
+
 cudaError_t launch_test_f32(const DevTables& t, int engine, const TestArgs& a,
                             cudaStream_t stream) {
-  if (engine == 0) {
-    using E = SlabEngine<VPIPG_SLAB_P, false>;
-    typename E::Params prm{t.slab[0], t.ox, t.oy};
-    return launch<E>(prm, a, stream);
-  }
-  if (engine == 1) {
-    using E = SlabEngine<VPIPG_SLAB_P, true>;
-    typename E::Params prm{t.slab[1], t.ox, t.oy};
-    return launch<E>(prm, a, stream);
-  }
+  if (engine == 0) return launch_slab<false>(t, 0, a, stream);
+  if (engine == 1) return launch_slab<true>(t, 1, a, stream);
   using E = CrossEngine<VPIPG_CROSS_P>;
   typename E::Params prm{t.cross, t.ox, t.oy};
   return launch<E>(prm, a, stream);

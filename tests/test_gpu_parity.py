@@ -535,3 +535,70 @@ def test_fused_multi_engine_pass_equals_separate_calls(m):
         for e in range(3):
             assert torch.equal(ws[e], ref[e][0]) and torch.equal(bs[e], ref[e][1]), e
             assert cs[e].item() == ref[e][2].item(), e
+
+
+def _offset_table_mode(vx, vy, steep=16):
+    """Python mirror of prep.cu slab_scatter's choice for the sign-of-offset
+    table of a CCW polygon: 1 = y-only, 2 = x-only, 0 = two sections."""
+    vx, vy = np.asarray(vx, float), np.asarray(vy, float)
+    a = -(vy - np.roll(vy, 1))
+    b = vx - np.roll(vx, 1)
+    k = float(1 << steep)
+    best, mode = None, 0
+    for m, ok, lo, hi in ((1, not np.any(np.abs(a) > np.abs(b) * k), np.sum(b > 0), np.sum(b < 0)),
+                          (2, not np.any(np.abs(b) > np.abs(a) * k), np.sum(a > 0), np.sum(a < 0))):
+        plo, phi = max((lo + 1) & ~1, 2), max((hi + 1) & ~1, 2)
+        cost = 4 * (plo + phi) + abs(plo - phi)
+        if ok and (best is None or cost < best):
+            best, mode = cost, m
+    return mode
+
+
+def _rot(vx, vy, t):
+    c, s = np.cos(t), np.sin(t)
+    vx, vy = np.asarray(vx, float), np.asarray(vy, float)
+    return c * vx - s * vy, s * vx + c * vy
+
+
+@pytest.mark.parametrize("shape", ["rect", "rect_tilted_1e-7", "one_vertical", "one_horizontal",
+                                   "c5", "c2", "triangle"])
+def test_slab_table_modes_match_outside_band(orc, shape):
+    """The slab tables come in three forms (prep.cu): every edge a bound on y
+    (one section), every edge a bound on x (one section, transposed), or the
+    general two-section table when the polygon has both (near-)vertical and
+    (near-)horizontal edges. Each form is held to the oracle outside the band,
+    through the streaming kernels (2^20 + 13 points)."""
+    if shape == "rect":
+        vx, vy = [0.0, 3.0, 3.0, 0.0], [0.0, 0.0, 1.0, 1.0]
+    elif shape == "rect_tilted_1e-7":
+        vx, vy = _rot([0.0, 3.0, 3.0, 0.0], [0.0, 0.0, 1.0, 1.0], 1e-7)
+    elif shape == "one_vertical":   # x = 2 exactly, no horizontal edge
+        vx, vy = [0.0, 2.0, 2.0, -0.5], [-1.0, -0.5, 1.5, 0.7]
+    elif shape == "one_horizontal":  # y = 0 exactly, no vertical edge
+        vx, vy = [-1.0, 2.0, 1.3, -0.2], [0.0, 0.0, 1.7, 1.1]
+    elif shape == "c5":
+        vx, vy = W.c5_polygon(orc.random_convex_polygon)
+    elif shape == "c2":
+        vx, vy = W.c2_polygon()
+    else:
+        vx, vy = [0.0, 1.0, 0.3], [0.0, 0.2, 0.9]
+    vx, vy = np.asarray(vx, float), np.asarray(vy, float)
+    want_mode = {"rect": 0, "rect_tilted_1e-7": 0, "one_vertical": 2, "one_horizontal": 1}
+    if shape in want_mode:
+        assert _offset_table_mode(vx, vy) == want_mode[shape]
+    m = (1 << 20) + 13
+    x0, x1, y0, y1 = vx.min(), vx.max(), vy.min(), vy.max()
+    pad = 0.3 * max(x1 - x0, y1 - y0)
+    rng = np.random.default_rng(77)
+    xs = rng.uniform(x0 - pad, x1 + pad, m).astype(np.float32)
+    ys = rng.uniform(y0 - pad, y1 + pad, m).astype(np.float32)
+    xs64, ys64 = xs.astype(np.float64), ys.astype(np.float64)
+    want = orc.masks(vx, vy, xs64, ys64)
+    band = band_mask(orc, vx, vy, xs64, ys64)
+    with vp.PreparedPolygon.prepare(vx, vy, vp.KIND_ALL) as p:
+        for e in (0, 1):
+            w, b, c = run_device(p, e, xs, ys)
+            assert np.array_equal(words_to_mask(w, m), b) and c == int(b.sum())
+            bad = (b != want[e]) & ~band
+            assert not bad.any(), (shape, e, np.flatnonzero(bad)[:5])
+            assert 0.05 < b.mean() < 0.95
