@@ -63,7 +63,7 @@ struct Handle {
 // The batch functions take the polygon / generator set by value semantics on
 // every call (engines.hpp:90-142), so a caller looping over batches of one
 // polygon would prepare the device tables each time. Prepared handles are
-// therefore cached by their exact input (bitwise, per kind and device), 16
+// therefore cached by their exact input (bitwise, per kind and device), 64
 // entries, least recently used out; handles are immutable and shared, so a
 // cached one may serve concurrent calls (engines.hpp:80-84).
 using HandlePtr = std::shared_ptr<Handle>;
