@@ -602,3 +602,62 @@ def test_slab_table_modes_match_outside_band(orc, shape):
             bad = (b != want[e]) & ~band
             assert not bad.any(), (shape, e, np.flatnonzero(bad)[:5])
             assert 0.05 < b.mean() < 0.95
+
+
+@pytest.mark.parametrize("shape", ["rect", "one_vertical", "one_horizontal", "triangle"])
+def test_fused_pass_on_every_table_form(shape):
+    """The fused kernel picks the slab table form at run time; for each form
+    (two-section, x-only, y-only) its words and counts equal the separate
+    single-form kernels' (2^20 + 5 points, so the fused plan applies)."""
+    vx, vy = {"rect": ([0.0, 3.0, 3.0, 0.0], [0.0, 0.0, 1.0, 1.0]),
+              "one_vertical": ([0.0, 2.0, 2.0, -0.5], [-1.0, -0.5, 1.5, 0.7]),
+              "one_horizontal": ([-1.0, 2.0, 1.3, -0.2], [0.0, 0.0, 1.7, 1.1]),
+              "triangle": ([0.0, 1.0, 0.3], [0.0, 0.2, 0.9])}[shape]
+    m = (1 << 20) + 5
+    rng = np.random.default_rng(5)
+    xs = torch.as_tensor(rng.uniform(-1.5, 3.5, m).astype(np.float32), device=DEV)
+    ys = torch.as_tensor(rng.uniform(-1.5, 2.5, m).astype(np.float32), device=DEV)
+    nw = (m + 31) // 32
+    with vp.PreparedPolygon.prepare(vx, vy, vp.KIND_ALL) as p:
+        ref = []
+        for e in range(3):
+            w = torch.zeros(nw, dtype=torch.int32, device=DEV)
+            c = torch.zeros(1, dtype=torch.int64, device=DEV)
+            p.test(e, xs, ys, words=w, count=c)
+            ref.append((w, c))
+        ws = [torch.zeros(nw, dtype=torch.int32, device=DEV) for _ in range(3)]
+        cs = [torch.zeros(1, dtype=torch.int64, device=DEV) for _ in range(3)]
+        p.test_multi(xs, ys, (0, 1, 2), words=ws, counts=cs)
+        torch.cuda.synchronize()
+        for e in range(3):
+            assert torch.equal(ws[e], ref[e][0]), (shape, e)
+            assert cs[e].item() == ref[e][1].item() > 0, (shape, e)
+
+
+def test_multi_partial_engine_sets_f64_and_missing_outputs(golden):
+    """vpipg_test_multi outside the fused plan: two of three engines, f64
+    points, and NULL outputs for some engines -- same answers as vpipg_test,
+    untouched buffers for the engines not asked for."""
+    vx, vy = golden["conv_c1_v"]
+    m = 70_001
+    rng = np.random.default_rng(9)
+    for dt in (torch.float32, torch.float64):
+        xs = torch.as_tensor(rng.uniform(-1.5, 1.5, m), device=DEV).to(dt)
+        ys = torch.as_tensor(rng.uniform(-1.5, 1.5, m), device=DEV).to(dt)
+        nw = (m + 31) // 32
+        with vp.PreparedPolygon.prepare(vx, vy, vp.KIND_ALL) as p:
+            ref = []
+            for e in range(3):
+                w = torch.zeros(nw, dtype=torch.int32, device=DEV)
+                p.test(e, xs, ys, words=w)
+                ref.append(w)
+            ws = [torch.full((nw,), 7, dtype=torch.int32, device=DEV) for _ in range(3)]
+            cs = [torch.zeros(1, dtype=torch.int64, device=DEV), None,
+                  torch.zeros(1, dtype=torch.int64, device=DEV)]
+            p.test_multi(xs, ys, (0, 2), words=ws, counts=cs)
+            torch.cuda.synchronize()
+            assert torch.equal(ws[0], ref[0]) and torch.equal(ws[2], ref[2]), dt
+            assert bool((ws[1] == 7).all()), dt  # engine 1 was not requested
+            for e in (0, 2):
+                bits = np.unpackbits(ws[e].cpu().numpy().view(np.uint8), bitorder="little")[:m]
+                assert cs[e].item() == int(bits.sum()), (dt, e)
