@@ -8,6 +8,7 @@ from __future__ import annotations
 
 import concurrent.futures as cf
 import os
+import shutil
 import subprocess
 import sys
 from pathlib import Path
@@ -72,6 +73,7 @@ def build_variant(tag: str, defines: list[str], sources: tuple[str, ...] = ("tes
             objs.append(OBJ / (s + ".o"))
     _run([NVCC, *ARCH, "-shared", "-o", str(out), *map(str, objs), "-cudart", "static",
           "-Xlinker", "--no-undefined", "-lrt", "-lpthread", "-ldl"])
+    shutil.rmtree(vdir, ignore_errors=True)  # keep the tree that ships to the GPU box small
     return out
 
 
