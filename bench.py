@@ -7,12 +7,15 @@ Headline workload (BASELINE.json configs[4], the config the metric "at
 [-1.5, 1.5]^2 from the counter-based stream, sharded evenly (1024-aligned,
 contiguous) over the ranks. One step = all three engines (Voronoi,
 sign-of-offset, ray-crossing) over every point + one NCCL all-reduce of the
-three inside counts. value = 3 * 2^31 point-polygon tests per step / step
+three inside counts. The three engines run as one fused kernel that reads
+each point once and writes three masks and counts (vpipg_test_multi);
+`--separate` launches the three per-engine kernels instead, and the line's
+`engines_separate` always reports their times for the per-engine roofline. value = 3 * 2^31 point-polygon tests per step / step
 time (max over ranks, CUDA events). Inputs (17 GB at N=1) are far larger than
 L2, so no flush is needed between steps.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
-                    [--workload c5|c2|c3:<n>|c1]
+                    [--workload c5|c2|c3:<n>|c3x:<n>|c4|c1] [--separate]
 
 `--impl reference` times the reference's own CPU implementation
 (oracle/_ref/libvpip_ref.so, the unmodified reference sources; the oracle port
@@ -394,7 +397,10 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--fused", action="store_true",
-                    help="one fused kernel for the three engines (vpipg_test_multi) instead of three")
+                    help="(default for f32 single-polygon workloads) one fused kernel for the "
+                         "three engines (vpipg_test_multi)")
+    ap.add_argument("--separate", action="store_true",
+                    help="three per-engine kernels per step instead of the fused one")
     ap.add_argument("--no-graph", action="store_true",
                     help="time eager launches instead of CUDA-graph replays of the step")
     ap.add_argument("--points", type=int, default=0, help="override the workload size (profiling)")
@@ -443,6 +449,9 @@ def main():
         flush_sink = torch.zeros(1, dtype=torch.int64, device="cuda")
     stream.synchronize()
     n_edges = job.n_edges
+    # the three engines in one kernel that reads every point once (f32, one
+    # polygon); the per-engine kernels are still timed below for the breakdown
+    fused = (not args.separate) and isinstance(job, PolygonJob) and not job.f64
 
     kevents = []  # per step, per engine: (start, end) on the launch stream
     sevents = []  # per step: (start, end) around the step's own work, flush excluded
@@ -457,7 +466,7 @@ def main():
             s0.record(stream)
         counts.zero_()
         pairs = []
-        if args.fused:  # one kernel: its time is reported once, for all three engines
+        if fused:  # one kernel: its time is reported once, for all three engines
             if record:
                 a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 a.record(stream)
@@ -465,7 +474,7 @@ def main():
             if record:
                 b.record(stream)
                 pairs = [(a, b)] * 3
-        for e in range(0 if args.fused else 3):
+        for e in range(0 if fused else 3):
             if record:
                 a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 a.record(stream)
@@ -495,7 +504,7 @@ def main():
         graph = torch.cuda.CUDAGraph()
         with torch.cuda.graph(graph, stream=stream):
             counts.zero_()
-            if args.fused:
+            if fused:
                 job.launch_all(words, [counts[e:e + 1] for e in range(3)], stream)
             else:
                 for e in range(3):
@@ -547,6 +556,27 @@ def main():
     per_kernel_ms = [statistics.mean(p[e][0].elapsed_time(p[e][1]) for p in kevents)
                      for e in range(3)]
     final_counts = counts.tolist()
+    sep_ms = None
+    if fused:
+        # per-engine breakdown: K eager steps of the three separate kernels
+        # (same inputs, same flush), outside the timed region
+        sep = []
+        with torch.cuda.stream(stream):
+            for _ in range(args.steps):
+                if flush is not None:
+                    flush_sink.copy_(flush.view(torch.int64).sum(dtype=torch.int64).view(1))
+                counts.zero_()
+                ev = []
+                for e in range(3):
+                    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    a.record(stream)
+                    job.launch(e, words[e], counts[e:e + 1], stream)
+                    b.record(stream)
+                    ev.append((a, b))
+                sep.append(ev)
+        torch.cuda.synchronize()
+        sep_ms = [statistics.mean(p[e][0].elapsed_time(p[e][1]) for p in sep) for e in range(3)]
+        assert counts.tolist() == final_counts or world > 1  # same answers as the fused kernel
 
     # ---- end-to-end through the public API with pinned host buffers ----
     e2e = None
@@ -594,28 +624,33 @@ def main():
     hbm_peak, hbm_src, fma_peak = load_peaks()
     bytes_per_launch = m * job.bytes_per_unit + 4 * ((m + 31) // 32)
     pe = int(m * n_edges)
-    kernels = []
-    fused = args.fused and isinstance(job, PolygonJob)
-    names = ("voronoi", "sign_of_offset", "ray_crossing")
-    for e, name in enumerate(names[:1] if fused else names):
-        t = per_kernel_ms[e] * 1e-3
-        work = 3 if fused else 1  # the fused kernel tests every point under all three engines
-        nbytes = bytes_per_launch + (2 * 4 * ((m + 31) // 32) if fused else 0)
-        kernels.append({"engine": "fused (voronoi + sign_of_offset + ray_crossing)" if fused else name,
-                        "ms": per_kernel_ms[e],
-                        "GB_per_s": nbytes / t / 1e9,
-                        "point_edge_per_s": work * pe / t,
-                        "tflops_alg": 4 * work * pe / t / 1e12})
     clk_hz = ((clocks or {}).get("sm_mhz") or 1965.0) * 1e6
     sms = torch.cuda.get_device_properties(local).multi_processor_count
     f64 = getattr(job, "f64", False)
-    for k in kernels:
+    names = ("voronoi", "sign_of_offset", "ray_crossing")
+    words_bytes = 4 * ((m + 31) // 32)
+
+    def kernel_entry(name, ms_k, engines):
+        """One kernel's rates: `engines` = the engine names it runs (3 for the fused one)."""
+        t = ms_k * 1e-3
+        nbytes = bytes_per_launch + (len(engines) - 1) * words_bytes
+        k = {"engine": name, "ms": ms_k, "GB_per_s": nbytes / t / 1e9,
+             "point_edge_per_s": len(engines) * pe / t,
+             "tflops_alg": 4 * len(engines) * pe / t / 1e12}
         if job.issue_cycles:
-            cyc = (sum(job.issue_cycles.values()) / 3 if fused else job.issue_cycles[k["engine"]])
-            peak_pe = sms * 4 * 32 * clk_hz / cyc
-            k["issue_model_frac"] = k["point_edge_per_s"] / peak_pe
+            cyc = sum(job.issue_cycles[e] for e in engines) / len(engines)
+            k["issue_model_frac"] = k["point_edge_per_s"] / (sms * 4 * 32 * clk_hz / cyc)
+        return k
+
     if fused:
+        kernels = [kernel_entry("fused", per_kernel_ms[0], names)]
         per_kernel_ms = per_kernel_ms[:1]
+        engines_separate = [kernel_entry(n, sep_ms[e], (n,)) for e, n in enumerate(names)]
+    else:
+        kernels = [kernel_entry(n, per_kernel_ms[e], (n,)) for e, n in enumerate(names)]
+        engines_separate = None
+    n_eng = 3 if fused else 1  # engine tests per point in one launch of the dominant kernel
+    alg_bytes = bytes_per_launch + (n_eng - 1) * words_bytes
     dom = max(range(len(kernels)), key=lambda e: per_kernel_ms[e])
     dk = kernels[dom]
     hbm_frac = dk["GB_per_s"] / hbm_peak
@@ -623,7 +658,7 @@ def main():
     if f64:  # DFMA issues at half the FFMA rate (profiles/pipe_peaks_r01.json)
         fma_tflops /= 2
     fma_frac = dk["tflops_alg"] / fma_tflops
-    compute_bound = (4 * (3 if fused else 1) * pe / (fma_tflops * 1e12)) > (bytes_per_launch / (hbm_peak * 1e9))
+    compute_bound = (4 * n_eng * pe / (fma_tflops * 1e12)) > (alg_bytes / (hbm_peak * 1e9))
     traffic = None
     try:  # DRAM bytes per launch from the committed ncu --set full capture (same kernel/config)
         tj = json.loads(TRAFFIC_FILE.read_text())[args.workload]
@@ -640,16 +675,18 @@ def main():
     roof.update({"kernel": dk["engine"], "hbm_GB_per_s": dk["GB_per_s"], "hbm_frac": hbm_frac,
                  "hbm_peak_source": hbm_src, "fma_frac": fma_frac,
                  "fma_peak_source": "tools/pipe_peaks.cu FFMA lane-ops/s x2 (profiles/pipe_peaks_r01.json)",
-                 "per_unit": f"{bytes_per_launch / m:.3f} B and {4 * n_edges} flops per test "
-                             f"(n={n_edges} edges, 4 flops per point-edge)",
-                 "algorithmic_bytes_per_launch": bytes_per_launch,
+                 "per_unit": (f"{alg_bytes / m:.3f} B and {4 * n_edges * n_eng} flops per point "
+                              f"({n_eng} engine test(s), n={n_edges} edges, 4 flops per "
+                              f"point-edge)"),
+                 "algorithmic_bytes_per_launch": alg_bytes,
                  "traffic_source": "profiles/traffic_r01.json (ncu --set full dram__bytes_read+write "
                                    "of this kernel on this workload, scaled to this launch)",
                  "issue_model_frac": dk.get("issue_model_frac"),
                  "issue_model": "dispatch cycles per point-edge: slab 2 (FFMA + FMNMX3/2), "
-                                "crossing 6 (2 FADD + FFMA + 1.5 LOP3); profiles/round1_summary.md"})
+                                "crossing 6 (2 FADD + FFMA + 1.5 LOP3); the fused kernel their "
+                                "mean over the three engines; profiles/round1_summary.md"})
     try:  # the ncu evidence for the same kernel and workload (issue / pipe utilisation)
-        nk = json.loads(NCU_FILE.with_name(f"ncu_full_r01_{args.workload.split(':')[0]}.json")
+        nk = json.loads(NCU_FILE.with_name(f"ncu_full_r01_{args.workload.replace(':', 'n')}.json")
                         .read_text())["kernels"][dk["engine"]]
         roof["ncu"] = {k.split(".")[0]: nk[k] for k in (
             "smsp__issue_active.avg.pct_of_peak_sustained_active",
@@ -667,12 +704,16 @@ def main():
         "dtype": "f64" if f64 else "f32",
         "data": "synthetic (seeded counter-based points, reference-sampler polygon)",
         "config": {**config_block(args, world), "n_edges": n_edges,
-                   "engines_fused": bool(args.fused),
+                   "engines_fused": fused,
                    "launch": ("eager launches" if args.no_graph else
-                              "one CUDA-graph replay per step (3 engine kernels + count "
-                              "all-reduce); per-kernel times from K eager steps before it")},
-        "gpu_launches": (1 if args.fused and isinstance(job, PolygonJob) else 3) * args.steps,
-        "roofline": roof, "kernels": kernels, "inside_counts": final_counts,
+                              "one CUDA-graph replay per step (" +
+                              ("the fused three-engine kernel" if fused else "3 engine kernels") +
+                              " + count all-reduce); per-kernel times from K eager steps before "
+                              "it" + ("; engines_separate: K eager steps of the three "
+                                      "per-engine kernels after it" if fused else ""))},
+        "gpu_launches": (1 if fused else 3) * args.steps,
+        "roofline": roof, "kernels": kernels, "engines_separate": engines_separate,
+        "inside_counts": final_counts,
         "prepare_ms": job.prep_ms,
         "clocks": clocks, "e2e": e2e, "cpu_baseline": cpu,
     }

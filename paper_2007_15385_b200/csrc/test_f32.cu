@@ -78,6 +78,11 @@ __device__ __forceinline__ float fmin3(float a, float b, float c) {
 // kNanInside: the answer for a point with a NaN coordinate, the reference's
 // IEEE behaviour -- Voronoi `inner_sq <= outer_sq` is false (outside),
 // sign-of-offset raises no flag, so flags == 0 (inside).
+struct SlabParams {
+  SlabTable tab;
+  float ox, oy;
+};
+
 // kMode: 0 = two sections (mixed table), 1 = y-only table, 2 = x-only table
 // (prep.cu slab_scatter), -1 = decided per launch from the table counts (the
 // fused kernel); the launcher instantiates the mode the table has, so each
@@ -88,10 +93,7 @@ struct SlabEngine {
   static constexpr bool kNanInside = kNanIn;
   static constexpr int kVote = kNanIn ? 1 : 0;  // see vote_in
   static constexpr bool kRegStream = true;  // ldg_kernel
-  struct Params {
-    SlabTable tab;
-    float ox, oy;
-  };
+  using Params = SlabParams;  // shared by every (P, NaN rule, form) instantiation
   static size_t table_bytes(const Params& p) { return (size_t)p.tab.total * sizeof(float2); }
   __device__ static const float4* global_table(const Params& p) {
     return reinterpret_cast<const float4*>(p.tab.coef);
@@ -533,19 +535,21 @@ __global__ void __launch_bounds__(kThreads, VPIPG_LDG_MINB)
 // turn, each writing its own mask words and count. Same slice schedule and
 // loads as ldg_kernel; the three tables sit side by side in shared memory.
 constexpr int kTriP = VPIPG_CROSS_P;  // the crossing engine's register budget sets P
-using TriV = SlabEngine<kTriP, false>;
-using TriO = SlabEngine<kTriP, true>;
 using TriC = CrossEngine<kTriP>;
 struct TriParams {
-  TriV::Params v;
-  TriO::Params o;
+  SlabParams v, o;
   TriC::Params c;
   uint32_t off_o, off_c;  // float4 offsets of the offset / crossing tables in shared memory
 };
 
+// kMode: the slab table form shared by the Voronoi and offset tables (their
+// lines coincide: each bisector is the edge line), -1 when they differ
+template <int kMode>
 __global__ void __launch_bounds__(kThreads, 2)
     tri_kernel(const TriParams prm, const TestArgs av, const TestArgs ao, const TestArgs ac,
                const uint64_t full_slices) {
+  using TriV = SlabEngine<kTriP, false, kMode>;
+  using TriO = SlabEngine<kTriP, true, kMode>;
   constexpr int P = kTriP;
   constexpr int kWarpPts = 32 * P;
   extern __shared__ __align__(128) unsigned char smem[];
@@ -664,6 +668,8 @@ cudaError_t launch(const typename Eng::Params& prm, const TestArgs& a, cudaStrea
 
 cudaError_t launch_test_f32_all(const DevTables& t, const TestArgs* a, cudaStream_t stream) {
   // one set of register-streamed loads feeds all three engines
+  using TriV = SlabEngine<kTriP, false>;
+  using TriO = SlabEngine<kTriP, true>;
   static_assert(TriV::kRegStream && TriO::kRegStream, "slab engines stream through registers");
   constexpr int kWarpPts = 32 * kTriP;
   TriParams prm{};
@@ -681,12 +687,17 @@ cudaError_t launch_test_f32_all(const DevTables& t, const TestArgs* a, cudaStrea
   const uint64_t full_slices = aligned ? a[0].m / kWarpPts : 0;
   if (smem > kSmemTableMax || full_slices < kWarps) return cudaErrorNotSupported;
   int sms = 0, per_sm = 0;
-  cudaError_t e = launch_config(reinterpret_cast<const void*>(tri_kernel), kThreads, smem, &sms, &per_sm);
+  auto form = [](const SlabTable& t) { return t.cnt[0] == 0 ? 1 : t.cnt[2] == 0 ? 2 : 0; };
+  const int fv = form(t.slab[0]), fo = form(t.slab[1]);
+  const int mode = fv == fo ? fv : -1;
+  auto kern = mode == 0 ? tri_kernel<0> : mode == 1 ? tri_kernel<1> : mode == 2 ? tri_kernel<2>
+                                                                              : tri_kernel<-1>;
+  cudaError_t e = launch_config(reinterpret_cast<const void*>(kern), kThreads, smem, &sms, &per_sm);
   if (e != cudaSuccess) return e;
   const uint64_t cap = (uint64_t)sms * per_sm;
   const uint64_t want = (full_slices + kWarps - 1) / kWarps;
   const int grid = (int)(want < cap ? want : cap);
-  tri_kernel<<<grid, kThreads, smem, stream>>>(prm, a[0], a[1], a[2], full_slices);
+  kern<<<grid, kThreads, smem, stream>>>(prm, a[0], a[1], a[2], full_slices);
   return cudaGetLastError();
 }
 

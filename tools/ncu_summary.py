@@ -106,6 +106,8 @@ def main():
     ap.add_argument("--out", required=True)
     ap.add_argument("--traffic")
     ap.add_argument("--key")
+    ap.add_argument("--merge", action="store_true",
+                    help="add these kernels to an existing --out file instead of replacing it")
     a = ap.parse_args()
     names = a.names.split(",")
     hdr, units, data = raw_rows(a.rep)
@@ -133,14 +135,21 @@ def main():
         k["instruction_mix"] = mix
         k["warp_stall_pct"] = stalls
         out["kernels"][name] = k
+    if a.merge and Path(a.out).exists():
+        prev = json.loads(Path(a.out).read_text())
+        prev["kernels"].update(out["kernels"])
+        prev["capture"] = prev["capture"] + " | " + a.label
+        out = prev
     Path(a.out).write_text(json.dumps(out, indent=1) + "\n")
     print(f"wrote {a.out}")
     if a.traffic:
         p = Path(a.traffic)
         tj = json.loads(p.read_text()) if p.exists() else {}
-        tj[a.key] = {"points": a.points,
-                     "dram_bytes_per_launch": {n: out["kernels"][n]["dram_bytes_per_launch"]
-                                               for n in names}}
+        ent = tj.get(a.key, {}) if a.merge else {}
+        ent["points"] = a.points
+        ent.setdefault("dram_bytes_per_launch", {}).update(
+            {n: out["kernels"][n]["dram_bytes_per_launch"] for n in names})
+        tj[a.key] = ent
         p.write_text(json.dumps(tj, indent=1) + "\n")
         print(f"updated {p} [{a.key}]")
 
