@@ -451,7 +451,8 @@ def main():
     n_edges = job.n_edges
     # the three engines in one kernel that reads every point once (f32, one
     # polygon); the per-engine kernels are still timed below for the breakdown
-    fused = (not args.separate) and isinstance(job, PolygonJob) and not job.f64
+    fused = ((not args.separate) and isinstance(job, PolygonJob) and not job.f64
+             and job.poly.multi_fused(job.xs, job.ys))  # the library's own plan (n <= 48, f32)
 
     kevents = []  # per step, per engine: (start, end) on the launch stream
     sevents = []  # per step: (start, end) around the step's own work, flush excluded

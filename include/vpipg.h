@@ -116,13 +116,21 @@ int vpipg_test(const vpipg_poly* poly, int engine, int dtype, const void* xs, co
 
 /* Several engines over one device batch: mask_words / mask_bytes / d_inside
  * indexed by engine (arrays of 3, entries may be NULL). With all three engines
- * on float32 points this is ONE fused kernel that reads every point once and
- * tests it under Voronoi, sign-of-offset and crossing in turn (the masks equal
- * three vpipg_test calls); otherwise the engines run one after another. */
+ * on float32 points (see vpipg_test_multi_fused for the exact plan) this is
+ * ONE fused kernel that reads every point once and tests it under Voronoi,
+ * sign-of-offset and crossing in turn; otherwise the engines run one after
+ * another. The masks and counts equal three vpipg_test calls either way. */
 int vpipg_test_multi(const vpipg_poly* poly, uint32_t engines, int dtype, const void* xs,
                      const void* ys, uint64_t m, uint32_t* const* mask_words,
                      uint8_t* const* mask_bytes, unsigned long long* const* d_inside,
                      void* stream);
+
+/* 1 when vpipg_test_multi would run this batch as ONE fused launch (all three
+ * engines, float32, 16-byte-aligned inputs of at least one slice per warp, a
+ * polygon of at most 48 edges whose tables fit shared memory -- above that the
+ * per-engine kernels are faster), else 0. Pure query: no device work. */
+int vpipg_test_multi_fused(const vpipg_poly* poly, uint32_t engines, int dtype, const void* xs,
+                           const void* ys, uint64_t m);
 
 /* Same with HOST buffers (pageable or pinned): chunked host->device copies,
  * the test kernel and device->host mask copies are pipelined over three

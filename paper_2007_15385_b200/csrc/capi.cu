@@ -359,6 +359,16 @@ int vpipg_test_multi(const vpipg_poly* p, uint32_t engines, int dtype, const voi
   return kOk;
 }
 
+int vpipg_test_multi_fused(const vpipg_poly* p, uint32_t engines, int dtype, const void* xs,
+                           const void* ys, uint64_t m) {
+  if (!p || engines != 7u || dtype != VPIPG_F32 || (p->kinds & VPIPG_KIND_ALL) != VPIPG_KIND_ALL ||
+      m == 0 || !xs || !ys)
+    return 0;
+  TestArgs a[3];
+  for (auto& x : a) x = TestArgs{xs, ys, m, nullptr, nullptr, nullptr};
+  return test_f32_all_plan(p->t, a, nullptr) ? 1 : 0;
+}
+
 int vpipg_prepare_csr(const uint32_t* offsets, const double* vx, const double* vy,
                       uint32_t npoly, uint32_t kinds, int device, void* stream, vpipg_db** out,
                       int32_t* per_poly_status) {

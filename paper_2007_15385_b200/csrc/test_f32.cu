@@ -75,7 +75,7 @@ __device__ __forceinline__ float fmin3(float a, float b, float c) {
 // Slab engine (Voronoi and sign-of-offset): inside iff
 //   max(XLO) <= x' <= min(XHI)  and  max(YLO) <= y' <= min(YHI)
 // where each group entry is t = B * (other coordinate) + C (see prep.cu).
-// kNanInside: the answer for a point with a NaN coordinate, the reference's
+// kNanIn: the answer for a point with a NaN coordinate, the reference's
 // IEEE behaviour -- Voronoi `inner_sq <= outer_sq` is false (outside),
 // sign-of-offset raises no flag, so flags == 0 (inside).
 struct SlabParams {
@@ -90,7 +90,6 @@ struct SlabParams {
 template <int P, bool kNanIn, int kMode = -1>
 struct SlabEngine {
   static constexpr int kP = P;
-  static constexpr bool kNanInside = kNanIn;
   static constexpr int kVote = kNanIn ? 1 : 0;  // see vote_in
   static constexpr bool kRegStream = true;  // ldg_kernel
   using Params = SlabParams;  // shared by every (P, NaN rule, form) instantiation
@@ -208,7 +207,6 @@ struct SlabEngine {
 template <int P>
 struct CrossEngine {
   static constexpr int kP = P;
-  static constexpr bool kNanInside = false;
   static constexpr int kVote = VPIPG_CROSS_VOTE;  // 2: a holds the parity word, sign bit = inside
 #ifndef VPIPG_CROSS_LDG
 #define VPIPG_CROSS_LDG 0
@@ -550,6 +548,8 @@ __global__ void __launch_bounds__(kThreads, 2)
                const uint64_t full_slices) {
   using TriV = SlabEngine<kTriP, false, kMode>;
   using TriO = SlabEngine<kTriP, true, kMode>;
+  // one set of register-streamed loads feeds all three engines
+  static_assert(TriV::kRegStream && TriO::kRegStream, "slab engines stream through registers");
   constexpr int P = kTriP;
   constexpr int kWarpPts = 32 * P;
   extern __shared__ __align__(128) unsigned char smem[];
@@ -666,12 +666,31 @@ cudaError_t launch(const typename Eng::Params& prm, const TestArgs& a, cudaStrea
 
 }  // namespace
 
+// Polygons with more edges than this run the per-engine kernels even when all
+// three engines are asked for: at n = 32 the fused kernel is 3.6 % faster than
+// the three separate ones (C5), at n = 64 it is within +-3 %, and at n = 256 /
+// 1024 the separate kernels (larger P for the slab engines) win by 5-6 %
+// (profiles/round1_summary.md)
+#ifndef VPIPG_FUSE_MAX_N
+#define VPIPG_FUSE_MAX_N 48
+#endif
+
+bool test_f32_all_plan(const DevTables& t, const TestArgs* a, size_t* smem_out) {
+  constexpr int kWarpPts = 32 * kTriP;
+  const size_t smem = ((size_t)t.slab[0].total / 2 + (size_t)t.slab[1].total / 2 + t.cross.n) *
+                      sizeof(float4);
+  const bool aligned =
+      ((reinterpret_cast<uintptr_t>(a[0].xs) | reinterpret_cast<uintptr_t>(a[0].ys)) & 15) == 0;
+  const uint64_t full_slices = aligned ? a[0].m / kWarpPts : 0;
+  if (smem_out) *smem_out = smem;
+  return t.cross.n <= VPIPG_FUSE_MAX_N && smem <= kSmemTableMax && full_slices >= kWarps;
+}
+
 cudaError_t launch_test_f32_all(const DevTables& t, const TestArgs* a, cudaStream_t stream) {
-  // one set of register-streamed loads feeds all three engines
   using TriV = SlabEngine<kTriP, false>;
   using TriO = SlabEngine<kTriP, true>;
-  static_assert(TriV::kRegStream && TriO::kRegStream, "slab engines stream through registers");
   constexpr int kWarpPts = 32 * kTriP;
+  if (!test_f32_all_plan(t, a, nullptr)) return cudaErrorNotSupported;
   TriParams prm{};
   prm.v = TriV::Params{t.slab[0], t.ox, t.oy};
   prm.o = TriO::Params{t.slab[1], t.ox, t.oy};
@@ -682,10 +701,7 @@ cudaError_t launch_test_f32_all(const DevTables& t, const TestArgs* a, cudaStrea
   prm.off_o = static_cast<uint32_t>(nv);
   prm.off_c = static_cast<uint32_t>(nv + no);
   const size_t smem = (nv + no + nc) * sizeof(float4);
-  const bool aligned =
-      ((reinterpret_cast<uintptr_t>(a[0].xs) | reinterpret_cast<uintptr_t>(a[0].ys)) & 15) == 0;
-  const uint64_t full_slices = aligned ? a[0].m / kWarpPts : 0;
-  if (smem > kSmemTableMax || full_slices < kWarps) return cudaErrorNotSupported;
+  const uint64_t full_slices = a[0].m / kWarpPts;
   int sms = 0, per_sm = 0;
   auto form = [](const SlabTable& t) { return t.cnt[0] == 0 ? 1 : t.cnt[2] == 0 ? 2 : 0; };
   const int fv = form(t.slab[0]), fo = form(t.slab[1]);

@@ -661,3 +661,22 @@ def test_multi_partial_engine_sets_f64_and_missing_outputs(golden):
             for e in (0, 2):
                 bits = np.unpackbits(ws[e].cpu().numpy().view(np.uint8), bitorder="little")[:m]
                 assert cs[e].item() == int(bits.sum()), (dt, e)
+
+
+def test_multi_fused_plan():
+    """vpipg_test_multi_fused reports the route vpipg_test_multi takes: one
+    fused launch for all three engines on float32 batches of polygons with at
+    most 48 edges, per-engine kernels otherwise."""
+    m = 1 << 20
+    xs = torch.zeros(m, dtype=torch.float32, device=DEV)
+    ys = torch.zeros_like(xs)
+    vx, vy = W.c5_polygon(vp.random_convex_polygon)  # 32 edges
+    with vp.PreparedPolygon.prepare(vx, vy, vp.KIND_ALL) as p:
+        assert p.multi_fused(xs, ys)
+        assert not p.multi_fused(xs, ys, (0, 2))
+        assert not p.multi_fused(xs.double(), ys.double())
+        assert not p.multi_fused(xs[:100], ys[:100])      # fewer slices than warps
+        assert not p.multi_fused(xs[1:], ys[1:])          # not 16-byte aligned
+    _, (vx, vy) = W.c3_named("c3x:64")
+    with vp.PreparedPolygon.prepare(vx, vy, vp.KIND_ALL) as p:
+        assert not p.multi_fused(xs, ys)                  # 64 edges: separate kernels are faster
