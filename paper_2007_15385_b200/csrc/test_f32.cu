@@ -533,6 +533,9 @@ __global__ void __launch_bounds__(kThreads, VPIPG_LDG_MINB)
 // turn, each writing its own mask words and count. Same slice schedule and
 // loads as ldg_kernel; the three tables sit side by side in shared memory.
 constexpr int kTriP = VPIPG_CROSS_P;  // the crossing engine's register budget sets P
+#ifndef VPIPG_TRI_TMA
+#define VPIPG_TRI_TMA 0  // 1: points through the per-warp TMA ring instead of direct loads
+#endif
 using TriC = CrossEngine<kTriP>;
 struct TriParams {
   SlabParams v, o;
@@ -553,7 +556,25 @@ __global__ void __launch_bounds__(kThreads, 2)
   constexpr int P = kTriP;
   constexpr int kWarpPts = 32 * P;
   extern __shared__ __align__(128) unsigned char smem[];
+#if VPIPG_TRI_TMA
+  // per-warp TMA ring (as stream_kernel), then barriers, then the tables
+  const int warp_ = threadIdx.x >> 5, lane_ = threadIdx.x & 31;
+  float* ring = reinterpret_cast<float*>(smem) + (size_t)warp_ * kStages * 2 * kWarpPts;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<float*>(smem) +
+                                               (size_t)kWarps * kStages * 2 * kWarpPts);
+  uint64_t* full = bars + warp_ * 2 * kStages;
+  uint64_t* empty = full + kStages;
+  float4* s_tab = reinterpret_cast<float4*>(bars + kWarps * 2 * kStages);
+  if (lane_ == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 32);
+    }
+    mbar_fence_init();
+  }
+#else
   float4* s_tab = reinterpret_cast<float4*>(smem);
+#endif
   TriV::stage(prm.v, s_tab);
   TriO::stage(prm.o, s_tab + prm.off_o);
   TriC::stage(prm.c, s_tab + prm.off_c);
@@ -572,8 +593,43 @@ __global__ void __launch_bounds__(kThreads, 2)
     for (int l = lane; l < 2 * kLines; l += 32)
       prefetch_l2((l < kLines ? xs : ys) + g * kWarpPts + (l % kLines) * 32);
   };
-  prefetch(g0);
   uint32_t cv = 0, co = 0, cc = 0;
+#if VPIPG_TRI_TMA
+  (void)prefetch;
+  uint64_t policy = 0;
+  if (lane == 0) {
+    policy = policy_evict_first();
+    for (int s = 0; s < kStages; ++s) {
+      const uint64_t g = g0 + s * W;
+      if (g >= full_slices) break;
+      mbar_arrive_expect_tx(&full[s], 2u * kWarpPts * sizeof(float));
+      bulk_g2s(ring + s * 2 * kWarpPts, xs + g * kWarpPts, kWarpPts * sizeof(float), &full[s], policy);
+      bulk_g2s(ring + s * 2 * kWarpPts + kWarpPts, ys + g * kWarpPts, kWarpPts * sizeof(float),
+               &full[s], policy);
+    }
+  }
+  uint32_t it = 0;
+  for (uint64_t g = g0; g < full_slices; g += W, ++it) {
+    const uint32_t s = it % kStages, ph = (it / kStages) & 1u;
+    mbar_wait(&full[s], ph);
+    const float* pr = ring + s * 2 * kWarpPts + lane;
+    float x[P], y[P], va[P], vb[P];
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+      x[p] = pr[32 * p];
+      y[p] = pr[kWarpPts + 32 * p];
+    }
+    mbar_arrive(&empty[s]);
+    const uint64_t gn = g + kStages * W;
+    if (lane == 0 && gn < full_slices) {
+      mbar_wait(&empty[s], ph);
+      mbar_arrive_expect_tx(&full[s], 2u * kWarpPts * sizeof(float));
+      bulk_g2s(ring + s * 2 * kWarpPts, xs + gn * kWarpPts, kWarpPts * sizeof(float), &full[s], policy);
+      bulk_g2s(ring + s * 2 * kWarpPts + kWarpPts, ys + gn * kWarpPts, kWarpPts * sizeof(float),
+               &full[s], policy);
+    }
+#else
+  prefetch(g0);
   for (uint64_t g = g0; g < full_slices; g += W) {
     prefetch(g + W);
     const float* px = xs + g * kWarpPts + lane;
@@ -584,6 +640,7 @@ __global__ void __launch_bounds__(kThreads, 2)
       x[p] = __ldcs(px + 32 * p);
       y[p] = __ldcs(py + 32 * p);
     }
+#endif
     TriV::eval(prm.v, tv, x, y, va, vb);
     cv += emit<false, TriV::kVote, P>(va, vb, g * kWarpPts, av, lane);
     TriO::eval(prm.o, to, x, y, va, vb);
@@ -700,7 +757,10 @@ cudaError_t launch_test_f32_all(const DevTables& t, const TestArgs* a, cudaStrea
   const size_t nc = TriC::table_bytes(prm.c) / sizeof(float4);
   prm.off_o = static_cast<uint32_t>(nv);
   prm.off_c = static_cast<uint32_t>(nv + no);
-  const size_t smem = (nv + no + nc) * sizeof(float4);
+  const size_t smem = (nv + no + nc) * sizeof(float4) +
+                      (VPIPG_TRI_TMA ? (size_t)kWarps * kStages * (2 * kWarpPts * sizeof(float) +
+                                                                  2 * sizeof(uint64_t))
+                                     : 0);
   const uint64_t full_slices = a[0].m / kWarpPts;
   int sms = 0, per_sm = 0;
   auto form = [](const SlabTable& t) { return t.cnt[0] == 0 ? 1 : t.cnt[2] == 0 ? 2 : 0; };
