@@ -357,8 +357,8 @@ class JoinJob:
         self.db.test(e, self.xs, self.ys, self.ids, words=words, count=count, stream=stream)
 
     def launch_all(self, words, counts, stream):
-        for e in range(3):
-            self.launch(e, words[e], counts[e], stream)
+        self.db.test_multi(self.xs, self.ys, self.ids, (0, 1, 2), words=words, counts=counts,
+                           stream=stream)
 
     def prepare_host(self):
         t = self.torch
@@ -451,8 +451,11 @@ def main():
     n_edges = job.n_edges
     # the three engines in one kernel that reads every point once (f32, one
     # polygon); the per-engine kernels are still timed below for the breakdown
-    fused = ((not args.separate) and isinstance(job, PolygonJob) and not job.f64
-             and job.poly.multi_fused(job.xs, job.ys))  # the library's own plan (n <= 48, f32)
+    if isinstance(job, JoinJob):  # the join fuses whenever all three engines run
+        fused = not args.separate
+    else:
+        fused = ((not args.separate) and not job.f64
+                 and job.poly.multi_fused(job.xs, job.ys))  # the library's own plan (n <= 48, f32)
 
     kevents = []  # per step, per engine: (start, end) on the launch stream
     sevents = []  # per step: (start, end) around the step's own work, flush excluded

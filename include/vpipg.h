@@ -215,6 +215,17 @@ int vpipg_test_gather(const vpipg_db* db, int engine, const float* xs, const flo
                       const uint32_t* ids, uint64_t m, uint32_t* mask_words, uint8_t* mask_bytes,
                       unsigned long long* d_inside, void* stream);
 
+/* All requested engines over one batch of (point, polygon id) pairs:
+ * mask_words / mask_bytes / d_inside indexed by engine (arrays of 3, entries
+ * may be NULL). With all three engines this is ONE fused kernel that reads
+ * every pair once and walks two polygon blocks per pair instead of three
+ * (sign-of-offset and crossing share the vertex rows); results equal three
+ * vpipg_test_gather calls. Asynchronous on `stream`. */
+int vpipg_test_gather_multi(const vpipg_db* db, uint32_t engines, const float* xs, const float* ys,
+                            const uint32_t* ids, uint64_t m, uint32_t* const* mask_words,
+                            uint8_t* const* mask_bytes, unsigned long long* const* d_inside,
+                            void* stream);
+
 /* The join over HOST buffers (pageable or pinned): every engine in the bit set
  * `engines` over one copy of the pairs, chunked and pipelined like
  * vpipg_test_host_multi (mask_words / mask_bytes / inside indexed by engine,

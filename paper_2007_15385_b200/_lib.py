@@ -54,6 +54,7 @@ SIGNATURES = {
     "vpipg_release_staging": (C.c_int, [C.c_int]),
     "vpipg_test_multi": (C.c_int, [_P, C.c_uint32, C.c_int, _P, _P, C.c_uint64, _P, _P, _P, _P]),
     "vpipg_test_multi_fused": (C.c_int, [_P, C.c_uint32, C.c_int, _P, _P, C.c_uint64]),
+    "vpipg_test_gather_multi": (C.c_int, [_P, C.c_uint32, _P, _P, _P, C.c_uint64, _P, _P, _P, _P]),
     "vpipg_test_gather_host": (C.c_int, [_P, C.c_uint32, _P, _P, _P, C.c_uint64, _P, _P,
                                          C.POINTER(C.c_uint64)]),
     "vpipg_nccl_version": (C.c_int, [C.POINTER(C.c_int)]),

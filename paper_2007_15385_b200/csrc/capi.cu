@@ -488,6 +488,32 @@ int vpipg_test_gather(const vpipg_db* db, int engine, const float* xs, const flo
   return cuda_code(launch_gather(db->t, engine, a, static_cast<cudaStream_t>(stream)));
 }
 
+int vpipg_test_gather_multi(const vpipg_db* db, uint32_t engines, const float* xs, const float* ys,
+                            const uint32_t* ids, uint64_t m, uint32_t* const* mask_words,
+                            uint8_t* const* mask_bytes, unsigned long long* const* d_inside,
+                            void* stream) {
+  if (!db || engines == 0 || (engines & ~7u)) return kInvalid;
+  for (int e = 0; e < 3; ++e) {
+    const uint32_t need = e == 0 ? kKindVoronoi : e == 1 ? kKindOffset : kKindCrossing;
+    if ((engines & (1u << e)) && !(db->kinds & need)) return kInvalid;
+  }
+  if (m == 0) return kOk;
+  if (!xs || !ys || !ids) return kInvalid;
+  DeviceGuard g(db->device);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  GatherArgs a[3];
+  for (int e = 0; e < 3; ++e)
+    a[e] = GatherArgs{xs, ys, ids, m, mask_words ? mask_words[e] : nullptr,
+                      mask_bytes ? mask_bytes[e] : nullptr, d_inside ? d_inside[e] : nullptr};
+  if (engines == 7u) return cuda_code(launch_gather_all(db->t, a, s));
+  for (int e = 0; e < 3; ++e)
+    if (engines & (1u << e)) {
+      const int rc = cuda_code(launch_gather(db->t, e, a[e], s));
+      if (rc) return rc;
+    }
+  return kOk;
+}
+
 int vpipg_fill_join_pairs(uint64_t seed, uint64_t first, uint64_t m, uint32_t npoly,
                           const double* centre_x, const double* centre_y, const double* radius,
                           float* xs, float* ys, uint32_t* ids, void* stream) {

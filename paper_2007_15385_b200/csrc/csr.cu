@@ -106,6 +106,10 @@ __global__ void prep_csr_kernel(CsrPrepArgs a) {
   const bool bad = convex && status != 0;
   const float nbits = __uint_as_float(static_cast<uint32_t>(n) | (bad ? kRangeInvalid : 0u));
   for (float2* t : {a.gen, a.ccw, a.raw}) t[blk] = make_float2(nbits, 0.f);
+  // the raw rows equal the validated ones unless validation reversed or
+  // rejected the polygon (or did not run)
+  if (!convex || bad || rev)
+    a.raw[blk] = make_float2(__uint_as_float(__float_as_uint(nbits) | kRawDiffers), 0.f);
   a.gen[blk + 1] = make_float2(gcx, gcy);
   a.ccw[blk + 1] = make_float2(fcx, fcy);
   a.raw[blk + 1] = make_float2(fcx, fcy);
@@ -118,6 +122,9 @@ __global__ void prep_csr_kernel(CsrPrepArgs a) {
 #define VPIPG_GMINB 8
 #endif
 constexpr int kGP = VPIPG_GP;  // pairs per lane
+#ifndef VPIPG_GMINB_ALL
+#define VPIPG_GMINB_ALL 5  // the fused join keeps two walks' state live: 48 registers (6 CTAs: 7.75 ms, 5: 6.98, 4: 7.27 at C4)
+#endif
 constexpr int kGThreads = 256;
 
 // 32-byte (256-bit) read-only load: four rows (or the header + two rows).
@@ -199,7 +206,7 @@ __global__ void __launch_bounds__(kGThreads, VPIPG_GMINB) gather_kernel(const Db
       // a polygon that failed validation only disables the convex engines: ray
       // crossing takes the raw vertices of any polygon (vpip.cpp:120-128)
       if (kEngine != 2) ok[p] = ok[p] && !(nf & kRangeInvalid);
-      const uint32_t n = nf & ~kRangeInvalid;
+      const uint32_t n = nf & ~(kRangeInvalid | kRawDiffers);
       rows[p] = (ok[p] && n > 0) ? (kEngine == 0 ? n : n + 1) : 0u;
       qx[p] = x - h.v[2];  // exact for points near their polygon (Sterbenz)
       qy[p] = y - h.v[3];
@@ -273,6 +280,126 @@ __global__ void __launch_bounds__(kGThreads, VPIPG_GMINB) gather_kernel(const Db
   if (lane == 0 && a.inside && count) atomicAdd(a.inside, (unsigned long long)count);
 }
 
+// Walk rows 2 .. rows-1 of a block (rows 0 and 1 came with the header load)
+// into one accumulator, or into two that share every row (kBoth: offset +
+// crossing over the same vertex rows).
+template <bool kBoth, class R1, class R2>
+__device__ __forceinline__ void walk(const float2* blk, uint32_t rows, float qx, float qy, R1& r1,
+                                     R2& r2) {
+  uint32_t k = 2;
+  for (; k + 3 < rows; k += 4) {
+    const Rows4 q4 = ld256(blk + k + 2);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      r1.next(qx, qy, q4.v[2 * u], q4.v[2 * u + 1]);
+      if (kBoth) r2.next(qx, qy, q4.v[2 * u], q4.v[2 * u + 1]);
+    }
+  }
+  if (k < rows) {
+    const Rows4 q4 = ld256(blk + k + 2);
+#pragma unroll
+    for (int u = 0; u < 3; ++u)
+      if (k + u < rows) {
+        r1.next(qx, qy, q4.v[2 * u], q4.v[2 * u + 1]);
+        if (kBoth) r2.next(qx, qy, q4.v[2 * u], q4.v[2 * u + 1]);
+      }
+  }
+}
+
+// Fused join: every (point, id) pair is read once and tested by all three
+// engines. Voronoi walks the generator block; sign-of-offset and crossing
+// share ONE walk over the raw vertex rows (the same rows and frame as the
+// validated ones unless the header says kRawDiffers, when offset walks its own
+// block), so a pair touches two polygon blocks instead of three.
+__global__ void __launch_bounds__(kGThreads, VPIPG_GMINB_ALL)
+    gather_all_kernel(const DbTables t, const GatherArgs av, const GatherArgs ao,
+                      const GatherArgs ac) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t gwarp = (uint64_t)blockIdx.x * (kGThreads / 32) + (threadIdx.x >> 5);
+  const uint64_t stride = (uint64_t)gridDim.x * (kGThreads / 32) * 32;
+  uint32_t cnt[3] = {0, 0, 0};
+  for (uint64_t base = gwarp * 32; base < av.m; base += stride) {
+    const uint64_t j = base + lane;
+    bool ok = j < av.m;
+    const uint32_t id = ok ? __ldcs(av.ids + j) : 0u;
+    const float x = ok ? __ldcs(av.xs + j) : 0.f;
+    const float y = ok ? __ldcs(av.ys + j) : 0.f;
+    ok = ok && id < t.npoly;
+    const uint64_t off = (uint64_t)(ok ? id : 0u) * t.stride;
+    bool in[3] = {false, false, false};
+    // ---- Voronoi: generator block, its own frame ----
+    {
+      const float2* blk = t.gen + off;
+      const Rows4 h = ok ? ld256(blk) : Rows4{};
+      const uint32_t nf = __float_as_uint(h.v[0]);
+      const uint32_t n = nf & ~(kRangeInvalid | kRawDiffers);
+      const uint32_t rows = (ok && !(nf & kRangeInvalid)) ? n : 0u;
+      const float qx = x - h.v[2], qy = y - h.v[3];
+      RowAcc<0> r;
+      if (rows > 0) r.first(qx, qy, h.v[4], h.v[5]);
+      if (rows > 1) r.next(qx, qy, h.v[6], h.v[7]);
+      walk<false>(blk, rows, qx, qy, r, r);
+      in[0] = rows > 0 && (qx != qx || qy != qy ? false : r.inside());
+    }
+    // ---- crossing (+ offset when the rows coincide): raw block ----
+    {
+      const float2* blk = t.raw + off;
+      const Rows4 h = ok ? ld256(blk) : Rows4{};
+      const uint32_t nf = __float_as_uint(h.v[0]);
+      const uint32_t n = nf & ~(kRangeInvalid | kRawDiffers);
+      const uint32_t rows = (ok && n > 0) ? n + 1 : 0u;
+      const bool shared = !(nf & kRawDiffers);
+      const float qx = x - h.v[2], qy = y - h.v[3];
+      RowAcc<2> rc;
+      RowAcc<1> ro;
+      if (rows > 0) {
+        rc.first(qx, qy, h.v[4], h.v[5]);
+        ro.first(qx, qy, h.v[4], h.v[5]);
+      }
+      if (rows > 1) {
+        rc.next(qx, qy, h.v[6], h.v[7]);
+        ro.next(qx, qy, h.v[6], h.v[7]);
+      }
+      if (shared)
+        walk<true>(blk, rows, qx, qy, rc, ro);
+      else
+        walk<false>(blk, rows, qx, qy, rc, rc);
+      in[2] = rows > 0 && rc.inside();
+      const bool nan = qx != qx || qy != qy;
+      if (shared) {
+        in[1] = rows > 0 && (nan || ro.inside());
+      } else if (ok && !(nf & kRangeInvalid)) {
+        // reversed by validation: offset walks the validated (CCW) rows
+        const float2* cb = t.ccw + off;
+        const Rows4 hc = ld256(cb);
+        const float cx = x - hc.v[2], cy = y - hc.v[3];
+        RowAcc<1> r;
+        r.first(cx, cy, hc.v[4], hc.v[5]);
+        if (rows > 1) r.next(cx, cy, hc.v[6], hc.v[7]);
+        walk<false>(cb, rows, cx, cy, r, r);
+        in[1] = rows > 0 && (nan || r.inside());
+      }
+    }
+    const GatherArgs* args[3] = {&av, &ao, &ac};
+#pragma unroll
+    for (int e = 0; e < 3; ++e) {
+      const GatherArgs& a = *args[e];
+      const uint32_t w = __ballot_sync(0xffffffffu, in[e]);
+      cnt[e] += in[e];
+      if (a.words && lane == 0) a.words[base >> 5] = w;
+      if (a.bytes && j < a.m) a.bytes[j] = in[e] ? 1 : 0;
+    }
+  }
+  const GatherArgs* args[3] = {&av, &ao, &ac};
+#pragma unroll
+  for (int e = 0; e < 3; ++e) {
+    uint32_t c = cnt[e];
+#pragma unroll
+    for (int s = 16; s > 0; s >>= 1) c += __shfl_xor_sync(0xffffffffu, c, s);
+    if (lane == 0 && args[e]->inside && c) atomicAdd(args[e]->inside, (unsigned long long)c);
+  }
+}
+
 __device__ __forceinline__ uint64_t mix_seed(uint64_t seed, uint64_t salt) {
   uint64_t z = seed + 0x9e3779b97f4a7c15ULL * (salt + 1);
   z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
@@ -325,6 +452,19 @@ cudaError_t launch_gather(const DbTables& t, int engine, const GatherArgs& a, cu
     case 1: gather_kernel<1><<<grid, kGThreads, 0, stream>>>(t, a); break;
     default: gather_kernel<2><<<grid, kGThreads, 0, stream>>>(t, a); break;
   }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gather_all(const DbTables& t, const GatherArgs* a, cudaStream_t stream) {
+  if (a[0].m == 0) return cudaSuccess;
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const uint64_t warps = (a[0].m + 31) / 32;
+  const uint64_t blocks = (warps + kGThreads / 32 - 1) / (kGThreads / 32);
+  const uint64_t cap = (uint64_t)sms * VPIPG_GMINB_ALL;
+  const int grid = static_cast<int>(blocks < cap ? blocks : cap);
+  gather_all_kernel<<<grid, kGThreads, 0, stream>>>(t, a[0], a[1], a[2]);
   return cudaGetLastError();
 }
 

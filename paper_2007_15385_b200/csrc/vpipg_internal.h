@@ -39,6 +39,10 @@ struct TestArgs {
 
 // ---- polygon database (CSR batch of polygons; csr.cu) ----
 constexpr uint32_t kRangeInvalid = 0x80000000u;  // polygon failed validation: tests outside
+// set in the crossing block's header when its rows differ from the offset
+// block's (validation reversed or rejected the polygon): the fused join then
+// cannot evaluate both engines from one pass over the raw rows
+constexpr uint32_t kRawDiffers = 0x40000000u;
 
 // Gather tables are compact, polygon-local, fixed-stride blocks: polygon i
 // owns `stride` float2 slots starting at slot i * stride (32-byte aligned):
@@ -88,6 +92,8 @@ struct GatherArgs {
 cudaError_t launch_prep(const PrepArgs& args, cudaStream_t stream);
 cudaError_t launch_prep_csr(const CsrPrepArgs& args, cudaStream_t stream);
 cudaError_t launch_gather(const DbTables& t, int engine, const GatherArgs& a, cudaStream_t stream);
+// all three engines per pair in one pass (a[0..2] share xs, ys, ids, m)
+cudaError_t launch_gather_all(const DbTables& t, const GatherArgs* a, cudaStream_t stream);
 cudaError_t launch_fill_pairs(uint64_t seed, uint64_t first, uint64_t m, uint32_t npoly,
                               const double* cx, const double* cy, const double* rad, float* xs,
                               float* ys, uint32_t* ids, cudaStream_t stream);

@@ -287,6 +287,28 @@ class PolygonDB:
                                        xs.numel(), ptr(words), ptr(bytes_), ptr(count),
                                        _stream_ptr(stream)), "vpipg_test_gather")
 
+    def test_multi(self, xs, ys, ids, engines=(0, 1, 2), words=None, bytes_=None, counts=None,
+                   stream=None) -> None:
+        """Several engines over one batch of device pairs (vpipg_test_gather_multi):
+        words / bytes_ / counts are lists of 3 (entries may be None). All three
+        engines run as one fused kernel. Asynchronous."""
+        import torch
+        m = xs.numel()
+        outs = []
+        for lst, need in ((words, (m + 31) // 32), (bytes_, m), (counts, 1)):
+            for t in (lst or []):
+                outs.append((t, need))
+        _check_device_batch(xs, ys, (torch.float32,), outs, ids=ids)
+        mask = 0
+        for e in engines:
+            mask |= 1 << _engine_id(e)
+        arr = lambda lst: (C.c_void_p * 3)(*[C.c_void_p(t.data_ptr() if t is not None else None)
+                                             for t in (lst or [None] * 3)])
+        check(load().vpipg_test_gather_multi(self._h, mask, C.c_void_p(xs.data_ptr()),
+                                             C.c_void_p(ys.data_ptr()), C.c_void_p(ids.data_ptr()),
+                                             m, arr(words), arr(bytes_), arr(counts),
+                                             _stream_ptr(stream)), "vpipg_test_gather_multi")
+
     def test_host(self, xs, ys, ids, engines=(0, 1, 2), words=None, counts_only: bool = False):
         """The join over host buffers (vpipg_test_gather_host): float32 xs / ys and
         uint32 / int32 ids, numpy arrays or (pinned) CPU tensors. Returns

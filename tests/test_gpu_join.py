@@ -227,3 +227,64 @@ def test_gather_host_buffers_equal_device_path(orc):
             words, cnt = db.test_host(*args, (0, 1, 2))
             for e in range(3):
                 assert np.array_equal(words[e], ref[e][0]) and cnt[e] == ref[e][1], e
+
+
+@pytest.mark.parametrize("m", [1, 33, 4099, 1 << 20])
+def test_fused_join_equals_separate_engines(m):
+    """vpipg_test_gather_multi with all three engines (one fused kernel: offset
+    and crossing share one walk over the vertex rows unless validation reversed
+    or rejected the polygon) gives exactly the words, bytes and counts of three
+    vpipg_test_gather calls -- on a database with the reference's error cases
+    and a clockwise (reversed) polygon, out-of-range ids and NaN points."""
+    off, vx, vy, cx, cy, r = _db_inputs(2048)
+    npoly = off.size - 1
+    dcx, dcy, dr = (torch.as_tensor(a, device=DEV) for a in (cx, cy, r))
+    xs = torch.empty(m, dtype=torch.float32, device=DEV)
+    ys = torch.empty_like(xs)
+    ids = torch.empty(m, dtype=torch.int32, device=DEV)
+    vp.fill_join_pairs(W.c4_pair_seed(), 0, xs, ys, ids, dcx, dcy, dr)
+    if m > 64:  # aim some pairs at the injected polygons, past the table, and at NaN
+        k = torch.arange(0, m, 97, device=DEV)
+        ids[k] = torch.as_tensor((npoly - 6 + (np.arange(k.numel()) % 8)).astype(np.int32),
+                                 device=DEV)
+        xs[k[::5]] = float("nan")
+    nw = (m + 31) // 32
+    with vp.PolygonDB.prepare(off, vx, vy, vp.KIND_ALL) as db:
+        ref = []
+        for e in range(3):
+            w = torch.zeros(nw, dtype=torch.int32, device=DEV)
+            b = torch.zeros(m, dtype=torch.uint8, device=DEV)
+            c = torch.zeros(1, dtype=torch.int64, device=DEV)
+            db.test(e, xs, ys, ids, words=w, bytes_=b, count=c)
+            ref.append((w, b, c))
+        ws = [torch.zeros(nw, dtype=torch.int32, device=DEV) for _ in range(3)]
+        bs = [torch.zeros(m, dtype=torch.uint8, device=DEV) for _ in range(3)]
+        cs = [torch.zeros(1, dtype=torch.int64, device=DEV) for _ in range(3)]
+        db.test_multi(xs, ys, ids, (0, 1, 2), words=ws, bytes_=bs, counts=cs)
+        torch.cuda.synchronize()
+        for e in range(3):
+            assert torch.equal(ws[e], ref[e][0]) and torch.equal(bs[e], ref[e][1]), e
+            assert cs[e].item() == ref[e][2].item(), e
+
+
+def test_fused_join_on_the_c4_database(orc):
+    """The real C4 database and 2^22 pairs: the fused join equals the separate
+    gather kernels (which test_c4_config_gather_vs_oracle holds to the oracle)."""
+    off, vx, vy, cx, cy, r = W.c4_polygons(vp.random_convex_polygon)
+    m = 1 << 22
+    dcx, dcy, dr = (torch.as_tensor(a, device=DEV) for a in (cx, cy, r))
+    xs = torch.empty(m, dtype=torch.float32, device=DEV)
+    ys = torch.empty_like(xs)
+    ids = torch.empty(m, dtype=torch.int32, device=DEV)
+    vp.fill_join_pairs(W.c4_pair_seed(), 12345, xs, ys, ids, dcx, dcy, dr)
+    nw = (m + 31) // 32
+    with vp.PolygonDB.prepare(off, vx, vy, vp.KIND_ALL) as db:
+        ws = [torch.zeros(nw, dtype=torch.int32, device=DEV) for _ in range(3)]
+        cs = [torch.zeros(1, dtype=torch.int64, device=DEV) for _ in range(3)]
+        db.test_multi(xs, ys, ids, words=ws, counts=cs)
+        for e in range(3):
+            w = torch.zeros(nw, dtype=torch.int32, device=DEV)
+            c = torch.zeros(1, dtype=torch.int64, device=DEV)
+            db.test(e, xs, ys, ids, words=w, count=c)
+            torch.cuda.synchronize()
+            assert torch.equal(ws[e], w) and cs[e].item() == c.item(), e

@@ -25,12 +25,19 @@ python tools/ncu_summary.py gpurun_out/full_fused_$tag.ncu-rep \
     --label "ncu --set full --clock-control none, C5, the fused three-engine kernel of the first timed step of \`$B\`" \
     --names fused --points 2147483648 --bytes-per-point 8.375 --merge \
     --out gpurun_out/ncu_full_${tag}_c5.json --traffic gpurun_out/traffic_$tag.json --key c5
-$B --workload c4 > gpurun_out/plain_c4_$tag.log 2>&1 && \
+$B --workload c4 --separate > gpurun_out/plain_c4_$tag.log 2>&1 && \
 ncu --set full --clock-control none --import-source on -k regex:gather_kernel -s 9 -c 3 \
-    -o gpurun_out/full_c4_$tag $B --workload c4 > gpurun_out/full_c4_$tag.log 2>&1 && \
+    -o gpurun_out/full_c4_$tag $B --workload c4 --separate > gpurun_out/full_c4_$tag.log 2>&1 && \
 python tools/ncu_summary.py gpurun_out/full_c4_$tag.ncu-rep \
-    --label "ncu --set full --clock-control none, C4 (65536 polygons, 2^28 pairs), the three kernels of the first timed step of \`$B --workload c4\`" \
+    --label "ncu --set full --clock-control none, C4 (65536 polygons, 2^28 pairs), the three per-engine kernels of the first timed step of \`$B --workload c4 --separate\`" \
     --names voronoi,sign_of_offset,ray_crossing --points 268435456 --bytes-per-point 12.125 \
     --out gpurun_out/ncu_full_${tag}_c4.json --traffic gpurun_out/traffic_$tag.json --key c4
-tail -n 2 gpurun_out/full_$tag.log gpurun_out/full_fused_$tag.log gpurun_out/full_c4_$tag.log
+$B --workload c4 > gpurun_out/plain_c4_fused_$tag.log 2>&1 && \
+ncu --set full --clock-control none --import-source on -k regex:gather_all_kernel -s 3 -c 1 \
+    -o gpurun_out/full_c4_fused_$tag $B --workload c4 > gpurun_out/full_c4_fused_$tag.log 2>&1 && \
+python tools/ncu_summary.py gpurun_out/full_c4_fused_$tag.ncu-rep \
+    --label "ncu --set full --clock-control none, C4, the fused three-engine join kernel of the first timed step of \`$B --workload c4\`" \
+    --names fused --points 268435456 --bytes-per-point 12.375 --merge \
+    --out gpurun_out/ncu_full_${tag}_c4.json --traffic gpurun_out/traffic_$tag.json --key c4
+tail -n 2 gpurun_out/full_$tag.log gpurun_out/full_fused_$tag.log gpurun_out/full_c4_$tag.log gpurun_out/full_c4_fused_$tag.log
 cat gpurun_out/bench_$tag.json
