@@ -8,11 +8,13 @@ Headline workload (BASELINE.json configs[4], the config the metric "at
 contiguous) over the ranks. One step = all three engines (Voronoi,
 sign-of-offset, ray-crossing) over every point + one NCCL all-reduce of the
 three inside counts. The three engines run as one fused kernel that reads
-each point once and writes three masks and counts (vpipg_test_multi);
+each point once and writes three masks and counts (vpipg_test_multi; for the
+C4 join vpipg_test_gather_multi) when the library's plan takes it;
 `--separate` launches the three per-engine kernels instead, and the line's
-`engines_separate` always reports their times for the per-engine roofline. value = 3 * 2^31 point-polygon tests per step / step
-time (max over ranks, CUDA events). Inputs (17 GB at N=1) are far larger than
-L2, so no flush is needed between steps.
+`engines_separate` always reports their times for the per-engine roofline.
+value = 3 * 2^31 point-polygon tests per step / step time (max over ranks,
+CUDA events). Inputs (17 GB at N=1) are far larger than L2, so no flush is
+needed between steps.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
                     [--workload c5|c2|c3:<n>|c3x:<n>|c4|c1] [--separate]
