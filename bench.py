@@ -456,8 +456,7 @@ def main():
     if isinstance(job, JoinJob):  # the join fuses whenever all three engines run
         fused = not args.separate
     else:
-        fused = ((not args.separate) and not job.f64
-                 and job.poly.multi_fused(job.xs, job.ys))  # the library's own plan (n <= 48, f32)
+        fused = (not args.separate) and job.poly.multi_fused(job.xs, job.ys)  # the library's plan
 
     kevents = []  # per step, per engine: (start, end) on the launch stream
     sevents = []  # per step: (start, end) around the step's own work, flush excluded

@@ -346,10 +346,12 @@ int vpipg_test_multi(const vpipg_poly* p, uint32_t engines, int dtype, const voi
   for (int e = 0; e < 3; ++e)
     a[e] = TestArgs{xs, ys, m, mask_words ? mask_words[e] : nullptr,
                     mask_bytes ? mask_bytes[e] : nullptr, d_inside ? d_inside[e] : nullptr};
-  if (engines == 7u && dtype == VPIPG_F32 && (p->kinds & VPIPG_KIND_ALL) == VPIPG_KIND_ALL && m > 0 &&
-      xs && ys) {
-    const cudaError_t e = launch_test_f32_all(p->t, a, s);
-    if (e != cudaErrorNotSupported) return cuda_code(e);
+  if (engines == 7u && (p->kinds & VPIPG_KIND_ALL) == VPIPG_KIND_ALL && m > 0 && xs && ys) {
+    if (dtype == VPIPG_F64) return cuda_code(launch_test_f64_all(p->t, a, s));
+    if (dtype == VPIPG_F32) {
+      const cudaError_t e = launch_test_f32_all(p->t, a, s);
+      if (e != cudaErrorNotSupported) return cuda_code(e);
+    }
   }
   for (int e = 0; e < 3; ++e)  // one engine at a time
     if (engines & (1u << e)) {
@@ -361,9 +363,10 @@ int vpipg_test_multi(const vpipg_poly* p, uint32_t engines, int dtype, const voi
 
 int vpipg_test_multi_fused(const vpipg_poly* p, uint32_t engines, int dtype, const void* xs,
                            const void* ys, uint64_t m) {
-  if (!p || engines != 7u || dtype != VPIPG_F32 || (p->kinds & VPIPG_KIND_ALL) != VPIPG_KIND_ALL ||
-      m == 0 || !xs || !ys)
+  if (!p || engines != 7u || (p->kinds & VPIPG_KIND_ALL) != VPIPG_KIND_ALL || m == 0 || !xs || !ys)
     return 0;
+  if (dtype == VPIPG_F64) return 1;  // the exact kernels fuse at any n
+  if (dtype != VPIPG_F32) return 0;
   TestArgs a[3];
   for (auto& x : a) x = TestArgs{xs, ys, m, nullptr, nullptr, nullptr};
   return test_f32_all_plan(p->t, a, nullptr) ? 1 : 0;

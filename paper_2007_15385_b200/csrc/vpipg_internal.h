@@ -101,6 +101,8 @@ cudaError_t launch_test_f32(const DevTables& t, int engine, const TestArgs& a, c
 // all three engines in one fused pass over the points (a[0..2] share xs, ys,
 // m); cudaErrorNotSupported when the tables or the batch do not fit its plan
 cudaError_t launch_test_f32_all(const DevTables& t, const TestArgs* a, cudaStream_t stream);
+// fp64: all three engines in one pass (reference-exact, any n)
+cudaError_t launch_test_f64_all(const DevTables& t, const TestArgs* a, cudaStream_t stream);
 // whether launch_test_f32_all takes this batch as one fused launch
 bool test_f32_all_plan(const DevTables& t, const TestArgs* a, size_t* smem);
 cudaError_t launch_test_f64(const DevTables& t, int engine, const TestArgs& a, cudaStream_t stream);

@@ -666,7 +666,7 @@ def test_multi_partial_engine_sets_f64_and_missing_outputs(golden):
 def test_multi_fused_plan():
     """vpipg_test_multi_fused reports the route vpipg_test_multi takes: one
     fused launch for all three engines on float32 batches of polygons with at
-    most 48 edges, per-engine kernels otherwise."""
+    most 48 edges and on any float64 batch, per-engine kernels otherwise."""
     m = 1 << 20
     xs = torch.zeros(m, dtype=torch.float32, device=DEV)
     ys = torch.zeros_like(xs)
@@ -674,9 +674,32 @@ def test_multi_fused_plan():
     with vp.PreparedPolygon.prepare(vx, vy, vp.KIND_ALL) as p:
         assert p.multi_fused(xs, ys)
         assert not p.multi_fused(xs, ys, (0, 2))
-        assert not p.multi_fused(xs.double(), ys.double())
+        assert p.multi_fused(xs.double(), ys.double())       # the exact f64 kernels fuse at any n
         assert not p.multi_fused(xs[:100], ys[:100])      # fewer slices than warps
         assert not p.multi_fused(xs[1:], ys[1:])          # not 16-byte aligned
     _, (vx, vy) = W.c3_named("c3x:64")
     with vp.PreparedPolygon.prepare(vx, vy, vp.KIND_ALL) as p:
         assert not p.multi_fused(xs, ys)                  # 64 edges: separate kernels are faster
+
+
+@pytest.mark.parametrize("m", [7, 4099, (1 << 20) + 3])
+def test_fused_f64_pass_is_reference_exact(golden, orc, m):
+    """All three engines on float64 points in one fused exact kernel: masks and
+    counts equal the separate exact kernels and the oracle, bit for bit."""
+    vx, vy = golden["conv_c1_v"]
+    xs, ys = orc.sample_points(m, W.C1_BOX, 99)
+    want = orc.masks(vx, vy, xs, ys)
+    xt, yt = torch.as_tensor(xs, device=DEV), torch.as_tensor(ys, device=DEV)
+    nw = (m + 31) // 32
+    with vp.PreparedPolygon.prepare(vx, vy, vp.KIND_ALL) as p:
+        assert p.multi_fused(xt, yt)
+        ws = [torch.zeros(nw, dtype=torch.int32, device=DEV) for _ in range(3)]
+        bs = [torch.zeros(m, dtype=torch.uint8, device=DEV) for _ in range(3)]
+        cs = [torch.zeros(1, dtype=torch.int64, device=DEV) for _ in range(3)]
+        p.test_multi(xt, yt, words=ws, bytes_=bs, counts=cs)
+        torch.cuda.synchronize()
+        for e in range(3):
+            got = bs[e].cpu().numpy()
+            assert np.array_equal(got, want[e]), e
+            assert np.array_equal(words_to_mask(ws[e].cpu().numpy().view(np.uint32), m), got)
+            assert cs[e].item() == int(want[e].sum())
