@@ -116,10 +116,11 @@ int vpipg_test(const vpipg_poly* poly, int engine, int dtype, const void* xs, co
 
 /* Several engines over one device batch: mask_words / mask_bytes / d_inside
  * indexed by engine (arrays of 3, entries may be NULL). With all three engines
- * on float32 points (see vpipg_test_multi_fused for the exact plan) this is
- * ONE fused kernel that reads every point once and tests it under Voronoi,
- * sign-of-offset and crossing in turn; otherwise the engines run one after
- * another. The masks and counts equal three vpipg_test calls either way. */
+ * (float64 points, or float32 within the plan vpipg_test_multi_fused reports)
+ * this is ONE fused kernel that reads every point once and tests it under
+ * Voronoi, sign-of-offset and crossing in turn; otherwise the engines run one
+ * after another. The masks and counts equal three vpipg_test calls either way
+ * (bit-identical to the reference for float64). */
 int vpipg_test_multi(const vpipg_poly* poly, uint32_t engines, int dtype, const void* xs,
                      const void* ys, uint64_t m, uint32_t* const* mask_words,
                      uint8_t* const* mask_bytes, unsigned long long* const* d_inside,
