@@ -283,10 +283,12 @@ __global__ void __launch_bounds__(kPrepThreads) prep_kernel(PrepArgs a) {
       r.pad_ = 0;
       a.ray[e] = r;
       // fp32 crossing record for vertex i (edge j -> i)
-      const float xl = static_cast<float>(ux - ox);
-      const float yl = static_cast<float>(uy - oy);
+      // (u.x, u.y, dvx/dvy, w.x) in the local frame; w.x is rounded exactly
+      // as vertex j's own .x, so either loop form of the kernel sees the
+      // same g for a vertex
       const float bk = (dvy != 0.0) ? static_cast<float>(dvx / dvy) : 0.f;
-      a.cross_vert[i] = make_float4(xl, yl, bk, 0.f);
+      a.cross_vert[i] = make_float4(static_cast<float>(ux - ox), static_cast<float>(uy - oy), bk,
+                                    static_cast<float>(wx - ox));
     }
   }
   // ---- band metric lines: edge k (v[k] -> v[k+1]) of the validated vertices,

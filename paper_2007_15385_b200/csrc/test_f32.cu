@@ -23,6 +23,7 @@
 // memory and read with warp-uniform 16-byte broadcasts. generic_kernel handles
 // unaligned inputs with guarded direct loads.
 #include <cstdint>
+#include <type_traits>
 
 #include "tma_pipe.cuh"
 #include "vpipg_device.cuh"
@@ -204,7 +205,12 @@ struct SlabEngine {
 // Points exactly on an edge line lie inside the 1e-5 parity band, so the
 // reference's closed-boundary latch (engines.cpp:194-196) is repeated only by
 // the exact f64 kernel.
-template <int P>
+struct CrossParams {
+  CrossTable tab;
+  float ox, oy;
+};
+
+template <int P, bool kGroupForm = false>
 struct CrossEngine {
   static constexpr int kP = P;
   static constexpr int kVote = VPIPG_CROSS_VOTE;  // 2: a holds the parity word, sign bit = inside
@@ -212,15 +218,41 @@ struct CrossEngine {
 #define VPIPG_CROSS_LDG 0
 #endif
   static constexpr bool kRegStream = VPIPG_CROSS_LDG;  // 0: stream_kernel (TMA ring)
-  struct Params {
-    CrossTable tab;
-    float ox, oy;
-  };
+  using Params = CrossParams;  // shared by both loop forms
   static size_t table_bytes(const Params& p) { return (size_t)p.tab.n * sizeof(float4); }
   __device__ static const float4* global_table(const Params& p) { return p.tab.vert; }
 
   __device__ static void stage(const Params& p, float4* s) {
     for (uint32_t i = threadIdx.x; i < p.tab.n; i += blockDim.x) s[i] = p.tab.vert[i];
+  }
+
+  // E consecutive edges: the crossing bits t_e = (H_e ^ H_{e-1}) & ~D_e,
+  // XOR-reduced in pairs (one LOP3 folds two bits into the parity word);
+  // hp carries h of the group's start vertex in and of its last vertex out
+  template <int E>
+  __device__ __forceinline__ static void group(const float4* v, const float (&x)[P],
+                                               const float (&y)[P], float (&hp)[P],
+                                               uint32_t (&par)[P]) {
+    float4 r[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) r[e] = v[e];
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+      float h0 = hp[p];
+      uint32_t t[E];
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        const float h = y[p] - r[e].y;
+        t[e] = (__float_as_uint(h) ^ __float_as_uint(h0)) & ~__float_as_uint(fmaf(h0, r[e].z, r[e].w - x[p]));
+        h0 = h;
+      }
+      uint32_t acc = par[p];
+#pragma unroll
+      for (int e = 0; e + 1 < E; e += 2) acc ^= t[e] ^ t[e + 1];
+      if (E & 1) acc ^= t[E - 1];
+      par[p] = acc;
+      hp[p] = h0;
+    }
   }
 
   // a[p] = +1 (odd crossing parity: inside) or -1 (even: outside), b[p] = 0
@@ -231,57 +263,78 @@ struct CrossEngine {
     uint32_t par[P];
 #pragma unroll
     for (int p = 0; p < P; ++p) par[p] = 0;
+    // record k = (u.x, u.y, dvx/dvy, w.x) of edge w = v[k-1] -> u = v[k]
+    // (prep.cu); two loop forms, separate kernel instantiations picked per
+    // polygon by the launcher (kCrossGroupMaxN), measured on B200:
+    //  - kGroupForm: 4-edge groups taking g = w.x - qx from the edge's own
+    //    record (.w), only h carried between groups (no per-slice g
+    //    preamble); the fused pass at n <= 16: 4-6 % faster at n = 4 / 8 /
+    //    16 and on C2
+    //  - otherwise h and g are both carried across 4-edge iterations, g
+    //    formed from the previous vertex (.x) (2-5 % faster from n = 24 up;
+    //    both forms in one kernel made either path slower)
     if (n > 0) {
       const float4 last = s[n - 1];
-      float hp[P], gp[P];
+      float hp[P];
 #pragma unroll
-      for (int p = 0; p < P; ++p) {
-        hp[p] = y[p] - last.y;
-        gp[p] = last.x - x[p];
-      }
-      uint32_t k = 0;
-      VPIPG_UNROLL(VPIPG_CROSS_UNROLL)
-      for (; k + 3 < n; k += 4) {
-        const float4 v0 = s[k], v1 = s[k + 1], v2 = s[k + 2], v3 = s[k + 3];
-#pragma unroll
-        for (int p = 0; p < P; ++p) {
-          const float h0 = y[p] - v0.y, g0 = v0.x - x[p];
-          const float h1 = y[p] - v1.y, g1 = v1.x - x[p];
-          const float h2 = y[p] - v2.y, g2 = v2.x - x[p];
-          const float h3 = y[p] - v3.y;
-          const uint32_t t0 = (__float_as_uint(h0) ^ __float_as_uint(hp[p])) & ~__float_as_uint(fmaf(hp[p], v0.z, gp[p]));
-          const uint32_t t1 = (__float_as_uint(h1) ^ __float_as_uint(h0)) & ~__float_as_uint(fmaf(h0, v1.z, g0));
-          const uint32_t t2 = (__float_as_uint(h2) ^ __float_as_uint(h1)) & ~__float_as_uint(fmaf(h1, v2.z, g1));
-          const uint32_t t3 = (__float_as_uint(h3) ^ __float_as_uint(h2)) & ~__float_as_uint(fmaf(h2, v3.z, g2));
-          par[p] ^= t0 ^ t1 ^ t2 ^ t3;
-          hp[p] = h3;
-          gp[p] = v3.x - x[p];
-        }
-      }
+      for (int p = 0; p < P; ++p) hp[p] = y[p] - last.y;
+      if constexpr (kGroupForm) {
+        uint32_t k = 0;
 #pragma unroll 1
-      for (; k + 1 < n; k += 2) {
-        const float4 v0 = s[k], v1 = s[k + 1];
-#pragma unroll
-        for (int p = 0; p < P; ++p) {
-          const float h0 = y[p] - v0.y;
-          const float d0 = fmaf(hp[p], v0.z, gp[p]);
-          const float g0 = v0.x - x[p];
-          const float h1 = y[p] - v1.y;
-          const float d1 = fmaf(h0, v1.z, g0);
-          const uint32_t t0 = (__float_as_uint(h0) ^ __float_as_uint(hp[p])) & ~__float_as_uint(d0);
-          const uint32_t t1 = (__float_as_uint(h1) ^ __float_as_uint(h0)) & ~__float_as_uint(d1);
-          par[p] ^= t0 ^ t1;
-          hp[p] = h1;
-          gp[p] = v1.x - x[p];
+        for (; k + 4 <= n; k += 4) group<4>(s + k, x, y, hp, par);
+        if (k + 2 <= n) {
+          group<2>(s + k, x, y, hp, par);
+          k += 2;
         }
-      }
-      if (k < n) {
-        const float4 v0 = s[k];
+        if (k < n) group<1>(s + k, x, y, hp, par);
+      } else {
+        float gp[P];
 #pragma unroll
-        for (int p = 0; p < P; ++p) {
-          const float h0 = y[p] - v0.y;
-          const float d0 = fmaf(hp[p], v0.z, gp[p]);
-          par[p] ^= (__float_as_uint(h0) ^ __float_as_uint(hp[p])) & ~__float_as_uint(d0);
+        for (int p = 0; p < P; ++p) gp[p] = last.x - x[p];
+        uint32_t k = 0;
+        VPIPG_UNROLL(VPIPG_CROSS_UNROLL)
+        for (; k + 3 < n; k += 4) {
+          const float4 v0 = s[k], v1 = s[k + 1], v2 = s[k + 2], v3 = s[k + 3];
+#pragma unroll
+          for (int p = 0; p < P; ++p) {
+            const float h0 = y[p] - v0.y, g0 = v0.x - x[p];
+            const float h1 = y[p] - v1.y, g1 = v1.x - x[p];
+            const float h2 = y[p] - v2.y, g2 = v2.x - x[p];
+            const float h3 = y[p] - v3.y;
+            const uint32_t t0 = (__float_as_uint(h0) ^ __float_as_uint(hp[p])) & ~__float_as_uint(fmaf(hp[p], v0.z, gp[p]));
+            const uint32_t t1 = (__float_as_uint(h1) ^ __float_as_uint(h0)) & ~__float_as_uint(fmaf(h0, v1.z, g0));
+            const uint32_t t2 = (__float_as_uint(h2) ^ __float_as_uint(h1)) & ~__float_as_uint(fmaf(h1, v2.z, g1));
+            const uint32_t t3 = (__float_as_uint(h3) ^ __float_as_uint(h2)) & ~__float_as_uint(fmaf(h2, v3.z, g2));
+            par[p] ^= t0 ^ t1 ^ t2 ^ t3;
+            hp[p] = h3;
+            gp[p] = v3.x - x[p];
+          }
+        }
+#pragma unroll 1
+        for (; k + 1 < n; k += 2) {
+          const float4 v0 = s[k], v1 = s[k + 1];
+#pragma unroll
+          for (int p = 0; p < P; ++p) {
+            const float h0 = y[p] - v0.y;
+            const float d0 = fmaf(hp[p], v0.z, gp[p]);
+            const float g0 = v0.x - x[p];
+            const float h1 = y[p] - v1.y;
+            const float d1 = fmaf(h0, v1.z, g0);
+            const uint32_t t0 = (__float_as_uint(h0) ^ __float_as_uint(hp[p])) & ~__float_as_uint(d0);
+            const uint32_t t1 = (__float_as_uint(h1) ^ __float_as_uint(h0)) & ~__float_as_uint(d1);
+            par[p] ^= t0 ^ t1;
+            hp[p] = h1;
+            gp[p] = v1.x - x[p];
+          }
+        }
+        if (k < n) {
+          const float4 v0 = s[k];
+#pragma unroll
+          for (int p = 0; p < P; ++p) {
+            const float h0 = y[p] - v0.y;
+            const float d0 = fmaf(hp[p], v0.z, gp[p]);
+            par[p] ^= (__float_as_uint(h0) ^ __float_as_uint(hp[p])) & ~__float_as_uint(d0);
+          }
         }
       }
     }
@@ -536,21 +589,21 @@ constexpr int kTriP = VPIPG_CROSS_P;  // the crossing engine's register budget s
 #ifndef VPIPG_TRI_TMA
 #define VPIPG_TRI_TMA 0  // 1: points through the per-warp TMA ring instead of direct loads
 #endif
-using TriC = CrossEngine<kTriP>;
 struct TriParams {
   SlabParams v, o;
-  TriC::Params c;
+  CrossParams c;
   uint32_t off_o, off_c;  // float4 offsets of the offset / crossing tables in shared memory
 };
 
 // kMode: the slab table form shared by the Voronoi and offset tables (their
 // lines coincide: each bisector is the edge line), -1 when they differ
-template <int kMode>
+template <int kMode, bool kGroupForm>
 __global__ void __launch_bounds__(kThreads, 2)
     tri_kernel(const TriParams prm, const TestArgs av, const TestArgs ao, const TestArgs ac,
                const uint64_t full_slices) {
   using TriV = SlabEngine<kTriP, false, kMode>;
   using TriO = SlabEngine<kTriP, true, kMode>;
+  using TriC = CrossEngine<kTriP, kGroupForm>;
   // one set of register-streamed loads feeds all three engines
   static_assert(TriV::kRegStream && TriO::kRegStream, "slab engines stream through registers");
   constexpr int P = kTriP;
@@ -682,6 +735,14 @@ __global__ void __launch_bounds__(kThreads) generic_kernel(const typename Eng::P
 
 constexpr size_t kSmemTableMax = 96 * 1024;
 
+// in the fused pass, polygons up to this many edges run the crossing engine's
+// 4-edge group form (CrossEngine<P, true>), larger ones the carried form
+// (measured, see CrossEngine::eval)
+#ifndef VPIPG_CROSS_GROUP_MAX_N
+#define VPIPG_CROSS_GROUP_MAX_N 16
+#endif
+constexpr uint32_t kCrossGroupMaxN = VPIPG_CROSS_GROUP_MAX_N;
+
 template <class Eng>
 cudaError_t launch(const typename Eng::Params& prm, const TestArgs& a, cudaStream_t stream) {
   constexpr int kWarpPts = 32 * Eng::kP;
@@ -751,10 +812,10 @@ cudaError_t launch_test_f32_all(const DevTables& t, const TestArgs* a, cudaStrea
   TriParams prm{};
   prm.v = TriV::Params{t.slab[0], t.ox, t.oy};
   prm.o = TriO::Params{t.slab[1], t.ox, t.oy};
-  prm.c = TriC::Params{t.cross, t.ox, t.oy};
+  prm.c = CrossParams{t.cross, t.ox, t.oy};
   const size_t nv = TriV::table_bytes(prm.v) / sizeof(float4);
   const size_t no = TriO::table_bytes(prm.o) / sizeof(float4);
-  const size_t nc = TriC::table_bytes(prm.c) / sizeof(float4);
+  const size_t nc = CrossEngine<kTriP>::table_bytes(prm.c) / sizeof(float4);
   prm.off_o = static_cast<uint32_t>(nv);
   prm.off_c = static_cast<uint32_t>(nv + no);
   const size_t smem = (nv + no + nc) * sizeof(float4) +
@@ -766,8 +827,12 @@ cudaError_t launch_test_f32_all(const DevTables& t, const TestArgs* a, cudaStrea
   auto form = [](const SlabTable& t) { return t.cnt[0] == 0 ? 1 : t.cnt[2] == 0 ? 2 : 0; };
   const int fv = form(t.slab[0]), fo = form(t.slab[1]);
   const int mode = fv == fo ? fv : -1;
-  auto kern = mode == 0 ? tri_kernel<0> : mode == 1 ? tri_kernel<1> : mode == 2 ? tri_kernel<2>
-                                                                              : tri_kernel<-1>;
+  auto pick = [mode](auto g) {
+    constexpr bool G = decltype(g)::value;
+    return mode == 0 ? tri_kernel<0, G> : mode == 1 ? tri_kernel<1, G>
+         : mode == 2 ? tri_kernel<2, G> : tri_kernel<-1, G>;
+  };
+  auto kern = t.cross.n <= kCrossGroupMaxN ? pick(std::true_type{}) : pick(std::false_type{});
   cudaError_t e = launch_config(reinterpret_cast<const void*>(kern), kThreads, smem, &sms, &per_sm);
   if (e != cudaSuccess) return e;
   const uint64_t cap = (uint64_t)sms * per_sm;
@@ -796,9 +861,9 @@ cudaError_t launch_test_f32(const DevTables& t, int engine, const TestArgs& a,
                             cudaStream_t stream) {
   if (engine == 0) return launch_slab<false>(t, 0, a, stream);
   if (engine == 1) return launch_slab<true>(t, 1, a, stream);
-  using E = CrossEngine<VPIPG_CROSS_P>;
-  typename E::Params prm{t.cross, t.ox, t.oy};
-  return launch<E>(prm, a, stream);
+  // the standalone crossing kernel keeps the carried form at every n (the
+  // group form measured equal at n = 8 and 2.5 % slower at n = 16 there)
+  return launch<CrossEngine<VPIPG_CROSS_P, false>>(CrossParams{t.cross, t.ox, t.oy}, a, stream);
 }
 
 }  // namespace vpipg
