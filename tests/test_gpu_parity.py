@@ -634,6 +634,33 @@ def test_fused_pass_on_every_table_form(shape):
             assert cs[e].item() == ref[e][1].item() > 0, (shape, e)
 
 
+@pytest.mark.parametrize("n", [5, 6, 7, 8, 12, 15, 16, 17, 24, 33, 48])
+def test_fused_crossing_loop_forms_equal_standalone(n):
+    """The fused pass runs the crossing engine's 4-edge group form for
+    n <= 16 and the carried form above (test_f32.cu CrossEngine); both form
+    h = qy - v.y, g = w.x - qx and d = fma(h, dvx/dvy, g) from the same
+    record values, so every n mod 4 tail and both sides of the switch give
+    the standalone crossing kernel's words and count bit for bit."""
+    rng = np.random.default_rng(1000 + n)
+    t = np.sort(rng.uniform(0.0, 2.0 * np.pi, n))
+    t += np.linspace(0.0, 0.5 / n, n)  # keep the angles distinct
+    vx, vy = np.cos(t), np.sin(t)
+    m = (1 << 20) + 77
+    xs = torch.as_tensor(rng.uniform(-1.3, 1.3, m).astype(np.float32), device=DEV)
+    ys = torch.as_tensor(rng.uniform(-1.3, 1.3, m).astype(np.float32), device=DEV)
+    nw = (m + 31) // 32
+    with vp.PreparedPolygon.prepare(vx, vy, vp.KIND_ALL) as p:
+        w = torch.zeros(nw, dtype=torch.int32, device=DEV)
+        c = torch.zeros(1, dtype=torch.int64, device=DEV)
+        p.test(2, xs, ys, words=w, count=c)
+        ws = [torch.zeros(nw, dtype=torch.int32, device=DEV) for _ in range(3)]
+        cs = [torch.zeros(1, dtype=torch.int64, device=DEV) for _ in range(3)]
+        p.test_multi(xs, ys, (0, 1, 2), words=ws, counts=cs)
+        torch.cuda.synchronize()
+        assert torch.equal(ws[2], w), n
+        assert cs[2].item() == c.item() > 0, n
+
+
 def test_multi_partial_engine_sets_f64_and_missing_outputs(golden):
     """vpipg_test_multi outside the fused plan: two of three engines, f64
     points, and NULL outputs for some engines -- same answers as vpipg_test,
