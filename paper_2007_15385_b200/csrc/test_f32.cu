@@ -786,11 +786,12 @@ cudaError_t launch(const typename Eng::Params& prm, const TestArgs& a, cudaStrea
 
 // Polygons with more edges than this run the per-engine kernels even when all
 // three engines are asked for: at n = 32 the fused kernel is 3.6 % faster than
-// the three separate ones (C5), at n = 64 it is within +-3 %, and at n = 256 /
-// 1024 the separate kernels (larger P for the slab engines) win by 5-6 %
-// (profiles/round1_summary.md)
+// the three separate ones (C5); on the exact-n c3x polygons (2^28 points) the
+// two are equal at n = 32 / 36 and the separate kernels win by 0.5 / 1.1 /
+// 1.5 % at n = 40 / 44 / 48, and by 5-6 % at n = 256 / 1024 (larger P for the
+// slab engines) (profiles/round1_summary.md)
 #ifndef VPIPG_FUSE_MAX_N
-#define VPIPG_FUSE_MAX_N 48
+#define VPIPG_FUSE_MAX_N 40
 #endif
 
 bool test_f32_all_plan(const DevTables& t, const TestArgs* a, size_t* smem_out) {

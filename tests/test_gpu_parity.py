@@ -634,7 +634,7 @@ def test_fused_pass_on_every_table_form(shape):
             assert cs[e].item() == ref[e][1].item() > 0, (shape, e)
 
 
-@pytest.mark.parametrize("n", [5, 6, 7, 8, 12, 15, 16, 17, 24, 33, 48])
+@pytest.mark.parametrize("n", [5, 6, 7, 8, 12, 15, 16, 17, 24, 33, 40])
 def test_fused_crossing_loop_forms_equal_standalone(n):
     """The fused pass runs the crossing engine's 4-edge group form for
     n <= 16 and the carried form above (test_f32.cu CrossEngine); both form
@@ -693,7 +693,7 @@ def test_multi_partial_engine_sets_f64_and_missing_outputs(golden):
 def test_multi_fused_plan():
     """vpipg_test_multi_fused reports the route vpipg_test_multi takes: one
     fused launch for all three engines on float32 batches of polygons with at
-    most 48 edges and on any float64 batch, per-engine kernels otherwise."""
+    most 40 edges and on any float64 batch, per-engine kernels otherwise."""
     m = 1 << 20
     xs = torch.zeros(m, dtype=torch.float32, device=DEV)
     ys = torch.zeros_like(xs)
@@ -707,6 +707,10 @@ def test_multi_fused_plan():
     _, (vx, vy) = W.c3_named("c3x:64")
     with vp.PreparedPolygon.prepare(vx, vy, vp.KIND_ALL) as p:
         assert not p.multi_fused(xs, ys)                  # 64 edges: separate kernels are faster
+    for n, fused in ((40, True), (44, False)):            # VPIPG_FUSE_MAX_N = 40
+        _, (vx, vy) = W.c3_named(f"c3x:{n}")
+        with vp.PreparedPolygon.prepare(vx, vy, vp.KIND_ALL) as p:
+            assert p.multi_fused(xs, ys) == fused, n
 
 
 @pytest.mark.parametrize("m", [7, 4099, (1 << 20) + 3])
