@@ -24,7 +24,7 @@ NVCC = str(CUDA_HOME / "bin" / "nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ARCH + [
     "-O3", "-lineinfo", "-std=c++20", "--expt-relaxed-constexpr",
-    "-Xcompiler", "-fPIC,-ffp-contract=off", "-Xptxas", "-warn-spills",
+    "-Xcompiler", "-fPIC,-ffp-contract=off", "-Xptxas", "-warn-spills", "-diag-suppress", "177",
     f"-I{ROOT / 'include'}", f"-I{CSRC}",
 ]
 CXX_FLAGS = ["-std=c++20", "-O2", "-fPIC", "-ffp-contract=off", "-Wall",

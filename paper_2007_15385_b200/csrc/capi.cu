@@ -97,6 +97,8 @@ int blob_pool(int device, cudaMemPool_t* out) {
   return kOk;
 }
 
+constexpr uint32_t kHostTableMax = 256;
+
 // Builds the blob, runs the prep kernel, reads back the status.
 int build(vpipg_poly* p, const double* vv, const double* vr, const double* gen, cudaStream_t s) {
   const size_t n = p->n;
@@ -176,6 +178,21 @@ int build(vpipg_poly* p, const double* vv, const double* vr, const double* gen, 
   t.cross.vert = a.cross_vert;
   t.cross.n = p->n;
   t.lines = a.lines;
+  // small tables also travel in the kernels' parameter bank (test_f32.cu)
+  if (p->n <= kHostTableMax) {
+    for (int e = 0; e < 2; ++e) {
+      p->h_slab[e].resize(t.slab[e].total);
+      if (t.slab[e].total)
+        VPIPG_TRY(cudaMemcpyAsync(p->h_slab[e].data(), t.slab[e].coef, t.slab[e].total * sizeof(float2),
+                                  cudaMemcpyDeviceToHost, s));
+      t.h_slab[e] = p->h_slab[e].data();
+    }
+    p->h_cross.resize(p->n);
+    VPIPG_TRY(cudaMemcpyAsync(p->h_cross.data(), t.cross.vert, p->n * sizeof(float4),
+                              cudaMemcpyDeviceToHost, s));
+    t.h_cross = p->h_cross.data();
+    VPIPG_TRY(cudaStreamSynchronize(s));
+  }
   p->inner_x = meta.inner_x;
   p->inner_y = meta.inner_y;
   return kOk;

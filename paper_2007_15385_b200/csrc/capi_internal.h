@@ -21,6 +21,8 @@ struct vpipg_poly {
   vpipg::DevTables t{};
   std::vector<double> vx, vy;  // validated (or raw, crossing-only) vertices
   double inner_x = 0, inner_y = 0;
+  std::vector<float2> h_slab[2];  // host copies of the f32 tables (DevTables::h_*)
+  std::vector<float4> h_cross;
 };
 
 struct vpipg_db {

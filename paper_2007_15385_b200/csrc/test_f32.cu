@@ -23,20 +23,23 @@
 // memory and read with warp-uniform 16-byte broadcasts. generic_kernel handles
 // unaligned inputs with guarded direct loads.
 #include <cstdint>
+#include <cstring>
 #include <type_traits>
 
 #include "tma_pipe.cuh"
 #include "vpipg_device.cuh"
 #include "vpipg_internal.h"
 
-// points per lane per slice (tuned on C5, profiles/round1_summary.md): the
-// slab kernel amortises its per-slice work best at 16, the crossing kernel
-// (more live registers per point) at 12; both run 2 CTAs of 8 warps per SM
+// points per lane per slice (tuned on C5, profiles/crossing_forms_r02.json):
+// the slab kernel amortises its per-slice work best at 20 (16: +0.6 %), the
+// crossing kernel, which carries one h per point, at 20 (12 / 16 / 24:
+// +8 / +4 / -1 %; 24 spills with shared-memory tables); all run 2 CTAs of
+// 8 warps per SM
 #ifndef VPIPG_SLAB_P
-#define VPIPG_SLAB_P 16
+#define VPIPG_SLAB_P 20
 #endif
 #ifndef VPIPG_CROSS_P
-#define VPIPG_CROSS_P 12
+#define VPIPG_CROSS_P 20
 #endif
 #ifndef VPIPG_CROSS_VOTE
 #define VPIPG_CROSS_VOTE 2
@@ -84,24 +87,45 @@ struct SlabParams {
   float ox, oy;
 };
 
+// Tables of up to kInlineMax float4 records can travel in the kernel's
+// parameter bank instead of shared memory (VPIPG_INLINE): the edge loops then
+// read them with uniform constant loads (LDCU) into uniform registers, so the
+// per-edge FFMA / FADD operands come from the uniform datapath and no vector
+// register or shared-memory load is spent on table values.
+#ifndef VPIPG_INLINE
+#define VPIPG_INLINE 1
+#endif
+constexpr int kInlineMax = 128;
+struct SlabParamsInl {
+  SlabTable tab;
+  float ox, oy;
+  float4 v[kInlineMax];
+};
+
 // kMode: 0 = two sections (mixed table), 1 = y-only table, 2 = x-only table
 // (prep.cu slab_scatter), -1 = decided per launch from the table counts (the
 // fused kernel); the launcher instantiates the mode the table has, so each
 // streaming kernel carries one code path
-template <int P, bool kNanIn, int kMode = -1>
+template <int P, bool kNanIn, int kMode = -1, bool kInline = false>
 struct SlabEngine {
   static constexpr int kP = P;
   static constexpr int kVote = kNanIn ? 1 : 0;  // see vote_in
   static constexpr bool kRegStream = true;  // ldg_kernel
-  using Params = SlabParams;  // shared by every (P, NaN rule, form) instantiation
-  static size_t table_bytes(const Params& p) { return (size_t)p.tab.total * sizeof(float2); }
+  static constexpr bool kInl = kInline;
+  static constexpr bool kUniform = false;
+  // shared by every (P, NaN rule, form) instantiation of one table placement
+  using Params = std::conditional_t<kInline, SlabParamsInl, SlabParams>;
+  static size_t table_bytes(const Params& p) { return kInline ? 0 : (size_t)p.tab.total * sizeof(float2); }
   __device__ static const float4* global_table(const Params& p) {
-    return reinterpret_cast<const float4*>(p.tab.coef);
+    if constexpr (kInline) return p.v;
+    else return reinterpret_cast<const float4*>(p.tab.coef);
   }
 
   __device__ static void stage(const Params& p, float4* s) {
-    const float4* src = reinterpret_cast<const float4*>(p.tab.coef);
-    for (uint32_t i = threadIdx.x; i < p.tab.total / 2; i += blockDim.x) s[i] = src[i];
+    if constexpr (!kInline) {
+      const float4* src = reinterpret_cast<const float4*>(p.tab.coef);
+      for (uint32_t i = threadIdx.x; i < p.tab.total / 2; i += blockDim.x) s[i] = src[i];
+    }
   }
 
   // Two groups that bound the coordinate w as a function of the other one, v
@@ -200,62 +224,65 @@ struct SlabEngine {
 //   in_range <=> (u.y > qy) != (w.y > qy) <=> sign(h_k) ^ sign(h_{k-1}),
 //                h = qy - v.y (a -0.0 from qy = -0.0 merely moves vertex k to
 //                "above" for both of its edges at once, which keeps the parity)
-//   on_left  <=> qx < x-of-edge-at-qy <=> d = (w.x - qx) + h_{k-1} * dvx/dvy > 0
-// crossing bit = (H_k ^ H_{k-1}) & ~D; parity accumulated by XOR in bit 31.
+//   on_left  <=> qx < x-of-edge-at-qy <=> d = (a.x - qx) + (qy - a.y) * dvx/dvy > 0
+//                for either endpoint a of the edge
+// crossing bit = (H_k ^ H_{k-1}) & ~D (one LOP3), XOR-reduced into the parity
+// word's bit 31 two bits per LOP3.
+//
+// Paired anchoring: edges k (v[k-1] -> v[k]) and k+1 (v[k] -> v[k+1]) both
+// take their x-intercept from their shared vertex v[k], so g = v[k].x - qx is
+// formed for every other vertex only and h_k serves both d's: per edge
+// 1 FADD (h) + 1/2 FADD (g) + 1 FFMA (d) + 3/2 LOP3, 5.5 dispatch cycles
+// against 6 for one g per vertex (B200, profiles/crossing_forms_r02.json:
+// C5 crossing 12.18 -> 11.20 ms at P = 12). The per-edge constants come from
+// the parameter bank as uniform registers (VPIPG_INLINE), so the FFMA has two
+// vector sources: with three (table in shared memory) it issues at 0.61 per
+// cycle instead of 0.96 (tools/pipe_peaks2.cu).
 // Points exactly on an edge line lie inside the 1e-5 parity band, so the
 // reference's closed-boundary latch (engines.cpp:194-196) is repeated only by
 // the exact f64 kernel.
+__device__ __forceinline__ uint32_t cross_bit(float h, float hprev, float d) {
+  return (__float_as_uint(h) ^ __float_as_uint(hprev)) & ~__float_as_uint(d);
+}
 struct CrossParams {
   CrossTable tab;
   float ox, oy;
 };
+struct CrossParamsInl {
+  CrossTable tab;
+  float ox, oy;
+  float4 v[kInlineMax];
+};
 
-template <int P, bool kGroupForm = false>
+template <int P, bool kInline = false>
 struct CrossEngine {
   static constexpr int kP = P;
+  static constexpr bool kInl = kInline;
+  // the uniform round loop (ldg_kernel): with parameter-bank tables the edge
+  // loop runs on uniform registers; with shared-memory tables (n > kInlineMax)
+  // it measured faster too (c3x:256 crossing 10.36 vs 11.27 ms)
+  static constexpr bool kUniform = true;
   static constexpr int kVote = VPIPG_CROSS_VOTE;  // 2: a holds the parity word, sign bit = inside
 #ifndef VPIPG_CROSS_LDG
-#define VPIPG_CROSS_LDG 0
+#define VPIPG_CROSS_LDG 1
 #endif
-  static constexpr bool kRegStream = VPIPG_CROSS_LDG;  // 0: stream_kernel (TMA ring)
-  using Params = CrossParams;  // shared by both loop forms
-  static size_t table_bytes(const Params& p) { return (size_t)p.tab.n * sizeof(float4); }
-  __device__ static const float4* global_table(const Params& p) { return p.tab.vert; }
+  // 1: ldg_kernel (register streaming), 0: stream_kernel (per-warp TMA ring);
+  // with parameter-bank tables the ring's barrier loops keep the compiler from
+  // using the uniform datapath in the edge loop (C5: 12.32 vs 11.20 ms)
+  static constexpr bool kRegStream = VPIPG_CROSS_LDG;
+  using Params = std::conditional_t<kInline, CrossParamsInl, CrossParams>;
+  static size_t table_bytes(const Params& p) { return kInline ? 0 : (size_t)p.tab.n * sizeof(float4); }
+  __device__ static const float4* global_table(const Params& p) {
+    if constexpr (kInline) return p.v;
+    else return p.tab.vert;
+  }
 
   __device__ static void stage(const Params& p, float4* s) {
-    for (uint32_t i = threadIdx.x; i < p.tab.n; i += blockDim.x) s[i] = p.tab.vert[i];
+    if constexpr (!kInline)
+      for (uint32_t i = threadIdx.x; i < p.tab.n; i += blockDim.x) s[i] = p.tab.vert[i];
   }
 
-  // E consecutive edges: the crossing bits t_e = (H_e ^ H_{e-1}) & ~D_e,
-  // XOR-reduced in pairs (one LOP3 folds two bits into the parity word);
-  // hp carries h of the group's start vertex in and of its last vertex out
-  template <int E>
-  __device__ __forceinline__ static void group(const float4* v, const float (&x)[P],
-                                               const float (&y)[P], float (&hp)[P],
-                                               uint32_t (&par)[P]) {
-    float4 r[E];
-#pragma unroll
-    for (int e = 0; e < E; ++e) r[e] = v[e];
-#pragma unroll
-    for (int p = 0; p < P; ++p) {
-      float h0 = hp[p];
-      uint32_t t[E];
-#pragma unroll
-      for (int e = 0; e < E; ++e) {
-        const float h = y[p] - r[e].y;
-        t[e] = (__float_as_uint(h) ^ __float_as_uint(h0)) & ~__float_as_uint(fmaf(h0, r[e].z, r[e].w - x[p]));
-        h0 = h;
-      }
-      uint32_t acc = par[p];
-#pragma unroll
-      for (int e = 0; e + 1 < E; e += 2) acc ^= t[e] ^ t[e + 1];
-      if (E & 1) acc ^= t[E - 1];
-      par[p] = acc;
-      hp[p] = h0;
-    }
-  }
-
-  // a[p] = +1 (odd crossing parity: inside) or -1 (even: outside), b[p] = 0
+  // a[p]: the parity word (sign bit set = odd crossing count = inside), b[p] = 0
   __device__ __forceinline__ static void eval(const Params& prm, const float4* s,
                                               const float (&x)[P], const float (&y)[P],
                                               float (&a)[P], float (&b)[P]) {
@@ -263,78 +290,47 @@ struct CrossEngine {
     uint32_t par[P];
 #pragma unroll
     for (int p = 0; p < P; ++p) par[p] = 0;
-    // record k = (u.x, u.y, dvx/dvy, w.x) of edge w = v[k-1] -> u = v[k]
-    // (prep.cu); two loop forms, separate kernel instantiations picked per
-    // polygon by the launcher (kCrossGroupMaxN), measured on B200:
-    //  - kGroupForm: 4-edge groups taking g = w.x - qx from the edge's own
-    //    record (.w), only h carried between groups (no per-slice g
-    //    preamble); the fused pass at n <= 16: 4-6 % faster at n = 4 / 8 /
-    //    16 and on C2
-    //  - otherwise h and g are both carried across 4-edge iterations, g
-    //    formed from the previous vertex (.x) (2-5 % faster from n = 24 up;
-    //    both forms in one kernel made either path slower)
+    // record k = (u.x, u.y, dvx/dvy, -) of edge w = v[k-1] -> u = v[k] (prep.cu)
     if (n > 0) {
       const float4 last = s[n - 1];
-      float hp[P];
+      float hp[P];  // h of the vertex before the current pair
 #pragma unroll
       for (int p = 0; p < P; ++p) hp[p] = y[p] - last.y;
-      if constexpr (kGroupForm) {
-        uint32_t k = 0;
-#pragma unroll 1
-        for (; k + 4 <= n; k += 4) group<4>(s + k, x, y, hp, par);
-        if (k + 2 <= n) {
-          group<2>(s + k, x, y, hp, par);
-          k += 2;
+      uint32_t k = 0;
+      VPIPG_UNROLL(VPIPG_CROSS_UNROLL)
+      for (; k + 3 < n; k += 4) {
+        const float4 v0 = s[k], v1 = s[k + 1], v2 = s[k + 2], v3 = s[k + 3];
+#pragma unroll
+        for (int p = 0; p < P; ++p) {
+          const float h0 = y[p] - v0.y, g0 = v0.x - x[p];
+          const float h1 = y[p] - v1.y;
+          const float h2 = y[p] - v2.y, g2 = v2.x - x[p];
+          const float h3 = y[p] - v3.y;
+          const uint32_t t0 = cross_bit(h0, hp[p], fmaf(h0, v0.z, g0));  // u-anchored at v[k]
+          const uint32_t t1 = cross_bit(h1, h0, fmaf(h0, v1.z, g0));     // w-anchored at v[k]
+          const uint32_t t2 = cross_bit(h2, h1, fmaf(h2, v2.z, g2));
+          const uint32_t t3 = cross_bit(h3, h2, fmaf(h2, v3.z, g2));
+          par[p] ^= t0 ^ t1 ^ t2 ^ t3;
+          hp[p] = h3;
         }
-        if (k < n) group<1>(s + k, x, y, hp, par);
-      } else {
-        float gp[P];
+      }
+      if (k + 1 < n) {
+        const float4 v0 = s[k], v1 = s[k + 1];
 #pragma unroll
-        for (int p = 0; p < P; ++p) gp[p] = last.x - x[p];
-        uint32_t k = 0;
-        VPIPG_UNROLL(VPIPG_CROSS_UNROLL)
-        for (; k + 3 < n; k += 4) {
-          const float4 v0 = s[k], v1 = s[k + 1], v2 = s[k + 2], v3 = s[k + 3];
-#pragma unroll
-          for (int p = 0; p < P; ++p) {
-            const float h0 = y[p] - v0.y, g0 = v0.x - x[p];
-            const float h1 = y[p] - v1.y, g1 = v1.x - x[p];
-            const float h2 = y[p] - v2.y, g2 = v2.x - x[p];
-            const float h3 = y[p] - v3.y;
-            const uint32_t t0 = (__float_as_uint(h0) ^ __float_as_uint(hp[p])) & ~__float_as_uint(fmaf(hp[p], v0.z, gp[p]));
-            const uint32_t t1 = (__float_as_uint(h1) ^ __float_as_uint(h0)) & ~__float_as_uint(fmaf(h0, v1.z, g0));
-            const uint32_t t2 = (__float_as_uint(h2) ^ __float_as_uint(h1)) & ~__float_as_uint(fmaf(h1, v2.z, g1));
-            const uint32_t t3 = (__float_as_uint(h3) ^ __float_as_uint(h2)) & ~__float_as_uint(fmaf(h2, v3.z, g2));
-            par[p] ^= t0 ^ t1 ^ t2 ^ t3;
-            hp[p] = h3;
-            gp[p] = v3.x - x[p];
-          }
+        for (int p = 0; p < P; ++p) {
+          const float h0 = y[p] - v0.y, g0 = v0.x - x[p];
+          const float h1 = y[p] - v1.y;
+          par[p] ^= cross_bit(h0, hp[p], fmaf(h0, v0.z, g0)) ^ cross_bit(h1, h0, fmaf(h0, v1.z, g0));
+          hp[p] = h1;
         }
-#pragma unroll 1
-        for (; k + 1 < n; k += 2) {
-          const float4 v0 = s[k], v1 = s[k + 1];
+        k += 2;
+      }
+      if (k < n) {
+        const float4 v0 = s[k];
 #pragma unroll
-          for (int p = 0; p < P; ++p) {
-            const float h0 = y[p] - v0.y;
-            const float d0 = fmaf(hp[p], v0.z, gp[p]);
-            const float g0 = v0.x - x[p];
-            const float h1 = y[p] - v1.y;
-            const float d1 = fmaf(h0, v1.z, g0);
-            const uint32_t t0 = (__float_as_uint(h0) ^ __float_as_uint(hp[p])) & ~__float_as_uint(d0);
-            const uint32_t t1 = (__float_as_uint(h1) ^ __float_as_uint(h0)) & ~__float_as_uint(d1);
-            par[p] ^= t0 ^ t1;
-            hp[p] = h1;
-            gp[p] = v1.x - x[p];
-          }
-        }
-        if (k < n) {
-          const float4 v0 = s[k];
-#pragma unroll
-          for (int p = 0; p < P; ++p) {
-            const float h0 = y[p] - v0.y;
-            const float d0 = fmaf(hp[p], v0.z, gp[p]);
-            par[p] ^= (__float_as_uint(h0) ^ __float_as_uint(hp[p])) & ~__float_as_uint(d0);
-          }
+        for (int p = 0; p < P; ++p) {
+          const float h0 = y[p] - v0.y;
+          par[p] ^= cross_bit(h0, hp[p], fmaf(h0, v0.z, v0.x - x[p]));
         }
       }
     }
@@ -387,9 +383,12 @@ __device__ __forceinline__ uint32_t vote_in(float a, float b, uint32_t& cnt) {
   return w;
 }
 
+// live == false (a warp whose slot in the last round is past the end; warp-
+// uniform): the votes run, nothing is stored or counted
 template <bool kGuard, int kVote, int P>
 __device__ __forceinline__ uint32_t emit(float (&av)[P], const float (&bv)[P], uint64_t base,
-                                         const TestArgs& a, int lane) {
+                                         const TestArgs& a, int lane, bool live = true) {
+  static_assert(kGuard || P % 4 == 0, "16-byte word stores need P % 4 == 0");
   uint32_t w[P];
   uint32_t cnt = 0;
 #pragma unroll
@@ -397,6 +396,7 @@ __device__ __forceinline__ uint32_t emit(float (&av)[P], const float (&bv)[P], u
     if (kGuard && base + 32u * p + lane >= a.m) av[p] = kVote == 2 ? 0.f : -INFINITY;
     w[p] = vote_in<kVote>(av[p], bv[p], cnt);
   }
+  if (!live) return 0;
   if (a.words && lane == 0) {
     const uint64_t w0 = base >> 5;
     if (!kGuard && (reinterpret_cast<uintptr_t>(a.words) & 15) == 0) {
@@ -445,12 +445,35 @@ __device__ __forceinline__ uint32_t guarded_tile(const typename Eng::Params& prm
   return emit<true, Eng::kVote, P>(va, vb, base, a, lane);
 }
 
+// Persistent slice schedule: warp w of CTA b takes slices (b + r * grid) *
+// kWarps + w for rounds r = 0 .. rounds - 1. `rounds` depends on the CTA
+// only, so every loop over it is uniform control flow for the compiler (the
+// per-edge table reads can then use the uniform datapath); a warp whose slot
+// in the last round lies past the end re-reads the last full slice and stores
+// nothing (emit's `live`).
+struct SliceRounds {
+  uint64_t W, b0, g0, rounds, last;
+  __device__ SliceRounds(uint64_t full_slices, int warp) {
+    W = (uint64_t)gridDim.x * kWarps;
+    b0 = (uint64_t)blockIdx.x * kWarps;
+    g0 = b0 + warp;
+    rounds = full_slices > b0 ? (full_slices - b0 + W - 1) / W : 0;
+    last = full_slices ? full_slices - 1 : 0;
+  }
+  __device__ uint64_t slice(uint64_t r) const {
+    const uint64_t g = g0 + r * W;
+    return g < last ? g : last;
+  }
+  __device__ bool live(uint64_t r) const { return g0 + r * W <= last; }
+};
+
 // kSmemTab: the polygon table is staged in shared memory once per CTA (the
 // normal case); polygons whose table exceeds kSmemTableMax read it from global
 // memory with warp-uniform loads instead.
 template <class Eng, bool kSmemTab>
 __global__ void __launch_bounds__(kThreads, 2)
-    stream_kernel(const typename Eng::Params prm, const TestArgs a, const uint64_t full_slices) {
+    stream_kernel(const __grid_constant__ typename Eng::Params prm, const TestArgs a,
+                  const uint64_t full_slices) {
   constexpr int P = Eng::kP;
   constexpr int kWarpPts = 32 * P;
   extern __shared__ __align__(128) unsigned char smem[];
@@ -470,19 +493,18 @@ __global__ void __launch_bounds__(kThreads, 2)
     mbar_fence_init();
   }
   if (kSmemTab) Eng::stage(prm, s_tab);
-  const float4* tab = kSmemTab ? s_tab : Eng::global_table(prm);
+  const float4* tab = (kSmemTab && !Eng::kInl) ? s_tab : Eng::global_table(prm);
   __syncthreads();
 
-  const uint64_t W = (uint64_t)gridDim.x * kWarps;
-  const uint64_t g0 = (uint64_t)blockIdx.x * kWarps + warp;
+  const SliceRounds sr(full_slices, warp);
   const float* xs = static_cast<const float*>(a.xs);
   const float* ys = static_cast<const float*>(a.ys);
   uint64_t policy = 0;
   if (lane == 0) {
     policy = policy_evict_first();
     for (int s = 0; s < kStages; ++s) {
-      const uint64_t g = g0 + s * W;
-      if (g >= full_slices) break;
+      if (s >= sr.rounds) break;
+      const uint64_t g = sr.slice(s);
       mbar_arrive_expect_tx(&full[s], 2u * kWarpPts * sizeof(float));
       bulk_g2s(ring + s * 2 * kWarpPts, xs + g * kWarpPts, kWarpPts * sizeof(float), &full[s], policy);
       bulk_g2s(ring + s * 2 * kWarpPts + kWarpPts, ys + g * kWarpPts, kWarpPts * sizeof(float),
@@ -490,9 +512,8 @@ __global__ void __launch_bounds__(kThreads, 2)
     }
   }
   uint32_t count = 0;
-  uint32_t it = 0;
-  for (uint64_t g = g0; g < full_slices; g += W, ++it) {
-    const uint32_t s = it % kStages, ph = (it / kStages) & 1u;
+  for (uint64_t r = 0; r < sr.rounds; ++r) {
+    const uint32_t s = r % kStages, ph = (r / kStages) & 1u;
     mbar_wait(&full[s], ph);
     const float* px = ring + s * 2 * kWarpPts + lane;
     float x[P], y[P], va[P], vb[P];
@@ -502,8 +523,8 @@ __global__ void __launch_bounds__(kThreads, 2)
       y[p] = px[kWarpPts + 32 * p];
     }
     mbar_arrive(&empty[s]);  // release: this lane's reads of stage s are done
-    const uint64_t gn = g + kStages * W;
-    if (lane == 0 && gn < full_slices) {
+    if (lane == 0 && r + kStages < sr.rounds) {
+      const uint64_t gn = sr.slice(r + kStages);
       mbar_wait(&empty[s], ph);
       mbar_arrive_expect_tx(&full[s], 2u * kWarpPts * sizeof(float));
       bulk_g2s(ring + s * 2 * kWarpPts, xs + gn * kWarpPts, kWarpPts * sizeof(float), &full[s], policy);
@@ -511,10 +532,10 @@ __global__ void __launch_bounds__(kThreads, 2)
                &full[s], policy);
     }
     Eng::eval(prm, tab, x, y, va, vb);
-    count += emit<false, Eng::kVote, P>(va, vb, g * kWarpPts, a, lane);
+    count += emit<false, Eng::kVote, P>(va, vb, sr.slice(r) * kWarpPts, a, lane, sr.live(r));
   }
   // partial last slice: the warp next in round-robin order, guarded loads
-  if (g0 == full_slices % W) {
+  if (sr.g0 == full_slices % sr.W) {
     for (uint64_t base = full_slices * kWarpPts; base < a.m; base += kWarpPts)
       count += guarded_tile<Eng>(prm, tab, a, base, lane);
   }
@@ -536,44 +557,75 @@ __device__ __forceinline__ void prefetch_l2(const void* p) {
 #endif
 template <class Eng, bool kSmemTab>
 __global__ void __launch_bounds__(kThreads, VPIPG_LDG_MINB)
-    ldg_kernel(const typename Eng::Params prm, const TestArgs a, const uint64_t full_slices) {
+    ldg_kernel(const __grid_constant__ typename Eng::Params prm, const TestArgs a,
+               const uint64_t full_slices) {
   constexpr int P = Eng::kP;
   constexpr int kWarpPts = 32 * P;
   extern __shared__ __align__(128) unsigned char smem[];
   float4* s_tab = reinterpret_cast<float4*>(smem);
   if (kSmemTab) Eng::stage(prm, s_tab);
-  const float4* tab = kSmemTab ? s_tab : Eng::global_table(prm);
+  const float4* tab = (kSmemTab && !Eng::kInl) ? s_tab : Eng::global_table(prm);
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint64_t W = (uint64_t)gridDim.x * kWarps;
-  const uint64_t g0 = (uint64_t)blockIdx.x * kWarps + warp;
+  const SliceRounds sr(full_slices, warp);
   const float* xs = static_cast<const float*>(a.xs);
   const float* ys = static_cast<const float*>(a.ys);
   constexpr int kLines = kWarpPts * 4 / 128;
-  auto prefetch = [&](uint64_t g) {
-    if (g >= full_slices) return;
+  auto prefetch = [&](uint64_t r) {
+    if (r >= sr.rounds) return;
+    const uint64_t g = sr.slice(r);
     for (int l = lane; l < 2 * kLines; l += 32)
       prefetch_l2((l < kLines ? xs : ys) + g * kWarpPts + (l % kLines) * 32);
   };
 #ifndef VPIPG_PF_AHEAD
 #define VPIPG_PF_AHEAD 1
 #endif
-  for (int d = 0; d < VPIPG_PF_AHEAD; ++d) prefetch(g0 + d * W);
   uint32_t count = 0;
-  for (uint64_t g = g0; g < full_slices; g += W) {
-    prefetch(g + VPIPG_PF_AHEAD * W);
-    const float* px = xs + g * kWarpPts + lane;
-    const float* py = ys + g * kWarpPts + lane;
-    float x[P], y[P], va[P], vb[P];
+  // the uniform round loop only pays where the edge loop reads the parameter
+  // bank through uniform registers (the crossing engine); the slab engines'
+  // FFMAs take two table operands, so they read the table into vector
+  // registers either way and keep the plain strided loop (C5: 5.24 vs 5.35 ms)
+#ifndef VPIPG_SLICE_ROUNDS
+#define VPIPG_SLICE_ROUNDS 0
+#endif
+  if constexpr (Eng::kUniform || VPIPG_SLICE_ROUNDS) {
+    for (int d = 0; d < VPIPG_PF_AHEAD; ++d) prefetch(d);
+    for (uint64_t r = 0; r < sr.rounds; ++r) {
+      prefetch(r + VPIPG_PF_AHEAD);
+      const uint64_t g = sr.slice(r);
+      const float* px = xs + g * kWarpPts + lane;
+      const float* py = ys + g * kWarpPts + lane;
+      float x[P], y[P], va[P], vb[P];
 #pragma unroll
-    for (int p = 0; p < P; ++p) {
-      x[p] = __ldcs(px + 32 * p);
-      y[p] = __ldcs(py + 32 * p);
+      for (int p = 0; p < P; ++p) {
+        x[p] = __ldcs(px + 32 * p);
+        y[p] = __ldcs(py + 32 * p);
+      }
+      Eng::eval(prm, tab, x, y, va, vb);
+      count += emit<false, Eng::kVote, P>(va, vb, g * kWarpPts, a, lane, sr.live(r));
     }
-    Eng::eval(prm, tab, x, y, va, vb);
-    count += emit<false, Eng::kVote, P>(va, vb, g * kWarpPts, a, lane);
+  } else {
+    auto pf = [&](uint64_t g) {
+      if (g >= full_slices) return;
+      for (int l = lane; l < 2 * kLines; l += 32)
+        prefetch_l2((l < kLines ? xs : ys) + g * kWarpPts + (l % kLines) * 32);
+    };
+    pf(sr.g0);
+    for (uint64_t g = sr.g0; g < full_slices; g += sr.W) {
+      pf(g + sr.W);
+      const float* px = xs + g * kWarpPts + lane;
+      const float* py = ys + g * kWarpPts + lane;
+      float x[P], y[P], va[P], vb[P];
+#pragma unroll
+      for (int p = 0; p < P; ++p) {
+        x[p] = __ldcs(px + 32 * p);
+        y[p] = __ldcs(py + 32 * p);
+      }
+      Eng::eval(prm, tab, x, y, va, vb);
+      count += emit<false, Eng::kVote, P>(va, vb, g * kWarpPts, a, lane);
+    }
   }
-  if (g0 == full_slices % W) {
+  if (sr.g0 == full_slices % sr.W) {
     for (uint64_t base = full_slices * kWarpPts; base < a.m; base += kWarpPts)
       count += guarded_tile<Eng>(prm, tab, a, base, lane);
   }
@@ -585,106 +637,70 @@ __global__ void __launch_bounds__(kThreads, VPIPG_LDG_MINB)
 // point is read once and tested by Voronoi, sign-of-offset and crossing in
 // turn, each writing its own mask words and count. Same slice schedule and
 // loads as ldg_kernel; the three tables sit side by side in shared memory.
-constexpr int kTriP = VPIPG_CROSS_P;  // the crossing engine's register budget sets P
-#ifndef VPIPG_TRI_TMA
-#define VPIPG_TRI_TMA 0  // 1: points through the per-warp TMA ring instead of direct loads
+// the three engines' live registers set P: 16 (C5 fused 19.47 ms; 12: 20.52,
+// 20: 19.87 with spills)
+#ifndef VPIPG_TRI_P
+#define VPIPG_TRI_P 16
 #endif
+constexpr int kTriP = VPIPG_TRI_P;
 struct TriParams {
   SlabParams v, o;
   CrossParams c;
   uint32_t off_o, off_c;  // float4 offsets of the offset / crossing tables in shared memory
 };
+constexpr int kTriInlineMax = 192;
+struct TriParamsInl {   // the three tables in the parameter bank (VPIPG_INLINE)
+  SlabParams v, o;
+  CrossParams c;
+  uint32_t off_o, off_c;  // float4 offsets of the offset / crossing tables in `t`
+  float4 t[kTriInlineMax];
+};
 
 // kMode: the slab table form shared by the Voronoi and offset tables (their
 // lines coincide: each bisector is the edge line), -1 when they differ
-template <int kMode, bool kGroupForm>
+template <int kMode, bool kInline = false>
 __global__ void __launch_bounds__(kThreads, 2)
-    tri_kernel(const TriParams prm, const TestArgs av, const TestArgs ao, const TestArgs ac,
-               const uint64_t full_slices) {
+    tri_kernel(const __grid_constant__ std::conditional_t<kInline, TriParamsInl, TriParams> prm,
+               const TestArgs av, const TestArgs ao, const TestArgs ac, const uint64_t full_slices) {
   using TriV = SlabEngine<kTriP, false, kMode>;
   using TriO = SlabEngine<kTriP, true, kMode>;
-  using TriC = CrossEngine<kTriP, kGroupForm>;
+  using TriC = CrossEngine<kTriP>;
   // one set of register-streamed loads feeds all three engines
   static_assert(TriV::kRegStream && TriO::kRegStream, "slab engines stream through registers");
   constexpr int P = kTriP;
   constexpr int kWarpPts = 32 * P;
   extern __shared__ __align__(128) unsigned char smem[];
-#if VPIPG_TRI_TMA
-  // per-warp TMA ring (as stream_kernel), then barriers, then the tables
-  const int warp_ = threadIdx.x >> 5, lane_ = threadIdx.x & 31;
-  float* ring = reinterpret_cast<float*>(smem) + (size_t)warp_ * kStages * 2 * kWarpPts;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<float*>(smem) +
-                                               (size_t)kWarps * kStages * 2 * kWarpPts);
-  uint64_t* full = bars + warp_ * 2 * kStages;
-  uint64_t* empty = full + kStages;
-  float4* s_tab = reinterpret_cast<float4*>(bars + kWarps * 2 * kStages);
-  if (lane_ == 0) {
-    for (int s = 0; s < kStages; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 32);
-    }
-    mbar_fence_init();
-  }
-#else
   float4* s_tab = reinterpret_cast<float4*>(smem);
-#endif
-  TriV::stage(prm.v, s_tab);
-  TriO::stage(prm.o, s_tab + prm.off_o);
-  TriC::stage(prm.c, s_tab + prm.off_c);
-  const float4* tv = s_tab;
-  const float4* to = s_tab + prm.off_o;
-  const float4* tc = s_tab + prm.off_c;
+  const float4* tv;
+  if constexpr (kInline) {
+    (void)s_tab;
+    tv = prm.t;
+  } else {
+    TriV::stage(prm.v, s_tab);
+    TriO::stage(prm.o, s_tab + prm.off_o);
+    TriC::stage(prm.c, s_tab + prm.off_c);
+    tv = s_tab;
+  }
+  const float4* to = tv + prm.off_o;
+  const float4* tc = tv + prm.off_c;
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint64_t W = (uint64_t)gridDim.x * kWarps;
-  const uint64_t g0 = (uint64_t)blockIdx.x * kWarps + warp;
+  const SliceRounds sr(full_slices, warp);
   const float* xs = static_cast<const float*>(av.xs);
   const float* ys = static_cast<const float*>(av.ys);
   constexpr int kLines = kWarpPts * 4 / 128;
-  auto prefetch = [&](uint64_t g) {
-    if (g >= full_slices) return;
+  auto prefetch = [&](uint64_t r) {
+    if (r >= sr.rounds) return;
+    const uint64_t g = sr.slice(r);
     for (int l = lane; l < 2 * kLines; l += 32)
       prefetch_l2((l < kLines ? xs : ys) + g * kWarpPts + (l % kLines) * 32);
   };
   uint32_t cv = 0, co = 0, cc = 0;
-#if VPIPG_TRI_TMA
-  (void)prefetch;
-  uint64_t policy = 0;
-  if (lane == 0) {
-    policy = policy_evict_first();
-    for (int s = 0; s < kStages; ++s) {
-      const uint64_t g = g0 + s * W;
-      if (g >= full_slices) break;
-      mbar_arrive_expect_tx(&full[s], 2u * kWarpPts * sizeof(float));
-      bulk_g2s(ring + s * 2 * kWarpPts, xs + g * kWarpPts, kWarpPts * sizeof(float), &full[s], policy);
-      bulk_g2s(ring + s * 2 * kWarpPts + kWarpPts, ys + g * kWarpPts, kWarpPts * sizeof(float),
-               &full[s], policy);
-    }
-  }
-  uint32_t it = 0;
-  for (uint64_t g = g0; g < full_slices; g += W, ++it) {
-    const uint32_t s = it % kStages, ph = (it / kStages) & 1u;
-    mbar_wait(&full[s], ph);
-    const float* pr = ring + s * 2 * kWarpPts + lane;
-    float x[P], y[P], va[P], vb[P];
-#pragma unroll
-    for (int p = 0; p < P; ++p) {
-      x[p] = pr[32 * p];
-      y[p] = pr[kWarpPts + 32 * p];
-    }
-    mbar_arrive(&empty[s]);
-    const uint64_t gn = g + kStages * W;
-    if (lane == 0 && gn < full_slices) {
-      mbar_wait(&empty[s], ph);
-      mbar_arrive_expect_tx(&full[s], 2u * kWarpPts * sizeof(float));
-      bulk_g2s(ring + s * 2 * kWarpPts, xs + gn * kWarpPts, kWarpPts * sizeof(float), &full[s], policy);
-      bulk_g2s(ring + s * 2 * kWarpPts + kWarpPts, ys + gn * kWarpPts, kWarpPts * sizeof(float),
-               &full[s], policy);
-    }
-#else
-  prefetch(g0);
-  for (uint64_t g = g0; g < full_slices; g += W) {
-    prefetch(g + W);
+  prefetch(0);
+  for (uint64_t r = 0; r < sr.rounds; ++r) {
+    prefetch(r + 1);
+    const uint64_t g = sr.slice(r);
+    const bool live = sr.live(r);
     const float* px = xs + g * kWarpPts + lane;
     const float* py = ys + g * kWarpPts + lane;
     float x[P], y[P], va[P], vb[P];
@@ -693,15 +709,14 @@ __global__ void __launch_bounds__(kThreads, 2)
       x[p] = __ldcs(px + 32 * p);
       y[p] = __ldcs(py + 32 * p);
     }
-#endif
     TriV::eval(prm.v, tv, x, y, va, vb);
-    cv += emit<false, TriV::kVote, P>(va, vb, g * kWarpPts, av, lane);
+    cv += emit<false, TriV::kVote, P>(va, vb, g * kWarpPts, av, lane, live);
     TriO::eval(prm.o, to, x, y, va, vb);
-    co += emit<false, TriO::kVote, P>(va, vb, g * kWarpPts, ao, lane);
+    co += emit<false, TriO::kVote, P>(va, vb, g * kWarpPts, ao, lane, live);
     TriC::eval(prm.c, tc, x, y, va, vb);
-    cc += emit<false, TriC::kVote, P>(va, vb, g * kWarpPts, ac, lane);
+    cc += emit<false, TriC::kVote, P>(va, vb, g * kWarpPts, ac, lane, live);
   }
-  if (g0 == full_slices % W) {
+  if (sr.g0 == full_slices % sr.W) {
     for (uint64_t base = full_slices * kWarpPts; base < av.m; base += kWarpPts) {
       cv += guarded_tile<TriV>(prm.v, tv, av, base, lane);
       co += guarded_tile<TriO>(prm.o, to, ao, base, lane);
@@ -714,7 +729,7 @@ __global__ void __launch_bounds__(kThreads, 2)
 }
 
 template <class Eng, bool kSmemTab>
-__global__ void __launch_bounds__(kThreads) generic_kernel(const typename Eng::Params prm,
+__global__ void __launch_bounds__(kThreads) generic_kernel(const __grid_constant__ typename Eng::Params prm,
                                                           const TestArgs a) {
   constexpr int kWarpPts = 32 * Eng::kP;
   extern __shared__ __align__(16) float4 s_gtab[];
@@ -722,7 +737,7 @@ __global__ void __launch_bounds__(kThreads) generic_kernel(const typename Eng::P
     Eng::stage(prm, s_gtab);
     __syncthreads();
   }
-  const float4* gtab = kSmemTab ? s_gtab : Eng::global_table(prm);
+  const float4* gtab = (kSmemTab && !Eng::kInl) ? s_gtab : Eng::global_table(prm);
   const int lane = threadIdx.x & 31;
   const uint64_t gwarp = (uint64_t)blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5);
   uint32_t count = 0;
@@ -735,13 +750,6 @@ __global__ void __launch_bounds__(kThreads) generic_kernel(const typename Eng::P
 
 constexpr size_t kSmemTableMax = 96 * 1024;
 
-// in the fused pass, polygons up to this many edges run the crossing engine's
-// 4-edge group form (CrossEngine<P, true>), larger ones the carried form
-// (measured, see CrossEngine::eval)
-#ifndef VPIPG_CROSS_GROUP_MAX_N
-#define VPIPG_CROSS_GROUP_MAX_N 16
-#endif
-constexpr uint32_t kCrossGroupMaxN = VPIPG_CROSS_GROUP_MAX_N;
 
 template <class Eng>
 cudaError_t launch(const typename Eng::Params& prm, const TestArgs& a, cudaStream_t stream) {
@@ -819,32 +827,54 @@ cudaError_t launch_test_f32_all(const DevTables& t, const TestArgs* a, cudaStrea
   const size_t nc = CrossEngine<kTriP>::table_bytes(prm.c) / sizeof(float4);
   prm.off_o = static_cast<uint32_t>(nv);
   prm.off_c = static_cast<uint32_t>(nv + no);
-  const size_t smem = (nv + no + nc) * sizeof(float4) +
-                      (VPIPG_TRI_TMA ? (size_t)kWarps * kStages * (2 * kWarpPts * sizeof(float) +
-                                                                  2 * sizeof(uint64_t))
-                                     : 0);
+  const bool inl = VPIPG_INLINE && t.h_cross && t.h_slab[0] && t.h_slab[1] && nv + no + nc <= kTriInlineMax;
+  const size_t smem = inl ? 0 : (nv + no + nc) * sizeof(float4);
   const uint64_t full_slices = a[0].m / kWarpPts;
   int sms = 0, per_sm = 0;
   auto form = [](const SlabTable& t) { return t.cnt[0] == 0 ? 1 : t.cnt[2] == 0 ? 2 : 0; };
   const int fv = form(t.slab[0]), fo = form(t.slab[1]);
   const int mode = fv == fo ? fv : -1;
-  auto pick = [mode](auto g) {
-    constexpr bool G = decltype(g)::value;
-    return mode == 0 ? tri_kernel<0, G> : mode == 1 ? tri_kernel<1, G>
-         : mode == 2 ? tri_kernel<2, G> : tri_kernel<-1, G>;
+  auto go = [&](auto il, const auto& params) -> cudaError_t {
+    constexpr bool I = decltype(il)::value;
+    auto kern = mode == 0 ? tri_kernel<0, I> : mode == 1 ? tri_kernel<1, I>
+              : mode == 2 ? tri_kernel<2, I> : tri_kernel<-1, I>;
+    cudaError_t e = launch_config(reinterpret_cast<const void*>(kern), kThreads, smem, &sms, &per_sm);
+    if (e != cudaSuccess) return e;
+    const uint64_t cap = (uint64_t)sms * per_sm;
+    const uint64_t want = (full_slices + kWarps - 1) / kWarps;
+    const int grid = (int)(want < cap ? want : cap);
+    kern<<<grid, kThreads, smem, stream>>>(params, a[0], a[1], a[2], full_slices);
+    return cudaGetLastError();
   };
-  auto kern = t.cross.n <= kCrossGroupMaxN ? pick(std::true_type{}) : pick(std::false_type{});
-  cudaError_t e = launch_config(reinterpret_cast<const void*>(kern), kThreads, smem, &sms, &per_sm);
-  if (e != cudaSuccess) return e;
-  const uint64_t cap = (uint64_t)sms * per_sm;
-  const uint64_t want = (full_slices + kWarps - 1) / kWarps;
-  const int grid = (int)(want < cap ? want : cap);
-  kern<<<grid, kThreads, smem, stream>>>(prm, a[0], a[1], a[2], full_slices);
-  return cudaGetLastError();
+  if (inl) {
+    TriParamsInl pi{};
+    pi.v = prm.v;
+    pi.o = prm.o;
+    pi.c = prm.c;
+    pi.off_o = prm.off_o;
+    pi.off_c = prm.off_c;
+    std::memcpy(pi.t, t.h_slab[0], nv * sizeof(float4));
+    std::memcpy(pi.t + nv, t.h_slab[1], no * sizeof(float4));
+    std::memcpy(pi.t + nv + no, t.h_cross, nc * sizeof(float4));
+    return go(std::true_type{}, pi);
+  }
+  return go(std::false_type{}, prm);
 }
 
 template <bool kNanIn, int kMode>
 cudaError_t launch_slab_mode(const DevTables& t, int engine, const TestArgs& a, cudaStream_t stream) {
+#ifndef VPIPG_SLAB_INLINE
+#define VPIPG_SLAB_INLINE 0
+#endif
+  if (VPIPG_SLAB_INLINE && t.h_slab[engine] && t.slab[engine].total / 2 <= (uint32_t)kInlineMax) {
+    using E = SlabEngine<VPIPG_SLAB_P, kNanIn, kMode, true>;
+    typename E::Params prm{};
+    prm.tab = t.slab[engine];
+    prm.ox = t.ox;
+    prm.oy = t.oy;
+    std::memcpy(prm.v, t.h_slab[engine], t.slab[engine].total * sizeof(float2));
+    return launch<E>(prm, a, stream);
+  }
   using E = SlabEngine<VPIPG_SLAB_P, kNanIn, kMode>;
   typename E::Params prm{t.slab[engine], t.ox, t.oy};
   return launch<E>(prm, a, stream);
@@ -862,9 +892,15 @@ cudaError_t launch_test_f32(const DevTables& t, int engine, const TestArgs& a,
                             cudaStream_t stream) {
   if (engine == 0) return launch_slab<false>(t, 0, a, stream);
   if (engine == 1) return launch_slab<true>(t, 1, a, stream);
-  // the standalone crossing kernel keeps the carried form at every n (the
-  // group form measured equal at n = 8 and 2.5 % slower at n = 16 there)
-  return launch<CrossEngine<VPIPG_CROSS_P, false>>(CrossParams{t.cross, t.ox, t.oy}, a, stream);
+  if (VPIPG_INLINE && t.h_cross && t.cross.n <= (uint32_t)kInlineMax) {
+    CrossParamsInl prm{};
+    prm.tab = t.cross;
+    prm.ox = t.ox;
+    prm.oy = t.oy;
+    std::memcpy(prm.v, t.h_cross, t.cross.n * sizeof(float4));
+    return launch<CrossEngine<VPIPG_CROSS_P, true>>(prm, a, stream);
+  }
+  return launch<CrossEngine<VPIPG_CROSS_P>>(CrossParams{t.cross, t.ox, t.oy}, a, stream);
 }
 
 }  // namespace vpipg

@@ -72,6 +72,10 @@ struct DevTables {
   // unit-normal supporting lines (a, b, c, 0) of the n edges, f64: the band
   // metric edge_line_distance (voronoi.cpp:73-82) of the validation kernels
   const double4* lines;
+  // host copies of the f32 tables (slab (B, C) pairs, crossing records) for
+  // launches that pass them in the kernel parameter bank; null when absent
+  const float2* h_slab[2];
+  const float4* h_cross;
 };
 
 // Written by the prep kernel, read back by the (synchronous) prepare call.

@@ -50,14 +50,14 @@ def test_kernels_use_fma_and_3way_minmax():
     assert blocks
     for body in blocks:
         assert "FMNMX3" in body and "FFMA" in body
-    # the crossing engine streams points through the bulk-copy (TMA) ring; the
-    # slab engines load them directly after an L2 prefetch (CCTL.E.PML2)
+    # every streaming kernel loads its points directly after an L2 prefetch
+    # (CCTL.E.PML2); the crossing engine's edge loop reads the parameter-bank
+    # table into uniform registers (LDCU) and its FFMAs take them as operands
     heads = [(b.split("\n")[0], b) for b in sass.split("Function :")]
-    stream = [b for h, b in heads if "stream_kernel" in h]
-    assert stream and all("UBLKCP" in b and "CrossEngine" in h for h, b in heads
-                          if "stream_kernel" in h)
-    ldg = [b for h, b in heads if "ldg_kernel" in h and "SlabEngine" in h]
+    ldg = [b for h, b in heads if "ldg_kernel" in h]
     assert ldg and all("CCTL.E.PML2" in b for b in ldg)
+    cross = [b for h, b in heads if "ldg_kernel" in h and "CrossEngineILi20ELb1E" in h]
+    assert cross and all("LDCU" in b and re.search(r"FFMA R\d+, R\d+, UR\d+, R\d+", b) for b in cross)
 
 
 def test_strerror_and_version():
