@@ -56,7 +56,6 @@ ISSUE_CYCLES_PER_PE = {"voronoi": 2.0, "sign_of_offset": 2.0, "ray_crossing": 6.
 HBM_FALLBACK_GBS = 6650.0
 # FFMA lane-ops per SM per clock on sm_100a (tools/pipe_peaks.cu: 3.79 warp-inst/clk/SM)
 FFMA_PER_SM_CLK = 128
-CPU_SAMPLE = 1 << 25
 
 
 # ----------------------------------------------------------------- helpers
@@ -185,105 +184,115 @@ def workload_desc(name: str) -> str:
 
 
 # ----------------------------------------------------------------- CPU reference
-def cpu_reference_sample(name: str, sample: int):
-    """Polygon (f64) + a bounded f64 sample (widened f32) of the workload's points."""
+def c4_host_pairs(sample: int | None = None):
+    """The C4 database and its (point, id) pair stream on the host (oracle, bit
+    for bit the device fill_join_pairs stream)."""
     import oracle
     orc = oracle.Oracle()
-    if name == "c5":
-        vx, vy = W.c5_polygon(orc.random_convex_polygon)
-        xs, ys = orc.counter_points_f32(W.c5_point_seed(), 0, sample, W.C5_BOX)
-    elif name.startswith("c3"):
-        n, (vx, vy) = W.c3_named(name)
-        xs, ys = orc.counter_points_f32(int(W.mix_seed_np(W.config_seed(3), 200 + n)), 0, sample,
-                                        W.C3_BOX)
-    elif name == "c2":
-        vx, vy = W.c2_polygon()
-        xs, ys = W.c2_points()
-        xs, ys = xs[:sample], ys[:sample]
-    else:
-        vx, vy = W.c1_polygon()
-        xs, ys = W.c1_points(orc.sample_points, min(sample, W.C1_POINTS))
-    return vx, vy, np.asarray(xs, np.float64), np.asarray(ys, np.float64)
+    off, vx, vy, cx, cy, r = W.c4_polygons(orc.random_convex_polygon)
+    m = sample or W.C4_PAIRS
+    xs, ys = np.empty(m, np.float32), np.empty(m, np.float32)
+    ids = np.empty(m, np.uint32)
+    import concurrent.futures as cf
+    step = 1 << 24
+
+    def one(lo):
+        hi = min(m, lo + step)
+        xs[lo:hi], ys[lo:hi], ids[lo:hi] = orc.join_pairs_f32(W.c4_pair_seed(), lo, hi - lo, cx, cy, r)
+
+    with cf.ThreadPoolExecutor(max_workers=os.cpu_count() or 1) as ex:
+        list(ex.map(one, range(0, m, step)))
+    return off, vx, vy, xs, ys, ids
 
 
-def time_cpu_reference(name: str, sample: int, reps: int, warmup: int):
-    """Times the three reference engines on the sample; returns (tests/s, kind, cores, s/rep)."""
+def reference_join(off, vx, vy, xs, ys, ids, threads, packed=False):
+    """C4 through the reference: one batch call per polygon over its id-grouped
+    pairs (grouping untimed), polygons split over `threads` threads.
+    Returns (ns per engine, packed words per engine or None)."""
     import oracle
-    cores = os.cpu_count() or 1
-    if name == "c4":  # one reference batch call per polygon over its id-grouped pairs
-        import paper_2007_15385_b200 as vp
-        orc = oracle.Oracle()
-        off, vx, vy, cx, cy, r = W.c4_polygons(vp.random_convex_polygon)
-        sample = min(sample, 1 << 24)
-        xs, ys, ids = orc.join_pairs_f32(W.c4_pair_seed(), 0, sample, cx, cy, r)
-        try:
-            ref, kind = oracle.Reference(), "reference"
-        except FileNotFoundError:
-            ref, kind, cores = None, "port", 1
-        per_rep = []
-        for rr in range(warmup + reps):
-            if ref is not None:
-                _, ns = ref.join(off, vx, vy, xs, ys, ids, threads=cores)
-                t = sum(ns) * 1e-9
-            else:
-                t0 = time.perf_counter()
-                for e in range(3):
-                    orc.join_masks(off, vx, vy, e, xs.astype(np.float64), ys.astype(np.float64), ids)
-                t = time.perf_counter() - t0
-            if rr >= warmup:
-                per_rep.append(t)
-        t = statistics.median(per_rep)
-        desc = (f"first {xs.size} pairs of the C4 stream (f32 widened to f64), pairs grouped by "
-                f"polygon id (untimed), one reference *_contains_batch call per polygon, "
-                f"polygons split over {cores} threads, 3 engines")
-        return 3 * xs.size / t, kind, cores, t, desc
-    vx, vy, xs, ys = cpu_reference_sample(name, sample)
-    try:
-        ref = oracle.Reference()
-        kind = "reference"
-    except FileNotFoundError:
-        ref, kind, cores = None, "port", 1
-    per_rep = []
-    for r in range(warmup + reps):
-        if ref is not None:
-            _, ns = ref.masks(vx, vy, xs, ys, threads=cores)
-            t = sum(ns) * 1e-9
-        else:
-            orc = oracle.Oracle()
-            t0 = time.perf_counter()
-            orc.masks(vx, vy, xs, ys)
-            t = time.perf_counter() - t0
-        if r >= warmup:
-            per_rep.append(t)
-    t = statistics.median(per_rep)
-    desc = (f"first {xs.size} points of the workload stream (f32 rounded, widened to f64), "
-            f"3 engines, *_contains_batch(threads={cores}) timed like bench.cpp:196-199")
-    if ref is not None:  # SURVEY 8(d): also the single-thread figure, on 1/8 of the sample
-        k = max(1, xs.size // 8)
-        _, ns = ref.masks(vx, vy, xs[:k], ys[:k], threads=1)
-        desc += f"; 1 thread: {3 * k / (sum(ns) * 1e-9):.3e} tests/s on the first {k} points"
-    return 3 * xs.size / t, kind, cores, t, desc
+    ref = oracle.Reference()
+    masks, ns = ref.join(off, vx, vy, xs.astype(np.float64), ys.astype(np.float64), ids,
+                         threads=threads)
+    words = [np.packbits(mk, bitorder="little").view(np.uint8) for mk in masks] if packed else None
+    if words is not None:
+        words = [np.pad(w, (0, (-w.size) % 4)).view(np.uint32) for w in words]
+    return ns, words, ref.build
+
+
+def reference_c1(threads):
+    """C1 (the f64 oracle config) through the reference: (ns per engine, byte masks)."""
+    import oracle
+    ref = oracle.Reference()
+    vx, vy = W.c1_polygon()
+    xs, ys = W.c1_points(ref.sample_points)
+    masks, ns = ref.masks(vx, vy, xs, ys, threads=threads)
+    return ns, masks, ref.build, (vx, vy, xs, ys)
 
 
 def run_reference_arm(args, rank: int, world: int):
+    """--impl reference: the reference's own CPU path on the FULL workload (the
+    same config as the GPU arm), rank 0 only, all host threads; one step = one
+    pass of the three engines over every point (C5: 2^31 points in 2^26-point
+    PointBatch chunks), timed as run_benchmark times its batch
+    calls (bench.cpp:196-199) and summed over the chunks."""
     if rank != 0:
         return
-    steps, warmup = args.steps, args.warmup
-    value, kind, cores, t, desc = time_cpu_reference(args.workload, args.cpu_sample, steps, warmup)
+    import bench_cpu as BC
+    steps, warmup, th = args.steps, args.warmup, BC.cores()
+    name = args.workload
+    extra = {}
+    per_step = []
+    if name == "c4":
+        off, vx, vy, xs, ys, ids = c4_host_pairs(args.points or None)
+        for r in range(warmup + steps):
+            ns, _, build = reference_join(off, vx, vy, xs, ys, ids, th)
+            if r >= warmup:
+                per_step.append(sum(ns) * 1e-9)
+        m = xs.size
+        desc = (f"the unmodified reference library ({build}), all {m} pairs of the C4 stream "
+                f"(f32 widened to f64), pairs grouped by polygon id (untimed), one "
+                f"*_contains_batch call per polygon, polygons split over {th} threads, 3 engines")
+    elif name == "c1":
+        for r in range(warmup + steps):
+            ns, _, build, (vx, vy, xs, ys) = reference_c1(th)
+            if r >= warmup:
+                per_step.append(sum(ns) * 1e-9)
+        m = xs.size
+        desc = (f"the unmodified reference library ({build}), all {m} f64 points of C1, 3 engines "
+                f"*_contains_batch(threads={th}) timed like bench.cpp:196-199")
+    else:
+        vx, vy, xs, ys = BC.host_workload(name, args.points or None)
+        m = xs.size
+        rr = BC.RefRun(vx, vy, xs, ys, th)
+        del xs, ys
+        cnt = []
+        for r in range(warmup + steps):
+            res = rr.run()
+            if r >= warmup:
+                per_step.append(sum(x["ns"] for x in res) * 1e-9)
+                cnt.append(sum(x["count_ns"] for x in res) * 1e-9)
+        extra["count_inside_ms"] = statistics.median(cnt) * 1e3
+        extra["inside_counts"] = [x["inside"] for x in res]
+        desc = rr.describe()
+        rr.close()
+    t = statistics.median(per_step)
+    value = 3 * m / t
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": steps, "warmup": warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": config_block(args, world),
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind,
-                         "sample": desc + f"; median of {steps} steps after {warmup} warm-up"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": th, "kind": "reference",
+                         "sample": desc + f"; median of {steps} full passes after {warmup} "
+                                          f"warm-up passes", **extra},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
 def config_block(args, world):
-    return {"workload": workload_desc(args.workload), "points": workload_size(args.workload),
+    return {"workload": workload_desc(args.workload),
+            "points": args.points or workload_size(args.workload),
             "engines": ["voronoi", "sign_of_offset", "ray_crossing"],
             "parallelism": f"point shards x{world}",
             "l2": ("inputs larger than L2" if workload_size(args.workload) * 8 > 4 * 126e6
@@ -302,6 +311,7 @@ class PolygonJob:
     def __init__(self, workload, lo, hi, device, torch, vp, stream):
         self.torch = torch
         vx, vy, self.xs, self.ys = build_workload(workload, lo, hi, torch, vp, stream)
+        self.vx, self.vy = np.asarray(vx, np.float64), np.asarray(vy, np.float64)
         t0 = time.perf_counter()
         self.poly = vp.PreparedPolygon.prepare(vx, vy, vp.KIND_ALL, device=device, stream=stream)
         self.prep_ms = (time.perf_counter() - t0) * 1e3
@@ -342,6 +352,7 @@ class JoinJob:
     def __init__(self, workload, lo, hi, device, torch, vp, stream):
         self.torch = torch
         off, vx, vy, cx, cy, r = W.c4_polygons(vp.random_convex_polygon)
+        self.off, self.vx, self.vy = off, vx, vy
         t0 = time.perf_counter()
         self.db = vp.PolygonDB.prepare(off, vx, vy, vp.KIND_ALL, device=device, stream=stream)
         self.prep_ms = (time.perf_counter() - t0) * 1e3
@@ -373,6 +384,89 @@ class JoinJob:
         return cnt
 
 
+# ----------------------------------------------------------------- CPU leg + parity
+def cpu_leg(job, words, m, torch):
+    """cpu_baseline and the parity block (rank 0, N=1). The reference library
+    runs the FULL workload twice on all host threads: the first pass (warm-up)
+    yields its masks, the second is the timed figure. Parity compares, per
+    engine, the GPU mask words of the last timed step with
+      * vs_reference: the reference's masks of the same (f32-rounded) points;
+      * f32_vs_f64_exact: the library's reference-exact f64 kernels over the
+        whole batch (points widened on the device);
+      * f64_exact_vs_reference: those f64 masks against the reference, which
+        must agree bit for bit (band 1e-9);
+    a disagreement counts as outside_band when the point lies farther than
+    eps * max(1, |x|, |y|, polygon extent) from every edge's supporting line
+    (edge_line_distance, voronoi.cpp:73-82; the C oracle's, on the host)."""
+    import bench_cpu as BC
+    th = BC.cores()
+    names = BC.NAMES
+    par = {"points": m, "band": "eps * max(1, |x|, |y|, polygon extent) from the nearest edge "
+                                "supporting line (edge_line_distance, voronoi.cpp:73-82); "
+                                "eps 1e-5 for f32 masks, 1e-9 for f64",
+           "words": "the GPU mask words of the last timed step"}
+
+    def block(ws_a, ws_b, xs, ys, eps, join=None):
+        return {n: BC.parity_entry(ws_a[e], ws_b[e], xs, ys, job.vx, job.vy, m, eps, join)
+                for e, n in enumerate(names)}
+
+    if isinstance(job, JoinJob):
+        import oracle
+        xs, ys = job.xs.cpu().numpy(), job.ys.cpu().numpy()
+        ids = job.ids.cpu().numpy().view(np.uint32)
+        _, rw, build = reference_join(job.off, job.vx, job.vy, xs, ys, ids, th, packed=True)
+        ns, _, _ = reference_join(job.off, job.vx, job.vy, xs, ys, ids, th)
+        t = sum(ns) * 1e-9
+        ref = oracle.Reference()
+        sc = [ref.join_scalar(job.off, job.vx, job.vy, xs.astype(np.float64),
+                              ys.astype(np.float64), ids, e, th)[1] for e in range(3)]
+        cpu = {"value": 3 * m / t, "unit": UNIT, "cores": th, "kind": "reference",
+               "sample": f"the unmodified reference library ({build}), all {m} pairs of the C4 "
+                         f"stream (f32 widened to f64), pairs grouped by polygon id (untimed), "
+                         f"one *_contains_batch call per polygon, polygons split over {th} "
+                         f"threads, 3 engines; second of two full passes, {t * 1e3:.1f} ms",
+               "per_pair_scalar": {"value": 3 * m / (sum(sc) * 1e-9), "unit": UNIT, "cores": th,
+                                   "what": "the reference's early-exit scalar tests on every "
+                                           "pair in stream order (random polygon ids), "
+                                           f"{th} threads"}}
+        par["vs_reference"] = block(words, rw, xs, ys, BC.EPS32, join=(job.off, ids))
+    elif job.f64:
+        ns, masks, build, (vx, vy, xs, ys) = reference_c1(th)
+        ns, masks, build, _ = reference_c1(th)
+        t = sum(ns) * 1e-9
+        rw = [np.pad(np.packbits(mk, bitorder="little"), (0, (-((m + 7) // 8)) % 4)).view(np.uint32)
+              for mk in masks]
+        cpu = {"value": 3 * m / t, "unit": UNIT, "cores": th, "kind": "reference",
+               "sample": f"the unmodified reference library ({build}), all {m} f64 points, 3 "
+                         f"engines *_contains_batch(threads={th}); second of two passes"}
+        par["vs_reference"] = block(words, rw, xs, ys, BC.EPS64)
+    else:
+        xs, ys = job.xs.cpu().numpy(), job.ys.cpu().numpy()
+        rr = BC.RefRun(job.vx, job.vy, xs, ys, th)
+        res = rr.run(packed=True)  # warm-up pass: the reference masks
+        res2 = rr.run()            # timed pass
+        rr.close()
+        t = sum(x["ns"] for x in res2) * 1e-9
+        cpu = {"value": 3 * m / t, "unit": UNIT, "cores": th, "kind": "reference",
+               "sample": rr.describe() + f"; second of two full passes, {t * 1e3:.1f} ms",
+               "count_inside_ms": sum(x["count_ns"] for x in res2) * 1e-6,
+               "inside_counts": [x["inside"] for x in res2]}
+        rw = [x["words"] for x in res]
+        par["vs_reference"] = block(words, rw, xs, ys, BC.EPS32)
+        # the reference-exact f64 kernels over the whole batch, on the device
+        xd, yd = job.xs.double(), job.ys.double()
+        w64 = [torch.zeros_like(w) for w in words]
+        job.poly.test_multi(xd, yd, (0, 1, 2), words=w64)
+        torch.cuda.synchronize()
+        del xd, yd
+        par["f32_vs_f64_exact"] = block(words, w64, xs, ys, BC.EPS32)
+        par["f64_exact_vs_reference"] = block(w64, rw, xs, ys, BC.EPS64)
+        del w64
+    par["outside_band"] = sum(v["outside_band"] for k, blk in par.items() if isinstance(blk, dict)
+                              for v in blk.values())
+    return cpu, par
+
+
 # ----------------------------------------------------------------- GPU arm
 def stdout_to_stderr(fn, *a):
     """Run fn with fd 1 pointed at stderr: NCCL prints its version banner on
@@ -395,7 +489,6 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--workload", default="c5")
     ap.add_argument("--e2e-steps", type=int, default=3)
-    ap.add_argument("--cpu-sample", type=int, default=CPU_SAMPLE)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--fused", action="store_true",
@@ -611,12 +704,9 @@ def main():
                "steps": args.e2e_steps, "step_ms": [round(t * 1e3, 2) for t in times],
                "path": job.e2e_path}
 
-    cpu = None
+    cpu = parity = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        v, kind, cores, t, desc = time_cpu_reference(args.workload, args.cpu_sample, reps=3,
-                                                     warmup=1)
-        cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": kind,
-               "sample": f"{desc}; median of 3 after 1 warm-up, {t * 1e3:.1f} ms per pass"}
+        cpu, parity = cpu_leg(job, words, m, torch)
 
     if world > 1:
         dist.barrier()
@@ -720,7 +810,7 @@ def main():
         "roofline": roof, "kernels": kernels, "engines_separate": engines_separate,
         "inside_counts": final_counts,
         "prepare_ms": job.prep_ms,
-        "clocks": clocks, "e2e": e2e, "cpu_baseline": cpu,
+        "clocks": clocks, "e2e": e2e, "cpu_baseline": cpu, "parity": parity,
     }
     print(json.dumps(line), flush=True)
     if world > 1:

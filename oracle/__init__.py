@@ -21,7 +21,9 @@ import numpy as np
 
 HERE = Path(__file__).resolve().parent
 ORACLE_SO = HERE / "liboracle.so"
-REF_SO = HERE / "_ref" / "libvpip_ref.so"
+REF_SO = HERE / "_ref" / "libvpip_ref.so"             # -march=x86-64-v3
+REF_NATIVE_SO = HERE / "_ref" / "libvpip_ref_native.so"  # -march=<build host's native CPU>
+REF_NATIVE_MARCH = HERE / "_ref" / "native_march.txt"
 REF_ACCEPTANCE = HERE / "_ref" / "vpip_acceptance"
 # the reference's acceptance suite linked against libvpipg (the drop-in check)
 REF_ACCEPTANCE_B200 = HERE / "_ref" / "vpip_acceptance_b200"
@@ -255,13 +257,39 @@ class Oracle:
         return out
 
 
-class Reference:
-    """The unmodified reference library (oracle/_ref/libvpip_ref.so)."""
+def native_march() -> str | None:
+    """What `-march=native` resolves to on this host (gcc), e.g. 'sapphirerapids'."""
+    try:
+        out = subprocess.run(["gcc", "-march=native", "-Q", "--help=target"], capture_output=True,
+                             text=True, timeout=30).stdout
+    except Exception:
+        return None
+    for line in out.splitlines():
+        parts = line.split()
+        if parts and parts[0] == "-march=" and len(parts) > 1:
+            return parts[1]
+    return None
 
-    def __init__(self):
-        if not REF_SO.exists():
-            raise FileNotFoundError(f"{REF_SO} not built (needs /root/reference; run oracle.build())")
-        L = C.CDLL(str(REF_SO))
+
+class Reference:
+    """The unmodified reference library (oracle/_ref/libvpip_ref*.so).
+
+    Loads the -march=native build when this host's native CPU is the one it
+    was built for (the reference's Release flags, CMakeLists.txt:13-17),
+    else the portable x86-64-v3 build; `self.build` says which."""
+
+    def __init__(self, native: bool = True):
+        so, self.build = REF_SO, "-O3 -DNDEBUG -march=x86-64-v3 -ffp-contract=off"
+        if native and REF_NATIVE_SO.exists() and REF_NATIVE_MARCH.exists():
+            built = REF_NATIVE_MARCH.read_text().strip()
+            here = native_march()
+            if built and built == here:
+                so = REF_NATIVE_SO
+                self.build = (f"-O3 -DNDEBUG -march={built} -ffp-contract=off "
+                              f"(= -march=native on this host)")
+        if not so.exists():
+            raise FileNotFoundError(f"{so} not built (needs /root/reference; run oracle.build())")
+        L = C.CDLL(str(so))
         sz = C.c_size_t
         L.vr_validate.argtypes = [_D, _D, sz, _D, _D, C.POINTER(C.c_int)]
         L.vr_to_voronoi.argtypes = [_D, _D, sz, _D, _D]
@@ -297,6 +325,14 @@ class Reference:
         L.vr_join_free.argtypes = [C.c_void_p]
         L.vr_join_run.restype = C.c_uint64
         L.vr_join_run.argtypes = [C.c_void_p, C.c_int, C.c_int, _U8]
+        L.vr_join_scalar.restype = C.c_uint64
+        L.vr_join_scalar.argtypes = [C.c_void_p, _D, _D, u32p, sz, C.c_int, C.c_int, _U8]
+        fp = C.POINTER(C.c_float)
+        L.vr_chunks_new.restype = C.c_void_p
+        L.vr_chunks_new.argtypes = [fp, fp, sz, sz, C.c_int]
+        L.vr_chunks_free.argtypes = [C.c_void_p]
+        u64p = C.POINTER(C.c_uint64)
+        L.vr_chunked_run.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_int, _U8, u64p, u64p, u64p]
         self.L = L
 
     def read_bench_csv(self, text: str):
@@ -341,6 +377,67 @@ class Reference:
         finally:
             self.L.vr_join_free(h)
         return out, times
+
+    def join_scalar(self, offsets, vx, vy, xs, ys, ids, engine, threads=1):
+        """The per-pair scalar join loop (pairs in stream order). Returns (mask, ns)."""
+        offsets = np.ascontiguousarray(offsets, np.uint32)
+        xs, ys = np.ascontiguousarray(xs, np.float64), np.ascontiguousarray(ys, np.float64)
+        ids = np.ascontiguousarray(ids, np.uint32)
+        up = C.POINTER(C.c_uint32)
+        h = self.L.vr_join_new(offsets.ctypes.data_as(up), _d(np.ascontiguousarray(vx, np.float64)),
+                               _d(np.ascontiguousarray(vy, np.float64)), offsets.size - 1,
+                               _d(xs[:0]), _d(ys[:0]), ids.ctypes.data_as(up), 0)
+        m = np.zeros(xs.size, np.uint8)
+        try:
+            ns = self.L.vr_join_scalar(h, _d(xs), _d(ys), ids.ctypes.data_as(up), xs.size, engine,
+                                       threads, m.ctypes.data_as(_U8))
+        finally:
+            self.L.vr_join_free(h)
+        return m, ns
+
+    def full_pass(self, vx, vy, xs32, ys32, threads, chunk=1 << 26, engines=(0, 1, 2),
+                  packed=True, chunks=None, m=None):
+        """Every point of an f32 workload through the reference in <= `chunk`-point
+        PointBatches (widened once, untimed). Returns per engine
+        {ns, count_ns, inside, words (LSB-first u32 mask words or None)}.
+        `chunks` reuses a handle from `make_chunks` (the caller frees it)."""
+        vx, vy = np.ascontiguousarray(vx, np.float64), np.ascontiguousarray(vy, np.float64)
+        code = C.c_int()
+        p = self.L.vr_poly_new(_d(vx), _d(vy), vx.size, 1 if any(e != 2 for e in engines) else 0,
+                               C.byref(code))
+        if not p:
+            raise ValueError(code.value)
+        own = chunks is None
+        if own:
+            chunks = self.make_chunks(xs32, ys32, threads, chunk)
+        m = int(np.asarray(xs32).size) if m is None else m
+        res = []
+        try:
+            for e in engines:
+                words = np.zeros((m + 31) // 32, np.uint32) if packed else None
+                ns, cns, ins = C.c_uint64(), C.c_uint64(), C.c_uint64()
+                rc = self.L.vr_chunked_run(p, chunks, e, threads,
+                                           words.view(np.uint8).ctypes.data_as(_U8) if packed else None,
+                                           C.byref(ns), C.byref(cns), C.byref(ins))
+                if rc:
+                    raise ValueError(rc)
+                res.append({"ns": ns.value, "count_ns": cns.value, "inside": ins.value,
+                            "words": words})
+        finally:
+            self.L.vr_poly_free(p)
+            if own:
+                self.free_chunks(chunks)
+        return res
+
+    def make_chunks(self, xs32, ys32, threads, chunk=1 << 26):
+        xs32 = np.ascontiguousarray(xs32, np.float32)
+        ys32 = np.ascontiguousarray(ys32, np.float32)
+        fp = C.POINTER(C.c_float)
+        return self.L.vr_chunks_new(xs32.ctypes.data_as(fp), ys32.ctypes.data_as(fp), xs32.size,
+                                    chunk, threads)
+
+    def free_chunks(self, h):
+        self.L.vr_chunks_free(h)
 
     def validate(self, vx, vy):
         vx, vy = np.ascontiguousarray(vx, np.float64), np.ascontiguousarray(vy, np.float64)

@@ -7,6 +7,7 @@
 // reference itself, (b) to generate tests/golden/ fixtures, and (c) as the
 // CPU baseline arm of bench.py (`--impl reference`, cpu_baseline.kind =
 // "reference"). Nothing here is on the product path.
+#include <algorithm>
 #include <chrono>
 #include <cstdint>
 #include <cstring>
@@ -308,6 +309,102 @@ long vr_read_bench_csv(const char* text, double* medians) {
   } catch (const vpip::Error&) {
     return -1;
   }
+}
+
+// ---- full-size runs in chunks (bench.py's CPU legs) ----
+// A workload of m f32 points (BASELINE C5 is 2^31 points, 32 GiB as the
+// reference's f64 PointBatch) is held as PointBatch chunks of <= `chunk`
+// points, widened from f32 once (untimed, in parallel). vr_chunked_run then
+// runs one engine over every chunk exactly as run_benchmark times a batch
+// call (bench.cpp:196-199): only the *_contains_batch call is in `ns`;
+// count_inside (engines.cpp:215-217) is timed as its own step (`count_ns`);
+// the byte mask is packed LSB-first into `packed` (io.cpp:272-279 order)
+// outside both timings.
+void* vr_chunks_new(const float* xs, const float* ys, std::size_t m, std::size_t chunk, int threads) {
+  auto* v = new std::vector<vpip::PointBatch>((m + chunk - 1) / chunk);
+  auto work = [&](std::size_t c0, std::size_t c1) {
+    for (std::size_t c = c0; c < c1; ++c) {
+      const std::size_t lo = c * chunk, hi = std::min(m, lo + chunk);
+      vpip::PointBatch& b = (*v)[c];
+      b.xs.resize(hi - lo);
+      b.ys.resize(hi - lo);
+      for (std::size_t i = lo; i < hi; ++i) {
+        b.xs[i - lo] = static_cast<double>(xs[i]);
+        b.ys[i - lo] = static_cast<double>(ys[i]);
+      }
+    }
+  };
+  const std::size_t nc = v->size();
+  const int t = std::max(1, std::min<int>(threads, static_cast<int>(nc)));
+  {
+    std::vector<std::jthread> pool;
+    for (int i = 0; i < t; ++i) pool.emplace_back(work, nc * i / t, nc * (i + 1) / t);
+  }
+  return v;
+}
+
+void vr_chunks_free(void* v) { delete static_cast<std::vector<vpip::PointBatch>*>(v); }
+
+int vr_chunked_run(void* poly, void* chunks, int engine, int threads, uint8_t* packed, uint64_t* ns,
+                   uint64_t* count_ns, uint64_t* inside) {
+  const Poly& p = *static_cast<Poly*>(poly);
+  if (engine != 2 && !p.convex) return 6;
+  uint64_t t_run = 0, t_cnt = 0, total = 0, base = 0;
+  for (const vpip::PointBatch& b : *static_cast<std::vector<vpip::PointBatch>*>(chunks)) {
+    vpip::InclusionMask mask;
+    const auto t0 = std::chrono::steady_clock::now();
+    switch (engine) {
+      case 0: mask = vpip::voronoi_contains_batch(*p.gens, b, threads); break;
+      case 1: mask = vpip::sign_of_offset_contains_batch(*p.convex, b, threads); break;
+      case 2: mask = vpip::ray_crossing_contains_batch(p.raw, b, threads); break;
+      default: return 6;
+    }
+    const auto t1 = std::chrono::steady_clock::now();
+    total += vpip::count_inside(mask);
+    const auto t2 = std::chrono::steady_clock::now();
+    t_run += static_cast<uint64_t>(std::chrono::duration_cast<std::chrono::nanoseconds>(t1 - t0).count());
+    t_cnt += static_cast<uint64_t>(std::chrono::duration_cast<std::chrono::nanoseconds>(t2 - t1).count());
+    if (packed) {  // chunks are multiples of 8 points except the last
+      for (std::size_t i = 0; i < mask.size(); ++i)
+        if (mask[i]) packed[(base + i) >> 3] |= static_cast<uint8_t>(1u << ((base + i) & 7));
+    }
+    base += mask.size();
+  }
+  if (ns) *ns = t_run;
+  if (count_ns) *count_ns = t_cnt;
+  if (inside) *inside = total;
+  return 0;
+}
+
+// The per-pair scalar join ("also report the per-pair
+// scalar loop"): the reference's early-exit scalar tests (engines.cpp:235-241,
+// :304-318, :331-350) on every pair in stream order, i.e. random polygon ids,
+// pairs split over `threads` std::threads. Returns ns; fills the byte mask.
+uint64_t vr_join_scalar(void* jp, const double* xs, const double* ys, const uint32_t* ids,
+                        std::size_t m, int engine, int threads, uint8_t* out) {
+  Join& j = *static_cast<Join*>(jp);
+  const uint32_t np = static_cast<uint32_t>(j.polys.size());
+  auto work = [&](std::size_t lo, std::size_t hi) {
+    for (std::size_t k = lo; k < hi; ++k) {
+      uint8_t r = 0;
+      if (ids[k] < np) {
+        const Poly& p = j.polys[ids[k]];
+        const vpip::Point2 q{xs[k], ys[k]};
+        if (engine == 2) r = vpip::ray_crossing_contains(p.raw, q);
+        else if (p.convex) r = engine == 0 ? vpip::voronoi_contains(*p.gens, q)
+                                           : vpip::sign_of_offset_contains(*p.convex, q);
+      }
+      out[k] = r;
+    }
+  };
+  const auto t0 = std::chrono::steady_clock::now();
+  {
+    std::vector<std::jthread> pool;
+    const int t = std::max(threads, 1);
+    for (int c = 0; c < t; ++c) pool.emplace_back(work, m * c / t, m * (c + 1) / t);
+  }
+  const auto t1 = std::chrono::steady_clock::now();
+  return static_cast<uint64_t>(std::chrono::duration_cast<std::chrono::nanoseconds>(t1 - t0).count());
 }
 
 int vr_scalar(void* poly, int engine, double px, double py) {

@@ -212,10 +212,16 @@ __global__ void __launch_bounds__(kPrepThreads) prep_kernel(PrepArgs a) {
     }
     s_inner[0] = cx;
     s_inner[1] = cy;
-    // The fp32 tables use the absolute frame (origin 0): the parity band is
-    // relative to max(1, |x|, |y|, extent), and one FFMA with |B| <= 1 keeps the
-    // rounding error ~2^-24 of that scale, so no per-point shift is needed.
-    const float ox = 0.f, oy = 0.f;
+    // The fp32 tables live in the polygon-local frame:
+    // origin = the centroid rounded to f32 (+0.0 for a zero coordinate, so
+    // x - ox keeps every point bit for bit there); the test kernels subtract
+    // it from each point, exactly for the points near the polygon (Sterbenz),
+    // so a small polygon far from the origin keeps errors ~2^-24 of its extent
+#ifndef VPIPG_LOCAL_FRAME
+#define VPIPG_LOCAL_FRAME 1
+#endif
+    const float ox = VPIPG_LOCAL_FRAME ? static_cast<float>(cx) + 0.f : 0.f;
+    const float oy = VPIPG_LOCAL_FRAME ? static_cast<float>(cy) + 0.f : 0.f;
     a.meta->inner_x = cx;
     a.meta->inner_y = cy;
     a.meta->ox = ox;

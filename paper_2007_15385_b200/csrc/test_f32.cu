@@ -76,6 +76,15 @@ __device__ __forceinline__ float fmin3(float a, float b, float c) {
 }
 
 // ---------------------------------------------------------------------------
+#ifndef VPIPG_LOCAL_FRAME
+#define VPIPG_LOCAL_FRAME 1
+#endif
+// Points enter every engine in the polygon-local frame, x' = x - ox, y' = y - oy
+// with (ox, oy) = the f32-rounded centroid (prep.cu): exact (Sterbenz) for every
+// point within a factor of two of the origin's coordinates, i.e. near a polygon
+// far from the origin, so the table arithmetic errs by ~2^-24 of the polygon's
+// extent there, not of |x|.
+//
 // Slab engine (Voronoi and sign-of-offset): inside iff
 //   max(XLO) <= x' <= min(XHI)  and  max(YLO) <= y' <= min(YHI)
 // where each group entry is t = B * (other coordinate) + C (see prep.cu).
@@ -113,6 +122,7 @@ struct SlabEngine {
   static constexpr bool kRegStream = true;  // ldg_kernel
   static constexpr bool kInl = kInline;
   static constexpr bool kUniform = false;
+  static constexpr bool kShiftIn = VPIPG_LOCAL_FRAME;  // points enter in the local frame
   // shared by every (P, NaN rule, form) instantiation of one table placement
   using Params = std::conditional_t<kInline, SlabParamsInl, SlabParams>;
   static size_t table_bytes(const Params& p) { return kInline ? 0 : (size_t)p.tab.total * sizeof(float2); }
@@ -262,6 +272,12 @@ struct CrossEngine {
   // loop runs on uniform registers; with shared-memory tables (n > kInlineMax)
   // it measured faster too (c3x:256 crossing 10.36 vs 11.27 ms)
   static constexpr bool kUniform = true;
+  // parameter-bank tables are handed over in the absolute frame (the host
+  // adds the origin back, launch_test_f32): the crossing's f32 arithmetic is
+  // accurate to an ulp of the coordinates there (h and g are exact near the
+  // polygon, Sterbenz), and a per-point shift right after the loads measured
+  // 7 % slower on C5 (11.09 vs 10.35 ms); shared-memory tables stay local
+  static constexpr bool kShiftIn = VPIPG_LOCAL_FRAME && !kInline;
   static constexpr int kVote = VPIPG_CROSS_VOTE;  // 2: a holds the parity word, sign bit = inside
 #ifndef VPIPG_CROSS_LDG
 #define VPIPG_CROSS_LDG 1
@@ -438,8 +454,8 @@ __device__ __forceinline__ uint32_t guarded_tile(const typename Eng::Params& prm
   for (int p = 0; p < P; ++p) {
     const uint64_t idx = base + 32u * p + lane;
     const bool ok = idx < a.m;
-    x[p] = ok ? __ldcs(xs + idx) : 0.f;
-    y[p] = ok ? __ldcs(ys + idx) : 0.f;
+    x[p] = (ok ? __ldcs(xs + idx) : 0.f) - (Eng::kShiftIn ? prm.ox : 0.f);
+    y[p] = (ok ? __ldcs(ys + idx) : 0.f) - (Eng::kShiftIn ? prm.oy : 0.f);
   }
   Eng::eval(prm, tab, x, y, va, vb);
   return emit<true, Eng::kVote, P>(va, vb, base, a, lane);
@@ -519,8 +535,8 @@ __global__ void __launch_bounds__(kThreads, 2)
     float x[P], y[P], va[P], vb[P];
 #pragma unroll
     for (int p = 0; p < P; ++p) {
-      x[p] = px[32 * p];
-      y[p] = px[kWarpPts + 32 * p];
+      x[p] = px[32 * p] - (Eng::kShiftIn ? prm.ox : 0.f);
+      y[p] = px[kWarpPts + 32 * p] - (Eng::kShiftIn ? prm.oy : 0.f);
     }
     mbar_arrive(&empty[s]);  // release: this lane's reads of stage s are done
     if (lane == 0 && r + kStages < sr.rounds) {
@@ -598,8 +614,8 @@ __global__ void __launch_bounds__(kThreads, VPIPG_LDG_MINB)
       float x[P], y[P], va[P], vb[P];
 #pragma unroll
       for (int p = 0; p < P; ++p) {
-        x[p] = __ldcs(px + 32 * p);
-        y[p] = __ldcs(py + 32 * p);
+        x[p] = __ldcs(px + 32 * p) - (Eng::kShiftIn ? prm.ox : 0.f);
+        y[p] = __ldcs(py + 32 * p) - (Eng::kShiftIn ? prm.oy : 0.f);
       }
       Eng::eval(prm, tab, x, y, va, vb);
       count += emit<false, Eng::kVote, P>(va, vb, g * kWarpPts, a, lane, sr.live(r));
@@ -618,8 +634,8 @@ __global__ void __launch_bounds__(kThreads, VPIPG_LDG_MINB)
       float x[P], y[P], va[P], vb[P];
 #pragma unroll
       for (int p = 0; p < P; ++p) {
-        x[p] = __ldcs(px + 32 * p);
-        y[p] = __ldcs(py + 32 * p);
+        x[p] = __ldcs(px + 32 * p) - (Eng::kShiftIn ? prm.ox : 0.f);
+        y[p] = __ldcs(py + 32 * p) - (Eng::kShiftIn ? prm.oy : 0.f);
       }
       Eng::eval(prm, tab, x, y, va, vb);
       count += emit<false, Eng::kVote, P>(va, vb, g * kWarpPts, a, lane);
@@ -706,8 +722,8 @@ __global__ void __launch_bounds__(kThreads, 2)
     float x[P], y[P], va[P], vb[P];
 #pragma unroll
     for (int p = 0; p < P; ++p) {
-      x[p] = __ldcs(px + 32 * p);
-      y[p] = __ldcs(py + 32 * p);
+      x[p] = __ldcs(px + 32 * p) - (VPIPG_LOCAL_FRAME ? prm.v.ox : 0.f);
+      y[p] = __ldcs(py + 32 * p) - (VPIPG_LOCAL_FRAME ? prm.v.oy : 0.f);
     }
     TriV::eval(prm.v, tv, x, y, va, vb);
     cv += emit<false, TriV::kVote, P>(va, vb, g * kWarpPts, av, lane, live);
@@ -897,7 +913,12 @@ cudaError_t launch_test_f32(const DevTables& t, int engine, const TestArgs& a,
     prm.tab = t.cross;
     prm.ox = t.ox;
     prm.oy = t.oy;
-    std::memcpy(prm.v, t.h_cross, t.cross.n * sizeof(float4));
+    for (uint32_t k = 0; k < t.cross.n; ++k) {  // local -> absolute frame
+      const float4 r = t.h_cross[k];
+      prm.v[k] = make_float4(static_cast<float>(static_cast<double>(r.x) + t.ox),
+                             static_cast<float>(static_cast<double>(r.y) + t.oy), r.z,
+                             static_cast<float>(static_cast<double>(r.w) + t.ox));
+    }
     return launch<CrossEngine<VPIPG_CROSS_P, true>>(prm, a, stream);
   }
   return launch<CrossEngine<VPIPG_CROSS_P>>(CrossParams{t.cross, t.ox, t.oy}, a, stream);

@@ -66,7 +66,7 @@ struct DevTables {
   const OffsetEdgeF64* off;  // n
   const RayEdgeF64* ray;     // n
   // f32 affine
-  float ox, oy;              // local-frame origin (f32; zero stored as -0.0f)
+  float ox, oy;              // local-frame origin (f32 centroid; a zero coordinate is +0.0f)
   SlabTable slab[2];         // [0] Voronoi (from generators), [1] sign-of-offset
   CrossTable cross;
   // unit-normal supporting lines (a, b, c, 0) of the n edges, f64: the band

@@ -12,13 +12,12 @@ pytestmark = pytest.mark.gpu
 ROOT = Path(__file__).resolve().parents[1]
 KEYS = {"metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step",
         "higher_is_better", "scaling", "vs_baseline", "dtype", "data", "config", "roofline",
-        "cpu_baseline", "e2e", "clocks", "gpu_launches"}
+        "cpu_baseline", "e2e", "clocks", "gpu_launches", "parity"}
 
 
 def _run(*extra):
     out = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--points", str(1 << 22),
-                          "--steps", "3", "--warmup", "3", "--e2e-steps", "1",
-                          "--cpu-sample", str(1 << 16), *extra],
+                          "--steps", "3", "--warmup", "3", "--e2e-steps", "1", *extra],
                          cwd=ROOT, capture_output=True, text=True, timeout=600)
     assert out.returncode == 0, out.stderr[-2000:]
     lines = [ln for ln in out.stdout.splitlines() if ln.strip()]
@@ -37,6 +36,12 @@ def test_bench_line_contract(mode):
     assert {"bound", "achieved", "peak", "unit", "frac", "traffic"} <= r.keys()
     assert 0 < r["frac"] < 1.5
     assert d["cpu_baseline"]["value"] > 0 and d["cpu_baseline"]["cores"] >= 1
+    # parity over the whole batch: the reference library and the exact f64 kernels
+    p = d["parity"]
+    assert p["points"] == 1 << 22 and p["outside_band"] == 0
+    for blk in ("vs_reference", "f32_vs_f64_exact", "f64_exact_vs_reference"):
+        assert set(p[blk]) == {"voronoi", "sign_of_offset", "ray_crossing"}
+    assert all(v["disagree"] == 0 for v in p["f64_exact_vs_reference"].values())
     assert d["e2e"]["value"] > 0 and d["e2e"]["h2d_bytes_per_step"] == 8 * (1 << 22)
     names = [k["engine"] for k in d["kernels"]]
     if mode == "fused":

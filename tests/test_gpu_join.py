@@ -104,6 +104,41 @@ def test_c4_config_gather_vs_oracle(orc):
     _gather_vs_oracle(orc, 1 << 22, *W.c4_polygons(vp.random_convex_polygon))
 
 
+def test_c4_full_scale_vs_reference_library():
+    """C4 at full size (65,536 polygons, 2^28 pairs): the fused join kernel
+    (the benchmarked step) against the unmodified reference library's
+    per-polygon batch calls on the same f32 pairs: every disagreement lies in
+    the pair's own polygon's 1e-5 relative band."""
+    import bench_cpu as BC
+    import oracle
+    try:
+        ref = oracle.Reference()
+    except FileNotFoundError:
+        pytest.skip("oracle/_ref not built")
+    off, vx, vy, cx, cy, r = W.c4_polygons(vp.random_convex_polygon)
+    m = W.C4_PAIRS
+    dcx, dcy, dr = (torch.as_tensor(a, device=DEV) for a in (cx, cy, r))
+    xs = torch.empty(m, dtype=torch.float32, device=DEV)
+    ys = torch.empty_like(xs)
+    ids = torch.empty(m, dtype=torch.int32, device=DEV)
+    vp.fill_join_pairs(W.c4_pair_seed(), 0, xs, ys, ids, dcx, dcy, dr)
+    hx, hy = xs.cpu().numpy(), ys.cpu().numpy()
+    hid = ids.cpu().numpy().view(np.uint32)
+    want, _ = ref.join(off, vx, vy, hx.astype(np.float64), hy.astype(np.float64), hid,
+                       threads=BC.cores())
+    with vp.PolygonDB.prepare(off, vx, vy, vp.KIND_ALL) as db:
+        fw = [torch.zeros((m + 31) // 32, dtype=torch.int32, device=DEV) for _ in range(3)]
+        fc = [torch.zeros(1, dtype=torch.int64, device=DEV) for _ in range(3)]
+        db.test_multi(xs, ys, ids, words=fw, counts=fc)
+        torch.cuda.synchronize()
+    for e in range(3):
+        rw = np.packbits(want[e], bitorder="little").view(np.uint32)
+        par = BC.parity_entry(fw[e], rw, hx, hy, vx, vy, m, BC.EPS32, join=(off, hid))
+        assert par["outside_band"] == 0, (e, par)
+        assert abs(fc[e].item() - int(want[e].sum())) <= par["disagree"]
+        print(f"C4 engine {e}: {par['disagree']} band disagreements vs the reference")
+
+
 def _gather_vs_oracle(orc, m, off, vx, vy, cx, cy, r):
     dcx, dcy, dr = (torch.as_tensor(a, device=DEV) for a in (cx, cy, r))
     xs = torch.empty(m, dtype=torch.float32, device=DEV)

@@ -734,3 +734,41 @@ def test_fused_f64_pass_is_reference_exact(golden, orc, m):
             assert np.array_equal(got, want[e]), e
             assert np.array_equal(words_to_mask(ws[e].cpu().numpy().view(np.uint32), m), got)
             assert cs[e].item() == int(want[e].sum())
+
+
+@pytest.mark.parametrize("centre", [(1e3, 1e3), (-2.5e4, 7e3)])
+def test_small_polygon_far_from_origin(orc, centre):
+    """A unit-radius polygon far from the origin (f32 tables in the polygon's
+    local frame): every engine, and the fused pass, equals the oracle outside a
+    band that scales with the polygon's extent plus two f32 ulps of the
+    coordinates, not with |x|."""
+    cx, cy = centre
+    vx, vy = vp.random_convex_polygon(24, 777, 1.0, (cx, cy))
+    m = 1 << 20
+    rs = np.random.default_rng(5)
+    xs = (cx + rs.uniform(-1.5, 1.5, m)).astype(np.float32)
+    ys = (cy + rs.uniform(-1.5, 1.5, m)).astype(np.float32)
+    # plus points on and within 1e-4 of every edge line
+    t = rs.uniform(0, 1, (len(vx), 64))
+    ex = vx[:, None] + t * (np.roll(vx, -1)[:, None] - vx[:, None])
+    ey = vy[:, None] + t * (np.roll(vy, -1)[:, None] - vy[:, None])
+    xs = np.concatenate([xs, ex.ravel().astype(np.float32)])
+    ys = np.concatenate([ys, (ey.ravel() + rs.uniform(-1e-4, 1e-4, ey.size)).astype(np.float32)])
+    xd, yd = xs.astype(np.float64), ys.astype(np.float64)
+    want = orc.masks(vx, vy, xd, yd)
+    ext = max(np.ptp(vx), np.ptp(vy))
+    ulp = np.spacing(np.maximum(np.abs(xs), np.abs(ys)).astype(np.float32)).astype(np.float64)
+    band = orc.edge_line_distances(vx, vy, xd, yd) <= EPS32 * max(1.0, ext) + 2 * ulp
+    assert band.mean() < 0.1
+    with vp.PreparedPolygon.prepare(vx, vy, vp.KIND_ALL) as p:
+        for e in range(3):
+            wn, bn, c = run_device(p, e, xs, ys)
+            bad = (bn != want[e]) & ~band
+            assert not bad.any(), (e, np.flatnonzero(bad)[:5])
+        xt, yt = torch.as_tensor(xs, device=DEV), torch.as_tensor(ys, device=DEV)
+        fw = [torch.zeros((xs.size + 31) // 32, dtype=torch.int32, device=DEV) for _ in range(3)]
+        p.test_multi(xt, yt, words=fw)
+        torch.cuda.synchronize()
+        for e in range(3):
+            got = words_to_mask(fw[e].cpu().numpy().view(np.uint32), xs.size)
+            assert not ((got != want[e]) & ~band).any(), e
