@@ -220,8 +220,21 @@ __global__ void __launch_bounds__(kPrepThreads) prep_kernel(PrepArgs a) {
 #ifndef VPIPG_LOCAL_FRAME
 #define VPIPG_LOCAL_FRAME 1
 #endif
-    const float ox = VPIPG_LOCAL_FRAME ? static_cast<float>(cx) + 0.f : 0.f;
-    const float oy = VPIPG_LOCAL_FRAME ? static_cast<float>(cy) + 0.f : 0.f;
+    // A polygon whose centroid lies within its own extent of the origin keeps
+    // the absolute frame (origin (0, 0): the kernels then skip the shift),
+    // as accurate there since |x| <= ~2 extent for every point near it.
+    const double* vsrc = a.vv ? a.vv : a.vr;
+    double lo_x = INFINITY, hi_x = -INFINITY, lo_y = INFINITY, hi_y = -INFINITY;
+    for (int i = 0; vsrc && i < n; ++i) {
+      lo_x = fmin(lo_x, vsrc[i]);
+      hi_x = fmax(hi_x, vsrc[i]);
+      lo_y = fmin(lo_y, vsrc[n + i]);
+      hi_y = fmax(hi_y, vsrc[n + i]);
+    }
+    const double extent = fmax(hi_x - lo_x, hi_y - lo_y);
+    const bool local = VPIPG_LOCAL_FRAME && !(fmax(fabs(cx), fabs(cy)) <= extent);
+    const float ox = local ? static_cast<float>(cx) + 0.f : 0.f;
+    const float oy = local ? static_cast<float>(cy) + 0.f : 0.f;
     a.meta->inner_x = cx;
     a.meta->inner_y = cy;
     a.meta->ox = ox;

@@ -85,6 +85,20 @@ __device__ __forceinline__ float fmin3(float a, float b, float c) {
 // far from the origin, so the table arithmetic errs by ~2^-24 of the polygon's
 // extent there, not of |x|.
 //
+// The shift is skipped (a uniform branch) when prep put the origin at (0, 0):
+// polygons whose centroid lies within their own extent of the origin, where
+// the absolute frame is as accurate (prep.cu).
+template <int P>
+__device__ __forceinline__ void to_local(float (&x)[P], float (&y)[P], float ox, float oy) {
+  if (ox != 0.f || oy != 0.f) {
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+      x[p] -= ox;
+      y[p] -= oy;
+    }
+  }
+}
+
 // Slab engine (Voronoi and sign-of-offset): inside iff
 //   max(XLO) <= x' <= min(XHI)  and  max(YLO) <= y' <= min(YHI)
 // where each group entry is t = B * (other coordinate) + C (see prep.cu).
@@ -443,7 +457,7 @@ __device__ __forceinline__ void flush_count(uint32_t cnt, const TestArgs& a) {
 }
 
 // Guarded warp tile straight from global memory (tails, unaligned inputs).
-template <class Eng>
+template <class Eng, bool kShift = Eng::kShiftIn>
 __device__ __forceinline__ uint32_t guarded_tile(const typename Eng::Params& prm, const float4* tab,
                                                  const TestArgs& a, uint64_t base, int lane) {
   constexpr int P = Eng::kP;
@@ -454,9 +468,10 @@ __device__ __forceinline__ uint32_t guarded_tile(const typename Eng::Params& prm
   for (int p = 0; p < P; ++p) {
     const uint64_t idx = base + 32u * p + lane;
     const bool ok = idx < a.m;
-    x[p] = (ok ? __ldcs(xs + idx) : 0.f) - (Eng::kShiftIn ? prm.ox : 0.f);
-    y[p] = (ok ? __ldcs(ys + idx) : 0.f) - (Eng::kShiftIn ? prm.oy : 0.f);
+    x[p] = ok ? __ldcs(xs + idx) : 0.f;
+    y[p] = ok ? __ldcs(ys + idx) : 0.f;
   }
+  if constexpr (kShift) to_local(x, y, prm.ox, prm.oy);
   Eng::eval(prm, tab, x, y, va, vb);
   return emit<true, Eng::kVote, P>(va, vb, base, a, lane);
 }
@@ -535,9 +550,10 @@ __global__ void __launch_bounds__(kThreads, 2)
     float x[P], y[P], va[P], vb[P];
 #pragma unroll
     for (int p = 0; p < P; ++p) {
-      x[p] = px[32 * p] - (Eng::kShiftIn ? prm.ox : 0.f);
-      y[p] = px[kWarpPts + 32 * p] - (Eng::kShiftIn ? prm.oy : 0.f);
+      x[p] = px[32 * p];
+      y[p] = px[kWarpPts + 32 * p];
     }
+    if constexpr (Eng::kShiftIn) to_local(x, y, prm.ox, prm.oy);
     mbar_arrive(&empty[s]);  // release: this lane's reads of stage s are done
     if (lane == 0 && r + kStages < sr.rounds) {
       const uint64_t gn = sr.slice(r + kStages);
@@ -614,9 +630,10 @@ __global__ void __launch_bounds__(kThreads, VPIPG_LDG_MINB)
       float x[P], y[P], va[P], vb[P];
 #pragma unroll
       for (int p = 0; p < P; ++p) {
-        x[p] = __ldcs(px + 32 * p) - (Eng::kShiftIn ? prm.ox : 0.f);
-        y[p] = __ldcs(py + 32 * p) - (Eng::kShiftIn ? prm.oy : 0.f);
+        x[p] = __ldcs(px + 32 * p);
+        y[p] = __ldcs(py + 32 * p);
       }
+      if constexpr (Eng::kShiftIn) to_local(x, y, prm.ox, prm.oy);
       Eng::eval(prm, tab, x, y, va, vb);
       count += emit<false, Eng::kVote, P>(va, vb, g * kWarpPts, a, lane, sr.live(r));
     }
@@ -634,9 +651,10 @@ __global__ void __launch_bounds__(kThreads, VPIPG_LDG_MINB)
       float x[P], y[P], va[P], vb[P];
 #pragma unroll
       for (int p = 0; p < P; ++p) {
-        x[p] = __ldcs(px + 32 * p) - (Eng::kShiftIn ? prm.ox : 0.f);
-        y[p] = __ldcs(py + 32 * p) - (Eng::kShiftIn ? prm.oy : 0.f);
+        x[p] = __ldcs(px + 32 * p);
+        y[p] = __ldcs(py + 32 * p);
       }
+      if constexpr (Eng::kShiftIn) to_local(x, y, prm.ox, prm.oy);
       Eng::eval(prm, tab, x, y, va, vb);
       count += emit<false, Eng::kVote, P>(va, vb, g * kWarpPts, a, lane);
     }
@@ -722,21 +740,32 @@ __global__ void __launch_bounds__(kThreads, 2)
     float x[P], y[P], va[P], vb[P];
 #pragma unroll
     for (int p = 0; p < P; ++p) {
-      x[p] = __ldcs(px + 32 * p) - (VPIPG_LOCAL_FRAME ? prm.v.ox : 0.f);
-      y[p] = __ldcs(py + 32 * p) - (VPIPG_LOCAL_FRAME ? prm.v.oy : 0.f);
+      x[p] = __ldcs(px + 32 * p);
+      y[p] = __ldcs(py + 32 * p);
     }
+    // the crossing engine first, on the points as loaded with its parameter-
+    // bank table in the absolute frame (exactly the standalone kernel's
+    // arithmetic, so both routes give the same masks); then the points move to
+    // the local frame for the slab engines
+    if constexpr (kInline) {
+      TriC::eval(prm.c, tc, x, y, va, vb);
+      cc += emit<false, TriC::kVote, P>(va, vb, g * kWarpPts, ac, lane, live);
+    }
+    to_local(x, y, prm.v.ox, prm.v.oy);
     TriV::eval(prm.v, tv, x, y, va, vb);
     cv += emit<false, TriV::kVote, P>(va, vb, g * kWarpPts, av, lane, live);
     TriO::eval(prm.o, to, x, y, va, vb);
     co += emit<false, TriO::kVote, P>(va, vb, g * kWarpPts, ao, lane, live);
-    TriC::eval(prm.c, tc, x, y, va, vb);
-    cc += emit<false, TriC::kVote, P>(va, vb, g * kWarpPts, ac, lane, live);
+    if constexpr (!kInline) {
+      TriC::eval(prm.c, tc, x, y, va, vb);
+      cc += emit<false, TriC::kVote, P>(va, vb, g * kWarpPts, ac, lane, live);
+    }
   }
   if (sr.g0 == full_slices % sr.W) {
     for (uint64_t base = full_slices * kWarpPts; base < av.m; base += kWarpPts) {
       cv += guarded_tile<TriV>(prm.v, tv, av, base, lane);
       co += guarded_tile<TriO>(prm.o, to, ao, base, lane);
-      cc += guarded_tile<TriC>(prm.c, tc, ac, base, lane);
+      cc += guarded_tile<TriC, !kInline>(prm.c, tc, ac, base, lane);
     }
   }
   flush_count(cv, av);
@@ -818,6 +847,14 @@ cudaError_t launch(const typename Eng::Params& prm, const TestArgs& a, cudaStrea
 #define VPIPG_FUSE_MAX_N 40
 #endif
 
+// a crossing record (u.x, u.y, dvx/dvy, w.x) from the local frame of the
+// device tables to the absolute frame of the parameter-bank launches
+float4 cross_record_abs(const float4& r, float ox, float oy) {
+  return make_float4(static_cast<float>(static_cast<double>(r.x) + ox),
+                     static_cast<float>(static_cast<double>(r.y) + oy), r.z,
+                     static_cast<float>(static_cast<double>(r.w) + ox));
+}
+
 bool test_f32_all_plan(const DevTables& t, const TestArgs* a, size_t* smem_out) {
   constexpr int kWarpPts = 32 * kTriP;
   const size_t smem = ((size_t)t.slab[0].total / 2 + (size_t)t.slab[1].total / 2 + t.cross.n) *
@@ -871,7 +908,7 @@ cudaError_t launch_test_f32_all(const DevTables& t, const TestArgs* a, cudaStrea
     pi.off_c = prm.off_c;
     std::memcpy(pi.t, t.h_slab[0], nv * sizeof(float4));
     std::memcpy(pi.t + nv, t.h_slab[1], no * sizeof(float4));
-    std::memcpy(pi.t + nv + no, t.h_cross, nc * sizeof(float4));
+    for (size_t k = 0; k < nc; ++k) pi.t[nv + no + k] = cross_record_abs(t.h_cross[k], t.ox, t.oy);
     return go(std::true_type{}, pi);
   }
   return go(std::false_type{}, prm);
@@ -913,12 +950,7 @@ cudaError_t launch_test_f32(const DevTables& t, int engine, const TestArgs& a,
     prm.tab = t.cross;
     prm.ox = t.ox;
     prm.oy = t.oy;
-    for (uint32_t k = 0; k < t.cross.n; ++k) {  // local -> absolute frame
-      const float4 r = t.h_cross[k];
-      prm.v[k] = make_float4(static_cast<float>(static_cast<double>(r.x) + t.ox),
-                             static_cast<float>(static_cast<double>(r.y) + t.oy), r.z,
-                             static_cast<float>(static_cast<double>(r.w) + t.ox));
-    }
+    for (uint32_t k = 0; k < t.cross.n; ++k) prm.v[k] = cross_record_abs(t.h_cross[k], t.ox, t.oy);
     return launch<CrossEngine<VPIPG_CROSS_P, true>>(prm, a, stream);
   }
   return launch<CrossEngine<VPIPG_CROSS_P>>(CrossParams{t.cross, t.ox, t.oy}, a, stream);
