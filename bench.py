@@ -47,12 +47,12 @@ METRIC = "point-polygon tests/sec"
 UNIT = "tests/s"
 PEAKS_FILE = ROOT / "MEASURED_PEAKS.json"
 PIPE_PEAKS_FILE = ROOT / "profiles" / "pipe_peaks_r01.json"
-TRAFFIC_FILE = ROOT / "profiles" / "traffic_r01.json"
-NCU_FILE = ROOT / "profiles" / "ncu_full_r01_c5.json"
+TRAFFIC_FILE = ROOT / "profiles" / "traffic_r02.json"
+NCU_FILE = ROOT / "profiles" / "ncu_full_r02_c5.json"
 # dispatch cycles per point-edge per warp lane-slot (tools/pipe_peaks.cu model:
 # FFMA/FADD 1 cycle, FMNMX3/LOP3 2): slab = FFMA + FMNMX3/2, crossing =
-# 2 FADD + FFMA + 1.5 LOP3
-ISSUE_CYCLES_PER_PE = {"voronoi": 2.0, "sign_of_offset": 2.0, "ray_crossing": 6.0}
+# 1.5 FADD + FFMA + 1.5 LOP3 (paired anchoring, test_f32.cu CrossEngine)
+ISSUE_CYCLES_PER_PE = {"voronoi": 2.0, "sign_of_offset": 2.0, "ray_crossing": 5.5}
 HBM_FALLBACK_GBS = 6650.0
 # FFMA lane-ops per SM per clock on sm_100a (tools/pipe_peaks.cu: 3.79 warp-inst/clk/SM)
 FFMA_PER_SM_CLK = 128
@@ -562,7 +562,7 @@ def main():
         if record:
             s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             s0.record(stream)
-        counts.zero_()
+        vp.zero_counts(counts, stream)
         pairs = []
         if fused:  # one kernel: its time is reported once, for all three engines
             if record:
@@ -601,7 +601,7 @@ def main():
         torch.cuda.synchronize()
         graph = torch.cuda.CUDAGraph()
         with torch.cuda.graph(graph, stream=stream):
-            counts.zero_()
+            vp.zero_counts(counts, stream)
             if fused:
                 job.launch_all(words, [counts[e:e + 1] for e in range(3)], stream)
             else:
@@ -663,7 +663,7 @@ def main():
             for _ in range(args.steps):
                 if flush is not None:
                     flush_sink.copy_(flush.view(torch.int64).sum(dtype=torch.int64).view(1))
-                counts.zero_()
+                vp.zero_counts(counts, stream)
                 ev = []
                 for e in range(3):
                     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -774,14 +774,15 @@ def main():
                               f"({n_eng} engine test(s), n={n_edges} edges, 4 flops per "
                               f"point-edge)"),
                  "algorithmic_bytes_per_launch": alg_bytes,
-                 "traffic_source": "profiles/traffic_r01.json (ncu --set full dram__bytes_read+write "
+                 "traffic_source": "profiles/traffic_r02.json (ncu --set full dram__bytes_read+write "
                                    "of this kernel on this workload, scaled to this launch)",
                  "issue_model_frac": dk.get("issue_model_frac"),
                  "issue_model": "dispatch cycles per point-edge: slab 2 (FFMA + FMNMX3/2), "
-                                "crossing 6 (2 FADD + FFMA + 1.5 LOP3); the fused kernel their "
-                                "mean over the three engines; profiles/round1_summary.md"})
+                                "crossing 5.5 (1.5 FADD + FFMA + 1.5 LOP3, paired anchoring); the "
+                                "fused kernel their mean over the three engines; "
+                                "profiles/crossing_forms_r02.json"})
     try:  # the ncu evidence for the same kernel and workload (issue / pipe utilisation)
-        nk = json.loads(NCU_FILE.with_name(f"ncu_full_r01_{args.workload.replace(':', 'n')}.json")
+        nk = json.loads(NCU_FILE.with_name(f"ncu_full_r02_{args.workload.replace(':', 'n')}.json")
                         .read_text())["kernels"][dk["engine"]]
         roof["ncu"] = {k.split(".")[0]: nk[k] for k in (
             "smsp__issue_active.avg.pct_of_peak_sustained_active",

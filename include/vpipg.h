@@ -129,8 +129,9 @@ int vpipg_test_multi(const vpipg_poly* poly, uint32_t engines, int dtype, const 
 /* 1 when vpipg_test_multi would run this batch as ONE fused launch: all three
  * engines and either float64 points (the exact kernels, any n) or float32
  * points in 16-byte-aligned buffers of at least one slice per warp with a
- * polygon of at most 48 edges whose tables fit shared memory (above that the
- * per-engine kernels are faster); else 0. Pure query: no device work. */
+ * polygon of at most VPIPG_FUSE_MAX_N (40) edges whose tables fit shared
+ * memory (above that the per-engine kernels are faster); else 0. Pure query:
+ * no device work. */
 int vpipg_test_multi_fused(const vpipg_poly* poly, uint32_t engines, int dtype, const void* xs,
                            const void* ys, uint64_t m);
 
@@ -271,6 +272,9 @@ int vpipg_comm_unique_id(uint8_t id[128]);
 int vpipg_comm_init(const uint8_t id[128], int nranks, int rank, int device, vpipg_comm** out);
 int vpipg_comm_init_all(int ndev, const int* devices, vpipg_comm** comms);
 int vpipg_comm_info(const vpipg_comm* comm, int* nranks, int* rank, int* device);
+/* Zero n device u64 counters on `stream` (a memset, no kernel launch; the
+ * test calls accumulate into their d_inside counters). */
+int vpipg_zero_counts(unsigned long long* d_counts, int n, void* stream);
 /* In-place sum of n device u64 counters over all ranks, on `stream`. */
 int vpipg_allreduce_counts(vpipg_comm* comm, unsigned long long* d_counts, int n, void* stream);
 /* The same for several communicators driven by one thread (vpipg_comm_init_all):

@@ -7,4 +7,5 @@ sources (csrc/), the build recipe and a thin Python host mirror over ctypes.
 from ._lib import LIB_PATH, VpipError, load  # noqa: F401
 from .engine import (F32, F64, KIND_ALL, KIND_CROSSING, KIND_OFFSET, KIND_VORONOI,  # noqa: F401
                      PolygonDB, PreparedPolygon, fill_join_pairs, fill_uniform_points, mix_seed,
-                     random_convex_polygon, regular_polygon, release_staging, sample_points)
+                     random_convex_polygon, regular_polygon, release_staging, sample_points,
+                     zero_counts)

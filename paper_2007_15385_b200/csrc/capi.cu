@@ -22,6 +22,7 @@
 #include <vector>
 
 #include "capi_internal.h"
+#include "exact_geom.cuh"
 
 using namespace vpipg;
 using namespace vpipg::capi;
@@ -43,37 +44,19 @@ int check_device(int device) {
   return ok[device] ? kOk : VPIPG_ERR_ARCH;
 }
 
-// validate_polygon (geometry.cpp:53-98): same checks in the same order, same
-// arithmetic (host code of this TU is compiled with -ffp-contract=off, as the
-// reference is, so no product is fused into an add).
+// validate_polygon (geometry.cpp:53-98) on the host: exact_geom.cuh's
+// validate_exact, the same definition the device CSR ingest runs; reverses the
+// vertices in place when they are clockwise.
 int validate(std::vector<double>& vx, std::vector<double>& vy, int* reversed) {
-  const size_t n = vx.size();
-  for (size_t i = 0; i < n; ++i)
-    if (!std::isfinite(vx[i]) || !std::isfinite(vy[i])) return kNonFinite;
-  if (n < 3) return kTooFew;
-  for (size_t i = 0, j = n - 1; i < n; j = i++) {
-    const double dx = vx[j] - vx[i], dy = vy[j] - vy[i];
-    if (dx * dx + dy * dy <= 1e-24) return kDegenerate;
-  }
-  double sum = 0.0;
-  for (size_t i = 0, j = n - 1; i < n; j = i++) sum += vx[j] * vy[i] - vx[i] * vy[j];
-  *reversed = 0;
-  if (sum < 0.0) {
+  bool rev = false;
+  const int rc = validate_exact([&](int k) { return make_double2(vx[k], vy[k]); },
+                                static_cast<int>(vx.size()), &rev);
+  *reversed = rev ? 1 : 0;
+  if (rc == 0 && rev) {
     std::reverse(vx.begin(), vx.end());
     std::reverse(vy.begin(), vy.end());
-    *reversed = 1;
   }
-  double total_turn = 0.0;
-  for (size_t i = 0; i < n; ++i) {
-    const size_t p = (i + n - 1) % n, q = (i + 1) % n;
-    const double inx = vx[i] - vx[p], iny = vy[i] - vy[p];
-    const double outx = vx[q] - vx[i], outy = vy[q] - vy[i];
-    const double cr = inx * outy - iny * outx;
-    if (cr <= 1e-12) return kNotConvex;
-    total_turn += std::atan2(cr, inx * outx + iny * outy);
-  }
-  if (total_turn >= 3.0 * std::numbers::pi) return kNotConvex;
-  return kOk;
+  return rc;
 }
 
 
@@ -376,6 +359,13 @@ int vpipg_test_multi(const vpipg_poly* p, uint32_t engines, int dtype, const voi
       if (rc) return rc;
     }
   return kOk;
+}
+
+int vpipg_zero_counts(unsigned long long* d_counts, int n, void* stream) {
+  if (n < 0 || (n > 0 && !d_counts)) return kInvalid;
+  if (n == 0) return kOk;
+  return cuda_code(cudaMemsetAsync(d_counts, 0, static_cast<size_t>(n) * sizeof(unsigned long long),
+                                   static_cast<cudaStream_t>(stream)));
 }
 
 int vpipg_test_multi_fused(const vpipg_poly* p, uint32_t engines, int dtype, const void* xs,

@@ -400,13 +400,6 @@ __global__ void __launch_bounds__(kGThreads, VPIPG_GMINB_ALL)
   }
 }
 
-__device__ __forceinline__ uint64_t mix_seed(uint64_t seed, uint64_t salt) {
-  uint64_t z = seed + 0x9e3779b97f4a7c15ULL * (salt + 1);
-  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
-  z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
-  return z ^ (z >> 31);
-}
-
 __device__ __forceinline__ double unit(uint64_t r) {
   return __dmul_rn(static_cast<double>(r >> 11), 0x1.0p-53);
 }

@@ -383,32 +383,46 @@ struct CrossEngine {
 // kVote 0: inside = (a >= b); 1: (a >= b or unordered), the NaN-inside rule;
 // 2: a's bit pattern is negative as an int (the crossing parity word, no
 // float conversion). One compare feeds both the ballot and a predicated count.
+// Per-lane inside counts: integer-valued floats (VPIPG_FCOUNT, the predicated
+// FADD issues at full rate on the FMA pipe) or u32; exact either way below
+// 2^24 points per lane (2^24 x 75,776 resident lanes per launch).
+#ifndef VPIPG_FCOUNT
+#define VPIPG_FCOUNT 1
+#endif
+using cnt_t = std::conditional_t<VPIPG_FCOUNT != 0, float, uint32_t>;
+#if VPIPG_FCOUNT
+#define VPIPG_CNT_ADD "@q add.f32 %1, %1, 0f3F800000;\n\t}"
+#define VPIPG_CNT_C "+f"
+#else
+#define VPIPG_CNT_ADD "@q add.u32 %1, %1, 1;\n\t}"
+#define VPIPG_CNT_C "+r"
+#endif
 template <int kVote>
-__device__ __forceinline__ uint32_t vote_in(float a, float b, uint32_t& cnt) {
+__device__ __forceinline__ uint32_t vote_in(float a, float b, cnt_t& cnt) {
   uint32_t w;
   if (kVote == 2)
     asm volatile(
         "{\n\t.reg .pred q;\n\t"
         "setp.lt.s32 q, %2, 0;\n\t"
         "vote.sync.ballot.b32 %0, q, 0xffffffff;\n\t"
-        "@q add.u32 %1, %1, 1;\n\t}"
-        : "=r"(w), "+r"(cnt)
+        VPIPG_CNT_ADD
+        : "=r"(w), VPIPG_CNT_C(cnt)
         : "r"(__float_as_uint(a)));
   else if (kVote == 1)
     asm volatile(
         "{\n\t.reg .pred q;\n\t"
         "setp.geu.f32 q, %2, %3;\n\t"
         "vote.sync.ballot.b32 %0, q, 0xffffffff;\n\t"
-        "@q add.u32 %1, %1, 1;\n\t}"
-        : "=r"(w), "+r"(cnt)
+        VPIPG_CNT_ADD
+        : "=r"(w), VPIPG_CNT_C(cnt)
         : "f"(a), "f"(b));
   else
     asm volatile(
         "{\n\t.reg .pred q;\n\t"
         "setp.ge.f32 q, %2, %3;\n\t"
         "vote.sync.ballot.b32 %0, q, 0xffffffff;\n\t"
-        "@q add.u32 %1, %1, 1;\n\t}"
-        : "=r"(w), "+r"(cnt)
+        VPIPG_CNT_ADD
+        : "=r"(w), VPIPG_CNT_C(cnt)
         : "f"(a), "f"(b));
   return w;
 }
@@ -416,11 +430,11 @@ __device__ __forceinline__ uint32_t vote_in(float a, float b, uint32_t& cnt) {
 // live == false (a warp whose slot in the last round is past the end; warp-
 // uniform): the votes run, nothing is stored or counted
 template <bool kGuard, int kVote, int P>
-__device__ __forceinline__ uint32_t emit(float (&av)[P], const float (&bv)[P], uint64_t base,
+__device__ __forceinline__ cnt_t emit(float (&av)[P], const float (&bv)[P], uint64_t base,
                                          const TestArgs& a, int lane, bool live = true) {
   static_assert(kGuard || P % 4 == 0, "16-byte word stores need P % 4 == 0");
   uint32_t w[P];
-  uint32_t cnt = 0;
+  cnt_t cnt = 0;
 #pragma unroll
   for (int p = 0; p < P; ++p) {
     if (kGuard && base + 32u * p + lane >= a.m) av[p] = kVote == 2 ? 0.f : -INFINITY;
@@ -450,7 +464,8 @@ __device__ __forceinline__ uint32_t emit(float (&av)[P], const float (&bv)[P], u
   return cnt;
 }
 
-__device__ __forceinline__ void flush_count(uint32_t cnt, const TestArgs& a) {
+__device__ __forceinline__ void flush_count(cnt_t fcnt, const TestArgs& a) {
+  uint32_t cnt = static_cast<uint32_t>(fcnt);
 #pragma unroll
   for (int s = 16; s > 0; s >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, s);
   if ((threadIdx.x & 31) == 0 && a.inside && cnt) atomicAdd(a.inside, (unsigned long long)cnt);
@@ -458,7 +473,7 @@ __device__ __forceinline__ void flush_count(uint32_t cnt, const TestArgs& a) {
 
 // Guarded warp tile straight from global memory (tails, unaligned inputs).
 template <class Eng, bool kShift = Eng::kShiftIn>
-__device__ __forceinline__ uint32_t guarded_tile(const typename Eng::Params& prm, const float4* tab,
+__device__ __forceinline__ cnt_t guarded_tile(const typename Eng::Params& prm, const float4* tab,
                                                  const TestArgs& a, uint64_t base, int lane) {
   constexpr int P = Eng::kP;
   const float* xs = static_cast<const float*>(a.xs);
@@ -542,7 +557,7 @@ __global__ void __launch_bounds__(kThreads, 2)
                &full[s], policy);
     }
   }
-  uint32_t count = 0;
+  cnt_t count = 0;
   for (uint64_t r = 0; r < sr.rounds; ++r) {
     const uint32_t s = r % kStages, ph = (r / kStages) & 1u;
     mbar_wait(&full[s], ph);
@@ -612,7 +627,7 @@ __global__ void __launch_bounds__(kThreads, VPIPG_LDG_MINB)
 #ifndef VPIPG_PF_AHEAD
 #define VPIPG_PF_AHEAD 1
 #endif
-  uint32_t count = 0;
+  cnt_t count = 0;
   // the uniform round loop only pays where the edge loop reads the parameter
   // bank through uniform registers (the crossing engine); the slab engines'
   // FFMAs take two table operands, so they read the table into vector
@@ -692,8 +707,17 @@ struct TriParamsInl {   // the three tables in the parameter bank (VPIPG_INLINE)
 
 // kMode: the slab table form shared by the Voronoi and offset tables (their
 // lines coincide: each bisector is the edge line), -1 when they differ
+// VPIPG_TRI_SLAB_SMEM: with parameter-bank tables, the two slab tables still
+// staged in shared memory (LDS.128 into vector registers, as the per-engine
+// slab kernels) and only the crossing table read as uniform registers
+#ifndef VPIPG_TRI_SLAB_SMEM
+#define VPIPG_TRI_SLAB_SMEM 1
+#endif
+#ifndef VPIPG_TRI_MINB
+#define VPIPG_TRI_MINB 2
+#endif
 template <int kMode, bool kInline = false>
-__global__ void __launch_bounds__(kThreads, 2)
+__global__ void __launch_bounds__(kThreads, VPIPG_TRI_MINB)
     tri_kernel(const __grid_constant__ std::conditional_t<kInline, TriParamsInl, TriParams> prm,
                const TestArgs av, const TestArgs ao, const TestArgs ac, const uint64_t full_slices) {
   using TriV = SlabEngine<kTriP, false, kMode>;
@@ -706,17 +730,23 @@ __global__ void __launch_bounds__(kThreads, 2)
   extern __shared__ __align__(128) unsigned char smem[];
   float4* s_tab = reinterpret_cast<float4*>(smem);
   const float4* tv;
-  if constexpr (kInline) {
+  const float4* tc;
+  if constexpr (kInline && !VPIPG_TRI_SLAB_SMEM) {
     (void)s_tab;
     tv = prm.t;
+    tc = prm.t + prm.off_c;
   } else {
     TriV::stage(prm.v, s_tab);
     TriO::stage(prm.o, s_tab + prm.off_o);
-    TriC::stage(prm.c, s_tab + prm.off_c);
     tv = s_tab;
+    if constexpr (kInline) {
+      tc = prm.t + prm.off_c;
+    } else {
+      TriC::stage(prm.c, s_tab + prm.off_c);
+      tc = s_tab + prm.off_c;
+    }
   }
   const float4* to = tv + prm.off_o;
-  const float4* tc = tv + prm.off_c;
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const SliceRounds sr(full_slices, warp);
@@ -729,7 +759,7 @@ __global__ void __launch_bounds__(kThreads, 2)
     for (int l = lane; l < 2 * kLines; l += 32)
       prefetch_l2((l < kLines ? xs : ys) + g * kWarpPts + (l % kLines) * 32);
   };
-  uint32_t cv = 0, co = 0, cc = 0;
+  cnt_t cv = 0, co = 0, cc = 0;
   prefetch(0);
   for (uint64_t r = 0; r < sr.rounds; ++r) {
     prefetch(r + 1);
@@ -785,7 +815,7 @@ __global__ void __launch_bounds__(kThreads) generic_kernel(const __grid_constant
   const float4* gtab = (kSmemTab && !Eng::kInl) ? s_gtab : Eng::global_table(prm);
   const int lane = threadIdx.x & 31;
   const uint64_t gwarp = (uint64_t)blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5);
-  uint32_t count = 0;
+  cnt_t count = 0;
   for (uint64_t base = gwarp * kWarpPts; base < a.m;
        base += (uint64_t)gridDim.x * (kThreads / 32) * kWarpPts)
     count += guarded_tile<Eng>(prm, gtab, a, base, lane);
@@ -881,7 +911,8 @@ cudaError_t launch_test_f32_all(const DevTables& t, const TestArgs* a, cudaStrea
   prm.off_o = static_cast<uint32_t>(nv);
   prm.off_c = static_cast<uint32_t>(nv + no);
   const bool inl = VPIPG_INLINE && t.h_cross && t.h_slab[0] && t.h_slab[1] && nv + no + nc <= kTriInlineMax;
-  const size_t smem = inl ? 0 : (nv + no + nc) * sizeof(float4);
+  const size_t smem = inl ? (VPIPG_TRI_SLAB_SMEM ? (nv + no) * sizeof(float4) : 0)
+                          : (nv + no + nc) * sizeof(float4);
   const uint64_t full_slices = a[0].m / kWarpPts;
   int sms = 0, per_sm = 0;
   auto form = [](const SlabTable& t) { return t.cnt[0] == 0 ? 1 : t.cnt[2] == 0 ? 2 : 0; };

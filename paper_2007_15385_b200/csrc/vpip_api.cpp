@@ -28,6 +28,7 @@
 #include "vpip/geometry.hpp"
 #include "vpip/sampling.hpp"
 #include "vpip/voronoi.hpp"
+#include "exact_geom.cuh"
 #include "vpipg.h"
 
 namespace vpip {
@@ -209,28 +210,26 @@ double signed_area(std::span<const Point2> v) {
 double signed_area(const ConvexPolygon& polygon) { return signed_area(polygon.vertices()); }
 
 ConvexPolygon validate_polygon(std::vector<Point2> vertices, double convexity_epsilon) {
-  const std::size_t n = vertices.size();
-  for (std::size_t i = 0; i < n; ++i)
-    if (!is_finite(vertices[i])) throw Error(ErrorCode::NonFinite, "vertex " + std::to_string(i));
-  if (n < 3) throw Error(ErrorCode::TooFewVertices, std::to_string(n) + " vertices");
-  for (std::size_t i = 0, j = n - 1; i < n; j = i++)
-    if (squared_distance(vertices[j], vertices[i]) <= tol::kDegenerateEdgeSq)
-      throw Error(ErrorCode::DegenerateEdge, "vertices " + std::to_string(j) + " and " + std::to_string(i));
-  double twice = 0.0;
-  for (std::size_t i = 0, j = n - 1; i < n; j = i++)
-    twice += vertices[j].x * vertices[i].y - vertices[i].x * vertices[j].y;
-  const bool reversed = twice < 0.0;
-  if (reversed) std::reverse(vertices.begin(), vertices.end());
-  double turn = 0.0;
-  for (std::size_t i = 0; i < n; ++i) {
-    const Point2 in = vertices[i] - vertices[(i + n - 1) % n];
-    const Point2 out = vertices[(i + 1) % n] - vertices[i];
-    const double c = cross(in, out);
-    if (c <= convexity_epsilon)
-      throw Error(ErrorCode::NotConvex, "collinear or reflex vertex at index " + std::to_string(i));
-    turn += std::atan2(c, dot(in, out));
+  // the checks are exact_geom.cuh's validate_exact, the single definition the
+  // C-ABI prepare and the device CSR ingest also run
+  const int n = static_cast<int>(vertices.size());
+  bool reversed = false;
+  int at = -1;
+  const int rc = vpipg::validate_exact(
+      [&](int k) { return make_double2(vertices[k].x, vertices[k].y); }, n, &reversed,
+      convexity_epsilon, &at);
+  switch (rc) {
+    case 0: break;
+    case 4: throw Error(ErrorCode::NonFinite, "vertex " + std::to_string(at));
+    case 1: throw Error(ErrorCode::TooFewVertices, std::to_string(n) + " vertices");
+    case 3:
+      throw Error(ErrorCode::DegenerateEdge,
+                  "vertices " + std::to_string((at + n - 1) % n) + " and " + std::to_string(at));
+    default:
+      throw Error(ErrorCode::NotConvex, at >= 0 ? "collinear or reflex vertex at index " + std::to_string(at)
+                                                : std::string("winds more than once"));
   }
-  if (turn >= 3.0 * std::numbers::pi) throw Error(ErrorCode::NotConvex, "winds more than once");
+  if (reversed) std::reverse(vertices.begin(), vertices.end());
   return ConvexPolygon(std::move(vertices), reversed);
 }
 
@@ -498,12 +497,7 @@ std::uint64_t mix_seed(std::uint64_t seed, std::uint64_t salt) { return vpipg_mi
 // ---------------------------------------------------------------- C-ABI samplers
 extern "C" {
 
-uint64_t vpipg_mix_seed(uint64_t seed, uint64_t salt) {
-  uint64_t z = seed + 0x9e3779b97f4a7c15ULL * (salt + 1);
-  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
-  z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
-  return z ^ (z >> 31);
-}
+uint64_t vpipg_mix_seed(uint64_t seed, uint64_t salt) { return vpipg::mix_seed(seed, salt); }
 
 static int sampler_status(const vpip::Error& e) { return static_cast<int>(e.code()) + 1; }
 

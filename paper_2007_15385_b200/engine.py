@@ -34,21 +34,43 @@ def _stream_ptr(stream) -> C.c_void_p:
     return C.c_void_p(stream.cuda_stream)  # torch.cuda.Stream
 
 
-def _check_device_batch(xs, ys, dtypes, outs=(), ids=None) -> None:
+def _out_specs(m, words=None, bytes_=None, count=None):
+    """(tensor, minimum numel, kind) for the output checks of _check_device_batch."""
+    return [(words, (m + 31) // 32, "words"), (bytes_, m, "bytes"), (count, 1, "count")]
+
+
+def _check_device_batch(xs, ys, dtypes, outs=(), ids=None, device=None) -> None:
     """The C-ABI takes raw pointers; the Python mirror checks what it can see
-    (vpip::Error InvalidParameter, code 6, on a mismatch)."""
+    (vpip::Error InvalidParameter, code 6, on a mismatch): inputs 1-D,
+    contiguous, same length and dtype; every tensor on the handle's GPU; mask
+    words 4-byte elements, byte masks 1-byte elements, counters 64-bit integers
+    (the kernels atomically add a u64), each large enough."""
+    import torch
     m = xs.numel()
     ok = (xs.is_cuda and ys.is_cuda and xs.dtype in dtypes and ys.dtype == xs.dtype
           and ys.numel() == m and xs.is_contiguous() and ys.is_contiguous())
+    tensors = [xs, ys]
     if ids is not None:
         ok = ok and ids.is_cuda and ids.numel() == m and ids.is_contiguous() and \
             ids.element_size() == 4
-    for t, need in outs:
-        if t is not None:
-            ok = ok and t.is_cuda and t.is_contiguous() and t.numel() >= need
+        tensors.append(ids)
+    for t, need, kind in outs:
+        if t is None:
+            continue
+        tensors.append(t)
+        ok = ok and t.is_cuda and t.is_contiguous() and t.numel() >= need
+        if kind == "words":
+            ok = ok and t.element_size() == 4 and not t.is_floating_point()
+        elif kind == "bytes":
+            ok = ok and t.element_size() == 1 and not t.is_floating_point()
+        else:
+            ok = ok and t.dtype in (torch.int64, getattr(torch, "uint64", torch.int64))
+    if ok and device is not None:
+        ok = all(t.device.index == device for t in tensors)
     if not ok:
         raise VpipError(6, "device batch: 1-D contiguous CUDA tensors of matching length "
-                           "and dtype (and large enough outputs) are required")
+                           "and dtype on the handle's device, int32 mask words, uint8 byte "
+                           "masks and int64 counters of sufficient size are required")
 
 
 def _engine_id(engine) -> int:
@@ -58,9 +80,10 @@ def _engine_id(engine) -> int:
 class PreparedPolygon:
     """A polygon converted on the device (validate_polygon + to_voronoi + edge tables)."""
 
-    def __init__(self, handle: C.c_void_p, n: int):
+    def __init__(self, handle: C.c_void_p, n: int, device: int = 0):
         self._h = handle
         self.n = n
+        self.device = device
 
     @classmethod
     def prepare(cls, vx, vy, kinds: int = KIND_ALL, device: int = 0, stream=None):
@@ -71,7 +94,7 @@ class PreparedPolygon:
         h = C.c_void_p()
         check(load().vpipg_prepare(_dptr(vx), _dptr(vy), vx.size, kinds, device,
                                    _stream_ptr(stream), C.byref(h)), "vpipg_prepare")
-        return cls(h, vx.size)
+        return cls(h, vx.size, device)
 
     @classmethod
     def from_generators(cls, inner, outer, device: int = 0, stream=None):
@@ -81,7 +104,7 @@ class PreparedPolygon:
         check(load().vpipg_prepare_generators(_dptr(inner), _dptr(outer), outer.shape[0], device,
                                               _stream_ptr(stream), C.byref(h)),
               "vpipg_prepare_generators")
-        return cls(h, outer.shape[0])
+        return cls(h, outer.shape[0], device)
 
     def close(self) -> None:
         if self._h:
@@ -131,7 +154,7 @@ class PreparedPolygon:
         import torch
         m = xs.numel()
         _check_device_batch(xs, ys, (torch.float32, torch.float64),
-                            ((words, (m + 31) // 32), (bytes_, m), (count, 1)))
+                            _out_specs(m, words, bytes_, count), device=self.device)
         dtype = F32 if xs.dtype == torch.float32 else F64
         ptr = lambda t: C.c_void_p(t.data_ptr()) if t is not None else C.c_void_p(None)
         check(load().vpipg_test(self._h, _engine_id(engine), dtype, ptr(xs), ptr(ys), m,
@@ -157,10 +180,10 @@ class PreparedPolygon:
         import torch
         m = xs.numel()
         outs = []
-        for lst, need in ((words, (m + 31) // 32), (bytes_, m), (counts, 1)):
-            for t in (lst or []):
-                outs.append((t, need))
-        _check_device_batch(xs, ys, (torch.float32, torch.float64), outs)
+        for e in range(3):
+            pick = lambda lst: lst[e] if lst is not None and e < len(lst) else None
+            outs += _out_specs(m, pick(words), pick(bytes_), pick(counts))
+        _check_device_batch(xs, ys, (torch.float32, torch.float64), outs, device=self.device)
         mask = 0
         for e in engines:
             mask |= 1 << _engine_id(e)
@@ -188,6 +211,7 @@ class PreparedPolygon:
     def validate(self, xs, ys, band: float = 1e-9, relative: bool = False, stream=None):
         """run_validation on the device (vpipg_validate): returns a dict report."""
         import torch
+        _check_device_batch(xs, ys, (torch.float32, torch.float64), device=self.device)
         rep = _lib.Report()
         dtype = F32 if xs.dtype == torch.float32 else F64
         check(load().vpipg_validate(self._h, dtype, C.c_void_p(xs.data_ptr()),
@@ -199,6 +223,9 @@ class PreparedPolygon:
                       stream=None):
         """Band classification of two masks of one batch (vpipg_compare_masks)."""
         import torch
+        m = xs.numel()
+        _check_device_batch(xs, ys, (torch.float32, torch.float64),
+                            _out_specs(m, words_a) + _out_specs(m, words_b), device=self.device)
         rep = _lib.Report()
         dtype = F32 if xs.dtype == torch.float32 else F64
         check(load().vpipg_compare_masks(self._h, dtype, C.c_void_p(xs.data_ptr()),
@@ -236,10 +263,11 @@ class PreparedPolygon:
 class PolygonDB:
     """A CSR batch of polygons prepared on the device (vpipg_prepare_csr)."""
 
-    def __init__(self, handle: C.c_void_p, npoly: int, status: np.ndarray):
+    def __init__(self, handle: C.c_void_p, npoly: int, status: np.ndarray, device: int = 0):
         self._h = handle
         self.npoly = npoly
         self.status = status
+        self.device = device
 
     @classmethod
     def prepare(cls, offsets, vx, vy, kinds: int = KIND_ALL, device: int = 0, stream=None):
@@ -252,7 +280,7 @@ class PolygonDB:
         check(load().vpipg_prepare_csr(C.c_void_p(offsets.ctypes.data), _dptr(vx), _dptr(vy),
                                        npoly, kinds, device, _stream_ptr(stream), C.byref(h),
                                        C.c_void_p(status.ctypes.data)), "vpipg_prepare_csr")
-        return cls(h, npoly, status[:npoly])
+        return cls(h, npoly, status[:npoly], device)
 
     def close(self) -> None:
         if self._h:
@@ -280,8 +308,8 @@ class PolygonDB:
         """Gathered test on device tensors (vpipg_test_gather); float32 points, int32 ids."""
         import torch
         m = xs.numel()
-        _check_device_batch(xs, ys, (torch.float32,),
-                            ((words, (m + 31) // 32), (bytes_, m), (count, 1)), ids=ids)
+        _check_device_batch(xs, ys, (torch.float32,), _out_specs(m, words, bytes_, count), ids=ids,
+                            device=self.device)
         ptr = lambda t: C.c_void_p(t.data_ptr()) if t is not None else C.c_void_p(None)
         check(load().vpipg_test_gather(self._h, _engine_id(engine), ptr(xs), ptr(ys), ptr(ids),
                                        xs.numel(), ptr(words), ptr(bytes_), ptr(count),
@@ -295,10 +323,10 @@ class PolygonDB:
         import torch
         m = xs.numel()
         outs = []
-        for lst, need in ((words, (m + 31) // 32), (bytes_, m), (counts, 1)):
-            for t in (lst or []):
-                outs.append((t, need))
-        _check_device_batch(xs, ys, (torch.float32,), outs, ids=ids)
+        for e in range(3):
+            pick = lambda lst: lst[e] if lst is not None and e < len(lst) else None
+            outs += _out_specs(m, pick(words), pick(bytes_), pick(counts))
+        _check_device_batch(xs, ys, (torch.float32,), outs, ids=ids, device=self.device)
         mask = 0
         for e in engines:
             mask |= 1 << _engine_id(e)
@@ -352,6 +380,15 @@ def _host_ptr(a) -> int:
 def release_staging(device: int = 0) -> None:
     """Free the per-device staging the host-buffer calls keep (vpipg_release_staging)."""
     check(load().vpipg_release_staging(device), "vpipg_release_staging")
+
+
+def zero_counts(counts, stream=None) -> None:
+    """Zero a device int64 / uint64 counter tensor on `stream` with a memset
+    (vpipg_zero_counts): no kernel launch, graph-capturable."""
+    if not (counts.is_cuda and counts.is_contiguous() and counts.element_size() == 8):
+        raise VpipError(6, "zero_counts: a contiguous CUDA tensor of 64-bit counters is required")
+    check(load().vpipg_zero_counts(C.c_void_p(counts.data_ptr()), counts.numel(),
+                                   _stream_ptr(stream)), "vpipg_zero_counts")
 
 
 def fill_uniform_points(seed: int, first: int, xs, ys, box, stream=None) -> None:

@@ -129,13 +129,13 @@ def test_python_mirror_rejects_bad_device_batches():
     mismatched lengths / dtypes, short outputs -> InvalidParameter (code 6)."""
     import torch
     p = object.__new__(vp.PreparedPolygon)
-    p._h = None
+    p._h, p.device = None, 0
     x = torch.zeros(64, dtype=torch.float32)
     with pytest.raises(vp.VpipError) as e:
         p.test(0, x, x)  # CPU tensors
     assert e.value.code == 6
     db = object.__new__(vp.PolygonDB)
-    db._h = None
+    db._h, db.device = None, 0
     with pytest.raises(vp.VpipError) as e:
         db.test(0, x, x, torch.zeros(63, dtype=torch.int32))
     assert e.value.code == 6

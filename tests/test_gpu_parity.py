@@ -772,3 +772,40 @@ def test_small_polygon_far_from_origin(orc, centre):
         for e in range(3):
             got = words_to_mask(fw[e].cpu().numpy().view(np.uint32), xs.size)
             assert not ((got != want[e]) & ~band).any(), e
+
+
+def test_python_mirror_rejects_bad_output_tensors():
+    """The ctypes mirror refuses outputs the kernels would overrun: counters
+    that are not 64-bit integers, mask words whose elements are not 4 bytes (or
+    floats), byte masks of wider elements, too-short outputs; nothing is
+    launched and no CUDA error is left behind."""
+    vx, vy = np.array([0., 1, 1, 0]), np.array([0., 0, 1, 1])
+    m = 100
+    xs = torch.rand(m, device=DEV)
+    ys = torch.rand(m, device=DEV)
+    nw = (m + 31) // 32
+    bad = [
+        dict(count=torch.zeros(1, dtype=torch.int32, device=DEV)),
+        dict(count=torch.zeros(1, dtype=torch.float64, device=DEV)),
+        dict(words=torch.zeros(4 * nw, dtype=torch.uint8, device=DEV)),
+        dict(words=torch.zeros(nw, dtype=torch.float32, device=DEV)),
+        dict(words=torch.zeros(nw, dtype=torch.int64, device=DEV)),
+        dict(words=torch.zeros(nw - 1, dtype=torch.int32, device=DEV)),
+        dict(bytes_=torch.zeros(m, dtype=torch.int32, device=DEV)),
+        dict(bytes_=torch.zeros(m - 1, dtype=torch.uint8, device=DEV)),
+        dict(count=torch.zeros(1, dtype=torch.int64)),  # host tensor
+    ]
+    with vp.PreparedPolygon.prepare(vx, vy, vp.KIND_ALL) as p:
+        for kw in bad:
+            with pytest.raises(vp.VpipError) as ei:
+                p.test(0, xs, ys, **kw)
+            assert ei.value.code == 6, kw
+            lists = {k if k != "count" else "counts": [v, None, None] for k, v in kw.items()}
+            with pytest.raises(vp.VpipError):
+                p.test_multi(xs, ys, **lists)
+        torch.cuda.synchronize()
+        w = torch.zeros(nw, dtype=torch.int32, device=DEV)
+        c = torch.zeros(1, dtype=torch.int64, device=DEV)
+        p.test(0, xs, ys, words=w, count=c)  # a good call still works
+        torch.cuda.synchronize()
+        assert c.item() == int(np.unpackbits(w.cpu().numpy().view(np.uint8)).sum())
