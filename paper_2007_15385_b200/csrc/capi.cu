@@ -400,21 +400,48 @@ int vpipg_prepare_csr(const uint32_t* offsets, const double* vx, const double* v
   db->kinds = kinds;
   db->offsets.assign(offsets, offsets + npoly + 1);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  // fixed-stride 32-byte-aligned blocks: header (2 slots) + up to n_max + 1 rows
-  uint32_t nmax = 0;
-  for (uint32_t i = 0; i < npoly; ++i) nmax = std::max(nmax, offsets[i + 1] - offsets[i]);
-  const uint32_t stride = (nmax + 3 + 3) & ~3u;
-  const uint64_t slots = uint64_t(npoly) * stride;
+  // one 32-byte-aligned record per polygon, packed back to back: the header
+  // (4 slots) and n rows, rounded up to whole 32-byte units (vpipg_internal.h)
+  // (a fixed stride of the largest record when that costs at most 1.5x the
+  // packed size -- C4's 4..16-gons -- saving the kernels a dependent load;
+  // packed with per-polygon offsets otherwise, so one large polygon costs only
+  // its own rows)
+  std::vector<uint32_t> rec(npoly);
+  uint64_t units = 0, umax = 0;
+  for (uint32_t i = 0; i < npoly; ++i) {
+    rec[i] = static_cast<uint32_t>(units);
+    const uint64_t nn = offsets[i + 1] - offsets[i];
+    const uint64_t u = 1 + 3 * std::max<uint64_t>(1, (nn + 7) / 8);  // header, 8-edge groups
+    units += u;
+    umax = std::max(umax, u);
+  }
+  uint32_t stride = 0;
+  if (npoly && umax * npoly <= units + units / 2 && umax <= 1024) {
+    stride = static_cast<uint32_t>(umax);
+    units = umax * npoly;
+    for (uint32_t i = 0; i < npoly; ++i) rec[i] = i * stride;
+  }
+  if (units > UINT32_MAX) {  // record offsets are u32 in 32-byte units (128 GiB)
+    delete db;
+    return kInvalid;
+  }
   size_t off = 0;
   auto take = [&](size_t bytes) { const size_t o = off; off = align256(off + bytes); return o; };
   const size_t o_offs = take((npoly + 1) * sizeof(uint32_t));
+  const size_t o_rec = take(npoly * sizeof(uint32_t));
   const size_t o_vx = take(nv * sizeof(double)), o_vy = take(nv * sizeof(double));
-  const size_t o_vvx = take(nv * sizeof(double)), o_vvy = take(nv * sizeof(double));
   const size_t o_inner = take(npoly * sizeof(double2)), o_outer = take(nv * sizeof(double2));
-  const size_t o_gen = take(slots * sizeof(float2)), o_ccw = take(slots * sizeof(float2));
-  const size_t o_raw = take(slots * sizeof(float2));
+  const size_t o_recs = take(units * 32);
   const size_t o_status = take(npoly * sizeof(int32_t));
-  cudaError_t e = cudaMalloc(&db->blob, off ? off : 256);
+  // stream-ordered allocation from the library's per-device pool (warm ingest
+  // pays no cudaMalloc), released stream-ordered by vpipg_db_destroy
+  cudaMemPool_t pool = nullptr;
+  rc = blob_pool(device, &pool);
+  if (rc) {
+    delete db;
+    return rc;
+  }
+  cudaError_t e = cudaMallocFromPoolAsync(&db->blob, off ? off : 256, pool, s);
   if (e != cudaSuccess) {
     delete db;
     return cuda_code(e);
@@ -422,23 +449,21 @@ int vpipg_prepare_csr(const uint32_t* offsets, const double* vx, const double* v
   char* b = static_cast<char*>(db->blob);
   CsrPrepArgs a{};
   a.offsets = reinterpret_cast<const uint32_t*>(b + o_offs);
-  a.stride = stride;
+  a.rec = reinterpret_cast<const uint32_t*>(b + o_rec);
   a.vx = reinterpret_cast<const double*>(b + o_vx);
   a.vy = reinterpret_cast<const double*>(b + o_vy);
   a.npoly = npoly;
   a.kinds = kinds;
-  a.vvx = reinterpret_cast<double*>(b + o_vvx);
-  a.vvy = reinterpret_cast<double*>(b + o_vvy);
   a.inner = reinterpret_cast<double2*>(b + o_inner);
   a.outer = reinterpret_cast<double2*>(b + o_outer);
-  a.gen = reinterpret_cast<float2*>(b + o_gen);
-  a.ccw = reinterpret_cast<float2*>(b + o_ccw);
-  a.raw = reinterpret_cast<float2*>(b + o_raw);
+  a.recs = reinterpret_cast<float2*>(b + o_recs);
   a.status = reinterpret_cast<int32_t*>(b + o_status);
   std::vector<int32_t> status(npoly);
   do {
-    if ((e = cudaMemsetAsync(b, 0, off, s)) != cudaSuccess) break;
+    // the generators of polygons that fail validation read back as zeros
+    if ((e = cudaMemsetAsync(b + o_inner, 0, o_recs - o_inner, s)) != cudaSuccess) break;
     if ((e = cudaMemcpyAsync(b + o_offs, offsets, (npoly + 1) * sizeof(uint32_t), cudaMemcpyHostToDevice, s)) != cudaSuccess) break;
+    if (npoly && (e = cudaMemcpyAsync(b + o_rec, rec.data(), npoly * sizeof(uint32_t), cudaMemcpyHostToDevice, s)) != cudaSuccess) break;
     if (nv && (e = cudaMemcpyAsync(b + o_vx, vx, nv * sizeof(double), cudaMemcpyHostToDevice, s)) != cudaSuccess) break;
     if (nv && (e = cudaMemcpyAsync(b + o_vy, vy, nv * sizeof(double), cudaMemcpyHostToDevice, s)) != cudaSuccess) break;
     if ((e = launch_prep_csr(a, s)) != cudaSuccess) break;
@@ -450,7 +475,7 @@ int vpipg_prepare_csr(const uint32_t* offsets, const double* vx, const double* v
     return cuda_code(e);
   }
   if (per_poly_status) std::copy(status.begin(), status.end(), per_poly_status);
-  db->t = DbTables{npoly, kinds, stride, a.gen, a.ccw, a.raw};
+  db->t = DbTables{npoly, kinds, stride, a.rec, a.recs};
   db->d_offsets = a.offsets;
   db->d_inner = a.inner;
   db->d_outer = a.outer;
@@ -462,7 +487,7 @@ void vpipg_db_destroy(vpipg_db* db) {
   if (!db) return;
   if (db->blob) {
     DeviceGuard g(db->device);
-    cudaFree(db->blob);
+    cudaFreeAsync(db->blob, nullptr);  // back to the pool, as vpipg_destroy
   }
   delete db;
 }

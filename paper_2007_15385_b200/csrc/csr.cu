@@ -2,25 +2,29 @@
 // preparation of a CSR polygon table and the gather test kernels.
 //
 // prep_csr_kernel, one thread per polygon:
-//   validate_polygon (geometry.cpp:53-98) -> per-polygon status, CCW order,
-//   to_voronoi (voronoi.cpp:60-71) with the reference's exact f64 arithmetic,
-//   then one fixed-stride, 32-byte-aligned block per polygon and engine: a
-//   16-byte header (n | invalid flag, frame origin c) and fp32 rows in the
-//   polygon-local frame: the n outer generators (Voronoi, c = the centroid
-//   rounded to f32, so the inner generator is the origin), the validated
-//   vertices (sign-of-offset) and the RAW vertices (ray crossing,
-//   vpip.cpp:120-128), both as v_{n-1}, v_0 .. v_{n-1} with c = the f32
-//   bounding-box centre.
-// gather_kernel: every (point, polygon id) pair reads its polygon's block in
-//   32-byte loads (header + 2 rows, then 4 rows at a time) from the
-//   L2-resident tables; q' = q - c is exact in f32 (Sterbenz) for points near
-//   their polygon. Per point-edge:
-//     Voronoi    |q'-pk'|^2 - |q'-p0'|^2 >= 0 (the reference's squared
-//                distances, engines.cpp:85-98): 5 FP ops
-//     offset     a_j*b_i - a_i*b_j >= 0 with (a, b) = q' - v': the cross
-//                product (q - v_j) x (v_i - v_j) of engines.cpp:150-152
-//     crossing   in_range = H_i ^ H_j, on_left = sign(s) ^ H_i (H = [v.y > qy],
-//                s the same cross product), parity by XOR (engines.cpp:187-196)
+//   validate_polygon (geometry.cpp:53-98) -> per-polygon status and
+//   orientation, to_voronoi (voronoi.cpp:60-71) with the reference's exact f64
+//   arithmetic (the generator set vpipg_db_generators reads back), then ONE
+//   32-byte-aligned record per polygon (vpipg_internal.h): a 32-byte header
+//   (n and flags, frame origin c, the centroid p0' - the inner generator - and
+//   the closing vertex) and the raw vertex rows, f32 in the polygon-local
+//   frame (c = the f32 bounding-box centre). Records are packed back to back
+//   (per-polygon offsets), so one polygon with many vertices costs only its
+//   own rows.
+// gather_all_kernel / gather_kernel: every (point, polygon id) pair reads its
+//   polygon's header and walks its rows once, in 32-byte loads, from the
+//   L2-resident records; q' = q - c is exact in f32 (Sterbenz) for points near
+//   their polygon. For the edge v_j -> v_i of consecutive rows:
+//     Voronoi    outer generator g = p0' - f n (the mirror of the centroid
+//                across the edge line with normal n, reflect_generator's Eq. 8;
+//                prep stores the scalar f per edge, n comes from the two rows),
+//                inside iff |q'-g|^2 >= |q'-p0'|^2 for every edge
+//                (engines.cpp:85-98, ties inside)
+//     offset     s = (q - v_j) x (q - v_i) >= 0 in the validated (CCW) order,
+//                i.e. s <= 0 on raw rows that validation reversed
+//                (engines.cpp:150-152)
+//     crossing   in_range = H_i ^ H_j, on_left = sign(s) ^ H_i (H = [v.y > qy]),
+//                parity by XOR (engines.cpp:187-196), on the raw order
 #include <climits>
 #include <cmath>
 #include <cstdint>
@@ -48,341 +52,230 @@ __global__ void prep_csr_kernel(CsrPrepArgs a) {
   if (i >= a.npoly) return;
   const uint32_t s = a.offsets[i];
   const int n = static_cast<int>(a.offsets[i + 1] - s);
-  const uint64_t blk = (uint64_t)i * a.stride;
+  float2* r = a.recs + 4 * (uint64_t)a.rec[i];
   const CsrView raw{a.vx + s, a.vy + s};
   int status = 0;
   bool rev = false;
   const bool convex = a.kinds & (kKindVoronoi | kKindOffset);
   if (convex) status = validate_exact(raw, n, &rev);
-  double* vvx = a.vvx + s;
-  double* vvy = a.vvy + s;
   double x0 = INFINITY, x1 = -INFINITY, y0 = INFINITY, y1 = -INFINITY;
   for (int k = 0; k < n; ++k) {
-    const double2 p = raw(rev ? n - 1 - k : k);
-    vvx[k] = p.x;
-    vvy[k] = p.y;
+    const double2 p = raw(k);
     if (isfinite(p.x) && isfinite(p.y)) {
       x0 = fmin(x0, p.x); x1 = fmax(x1, p.x);
       y0 = fmin(y0, p.y); y1 = fmax(y1, p.y);
     }
   }
-  // polygon-local frame: f32 centre of the bounding box (exactly representable)
+  // polygon-local frame: f32 centre of the bounding box
   const float fcx = (x0 <= x1) ? static_cast<float>(0.5 * (x0 + x1)) : 0.f;
   const float fcy = (y0 <= y1) ? static_cast<float>(0.5 * (y0 + y1)) : 0.f;
   const double cx = fcx, cy = fcy;
-  const CsrView val{vvx, vvy};
-  // Voronoi frame: the centroid rounded to f32, so p0' = p0 - c is below half
-  // an ulp of |p0| (< 6e-8 max(1, |p0|), far inside the 1e-5 band) and is
-  // taken as 0 -- the block carries the n generators only
-  float gcx = fcx, gcy = fcy;
+  // validated (CCW) order = the raw rows read backwards when reversed
+  auto val = [&](int k) { return raw(rev ? n - 1 - k : k); };
+  float2 p0 = make_float2(0.f, 0.f);
+  // record body: groups of 8 edges, group g at slot 4 + 12 g: its 8 rows, then
+  // its 8 f values (vpipg_internal.h)
+  auto row = [&](int k) -> float2& { return r[4 + 12 * (k >> 3) + (k & 7)]; };
+  auto fval = [&](int k) -> float& {
+    return reinterpret_cast<float*>(r + 12 + 12 * (k >> 3))[k & 7];
+  };
   if (status == 0 && (a.kinds & kKindVoronoi)) {
     double px, py;
     centroid_exact(val, n, &px, &py);
     a.inner[i] = make_double2(px, py);
-    gcx = static_cast<float>(px);
-    gcy = static_cast<float>(py);
+    p0 = local(make_double2(px, py), cx, cy);
     for (int k = 0; k < n && status == 0; ++k) {
       double2 g;
       status = reflect_exact(val(k), val((k + 1) % n), px, py, &g);
-      if (status) break;
-      a.outer[s + k] = g;
-      a.gen[blk + 2 + k] = local(g, gcx, gcy);
+      if (status == 0) a.outer[s + k] = g;
     }
-  }
-  // offset / crossing: v_{n-1}, v_0 .. v_{n-1} -- the leading copy of the last
-  // vertex closes the ring without a register pair held across the row loop
-  // (that pair costs the crossing kernel a CTA per SM or a spill)
-  if (status == 0 && (a.kinds & kKindOffset) && n > 0) {
-    a.ccw[blk + 2] = local(val(n - 1), cx, cy);
-    for (int k = 0; k < n; ++k) a.ccw[blk + 3 + k] = local(val(k), cx, cy);
-  }
-  if ((a.kinds & kKindCrossing) && n > 0) {
-    a.raw[blk + 2] = local(raw(n - 1), cx, cy);
-    for (int k = 0; k < n; ++k) a.raw[blk + 3 + k] = local(raw(k), cx, cy);
+    // the outer generator of raw edge v_{k-1} -> v_k as g = p0 - f_k n_k with
+    // n_k = (v_{k-1}.y - v_k.y, v_k.x - v_{k-1}.x) from the f32 rows the
+    // kernels read: f_k = -(g - p0).n_k / |n_k|^2 (g - p0 is parallel to n_k;
+    // the rows' rounding only turns it by < 1e-7 rad)
+    for (int k = 0; k < n && status == 0; ++k) {
+      const float2 vj = local(raw((k + n - 1) % n), cx, cy), vi = local(raw(k), cx, cy);
+      const double nx = static_cast<double>(vj.y) - vi.y, ny = static_cast<double>(vi.x) - vj.x;
+      const int vk = rev ? n - 1 - k : (k + n - 1) % n;  // the validated edge this raw edge is
+      const double2 g = a.outer[s + vk];
+      const double dd = nx * nx + ny * ny;
+      fval(k) = dd > 0.0 ? static_cast<float>(-((g.x - px) * nx + (g.y - py) * ny) / dd) : 0.f;
+    }
   }
   a.status[i] = status;
   // a failed polygon tests outside under Voronoi / sign-of-offset (crossing
   // ignores the flag: it accepts any polygon)
-  const bool bad = convex && status != 0;
-  const float nbits = __uint_as_float(static_cast<uint32_t>(n) | (bad ? kRangeInvalid : 0u));
-  for (float2* t : {a.gen, a.ccw, a.raw}) t[blk] = make_float2(nbits, 0.f);
-  // the raw rows equal the validated ones unless validation reversed or
-  // rejected the polygon (or did not run)
-  if (!convex || bad || rev)
-    a.raw[blk] = make_float2(__uint_as_float(__float_as_uint(nbits) | kRawDiffers), 0.f);
-  a.gen[blk + 1] = make_float2(gcx, gcy);
-  a.ccw[blk + 1] = make_float2(fcx, fcy);
-  a.raw[blk + 1] = make_float2(fcx, fcy);
+  const uint32_t nf = static_cast<uint32_t>(n) | ((convex && status != 0) ? kRangeInvalid : 0u) |
+                      (rev ? kReversed : 0u);
+  r[0] = make_float2(__uint_as_float(nf), 0.f);
+  r[1] = make_float2(fcx, fcy);
+  r[2] = p0;
+  if (n > 0) {
+    r[3] = local(raw(n - 1), cx, cy);
+    for (int k = 0; k < n; ++k) row(k) = local(raw(k), cx, cy);
+  }
 }
 
-#ifndef VPIPG_GP
-#define VPIPG_GP 1
-#endif
 #ifndef VPIPG_GMINB
-#define VPIPG_GMINB 8
+#define VPIPG_GMINB 5
 #endif
-constexpr int kGP = VPIPG_GP;  // pairs per lane
+#ifndef VPIPG_GSTREAM_AHEAD
+#define VPIPG_GSTREAM_AHEAD 1
+#endif
 #ifndef VPIPG_GMINB_ALL
-#define VPIPG_GMINB_ALL 5  // the fused join keeps two walks' state live: 48 registers (6 CTAs: 7.75 ms, 5: 6.98, 4: 7.27 at C4)
+#define VPIPG_GMINB_ALL 4
 #endif
 constexpr int kGThreads = 256;
 
-// 32-byte (256-bit) read-only load: four rows (or the header + two rows).
+// 32-byte (256-bit) read-only load: four rows (or the header).
 struct Rows4 {
   float v[8];
 };
 __device__ __forceinline__ Rows4 ld256(const float2* p) {
   Rows4 r;
-  asm volatile("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+  // not volatile: the compiler may hoist the next chunk's load above this
+  // chunk's arithmetic (the tables are read-only for the kernel's lifetime)
+  asm("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
                : "=f"(r.v[0]), "=f"(r.v[1]), "=f"(r.v[2]), "=f"(r.v[3]), "=f"(r.v[4]),
                  "=f"(r.v[5]), "=f"(r.v[6]), "=f"(r.v[7])
                : "l"(p));
   return r;
 }
 
-// Per-engine accumulation over a polygon's rows (row 0 first): Voronoi rows
-// are the n outer generators (the inner one is the origin); offset / crossing
-// rows are v_{n-1}, v_0 .. v_{n-1}, row 0 only seeding the previous vertex.
-template <int kEngine>
-struct RowAcc {
-  uint32_t acc = 0;
-  float pa = 0.f, pb = 0.f;  // previous row relative to q' (offset / crossing), or |q'-p0'|^2
-  __device__ __forceinline__ void first(float qx, float qy, float rx, float ry) {
-    if (kEngine == 0) {
-      pa = fmaf(qx, qx, qy * qy);  // inner_sq with p0' = 0
-      next(qx, qy, rx, ry);
-    } else {
-      pa = qx - rx;
-      pb = qy - ry;
+
+// The three engines' state for one pair over one polygon's edges.
+template <bool kV, bool kO, bool kC>
+struct PairAcc {
+  float qx, qy;       // q' (local frame)
+  float qpx, qpy;     // q' - p0' (p0' the inner generator)
+  float d0;           // |q' - p0'|^2
+  float pa, pb;       // q' - v_j of the previous row
+  float px, py;       // v_j' itself (the Voronoi edge normal)
+  uint32_t vor = 0;   // sign bits of |q'-g|^2 - |q'-p0'|^2 (any set: outside)
+  uint32_t off = 0;   // sign bits of the oriented cross products (any set: outside)
+  uint32_t par = 0;   // crossing parity (bit 31)
+  uint32_t flip = 0;  // 0x80000000 when the raw rows run clockwise
+
+  __device__ __forceinline__ void start(float x, float y, float cx, float cy, float gx, float gy,
+                                        float lx, float ly, uint32_t rev) {
+    qx = x - cx;  // exact for points near their polygon (Sterbenz)
+    qy = y - cy;
+    if (kV) {
+      qpx = qx - gx;
+      qpy = qy - gy;
+      d0 = fmaf(qpx, qpx, qpy * qpy);
     }
+    pa = qx - lx;
+    pb = qy - ly;
+    px = lx;
+    py = ly;
+    flip = rev ? 0x80000000u : 0u;
   }
-  __device__ __forceinline__ void next(float qx, float qy, float rx, float ry) {
+  // edge v_j -> v_i with v_j the previous row, v_i = (rx, ry) and f the
+  // edge's generator coefficient (the outer generator g = p0' - f n)
+  __device__ __forceinline__ void edge(float rx, float ry, float f) {
     const float a = qx - rx, b = qy - ry;
-    if (kEngine == 0) {  // |q'-pk'|^2 - |q'-p0'|^2 >= 0 for every outer generator
-      acc |= __float_as_uint(fmaf(a, a, b * b) - pa);
-    } else {
-      const float s = fmaf(pa, b, -(a * pb));  // (q - v_j) x (q - v_i)
-      if (kEngine == 1) {
-        acc |= __float_as_uint(s);
-      } else {
-        const uint32_t hi = __float_as_uint(b), hj = __float_as_uint(pb);
-        acc ^= (hi ^ hj) & (__float_as_uint(s) ^ hi);
-      }
-      pa = a;
-      pb = b;
+    if (kV) {
+      // n = (v_j.y - v_i.y, v_i.x - v_j.x), the edge line's normal
+      // (edge_coefficients, voronoi.cpp:23-31); q' - g = (q' - p0') + f n
+      const float nx = py - ry, ny = rx - px;
+      const float ex = fmaf(f, nx, qpx), ey = fmaf(f, ny, qpy);
+      vor |= __float_as_uint(fmaf(ex, ex, ey * ey) - d0);  // |q'-g|^2 - |q'-p0'|^2
     }
-  }
-  __device__ __forceinline__ bool inside() const {
-    return kEngine == 2 ? (acc >> 31) != 0 : !(acc >> 31);
+    if (kO || kC) {
+      const float s = fmaf(pa, b, -(a * pb));  // (q - v_j) x (q - v_i)
+      if (kO) off |= __float_as_uint(s) ^ flip;
+      if (kC) {
+        const uint32_t hi = __float_as_uint(b), hj = __float_as_uint(pb);
+        par ^= (hi ^ hj) & (__float_as_uint(s) ^ hi);
+      }
+    }
+    pa = a;
+    pb = b;
+    px = rx;
+    py = ry;
   }
 };
 
-template <int kEngine>  // 0 voronoi, 1 offset, 2 crossing
-__global__ void __launch_bounds__(kGThreads, VPIPG_GMINB) gather_kernel(const DbTables t,
-                                                                        const GatherArgs a) {
-  const int lane = threadIdx.x & 31;
-  const uint64_t gwarp = (uint64_t)blockIdx.x * (kGThreads / 32) + (threadIdx.x >> 5);
-  const uint64_t stride = (uint64_t)gridDim.x * (kGThreads / 32) * 32 * kGP;
-  const float2* tab = kEngine == 0 ? t.gen : kEngine == 1 ? t.ccw : t.raw;
-  uint32_t count = 0;
-  for (uint64_t base = gwarp * 32 * kGP; base < a.m; base += stride) {
-    float qx[kGP], qy[kGP];
-    const float2* blk[kGP];
-    uint32_t rows[kGP];  // rows to read (n Voronoi, n + 1 otherwise), 0 = outside regardless
-    bool ok[kGP];
-    RowAcc<kEngine> r[kGP];
-    uint32_t rmax = 0;
+// One pair against its polygon's record; `in` receives the requested engines'
+// answers (a NaN coordinate gets the reference's IEEE answer: Voronoi outside,
+// sign-of-offset inside).
+template <bool kV, bool kO, bool kC>
+__device__ __forceinline__ void test_pair(const DbTables& t, bool ok, uint32_t id, float x, float y,
+                                          bool (&in)[3]) {
+  // fixed-stride records (t.stride 32-byte units, id * stride) when the sizes
+  // are uniform enough; per-polygon offsets otherwise (one dependent load more)
+  const uint64_t unit = t.stride ? (uint64_t)id * t.stride : (uint64_t)(ok ? __ldg(t.rec + id) : 0u);
+  const float2* r = t.recs + 4 * (ok ? unit : 0u);
+  const Rows4 h = ld256(r);
+  const uint32_t nf = __float_as_uint(h.v[0]);
+  const uint32_t n = ok ? nf & kNMask : 0u;
+  PairAcc<kV, kO, kC> acc;
+  acc.start(x, y, h.v[2], h.v[3], h.v[4], h.v[5], h.v[6], h.v[7], nf & kReversed);
+  // group 0 (edges 0..7) is read together with the header -- its address does
+  // not depend on n -- and later groups after it, three 32-byte loads each
+  auto group = [&](uint32_t g, const Rows4& h0, const Rows4& h1, const Rows4& f) {
 #pragma unroll
-    for (int p = 0; p < kGP; ++p) {
-      const uint64_t j = base + 32u * p + lane;
-      ok[p] = j < a.m;
-      const uint32_t id = ok[p] ? __ldcs(a.ids + j) : 0u;
-      const float x = ok[p] ? __ldcs(a.xs + j) : 0.f;
-      const float y = ok[p] ? __ldcs(a.ys + j) : 0.f;
-      ok[p] = ok[p] && id < t.npoly;
-      blk[p] = tab + (uint64_t)(ok[p] ? id : 0u) * t.stride;
-      const Rows4 h = ok[p] ? ld256(blk[p]) : Rows4{};
-      const uint32_t nf = __float_as_uint(h.v[0]);
-      // a polygon that failed validation only disables the convex engines: ray
-      // crossing takes the raw vertices of any polygon (vpip.cpp:120-128)
-      if (kEngine != 2) ok[p] = ok[p] && !(nf & kRangeInvalid);
-      const uint32_t n = nf & ~(kRangeInvalid | kRawDiffers);
-      rows[p] = (ok[p] && n > 0) ? (kEngine == 0 ? n : n + 1) : 0u;
-      qx[p] = x - h.v[2];  // exact for points near their polygon (Sterbenz)
-      qy[p] = y - h.v[3];
-      if (rows[p] > 0) r[p].first(qx[p], qy[p], h.v[4], h.v[5]);
-      if (rows[p] > 1) r[p].next(qx[p], qy[p], h.v[6], h.v[7]);
-      rmax = rows[p] > rmax ? rows[p] : rmax;
-    }
-    if (kEngine == 1) {
-      // sign-of-offset: per-row predicates (the split loop below spills its
-      // extra live values at 32 registers for this engine)
-      for (uint32_t k = 2; k < rmax; k += 4) {  // rows k .. k+3 = slots k+2 .. k+5
-#pragma unroll
-        for (int p = 0; p < kGP; ++p) {
-          if (k < rows[p]) {
-            const Rows4 q4 = ld256(blk[p] + k + 2);
-#pragma unroll
-            for (int u = 0; u < 4; ++u)
-              if (k + u < rows[p]) r[p].next(qx[p], qy[p], q4.v[2 * u], q4.v[2 * u + 1]);
-          }
-        }
-      }
-    } else {
-#pragma unroll
-      for (int p = 0; p < kGP; ++p) {
-        // full 4-row chunks without per-row predicates, then a tail of <= 3
-        uint32_t k = 2;
-        for (; k + 3 < rows[p]; k += 4) {
-          const Rows4 q4 = ld256(blk[p] + k + 2);
-#pragma unroll
-          for (int u = 0; u < 4; ++u) r[p].next(qx[p], qy[p], q4.v[2 * u], q4.v[2 * u + 1]);
-        }
-        if (k < rows[p]) {
-          const Rows4 q4 = ld256(blk[p] + k + 2);
-          r[p].next(qx[p], qy[p], q4.v[0], q4.v[1]);
-          if (k + 1 < rows[p]) r[p].next(qx[p], qy[p], q4.v[2], q4.v[3]);
-          if (k + 2 < rows[p]) r[p].next(qx[p], qy[p], q4.v[4], q4.v[5]);
-        }
+    for (int u = 0; u < 8; ++u) {
+      if (8 * g + u < n) {
+        const Rows4& q = u < 4 ? h0 : h1;
+        acc.edge(q.v[2 * (u & 3)], q.v[2 * (u & 3) + 1], kV ? f.v[u] : 0.f);
       }
     }
-    bool in[kGP];
-#pragma unroll
-    for (int p = 0; p < kGP; ++p) {
-      in[p] = ok[p] && rows[p] > 0 && r[p].inside();
-      // a NaN coordinate: the reference's IEEE answer (Voronoi compares are
-      // false -> outside; sign-of-offset raises no flag -> inside)
-      if (kEngine != 2 && ok[p] && rows[p] > 0 && (qx[p] != qx[p] || qy[p] != qy[p]))
-        in[p] = kEngine == 1;
-    }
-    uint32_t w[kGP];
-#pragma unroll
-    for (int p = 0; p < kGP; ++p) {
-      w[p] = __ballot_sync(0xffffffffu, in[p]);
-      count += in[p];
-    }
-    if (a.words && lane == 0) {
-      const uint64_t w0 = base >> 5, nwords = (a.m + 31) >> 5;
-#pragma unroll
-      for (int p = 0; p < kGP; ++p)
-        if (w0 + p < nwords) a.words[w0 + p] = w[p];
-    }
-    if (a.bytes) {
-#pragma unroll
-      for (int p = 0; p < kGP; ++p) {
-        const uint64_t j = base + 32u * p + lane;
-        if (j < a.m) a.bytes[j] = in[p] ? 1 : 0;
-      }
-    }
+  };
+  {
+    const Rows4 r0 = ld256(r + 4), r1 = ld256(r + 8);
+    const Rows4 f0 = kV ? ld256(r + 12) : Rows4{};
+    group(0, r0, r1, f0);
   }
-#pragma unroll
-  for (int s = 16; s > 0; s >>= 1) count += __shfl_xor_sync(0xffffffffu, count, s);
-  if (lane == 0 && a.inside && count) atomicAdd(a.inside, (unsigned long long)count);
+  for (uint32_t g = 1; 8 * g < n; ++g) {
+    const float2* b = r + 4 + 12 * g;
+    const Rows4 r0 = ld256(b), r1 = ld256(b + 4);
+    const Rows4 f0 = kV ? ld256(b + 8) : Rows4{};
+    group(g, r0, r1, f0);
+  }
+  const bool convex_ok = n > 0 && !(nf & kRangeInvalid);
+  const bool nan = acc.qx != acc.qx || acc.qy != acc.qy;
+  in[0] = kV && convex_ok && !nan && !(acc.vor >> 31);
+  in[1] = kO && convex_ok && (nan || !(acc.off >> 31));
+  in[2] = kC && n > 0 && (acc.par >> 31);
 }
 
-// Walk rows 2 .. rows-1 of a block (rows 0 and 1 came with the header load)
-// into one accumulator, or into two that share every row (kBoth: offset +
-// crossing over the same vertex rows).
-template <bool kBoth, class R1, class R2>
-__device__ __forceinline__ void walk(const float2* blk, uint32_t rows, float qx, float qy, R1& r1,
-                                     R2& r2) {
-  uint32_t k = 2;
-  for (; k + 3 < rows; k += 4) {
-    const Rows4 q4 = ld256(blk + k + 2);
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      r1.next(qx, qy, q4.v[2 * u], q4.v[2 * u + 1]);
-      if (kBoth) r2.next(qx, qy, q4.v[2 * u], q4.v[2 * u + 1]);
-    }
-  }
-  if (k < rows) {
-    const Rows4 q4 = ld256(blk + k + 2);
-#pragma unroll
-    for (int u = 0; u < 3; ++u)
-      if (k + u < rows) {
-        r1.next(qx, qy, q4.v[2 * u], q4.v[2 * u + 1]);
-        if (kBoth) r2.next(qx, qy, q4.v[2 * u], q4.v[2 * u + 1]);
-      }
-  }
-}
-
-// Fused join: every (point, id) pair is read once and tested by all three
-// engines. Voronoi walks the generator block; sign-of-offset and crossing
-// share ONE walk over the raw vertex rows (the same rows and frame as the
-// validated ones unless the header says kRawDiffers, when offset walks its own
-// block), so a pair touches two polygon blocks instead of three.
-__global__ void __launch_bounds__(kGThreads, VPIPG_GMINB_ALL)
-    gather_all_kernel(const DbTables t, const GatherArgs av, const GatherArgs ao,
-                      const GatherArgs ac) {
+// kMask: bit e = engine e (Voronoi, offset, crossing) of this launch; a[e]
+// its outputs (all share xs, ys, ids, m)
+template <int kMask>
+__global__ void __launch_bounds__(kGThreads, kMask == 7 ? VPIPG_GMINB_ALL : VPIPG_GMINB)
+    gather_kernel(const DbTables t, const GatherArgs av, const GatherArgs ao, const GatherArgs ac) {
+  constexpr bool kV = kMask & 1, kO = kMask & 2, kC = kMask & 4;
+  const GatherArgs& a0 = kV ? av : kO ? ao : ac;
   const int lane = threadIdx.x & 31;
   const uint64_t gwarp = (uint64_t)blockIdx.x * (kGThreads / 32) + (threadIdx.x >> 5);
   const uint64_t stride = (uint64_t)gridDim.x * (kGThreads / 32) * 32;
   uint32_t cnt[3] = {0, 0, 0};
-  for (uint64_t base = gwarp * 32; base < av.m; base += stride) {
+  // the next pair's stream words are loaded one iteration ahead
+  auto load = [&](uint64_t j, uint32_t& id, float& x, float& y) {
+    const bool in = j < a0.m;
+    id = in ? __ldcs(a0.ids + j) : 0u;
+    x = in ? __ldcs(a0.xs + j) : 0.f;
+    y = in ? __ldcs(a0.ys + j) : 0.f;
+  };
+  uint32_t nid;
+  float nx, ny;
+  load(gwarp * 32 + lane, nid, nx, ny);
+  for (uint64_t base = gwarp * 32; base < a0.m; base += stride) {
     const uint64_t j = base + lane;
-    bool ok = j < av.m;
-    const uint32_t id = ok ? __ldcs(av.ids + j) : 0u;
-    const float x = ok ? __ldcs(av.xs + j) : 0.f;
-    const float y = ok ? __ldcs(av.ys + j) : 0.f;
+    const uint32_t id = nid;
+    const float x = nx, y = ny;
+    if (VPIPG_GSTREAM_AHEAD) load(j + stride, nid, nx, ny);
+    bool ok = j < a0.m;
     ok = ok && id < t.npoly;
-    const uint64_t off = (uint64_t)(ok ? id : 0u) * t.stride;
-    bool in[3] = {false, false, false};
-    // ---- Voronoi: generator block, its own frame ----
-    {
-      const float2* blk = t.gen + off;
-      const Rows4 h = ok ? ld256(blk) : Rows4{};
-      const uint32_t nf = __float_as_uint(h.v[0]);
-      const uint32_t n = nf & ~(kRangeInvalid | kRawDiffers);
-      const uint32_t rows = (ok && !(nf & kRangeInvalid)) ? n : 0u;
-      const float qx = x - h.v[2], qy = y - h.v[3];
-      RowAcc<0> r;
-      if (rows > 0) r.first(qx, qy, h.v[4], h.v[5]);
-      if (rows > 1) r.next(qx, qy, h.v[6], h.v[7]);
-      walk<false>(blk, rows, qx, qy, r, r);
-      in[0] = rows > 0 && (qx != qx || qy != qy ? false : r.inside());
-    }
-    // ---- crossing (+ offset when the rows coincide): raw block ----
-    {
-      const float2* blk = t.raw + off;
-      const Rows4 h = ok ? ld256(blk) : Rows4{};
-      const uint32_t nf = __float_as_uint(h.v[0]);
-      const uint32_t n = nf & ~(kRangeInvalid | kRawDiffers);
-      const uint32_t rows = (ok && n > 0) ? n + 1 : 0u;
-      const bool shared = !(nf & kRawDiffers);
-      const float qx = x - h.v[2], qy = y - h.v[3];
-      RowAcc<2> rc;
-      RowAcc<1> ro;
-      if (rows > 0) {
-        rc.first(qx, qy, h.v[4], h.v[5]);
-        ro.first(qx, qy, h.v[4], h.v[5]);
-      }
-      if (rows > 1) {
-        rc.next(qx, qy, h.v[6], h.v[7]);
-        ro.next(qx, qy, h.v[6], h.v[7]);
-      }
-      if (shared)
-        walk<true>(blk, rows, qx, qy, rc, ro);
-      else
-        walk<false>(blk, rows, qx, qy, rc, rc);
-      in[2] = rows > 0 && rc.inside();
-      const bool nan = qx != qx || qy != qy;
-      if (shared) {
-        in[1] = rows > 0 && (nan || ro.inside());
-      } else if (ok && !(nf & kRangeInvalid)) {
-        // reversed by validation: offset walks the validated (CCW) rows
-        const float2* cb = t.ccw + off;
-        const Rows4 hc = ld256(cb);
-        const float cx = x - hc.v[2], cy = y - hc.v[3];
-        RowAcc<1> r;
-        r.first(cx, cy, hc.v[4], hc.v[5]);
-        if (rows > 1) r.next(cx, cy, hc.v[6], hc.v[7]);
-        walk<false>(cb, rows, cx, cy, r, r);
-        in[1] = rows > 0 && (nan || r.inside());
-      }
-    }
+    bool in[3];
+    test_pair<kV, kO, kC>(t, ok, id, x, y, in);
+    if (!VPIPG_GSTREAM_AHEAD) load(j + stride, nid, nx, ny);
     const GatherArgs* args[3] = {&av, &ao, &ac};
 #pragma unroll
     for (int e = 0; e < 3; ++e) {
+      if (!(kMask & (1 << e))) continue;
       const GatherArgs& a = *args[e];
       const uint32_t w = __ballot_sync(0xffffffffu, in[e]);
       cnt[e] += in[e];
@@ -393,6 +286,7 @@ __global__ void __launch_bounds__(kGThreads, VPIPG_GMINB_ALL)
   const GatherArgs* args[3] = {&av, &ao, &ac};
 #pragma unroll
   for (int e = 0; e < 3; ++e) {
+    if (!(kMask & (1 << e))) continue;
     uint32_t c = cnt[e];
 #pragma unroll
     for (int s = 16; s > 0; s >>= 1) c += __shfl_xor_sync(0xffffffffu, c, s);
@@ -431,34 +325,34 @@ cudaError_t launch_prep_csr(const CsrPrepArgs& a, cudaStream_t stream) {
   return cudaGetLastError();
 }
 
+namespace {
+template <int kMask>
+cudaError_t launch_gather_mask(const DbTables& t, const GatherArgs& av, const GatherArgs& ao,
+                               const GatherArgs& ac, uint64_t m, cudaStream_t stream) {
+  int sms = 0, per_sm = 0;
+  auto k = gather_kernel<kMask>;
+  const cudaError_t e = launch_config(reinterpret_cast<const void*>(k), kGThreads, 0, &sms, &per_sm);
+  if (e != cudaSuccess) return e;
+  const uint64_t warps = (m + 31) / 32;
+  const uint64_t blocks = (warps + kGThreads / 32 - 1) / (kGThreads / 32);
+  const uint64_t cap = (uint64_t)sms * per_sm;
+  k<<<static_cast<int>(blocks < cap ? blocks : cap), kGThreads, 0, stream>>>(t, av, ao, ac);
+  return cudaGetLastError();
+}
+}  // namespace
+
 cudaError_t launch_gather(const DbTables& t, int engine, const GatherArgs& a, cudaStream_t stream) {
   if (a.m == 0) return cudaSuccess;
-  int dev = 0, sms = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const uint64_t warps = (a.m + 32 * kGP - 1) / (32 * kGP);
-  const uint64_t blocks = (warps + kGThreads / 32 - 1) / (kGThreads / 32);
-  const uint64_t cap = (uint64_t)sms * 8;
-  const int grid = static_cast<int>(blocks < cap ? blocks : cap);
   switch (engine) {
-    case 0: gather_kernel<0><<<grid, kGThreads, 0, stream>>>(t, a); break;
-    case 1: gather_kernel<1><<<grid, kGThreads, 0, stream>>>(t, a); break;
-    default: gather_kernel<2><<<grid, kGThreads, 0, stream>>>(t, a); break;
+    case 0: return launch_gather_mask<1>(t, a, a, a, a.m, stream);
+    case 1: return launch_gather_mask<2>(t, a, a, a, a.m, stream);
+    default: return launch_gather_mask<4>(t, a, a, a, a.m, stream);
   }
-  return cudaGetLastError();
 }
 
 cudaError_t launch_gather_all(const DbTables& t, const GatherArgs* a, cudaStream_t stream) {
   if (a[0].m == 0) return cudaSuccess;
-  int dev = 0, sms = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const uint64_t warps = (a[0].m + 31) / 32;
-  const uint64_t blocks = (warps + kGThreads / 32 - 1) / (kGThreads / 32);
-  const uint64_t cap = (uint64_t)sms * VPIPG_GMINB_ALL;
-  const int grid = static_cast<int>(blocks < cap ? blocks : cap);
-  gather_all_kernel<<<grid, kGThreads, 0, stream>>>(t, a[0], a[1], a[2]);
-  return cudaGetLastError();
+  return launch_gather_mask<7>(t, a[0], a[1], a[2], a[0].m, stream);
 }
 
 cudaError_t launch_fill_pairs(uint64_t seed, uint64_t first, uint64_t m, uint32_t npoly,

@@ -38,45 +38,45 @@ struct TestArgs {
 };
 
 // ---- polygon database (CSR batch of polygons; csr.cu) ----
-constexpr uint32_t kRangeInvalid = 0x80000000u;  // polygon failed validation: tests outside
-// set in the crossing block's header when its rows differ from the offset
-// block's (validation reversed or rejected the polygon): the fused join then
-// cannot evaluate both engines from one pass over the raw rows
-constexpr uint32_t kRawDiffers = 0x40000000u;
+constexpr uint32_t kRangeInvalid = 0x80000000u;  // polygon failed validation: Voronoi / offset outside
+constexpr uint32_t kReversed = 0x40000000u;      // validation reversed the (clockwise) raw order
+constexpr uint32_t kNMask = 0x3fffffffu;
 
-// Gather tables are compact, polygon-local, fixed-stride blocks: polygon i
-// owns `stride` float2 slots starting at slot i * stride (32-byte aligned):
-//   slots 0-1  header (n | kRangeInvalid as u32 bits, unused, f32 centre cx, cy)
-//   slots 2..  n + 1 rows relative to the centre:
-//              Voronoi  [inner, outer_0 .. outer_{n-1}]
-//              offset   [v_{n-1}, v_0 .. v_{n-1}] (validated, CCW)
-//              crossing [v_{n-1}, v_0 .. v_{n-1}] (raw order)
-// so one 32-byte load brings the header with the first two rows and every
-// further load four rows; consecutive rows are the engine's edges.
+// ONE record per polygon, 32-byte aligned, at float2 slot 4 * rec[i] (rec[i] =
+// i * stride when the database uses a fixed stride):
+//   slot 0   (n | kRangeInvalid | kReversed as u32 bits, 0)
+//   slot 1   frame origin c (f32 centre of the bounding box)
+//   slot 2   p0' = centroid - c (f32; the Voronoi inner generator)
+//   slot 3   v_{n-1}' (closes the ring)
+//   then groups of 8 edges, group g at slot 4 + 12 g: the rows v_{8g}' ..
+//   v_{8g+7}' (the RAW vertices relative to c, 64 bytes) and 8 floats f_k (32
+//   bytes): the outer generator of raw edge v_{k-1} -> v_k is p0' - f_k n_k,
+//   n_k the edge's normal; group 0 is present (and read) for every polygon
+// so a pair reads one header (the first 32-byte load brings slots 0-3) and one
+// walk of n rows for all three engines: crossing on the raw order
+// (vpip.cpp:120-128), sign-of-offset on the same rows with the orientation
+// taken from kReversed (the validated order is their reverse), Voronoi with
+// each outer generator rebuilt from its edge's rows and f_k (4 bytes per edge
+// instead of an 8-byte generator row).
 struct CsrPrepArgs {
   const uint32_t* offsets;  // npoly + 1 (input CSR)
   const double* vx;         // raw vertices (device)
   const double* vy;
   uint32_t npoly;
   uint32_t kinds;
-  uint32_t stride;          // slots per polygon block (multiple of 4)
-  double* vvx;              // validated (CCW) vertices, input CSR layout
-  double* vvy;
+  const uint32_t* rec;      // npoly record offsets, 32-byte units
   double2* inner;           // npoly generators (f64, exact)
-  double2* outer;           // nverts generators (f64, exact), input CSR layout
-  float2* gen;              // npoly * stride slots (Voronoi)
-  float2* ccw;              // npoly * stride slots (sign-of-offset)
-  float2* raw;              // npoly * stride slots (ray crossing)
+  double2* outer;           // nverts generators (f64, exact), input CSR layout (validated order)
+  float2* recs;             // the records
   int32_t* status;          // npoly: 0 or ErrorCode + 1
 };
 
 struct DbTables {
   uint32_t npoly;
   uint32_t kinds;
-  uint32_t stride;
-  const float2* gen;
-  const float2* ccw;
-  const float2* raw;
+  uint32_t stride;        // > 0: record i at 32-byte unit i * stride; 0: at rec[i]
+  const uint32_t* rec;
+  const float2* recs;
 };
 
 struct GatherArgs {
