@@ -384,6 +384,77 @@ class JoinJob:
         return cnt
 
 
+# ----------------------------------------------------------------- convert phase
+def convert_block(vp, device, stream):
+    """Warm preparation cost beside the reference's conversion phase
+    (run_benchmark times to_voronoi, bench.cpp:165-170; validate_polygon,
+    geometry.cpp:53-98, is timed separately). GPU: the C-ABI vpipg_prepare
+    call (host validation + the enqueued device conversion; returns without
+    waiting) and, separately, prepare + vpipg_poly_status (until the handle is
+    usable), medians of 50 warm calls through ctypes; the 65,536-polygon C4
+    ingest (vpipg_prepare_csr, synchronous: it returns per-polygon status),
+    median of 5 warm calls."""
+    import ctypes as C
+    L = vp.load()
+    sptr = C.c_void_p(stream.cuda_stream)
+    polys = [(8, vp.random_convex_polygon(8, 11, 1.0)), (32, W.c5_polygon(vp.random_convex_polygon)),
+             (1024, vp.regular_polygon(1024, 1.0))]
+    try:
+        import oracle
+        ref = oracle.Reference()
+    except Exception:
+        ref = None
+    single = []
+    for n, (vx, vy) in polys:
+        vx, vy = np.ascontiguousarray(vx, np.float64), np.ascontiguousarray(vy, np.float64)
+        px, py = vx.ctypes.data_as(C.POINTER(C.c_double)), vy.ctypes.data_as(C.POINTER(C.c_double))
+        enq, rdy = [], []
+        for r in range(60):
+            h = C.c_void_p()
+            t0 = time.perf_counter()
+            rc = L.vpipg_prepare(px, py, n, vp.KIND_ALL, device, sptr, C.byref(h))
+            t1 = time.perf_counter()
+            st = L.vpipg_poly_status(h)
+            t2 = time.perf_counter()
+            L.vpipg_destroy(h)
+            if rc or st:
+                raise SystemExit(f"prepare n={n}: {rc} {st}")
+            if r >= 10:
+                enq.append(t1 - t0)
+                rdy.append(t2 - t0)
+        e = {"n": n, "prepare_enqueue_us": statistics.median(enq) * 1e6,
+             "prepare_ready_us": statistics.median(rdy) * 1e6}
+        if ref is not None:
+            tv, tc = ref.time_convert(vx, vy)
+            e.update({"reference_validate_us": tv / 1e3, "reference_to_voronoi_us": tc / 1e3})
+        single.append(e)
+    ct = []
+    for r in range(200):  # the ctypes call overhead included in the figures above
+        t0 = time.perf_counter()
+        L.vpipg_abi_version()
+        ct.append(time.perf_counter() - t0)
+    off, cvx, cvy, *_ = W.c4_polygons(vp.random_convex_polygon)
+    ing = []
+    for r in range(7):
+        t0 = time.perf_counter()
+        db = vp.PolygonDB.prepare(off, cvx, cvy, vp.KIND_ALL, device=device, stream=stream)
+        t1 = time.perf_counter()
+        db.close()
+        if r >= 2:
+            ing.append(t1 - t0)
+    c4 = {"polygons": int(off.size - 1), "ingest_ms": statistics.median(ing) * 1e3}
+    if ref is not None:
+        tv, tc = ref.time_convert_csr(off, cvx, cvy)
+        c4.update({"reference_validate_ms": tv / 1e6, "reference_to_voronoi_ms": tc / 1e6,
+                   "reference_threads": 1})
+    return {"single": single, "c4": c4, "ctypes_call_us": statistics.median(ct) * 1e6,
+            "what": "warm medians; GPU: vpipg_prepare = host validate_polygon + enqueued device "
+                    "conversion (generators, f32 tables), ready = until vpipg_poly_status "
+                    "returns; C4: vpipg_prepare_csr of the 65,536-polygon database. Reference: "
+                    "validate_polygon and to_voronoi (the convert phase of bench.cpp:165-170) "
+                    "of the same polygons, single-threaded as run_benchmark runs them"}
+
+
 # ----------------------------------------------------------------- CPU leg + parity
 def cpu_leg(job, words, m, torch):
     """cpu_baseline and the parity block (rank 0, N=1). The reference library
@@ -491,6 +562,7 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-convert", action="store_true")
     ap.add_argument("--fused", action="store_true",
                     help="(default for f32 single-polygon workloads) one fused kernel for the "
                          "three engines (vpipg_test_multi)")
@@ -704,9 +776,11 @@ def main():
                "steps": args.e2e_steps, "step_ms": [round(t * 1e3, 2) for t in times],
                "path": job.e2e_path}
 
-    cpu = parity = None
+    cpu = parity = convert = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu, parity = cpu_leg(job, words, m, torch)
+    if rank == 0 and not args.no_convert:
+        convert = convert_block(vp, local, stream)
 
     if world > 1:
         dist.barrier()
@@ -811,7 +885,7 @@ def main():
         "roofline": roof, "kernels": kernels, "engines_separate": engines_separate,
         "inside_counts": final_counts,
         "prepare_ms": job.prep_ms,
-        "clocks": clocks, "e2e": e2e, "cpu_baseline": cpu, "parity": parity,
+        "clocks": clocks, "e2e": e2e, "cpu_baseline": cpu, "parity": parity, "convert": convert,
     }
     print(json.dumps(line), flush=True)
     if world > 1:

@@ -79,8 +79,11 @@ int vpipg_abi_version(void);
  * polygon is validated with the reference rules (error codes 1-4) and, for
  * VORONOI, converted on the device (centroid + one reflection per edge, the
  * reference's operation order; code 5 on a collision). CROSSING alone takes
- * the raw vertices unvalidated, any orientation (vpip.cpp:120-128). The
- * call is synchronous (it returns the status) and uses `stream`. */
+ * the raw vertices unvalidated, any orientation (vpip.cpp:120-128).
+ * Validation (codes 1-4) runs on the host before the call returns; the device
+ * conversion is only ENQUEUED on `stream` (no synchronisation): its status
+ * (code 5 on a collision) is returned by the first call that uses the handle,
+ * or by vpipg_poly_status. */
 int vpipg_prepare(const double* vx, const double* vy, uint32_t n, uint32_t kinds, int device,
                   void* stream, vpipg_poly** out);
 
@@ -94,6 +97,9 @@ int vpipg_prepare_generators(const double* inner_xy, const double* outer_xy, uin
  * the legacy default stream, no device-wide synchronisation). Work that still
  * uses the handle on other streams must have completed. */
 void vpipg_destroy(vpipg_poly* poly);
+
+/* Waits for the handle's device conversion; 0 or its error code (5). */
+int vpipg_poly_status(const vpipg_poly* poly);
 
 /* n, prepared kinds, and whether validation reversed a clockwise input
  * (ConvexPolygon::was_reversed, geometry.hpp:95). Any pointer may be NULL. */

@@ -328,6 +328,10 @@ class Reference:
         L.vr_join_scalar.restype = C.c_uint64
         L.vr_join_scalar.argtypes = [C.c_void_p, _D, _D, u32p, sz, C.c_int, C.c_int, _U8]
         fp = C.POINTER(C.c_float)
+        L.vr_time_convert.argtypes = [_D, _D, sz, C.c_int, C.POINTER(C.c_uint64),
+                                      C.POINTER(C.c_uint64)]
+        L.vr_time_convert_csr.argtypes = [C.POINTER(C.c_uint32), _D, _D, C.c_uint32,
+                                          C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]
         L.vr_chunks_new.restype = C.c_void_p
         L.vr_chunks_new.argtypes = [fp, fp, sz, sz, C.c_int]
         L.vr_chunks_free.argtypes = [C.c_void_p]
@@ -428,6 +432,25 @@ class Reference:
             if own:
                 self.free_chunks(chunks)
         return res
+
+    def time_convert(self, vx, vy, reps=101):
+        """Medians (ns) of validate_polygon and of to_voronoi (bench.cpp:165-170)."""
+        vx, vy = np.ascontiguousarray(vx, np.float64), np.ascontiguousarray(vy, np.float64)
+        tv, tc = C.c_uint64(), C.c_uint64()
+        rc = self.L.vr_time_convert(_d(vx), _d(vy), vx.size, reps, C.byref(tv), C.byref(tc))
+        if rc:
+            raise ValueError(rc)
+        return tv.value, tc.value
+
+    def time_convert_csr(self, offsets, vx, vy):
+        """Total ns of validate_polygon and to_voronoi over a CSR database (1 thread)."""
+        offsets = np.ascontiguousarray(offsets, np.uint32)
+        tv, tc = C.c_uint64(), C.c_uint64()
+        self.L.vr_time_convert_csr(offsets.ctypes.data_as(C.POINTER(C.c_uint32)),
+                                   _d(np.ascontiguousarray(vx, np.float64)),
+                                   _d(np.ascontiguousarray(vy, np.float64)), offsets.size - 1,
+                                   C.byref(tv), C.byref(tc))
+        return tv.value, tc.value
 
     def make_chunks(self, xs32, ys32, threads, chunk=1 << 26):
         xs32 = np.ascontiguousarray(xs32, np.float32)

@@ -407,6 +407,63 @@ uint64_t vr_join_scalar(void* jp, const double* xs, const double* ys, const uint
   return static_cast<uint64_t>(std::chrono::duration_cast<std::chrono::nanoseconds>(t1 - t0).count());
 }
 
+// The conversion phase of run_benchmark (bench.cpp:165-170: to_voronoi of an
+// already validated polygon) and, separately, validate_polygon
+// (geometry.cpp:53-98): medians over `reps` calls, ns. Returns 0 or the code.
+int vr_time_convert(const double* vx, const double* vy, std::size_t n, int reps,
+                    uint64_t* ns_validate, uint64_t* ns_convert) {
+  try {
+    const std::vector<vpip::Point2> raw = to_points(vx, vy, n);
+    std::vector<uint64_t> tv, tc;
+    uint64_t sink = 0;
+    for (int r = 0; r < reps; ++r) {
+      const auto t0 = std::chrono::steady_clock::now();
+      const vpip::ConvexPolygon p = vpip::validate_polygon(raw);
+      const auto t1 = std::chrono::steady_clock::now();
+      const vpip::GeneratorSet g = vpip::to_voronoi(p);
+      const auto t2 = std::chrono::steady_clock::now();
+      sink += g.outer.size();
+      tv.push_back(std::chrono::duration_cast<std::chrono::nanoseconds>(t1 - t0).count());
+      tc.push_back(std::chrono::duration_cast<std::chrono::nanoseconds>(t2 - t1).count());
+    }
+    std::sort(tv.begin(), tv.end());
+    std::sort(tc.begin(), tc.end());
+    *ns_validate = tv[tv.size() / 2] + (sink == 0 ? 1 : 0);
+    *ns_convert = tc[tc.size() / 2];
+    return 0;
+  } catch (const vpip::Error& e) {
+    return code_of(e);
+  }
+}
+
+// The same phases over a CSR polygon database, one thread, all polygons:
+// total ns of validate_polygon and of to_voronoi (failures skip to_voronoi).
+void vr_time_convert_csr(const uint32_t* offsets, const double* vx, const double* vy,
+                         uint32_t npoly, uint64_t* ns_validate, uint64_t* ns_convert) {
+  uint64_t tv = 0, tc = 0, sink = 0;
+  for (uint32_t i = 0; i < npoly; ++i) {
+    const std::vector<vpip::Point2> raw =
+        to_points(vx + offsets[i], vy + offsets[i], offsets[i + 1] - offsets[i]);
+    const auto t0 = std::chrono::steady_clock::now();
+    std::optional<vpip::ConvexPolygon> p;
+    try {
+      p.emplace(vpip::validate_polygon(raw));
+    } catch (const vpip::Error&) {
+    }
+    const auto t1 = std::chrono::steady_clock::now();
+    tv += std::chrono::duration_cast<std::chrono::nanoseconds>(t1 - t0).count();
+    if (p) {
+      try {
+        sink += vpip::to_voronoi(*p).outer.size();
+      } catch (const vpip::Error&) {
+      }
+      tc += std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now() - t1).count();
+    }
+  }
+  *ns_validate = tv + (sink == 0 ? 1 : 0);
+  *ns_convert = tc;
+}
+
 int vr_scalar(void* poly, int engine, double px, double py) {
   const Poly& p = *static_cast<Poly*>(poly);
   switch (engine) {

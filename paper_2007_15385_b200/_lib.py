@@ -64,6 +64,7 @@ SIGNATURES = {
     "vpipg_comm_info": (C.c_int, [_P, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int)]),
     "vpipg_allreduce_counts": (C.c_int, [_P, _P, C.c_int, _P]),
     "vpipg_zero_counts": (C.c_int, [_P, C.c_int, _P]),
+    "vpipg_poly_status": (C.c_int, [_P]),
     "vpipg_allreduce_counts_group": (C.c_int, [C.c_int, _P, _P, C.c_int, _P]),
     "vpipg_comm_destroy": (C.c_int, [_P]),
     "vpipg_voronoi_work": (C.c_int, [_P, C.c_uint64, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),

@@ -82,7 +82,96 @@ int blob_pool(int device, cudaMemPool_t* out) {
 
 constexpr uint32_t kHostTableMax = 256;
 
-// Builds the blob, runs the prep kernel, reads back the status.
+// Pinned host blocks for the asynchronous prepare (uploads and the download of
+// the status and f32 tables): power-of-two size classes carved from 4 MiB
+// cudaHostAlloc chunks and recycled, so a prepare makes no pinned allocation
+// once warm. Portable across devices.
+class PinnedArena {
+ public:
+  static PinnedArena& get() {
+    static PinnedArena a;
+    return a;
+  }
+  char* take(size_t bytes, size_t* got) {
+    int cls = 12;  // 4 KiB minimum
+    while ((size_t(1) << cls) < bytes) ++cls;
+    const size_t size = size_t(1) << cls;
+    std::lock_guard<std::mutex> lock(mu_);
+    auto& fl = free_[cls];
+    if (!fl.empty()) {
+      char* b = fl.back();
+      fl.pop_back();
+      *got = size;
+      return b;
+    }
+    if (size > kChunk) {  // large: its own allocation
+      void* h = nullptr;
+      if (cudaHostAlloc(&h, size, cudaHostAllocPortable) != cudaSuccess) return nullptr;
+      *got = size;
+      return static_cast<char*>(h);
+    }
+    if (left_ < size) {
+      void* h = nullptr;
+      if (cudaHostAlloc(&h, kChunk, cudaHostAllocPortable) != cudaSuccess) return nullptr;
+      cur_ = static_cast<char*>(h);
+      left_ = kChunk;
+    }
+    char* b = cur_;
+    cur_ += size;
+    left_ -= size;
+    *got = size;
+    return b;
+  }
+  void give(char* b, size_t size) {
+    if (!b) return;
+    int cls = 12;
+    while ((size_t(1) << cls) < size) ++cls;
+    std::lock_guard<std::mutex> lock(mu_);
+    free_[cls].push_back(b);
+  }
+
+ private:
+  static constexpr size_t kChunk = size_t(4) << 20;
+  std::mutex mu_;
+  std::map<int, std::vector<char*>> free_;
+  char* cur_ = nullptr;
+  size_t left_ = 0;
+};
+
+// Per-device pool of cudaEventDisableTiming events for the prepare handles.
+class EventPool {
+ public:
+  static EventPool& get() {
+    static EventPool p;
+    return p;
+  }
+  cudaEvent_t take(int device) {
+    {
+      std::lock_guard<std::mutex> lock(mu_);
+      auto& v = free_[device];
+      if (!v.empty()) {
+        cudaEvent_t e = v.back();
+        v.pop_back();
+        return e;
+      }
+    }
+    cudaEvent_t e = nullptr;
+    return cudaEventCreateWithFlags(&e, cudaEventDisableTiming) == cudaSuccess ? e : nullptr;
+  }
+  void give(int device, cudaEvent_t e) {
+    if (!e) return;
+    std::lock_guard<std::mutex> lock(mu_);
+    free_[device].push_back(e);
+  }
+
+ private:
+  std::mutex mu_;
+  std::map<int, std::vector<cudaEvent_t>> free_;
+};
+
+// Builds the blob and enqueues the prep kernel: uploads from a pinned block,
+// downloads the status, slab counts and (small) f32 tables into it, records
+// the handle's event. Nothing waits here; ensure_ready finishes the handle.
 int build(vpipg_poly* p, const double* vv, const double* vr, const double* gen, cudaStream_t s) {
   const size_t n = p->n;
   size_t off = 0;
@@ -93,11 +182,23 @@ int build(vpipg_poly* p, const double* vv, const double* vr, const double* gen, 
   const size_t o_outer = take(n * sizeof(double2));
   const size_t o_off = take(n * sizeof(OffsetEdgeF64));
   const size_t o_ray = take(n * sizeof(RayEdgeF64));
+  const size_t o_lines = take(n * sizeof(double4));
+  // the download span: status + counts, then the f32 tables, contiguous
+  const size_t o_meta = take(sizeof(PrepMeta));
   const size_t o_s0 = take((n + 4) * sizeof(float2));
   const size_t o_s1 = take((n + 4) * sizeof(float2));
   const size_t o_cross = take(n * sizeof(float4));
-  const size_t o_lines = take(n * sizeof(double4));
-  const size_t o_meta = take(sizeof(PrepMeta));
+  const size_t o_end = off;
+  p->host_tables = n <= kHostTableMax;
+  const size_t dl = p->host_tables ? o_end - o_meta : o_s0 - o_meta;
+  p->host = PinnedArena::get().take(o_outer + dl, &p->host_bytes);
+  if (!p->host) return kInvalid;
+  p->dl_meta = o_outer;
+  p->dl_slab[0] = o_outer + (o_s0 - o_meta);
+  p->dl_slab[1] = o_outer + (o_s1 - o_meta);
+  p->dl_cross = o_outer + (o_cross - o_meta);
+  p->ready = EventPool::get().take(p->device);
+  if (!p->ready) return kInvalid;
   // stream-ordered allocation from the library's per-device pool (no device
   // synchronisation on prepare / destroy), one packed upload of the inputs
   cudaMemPool_t pool = nullptr;
@@ -105,24 +206,41 @@ int build(vpipg_poly* p, const double* vv, const double* vr, const double* gen, 
   if (rc) return rc;
   VPIPG_TRY(cudaMallocFromPoolAsync(&p->blob, off, pool, s));
   char* b = static_cast<char*>(p->blob);
-  VPIPG_TRY(cudaMemsetAsync(b, 0, off, s));
-  std::vector<char> up(o_outer, 0);  // [vv | vr | gen] in the blob's own layout
-  PrepArgs a{};
+  PrepArgs& a = p->args;
   a.n = p->n;
   a.kinds = p->kinds;
-  if (vv) {
-    std::memcpy(up.data() + o_vv, vv, 2 * n * sizeof(double));
-    a.vv = reinterpret_cast<const double*>(b + o_vv);
+  // small inputs ride in the prep kernel's parameters; larger ones are one
+  // upload from the pinned block in the blob's own layout [vv | vr | gen]
+  const size_t need = (vv ? 2 * n : 0) + (vr ? 2 * n : 0) + (gen ? 2 + 2 * n : 0);
+  PrepInline inl;
+  const bool inline_in = need <= size_t(kPrepInlineMax);
+  if (inline_in) {
+    int32_t at = 0;
+    auto put = [&](const double* src, size_t cnt, int32_t* where) {
+      if (!src) return;
+      std::memcpy(inl.v + at, src, cnt * sizeof(double));
+      *where = at;
+      at += static_cast<int32_t>(cnt);
+    };
+    put(vv, 2 * n, &inl.vv_at);
+    put(vr, 2 * n, &inl.vr_at);
+    put(gen, 2 + 2 * n, &inl.gen_at);
+  } else {
+    char* up = p->host;
+    if (vv) {
+      std::memcpy(up + o_vv, vv, 2 * n * sizeof(double));
+      a.vv = reinterpret_cast<const double*>(b + o_vv);
+    }
+    if (vr) {
+      std::memcpy(up + o_vr, vr, 2 * n * sizeof(double));
+      a.vr = reinterpret_cast<const double*>(b + o_vr);
+    }
+    if (gen) {
+      std::memcpy(up + o_gen, gen, (2 + 2 * n) * sizeof(double));
+      a.gen_in = reinterpret_cast<const double*>(b + o_gen);
+    }
+    if (o_outer) VPIPG_TRY(cudaMemcpyAsync(b, up, o_outer, cudaMemcpyHostToDevice, s));
   }
-  if (vr) {
-    std::memcpy(up.data() + o_vr, vr, 2 * n * sizeof(double));
-    a.vr = reinterpret_cast<const double*>(b + o_vr);
-  }
-  if (gen) {
-    std::memcpy(up.data() + o_gen, gen, (2 + 2 * n) * sizeof(double));
-    a.gen_in = reinterpret_cast<const double*>(b + o_gen);
-  }
-  if (o_outer) VPIPG_TRY(cudaMemcpyAsync(b, up.data(), o_outer, cudaMemcpyHostToDevice, s));
   a.outer = reinterpret_cast<double2*>(b + o_outer);
   a.off = reinterpret_cast<OffsetEdgeF64*>(b + o_off);
   a.ray = reinterpret_cast<RayEdgeF64*>(b + o_ray);
@@ -131,12 +249,31 @@ int build(vpipg_poly* p, const double* vv, const double* vr, const double* gen, 
   a.cross_vert = reinterpret_cast<float4*>(b + o_cross);
   a.lines = reinterpret_cast<double4*>(b + o_lines);
   a.meta = reinterpret_cast<PrepMeta*>(b + o_meta);
-  VPIPG_TRY(launch_prep(a, s));
-  PrepMeta meta;
-  VPIPG_TRY(cudaMemcpyAsync(&meta, a.meta, sizeof(meta), cudaMemcpyDeviceToHost, s));
-  VPIPG_TRY(cudaStreamSynchronize(s));
-  if (meta.status != 0) return meta.status;
+  VPIPG_TRY(launch_prep(a, inline_in ? &inl : nullptr, s));
+  VPIPG_TRY(cudaMemcpyAsync(p->host + p->dl_meta, b + o_meta, dl, cudaMemcpyDeviceToHost, s));
+  VPIPG_TRY(cudaEventRecord(p->ready, s));
+  p->state.store(-1, std::memory_order_release);
+  return kOk;
+}
 
+}  // namespace
+
+int vpipg::capi::ensure_ready(const vpipg_poly* p) {
+  int st = p->state.load(std::memory_order_acquire);
+  if (st >= 0) return st;
+  std::lock_guard<std::mutex> lock(p->mu);
+  st = p->state.load(std::memory_order_relaxed);
+  if (st >= 0) return st;
+  DeviceGuard g(p->device);
+  const cudaError_t e = cudaEventSynchronize(p->ready);
+  if (e != cudaSuccess) return cuda_code(e);  // stays pending: a later call retries
+  PrepMeta meta;
+  std::memcpy(&meta, p->host + p->dl_meta, sizeof(meta));
+  if (meta.status != 0) {
+    p->state.store(meta.status, std::memory_order_release);
+    return meta.status;
+  }
+  const PrepArgs& a = p->args;
   DevTables& t = p->t;
   t.n = p->n;
   t.kinds = p->kinds;
@@ -147,41 +284,28 @@ int build(vpipg_poly* p, const double* vv, const double* vr, const double* gen, 
   t.ray = a.ray;
   t.ox = meta.ox;
   t.oy = meta.oy;
-  for (int e = 0; e < 2; ++e) {
-    SlabTable& st = t.slab[e];
-    st.coef = a.slab_coef[e];
+  for (int k = 0; k < 2; ++k) {
+    SlabTable& stb = t.slab[k];
+    stb.coef = a.slab_coef[k];
     uint32_t acc = 0;
-    for (int g = 0; g < kGroups; ++g) {
-      st.off[g] = acc;
-      st.cnt[g] = meta.cnt[e][g];
-      acc += meta.cnt[e][g];
+    for (int gi = 0; gi < kGroups; ++gi) {
+      stb.off[gi] = acc;
+      stb.cnt[gi] = meta.cnt[k][gi];
+      acc += meta.cnt[k][gi];
     }
-    st.total = acc;
+    stb.total = acc;
+    // small tables also travel in the kernels' parameter bank (test_f32.cu)
+    t.h_slab[k] = p->host_tables ? reinterpret_cast<const float2*>(p->host + p->dl_slab[k]) : nullptr;
   }
   t.cross.vert = a.cross_vert;
   t.cross.n = p->n;
+  t.h_cross = p->host_tables ? reinterpret_cast<const float4*>(p->host + p->dl_cross) : nullptr;
   t.lines = a.lines;
-  // small tables also travel in the kernels' parameter bank (test_f32.cu)
-  if (p->n <= kHostTableMax) {
-    for (int e = 0; e < 2; ++e) {
-      p->h_slab[e].resize(t.slab[e].total);
-      if (t.slab[e].total)
-        VPIPG_TRY(cudaMemcpyAsync(p->h_slab[e].data(), t.slab[e].coef, t.slab[e].total * sizeof(float2),
-                                  cudaMemcpyDeviceToHost, s));
-      t.h_slab[e] = p->h_slab[e].data();
-    }
-    p->h_cross.resize(p->n);
-    VPIPG_TRY(cudaMemcpyAsync(p->h_cross.data(), t.cross.vert, p->n * sizeof(float4),
-                              cudaMemcpyDeviceToHost, s));
-    t.h_cross = p->h_cross.data();
-    VPIPG_TRY(cudaStreamSynchronize(s));
-  }
   p->inner_x = meta.inner_x;
   p->inner_y = meta.inner_y;
-  return kOk;
+  p->state.store(0, std::memory_order_release);
+  return 0;
 }
-
-}  // namespace
 
 int vpipg::capi::dispatch(const vpipg_poly* p, int engine, int dtype, const TestArgs& a,
                           cudaStream_t s) {
@@ -191,6 +315,7 @@ int vpipg::capi::dispatch(const vpipg_poly* p, int engine, int dtype, const Test
                                                           : 0u;
   if (need == 0 || !(p->kinds & need)) return kInvalid;
   if (dtype != VPIPG_F32 && dtype != VPIPG_F64) return kInvalid;
+  if (const int st = ensure_ready(p)) return st;
   if (a.m == 0) return kOk;
   if (!a.xs || !a.ys) return kInvalid;
   const cudaError_t e = (dtype == VPIPG_F32) ? launch_test_f32(p->t, engine, a, s)
@@ -292,6 +417,13 @@ int vpipg_prepare_generators(const double* inner_xy, const double* outer_xy, uin
 
 void vpipg_destroy(vpipg_poly* p) {
   if (!p) return;
+  if (p->ready) {
+    // the download into the pinned block may still be in flight
+    DeviceGuard g(p->device);
+    cudaEventSynchronize(p->ready);
+    EventPool::get().give(p->device, p->ready);
+  }
+  PinnedArena::get().give(p->host, p->host_bytes);
   if (p->blob) {
     // back to the pool, ordered after all work on the legacy default stream;
     // work the caller still has in flight on other streams must be finished
@@ -300,6 +432,11 @@ void vpipg_destroy(vpipg_poly* p) {
     cudaFreeAsync(p->blob, nullptr);
   }
   delete p;
+}
+
+int vpipg_poly_status(const vpipg_poly* p) {
+  if (!p) return kInvalid;
+  return ensure_ready(p);
 }
 
 int vpipg_poly_info(const vpipg_poly* p, uint32_t* n, uint32_t* kinds, int* reversed) {
@@ -313,6 +450,7 @@ int vpipg_poly_info(const vpipg_poly* p, uint32_t* n, uint32_t* kinds, int* reve
 int vpipg_poly_generators(const vpipg_poly* p, double* inner_xy, double* outer_xy) {
   if (!p || !(p->kinds & kKindVoronoi) || !inner_xy || (p->n && !outer_xy)) return kInvalid;
   DeviceGuard g(p->device);
+  if (const int st = ensure_ready(p)) return st;
   inner_xy[0] = p->inner_x;
   inner_xy[1] = p->inner_y;
   if (p->n) VPIPG_TRY(cudaMemcpy(outer_xy, p->t.outer, p->n * sizeof(double2), cudaMemcpyDeviceToHost));
@@ -347,6 +485,7 @@ int vpipg_test_multi(const vpipg_poly* p, uint32_t engines, int dtype, const voi
     a[e] = TestArgs{xs, ys, m, mask_words ? mask_words[e] : nullptr,
                     mask_bytes ? mask_bytes[e] : nullptr, d_inside ? d_inside[e] : nullptr};
   if (engines == 7u && (p->kinds & VPIPG_KIND_ALL) == VPIPG_KIND_ALL && m > 0 && xs && ys) {
+    if (const int st = ensure_ready(p)) return st;
     if (dtype == VPIPG_F64) return cuda_code(launch_test_f64_all(p->t, a, s));
     if (dtype == VPIPG_F32) {
       const cudaError_t e = launch_test_f32_all(p->t, a, s);
@@ -376,6 +515,7 @@ int vpipg_test_multi_fused(const vpipg_poly* p, uint32_t engines, int dtype, con
   if (dtype != VPIPG_F32) return 0;
   TestArgs a[3];
   for (auto& x : a) x = TestArgs{xs, ys, m, nullptr, nullptr, nullptr};
+  if (ensure_ready(p)) return 0;
   return test_f32_all_plan(p->t, a, nullptr) ? 1 : 0;
 }
 
@@ -576,6 +716,7 @@ int classify(const vpipg_poly* p, int dtype, const void* xs, const void* ys, uin
     if (e != cudaSuccess && rc == kOk) rc = cuda_code(e);
     return rc != kOk;
   };
+  if (const int st = ensure_ready(p)) return st;
   ClassifyArgs a{{w0, w1, w2}, xs, ys, dtype, m, band, relative, poly_extent(p), p->t.lines,
                  p->n, rep};
   // counters only (the sample arrays are written before they are read)

@@ -5,24 +5,40 @@
 
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstddef>
 #include <cstdint>
+#include <mutex>
 #include <vector>
 
 #include "vpipg.h"
 #include "vpipg_internal.h"
 
+// A prepared polygon. vpipg_prepare only enqueues the device conversion
+// (upload, prep kernel, download of the status / slab counts / f32 tables into
+// pinned host memory, an event) and returns; the first call that needs the
+// results waits for the event and finishes the handle (capi::ensure_ready),
+// once, under `mu`. Finished handles are immutable.
 struct vpipg_poly {
   int device = 0;
   uint32_t n = 0;
   uint32_t kinds = 0;
   int reversed = 0;
   void* blob = nullptr;
-  vpipg::DevTables t{};
   std::vector<double> vx, vy;  // validated (or raw, crossing-only) vertices
-  double inner_x = 0, inner_y = 0;
-  std::vector<float2> h_slab[2];  // host copies of the f32 tables (DevTables::h_*)
-  std::vector<float4> h_cross;
+  // ---- asynchronous preparation ----
+  cudaEvent_t ready = nullptr;   // recorded after the download
+  char* host = nullptr;          // pinned block: uploads, then the download
+  size_t host_bytes = 0;
+  size_t dl_meta = 0;            // offsets in `host` of the downloaded
+  size_t dl_slab[2] = {0, 0};    //   PrepMeta, slab tables and crossing table
+  size_t dl_cross = 0;
+  bool host_tables = false;      // the f32 tables were downloaded (n small)
+  vpipg::PrepArgs args{};        // device table pointers (into blob)
+  mutable std::mutex mu;
+  mutable std::atomic<int> state{-1};  // -1 pending, 0 ready, > 0 the prep error code
+  mutable vpipg::DevTables t{};
+  mutable double inner_x = 0, inner_y = 0;
 };
 
 struct vpipg_db {
@@ -69,6 +85,10 @@ struct DeviceGuard {
     if (prev >= 0 && cur != prev) cudaSetDevice(prev);
   }
 };
+
+// Waits for a handle's asynchronous preparation (once) and fills its tables;
+// 0 or the prep kernel's error code (capi.cu).
+int ensure_ready(const vpipg_poly* p);
 
 // Launches engine `engine` of a prepared polygon on device buffers (capi.cu).
 int dispatch(const vpipg_poly* p, int engine, int dtype, const TestArgs& a, cudaStream_t s);

@@ -187,11 +187,22 @@ __device__ int off_class(int e, const void* ctx, float2* bc, int mode) {
   return slab_classify(-dvy, dvx, wx * dvy - wy * dvx, bc, mode);
 }
 
-__global__ void __launch_bounds__(kPrepThreads) prep_kernel(PrepArgs a) {
+// kInline: the input vertices / generators travel in the kernel's parameter
+// bank (small polygons: no upload call); offsets in doubles, -1 = absent
+template <bool kInline>
+__global__ void __launch_bounds__(kPrepThreads) prep_kernel(const PrepArgs a0,
+                                                            const __grid_constant__ PrepInline in) {
   __shared__ double s_inner[2];
   __shared__ int s_fail;  // min over failing edges of (edge * 8 + code): the first throw wins
+  PrepArgs a = a0;
+  if constexpr (kInline) {
+    a.vv = in.vv_at >= 0 ? in.v + in.vv_at : nullptr;
+    a.vr = in.vr_at >= 0 ? in.v + in.vr_at : nullptr;
+    a.gen_in = in.gen_at >= 0 ? in.v + in.gen_at : nullptr;
+  }
   const int tid = threadIdx.x;
   const int n = static_cast<int>(a.n);
+  if (tid < 2 * kGroups) a.meta->cnt[tid / kGroups][tid % kGroups] = 0;  // kinds not prepared
   if (tid == 0) {
     s_fail = INT_MAX;
     double cx = 0.0, cy = 0.0;
@@ -338,8 +349,13 @@ __global__ void __launch_bounds__(kPrepThreads) prep_kernel(PrepArgs a) {
 
 }  // namespace
 
-cudaError_t launch_prep(const PrepArgs& args, cudaStream_t stream) {
-  prep_kernel<<<1, kPrepThreads, 0, stream>>>(args);
+cudaError_t launch_prep(const PrepArgs& args, const PrepInline* in, cudaStream_t stream) {
+  if (in) {
+    prep_kernel<true><<<1, kPrepThreads, 0, stream>>>(args, *in);
+  } else {
+    static const PrepInline none{};
+    prep_kernel<false><<<1, kPrepThreads, 0, stream>>>(args, none);
+  }
   return cudaGetLastError();
 }
 

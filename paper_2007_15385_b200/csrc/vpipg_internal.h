@@ -28,6 +28,14 @@ struct PrepArgs {
   PrepMeta* meta;
 };
 
+// Small prepare inputs in the prep kernel's parameter bank (no upload call):
+// vv / vr / gen laid out in v[], offsets in doubles, -1 = absent.
+constexpr int kPrepInlineMax = 512;
+struct PrepInline {
+  int32_t vv_at = -1, vr_at = -1, gen_at = -1, pad_ = 0;
+  double v[kPrepInlineMax];
+};
+
 struct TestArgs {
   const void* xs;
   const void* ys;
@@ -89,7 +97,7 @@ struct GatherArgs {
   unsigned long long* inside;
 };
 
-cudaError_t launch_prep(const PrepArgs& args, cudaStream_t stream);
+cudaError_t launch_prep(const PrepArgs& args, const PrepInline* in, cudaStream_t stream);
 cudaError_t launch_prep_csr(const CsrPrepArgs& args, cudaStream_t stream);
 cudaError_t launch_gather(const DbTables& t, int engine, const GatherArgs& a, cudaStream_t stream);
 // all three engines per pair in one pass (a[0..2] share xs, ys, ids, m)

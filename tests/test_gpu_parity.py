@@ -809,3 +809,38 @@ def test_python_mirror_rejects_bad_output_tensors():
         p.test(0, xs, ys, words=w, count=c)  # a good call still works
         torch.cuda.synchronize()
         assert c.item() == int(np.unpackbits(w.cpu().numpy().view(np.uint8)).sum())
+
+
+def test_prepare_is_asynchronous_and_reports_device_status_on_first_use():
+    """vpipg_prepare validates on the host (codes 1-4 at once) and only
+    enqueues the device conversion: a GeneratorCollision (code 5, the
+    reference's to_voronoi throw site, voronoi.cpp:46-58) surfaces at the first
+    use of the handle and from vpipg_poly_status; the reference throws it for
+    the same polygon."""
+    # a valid but extremely thin triangle: the centroid lies within
+    # 1e-12 |edge|^2 of the long edge's line
+    vx, vy = np.array([0.0, 1.0, 0.5]), np.array([0.0, 0.0, 2e-12])
+    with pytest.raises(vp.VpipError) as ei:  # host validation still raises at once
+        vp.PreparedPolygon.prepare(np.array([0., 1, 2]), np.array([0., 0, 0]), vp.KIND_ALL)
+    assert ei.value.code == 2
+    p = vp.PreparedPolygon.prepare(vx, vy, vp.KIND_ALL)
+    assert vp.load().vpipg_poly_status(p.handle) == 5
+    xs = torch.zeros(64, dtype=torch.float32, device=DEV)
+    with pytest.raises(vp.VpipError) as ei:
+        p.test(0, xs, xs, count=torch.zeros(1, dtype=torch.int64, device=DEV))
+    assert ei.value.code == 5
+    p.close()
+    import oracle
+    try:
+        ref = oracle.Reference()
+    except FileNotFoundError:
+        return
+    rc, _, _ = ref.to_voronoi(vx, vy)
+    assert rc == 5
+    # a good polygon is usable right after the (asynchronous) prepare
+    q = vp.PreparedPolygon.prepare(*vp.regular_polygon(32, 1.0), vp.KIND_ALL)
+    c = torch.zeros(1, dtype=torch.int64, device=DEV)
+    q.test(2, xs, xs, count=c)
+    torch.cuda.synchronize()
+    assert c.item() == 64  # (0, 0) is inside
+    q.close()
