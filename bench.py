@@ -873,7 +873,8 @@ def main():
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "f64" if f64 else "f32",
         "data": "synthetic (seeded counter-based points, reference-sampler polygon)",
-        "config": {**config_block(args, world), "n_edges": n_edges,
+        "config": config_block(args, world),
+        "execution": {"n_edges": n_edges,
                    "engines_fused": fused,
                    "launch": ("eager launches" if args.no_graph else
                               "one CUDA-graph replay per step (" +

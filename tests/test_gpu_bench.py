@@ -30,7 +30,7 @@ def test_bench_line_contract(mode):
     d = _run(*(["--separate"] if mode == "separate" else []))
     assert KEYS <= d.keys()
     assert d["n_gpus"] == 1 and d["steps"] == 3 and d["value"] > 0
-    assert d["config"]["engines_fused"] is (mode == "fused")
+    assert d["execution"]["engines_fused"] is (mode == "fused")
     assert d["gpu_launches"] == (1 if mode == "fused" else 3) * 3
     r = d["roofline"]
     assert {"bound", "achieved", "peak", "unit", "frac", "traffic"} <= r.keys()
