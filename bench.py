@@ -53,6 +53,15 @@ NCU_FILE = ROOT / "profiles" / "ncu_full_r02_c5.json"
 # FFMA/FADD 1 cycle, FMNMX3/LOP3 2): slab = FFMA + FMNMX3/2, crossing =
 # 1.5 FADD + FFMA + 1.5 LOP3 (paired anchoring, test_f32.cu CrossEngine)
 ISSUE_CYCLES_PER_PE = {"voronoi": 2.0, "sign_of_offset": 2.0, "ray_crossing": 5.5}
+# the exact f64 kernels (test_f64.cu): the reference's own operation sequence
+# on the FP64 pipe (16 lanes per SMSP: every DADD / DMUL / DSETP holds it 2
+# cycles): Voronoi 3 DADD + 2 DMUL + DSETP, offset 2 DMUL + DADD + DSETP,
+# crossing 2 DMUL + DADD + 3 DSETP (in range, lhs > rhs, lhs == rhs; the
+# on-segment box only on a tie) -- the FP64-pipe bound, not counting the
+# predicate / integer logic around it
+# (ncu, profiles/ncu_full_r02_c5f64.json: 17.44 DADD / DMUL / DSETP per
+# point-edge over the three engines, crossing's share 7.44 with its tie test)
+ISSUE_CYCLES_PER_PE_F64 = {"voronoi": 12.0, "sign_of_offset": 8.0, "ray_crossing": 14.9}
 HBM_FALLBACK_GBS = 6650.0
 # FFMA lane-ops per SM per clock on sm_100a (tools/pipe_peaks.cu: 3.79 warp-inst/clk/SM)
 FFMA_PER_SM_CLK = 128
@@ -308,9 +317,14 @@ class PolygonJob:
     e2e_path = ("vpipg_test_host_multi (C-ABI, pinned host buffers, chunks of m/8 (1-16 Mi "
                 "points) on 3 streams; one H2D per chunk feeds all 3 engines)")
 
-    def __init__(self, workload, lo, hi, device, torch, vp, stream):
+    def __init__(self, workload, lo, hi, device, torch, vp, stream, dtype="f32"):
         self.torch = torch
+        self.workload = workload
         vx, vy, self.xs, self.ys = build_workload(workload, lo, hi, torch, vp, stream)
+        if dtype == "f64" and self.xs.dtype == torch.float32:
+            # the reference's own precision: the f32 stream widened exactly, run
+            # through the reference-exact f64 kernels
+            self.xs, self.ys = self.xs.double(), self.ys.double()
         self.vx, self.vy = np.asarray(vx, np.float64), np.asarray(vy, np.float64)
         t0 = time.perf_counter()
         self.poly = vp.PreparedPolygon.prepare(vx, vy, vp.KIND_ALL, device=device, stream=stream)
@@ -320,7 +334,7 @@ class PolygonJob:
         self.f64 = self.xs.dtype == torch.float64
         if self.f64:
             self.bytes_per_unit = 16
-            self.issue_cycles = None
+            self.issue_cycles = ISSUE_CYCLES_PER_PE_F64
 
     def launch(self, e, words, count, stream):
         self.poly.test(e, self.xs, self.ys, words=words, count=count, stream=stream)
@@ -349,7 +363,9 @@ class JoinJob:
     e2e_path = ("vpipg_test_gather_host (C-ABI, pinned host pairs, chunks of m/8 on 3 streams; "
                 "one H2D per chunk feeds all 3 engines)")
 
-    def __init__(self, workload, lo, hi, device, torch, vp, stream):
+    def __init__(self, workload, lo, hi, device, torch, vp, stream, dtype="f32"):
+        if dtype != "f32":
+            raise SystemExit("the C4 join runs on f32 pairs")
         self.torch = torch
         off, vx, vy, cx, cy, r = W.c4_polygons(vp.random_convex_polygon)
         self.off, self.vx, self.vy = off, vx, vy
@@ -501,7 +517,7 @@ def cpu_leg(job, words, m, torch):
                                            "pair in stream order (random polygon ids), "
                                            f"{th} threads"}}
         par["vs_reference"] = block(words, rw, xs, ys, BC.EPS32, join=(job.off, ids))
-    elif job.f64:
+    elif job.f64 and job.workload == "c1":
         ns, masks, build, (vx, vy, xs, ys) = reference_c1(th)
         ns, masks, build, _ = reference_c1(th)
         t = sum(ns) * 1e-9
@@ -512,7 +528,8 @@ def cpu_leg(job, words, m, torch):
                          f"engines *_contains_batch(threads={th}); second of two passes"}
         par["vs_reference"] = block(words, rw, xs, ys, BC.EPS64)
     else:
-        xs, ys = job.xs.cpu().numpy(), job.ys.cpu().numpy()
+        # (f64 runs: the widened f32 stream, so .float() is exact)
+        xs, ys = job.xs.float().cpu().numpy(), job.ys.float().cpu().numpy()
         rr = BC.RefRun(job.vx, job.vy, xs, ys, th)
         res = rr.run(packed=True)  # warm-up pass: the reference masks
         res2 = rr.run()            # timed pass
@@ -523,7 +540,10 @@ def cpu_leg(job, words, m, torch):
                "count_inside_ms": sum(x["count_ns"] for x in res2) * 1e-6,
                "inside_counts": [x["inside"] for x in res2]}
         rw = [x["words"] for x in res]
-        par["vs_reference"] = block(words, rw, xs, ys, BC.EPS32)
+        par["vs_reference"] = block(words, rw, xs, ys, BC.EPS64 if job.f64 else BC.EPS32)
+        if job.f64:  # the step itself ran the exact kernels: bit-exact or nothing
+            par["outside_band"] = sum(v["outside_band"] for v in par["vs_reference"].values())
+            return cpu, par
         # the reference-exact f64 kernels over the whole batch, on the device
         xd, yd = job.xs.double(), job.ys.double()
         w64 = [torch.zeros_like(w) for w in words]
@@ -563,6 +583,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-convert", action="store_true")
+    ap.add_argument("--dtype", default="f32", choices=["f32", "f64"],
+                    help="f64: the workload's points widened exactly to f64 and tested by the "
+                         "reference-exact f64 kernels (the reference's own precision)")
     ap.add_argument("--fused", action="store_true",
                     help="(default for f32 single-polygon workloads) one fused kernel for the "
                          "three engines (vpipg_test_multi)")
@@ -609,7 +632,7 @@ def main():
     m = hi - lo
     with torch.cuda.stream(stream):
         job = (JoinJob if args.workload == "c4" else PolygonJob)(args.workload, lo, hi, local,
-                                                                 torch, vp, stream)
+                                                                 torch, vp, stream, args.dtype)
         words = [torch.zeros((m + 31) // 32, dtype=torch.int32, device="cuda") for _ in range(3)]
         counts = torch.zeros(3, dtype=torch.int64, device="cuda")
         flush = torch.ones(256 << 20, dtype=torch.uint8, device="cuda") if M * 8 <= 4 * 126e6 else None
@@ -834,7 +857,15 @@ def main():
         traffic = tj["dram_bytes_per_launch"][dk["engine"]] * m / tj["points"]
     except Exception:
         pass
-    if compute_bound:
+    if f64:
+        # the exact kernels issue the reference's DADD / DMUL / DSETP sequence:
+        # their bound is the FP64 pipe (2 dispatch cycles per instruction)
+        cyc = sum(job.issue_cycles[e] for e in names if (dk["engine"] == "fused" or e == dk["engine"]))
+        achieved = (cyc / 2) * pe / 32 / (per_kernel_ms[dom] * 1e-3) / 1e12
+        peak = sms * 4 * clk_hz / 2 / 1e12
+        roof = {"bound": "fp64-pipe", "achieved": achieved, "peak": peak,
+                "unit": "T FP64 warp-instructions/s", "frac": achieved / peak, "traffic": traffic}
+    elif compute_bound:
         roof = {"bound": "fp64-fma" if f64 else "fp32-fma", "achieved": dk["tflops_alg"],
                 "peak": fma_tflops,
                 "unit": "TFLOP/s", "frac": fma_frac, "traffic": traffic}
@@ -851,10 +882,13 @@ def main():
                  "traffic_source": "profiles/traffic_r02.json (ncu --set full dram__bytes_read+write "
                                    "of this kernel on this workload, scaled to this launch)",
                  "issue_model_frac": dk.get("issue_model_frac"),
-                 "issue_model": "dispatch cycles per point-edge: slab 2 (FFMA + FMNMX3/2), "
-                                "crossing 5.5 (1.5 FADD + FFMA + 1.5 LOP3, paired anchoring); the "
-                                "fused kernel their mean over the three engines; "
-                                "profiles/crossing_forms_r02.json"})
+                 "issue_model": ("FP64-pipe cycles per point-edge (2 per DADD / DMUL / DSETP): "
+                                 "Voronoi 12, offset 8, crossing 14.9 "
+                                 "(profiles/ncu_full_r02_c5f64.json)" if f64 else
+                                 "dispatch cycles per point-edge: slab 2 (FFMA + FMNMX3/2), "
+                                 "crossing 5.5 (1.5 FADD + FFMA + 1.5 LOP3, paired anchoring); the "
+                                 "fused kernel their mean over the three engines; "
+                                 "profiles/crossing_forms_r02.json")})
     try:  # the ncu evidence for the same kernel and workload (issue / pipe utilisation)
         nk = json.loads(NCU_FILE.with_name(f"ncu_full_r02_{args.workload.replace(':', 'n')}.json")
                         .read_text())["kernels"][dk["engine"]]

@@ -97,20 +97,40 @@ __device__ __forceinline__ void exact_eval(uint32_t n, double inner_x, double in
 #pragma unroll
     for (int p = 0; p < P; ++p) in[p] = (flags[p] == 0u) | (flags[p] == n);
   } else {
+    // The same comparisons with the same operands as ray_kernel, fewer issued:
+    //  - (w.y > qy) of edge e is (u.y > qy) of edge e-1 (record e's wy is
+    //    record e-1's uy, the same vertex): carried, one DSETP per edge;
+    //  - lhs != rhs is !(lhs == rhs) (IEEE, NaN included): one DSETP less;
+    //  - the on-segment box (four DSETP) is evaluated only when some point of
+    //    the warp lies exactly on the edge line (lhs == rhs), i.e. almost never.
     const RayEdgeF64* s = static_cast<const RayEdgeF64*>(tab);
-    bool parity[P], on_edge[P];
+    bool parity[P], on_edge[P], above[P];
 #pragma unroll
-    for (int p = 0; p < P; ++p) { parity[p] = false; on_edge[p] = false; }
+    for (int p = 0; p < P; ++p) {
+      parity[p] = false;
+      on_edge[p] = false;
+      above[p] = n > 0 && s[n - 1].uy > y[p];
+    }
     for (uint32_t e = 0; e < n; ++e) {
       const RayEdgeF64 r = s[e];
+      bool eq[P];
+      bool any_eq = false;
 #pragma unroll
       for (int p = 0; p < P; ++p) {
-        const bool in_range = (r.uy > y[p]) != (r.wy > y[p]);
+        const bool above_u = r.uy > y[p];
+        const bool in_range = above_u != above[p];
+        above[p] = above_u;
         const double lhs = dsub(dmul(y[p], r.dvx), dmul(x[p], r.dvy));
-        const bool on_left = (lhs != r.rhs) & ((lhs > r.rhs) == (r.going_up != 0));
+        eq[p] = lhs == r.rhs;
+        const bool on_left = !eq[p] & ((lhs > r.rhs) == (r.going_up != 0));
         parity[p] ^= in_range & on_left;
-        on_edge[p] |= (lhs == r.rhs) & (x[p] >= r.min_x) & (x[p] <= r.max_x) &
-                      (y[p] >= r.min_y) & (y[p] <= r.max_y);
+        any_eq |= eq[p];
+      }
+      if (__builtin_expect(__any_sync(0xffffffffu, any_eq), 0)) {
+#pragma unroll
+        for (int p = 0; p < P; ++p)
+          on_edge[p] |= eq[p] & (x[p] >= r.min_x) & (x[p] <= r.max_x) & (y[p] >= r.min_y) &
+                        (y[p] <= r.max_y);
       }
     }
 #pragma unroll

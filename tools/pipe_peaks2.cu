@@ -16,11 +16,14 @@ template <int kOp>
 __global__ void __launch_bounds__(256) pipe_kernel(float* out, int iters, float a, float b) {
   float v[kChains], w[kChains];
   unsigned u[kChains];
+  double dv[kChains], dw[kChains];
 #pragma unroll
   for (int i = 0; i < kChains; ++i) {
     v[i] = out[threadIdx.x] + i;
     w[i] = v[i] * 0.5f + 1.f;
     u[i] = __float_as_uint(v[i]);
+    dv[i] = v[i];
+    dw[i] = w[i];
   }
   for (int it = 0; it < iters; ++it) {
 #pragma unroll
@@ -48,6 +51,14 @@ __global__ void __launch_bounds__(256) pipe_kernel(float* out, int iters, float 
         asm volatile("max.s32 %0, %0, %1;" : "+r"(u[i]) : "r"(u[j]));
       } else if constexpr (kOp == 10) {  // PRMT
         asm volatile("prmt.b32 %0, %0, %1, 0x3210;" : "+r"(u[i]) : "r"(u[j]));
+      } else if constexpr (kOp == 12) {  // DADD
+        asm volatile("add.rn.f64 %0, %0, %1;" : "+d"(dv[i]) : "d"(dw[j]));
+      } else if constexpr (kOp == 13) {  // DMUL
+        asm volatile("mul.rn.f64 %0, %0, %1;" : "+d"(dv[i]) : "d"(dw[j]));
+      } else if constexpr (kOp == 14) {  // DSETP + predicated integer add (the flag count)
+        asm volatile("{.reg .pred p; setp.lt.f64 p, %1, %2; @p add.u32 %0, %0, 1;}" : "+r"(u[i]) : "d"(dv[j]), "d"(dw[k]));
+      } else if constexpr (kOp == 15) {  // DSETP into a bool AND (the Voronoi accumulation)
+        asm volatile("{.reg .pred p, q; setp.ne.u32 q, %0, 0; setp.le.and.f64 p, %1, %2, q; selp.u32 %0, 1, 0, p;}" : "+r"(u[i]) : "d"(dv[j]), "d"(dw[k]));
       } else if constexpr (kOp == 11) {  // FFMA 3v + FADD 2v, 1:1
         asm volatile("fma.rn.f32 %0, %0, %1, %2;" : "+f"(v[i]) : "f"(w[j]), "f"(w[k]));
         asm volatile("add.f32 %0, %0, %1;" : "+f"(w[i]) : "f"(v[k]));
@@ -99,5 +110,9 @@ int main() {
   run<9>("imnmx", 1, sms, mhz);
   run<10>("prmt", 1, sms, mhz);
   run<11>("ffma3v+fadd", 2, sms, mhz);
+  run<12>("dadd", 1, sms, mhz);
+  run<13>("dmul", 1, sms, mhz);
+  run<14>("dsetp+pred_iadd", 2, sms, mhz);
+  run<15>("dsetp.and+sel", 3, sms, mhz);
   return 0;
 }
