@@ -697,7 +697,7 @@ struct TriParams {
   CrossParams c;
   uint32_t off_o, off_c;  // float4 offsets of the offset / crossing tables in shared memory
 };
-constexpr int kTriInlineMax = 192;
+constexpr int kTriInlineMax = 256;
 struct TriParamsInl {   // the three tables in the parameter bank (VPIPG_INLINE)
   SlabParams v, o;
   CrossParams c;
@@ -868,13 +868,13 @@ cudaError_t launch(const typename Eng::Params& prm, const TestArgs& a, cudaStrea
 }  // namespace
 
 // Polygons with more edges than this run the per-engine kernels even when all
-// three engines are asked for: at n = 32 the fused kernel is 3.6 % faster than
-// the three separate ones (C5); on the exact-n c3x polygons (2^28 points) the
-// two are equal at n = 32 / 36 and the separate kernels win by 0.5 / 1.1 /
-// 1.5 % at n = 40 / 44 / 48, and by 5-6 % at n = 256 / 1024 (larger P for the
-// slab engines) (profiles/round1_summary.md)
+// three engines are asked for. With parameter-bank tables the fused kernel
+// stays 4-6 % ahead of the three per-engine kernels up to n = 96 on the
+// exact-n c3x polygons (2^28 points: n = 40 2.95 vs 3.12 ms, 64 4.52 vs 4.8,
+// 96 6.63; profiles/sweep_r02.json); past that its tables no longer fit the
+// parameter bank (kTriInlineMax float4 records)
 #ifndef VPIPG_FUSE_MAX_N
-#define VPIPG_FUSE_MAX_N 40
+#define VPIPG_FUSE_MAX_N 96
 #endif
 
 // a crossing record (u.x, u.y, dvx/dvy, w.x) from the local frame of the

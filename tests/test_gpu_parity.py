@@ -693,7 +693,7 @@ def test_multi_partial_engine_sets_f64_and_missing_outputs(golden):
 def test_multi_fused_plan():
     """vpipg_test_multi_fused reports the route vpipg_test_multi takes: one
     fused launch for all three engines on float32 batches of polygons with at
-    most 40 edges and on any float64 batch, per-engine kernels otherwise."""
+    most 96 edges and on any float64 batch, per-engine kernels otherwise."""
     m = 1 << 20
     xs = torch.zeros(m, dtype=torch.float32, device=DEV)
     ys = torch.zeros_like(xs)
@@ -704,10 +704,10 @@ def test_multi_fused_plan():
         assert p.multi_fused(xs.double(), ys.double())       # the exact f64 kernels fuse at any n
         assert not p.multi_fused(xs[:100], ys[:100])      # fewer slices than warps
         assert not p.multi_fused(xs[1:], ys[1:])          # not 16-byte aligned
-    _, (vx, vy) = W.c3_named("c3x:64")
+    _, (vx, vy) = W.c3_named("c3x:128")
     with vp.PreparedPolygon.prepare(vx, vy, vp.KIND_ALL) as p:
-        assert not p.multi_fused(xs, ys)                  # 64 edges: separate kernels are faster
-    for n, fused in ((40, True), (44, False)):            # VPIPG_FUSE_MAX_N = 40
+        assert not p.multi_fused(xs, ys)                  # 128 edges: separate kernels are faster
+    for n, fused in ((96, True), (100, False)):           # VPIPG_FUSE_MAX_N = 96
         _, (vx, vy) = W.c3_named(f"c3x:{n}")
         with vp.PreparedPolygon.prepare(vx, vy, vp.KIND_ALL) as p:
             assert p.multi_fused(xs, ys) == fused, n
