@@ -853,7 +853,7 @@ def main():
     compute_bound = (4 * n_eng * pe / (fma_tflops * 1e12)) > (alg_bytes / (hbm_peak * 1e9))
     traffic = None
     try:  # DRAM bytes per launch from the committed ncu --set full capture (same kernel/config)
-        tj = json.loads(TRAFFIC_FILE.read_text())[args.workload]
+        tj = json.loads(TRAFFIC_FILE.read_text())[args.workload + ("f64" if f64 else "")]
         traffic = tj["dram_bytes_per_launch"][dk["engine"]] * m / tj["points"]
     except Exception:
         pass
@@ -890,8 +890,9 @@ def main():
                                  "fused kernel their mean over the three engines; "
                                  "profiles/crossing_forms_r02.json")})
     try:  # the ncu evidence for the same kernel and workload (issue / pipe utilisation)
-        nk = json.loads(NCU_FILE.with_name(f"ncu_full_r02_{args.workload.replace(':', 'n')}.json")
-                        .read_text())["kernels"][dk["engine"]]
+        nk = json.loads(NCU_FILE.with_name(
+            f"ncu_full_r02_{args.workload.replace(':', 'n')}{'f64' if f64 else ''}.json")
+                        .read_text())["kernels"][dk["engine"] + ("_f64" if f64 else "")]
         roof["ncu"] = {k.split(".")[0]: nk[k] for k in (
             "smsp__issue_active.avg.pct_of_peak_sustained_active",
             "sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active",

@@ -87,3 +87,30 @@ def test_shard_properties():
                 assert (a % 1024 == 0 or a == b == m) and a <= b
     with pytest.raises(ValueError):
         shard(10, 0, 2, align=48)
+
+
+def test_bench_reference_arm_two_ranks_under_torchrun():
+    """The driver's N > 1 launch path, end to end on the CPU: `bench.py --gpus 2`
+    relaunches itself under torch.distributed.run (127.0.0.1), rank 0 runs the
+    reference arm on the full (here: reduced) config and prints ONE JSON line,
+    rank 1 exits 0 without work."""
+    import json
+    import subprocess
+    import sys
+    from pathlib import Path
+    root = Path(__file__).resolve().parents[1]
+    import oracle
+    try:
+        oracle.Reference()
+    except FileNotFoundError:
+        pytest.skip("oracle/_ref not built")
+    env = {k: v for k, v in os.environ.items() if k not in ("RANK", "WORLD_SIZE", "LOCAL_RANK")}
+    out = subprocess.run([sys.executable, str(root / "bench.py"), "--impl", "reference", "--gpus", "2",
+                          "--points", str(1 << 16), "--steps", "1", "--warmup", "1"],
+                         cwd=root, capture_output=True, text=True, timeout=600, env=env)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.strip().startswith("{")]
+    assert len(lines) == 1, out.stdout[-2000:]
+    d = json.loads(lines[0])
+    assert d["impl"] == "reference" and d["n_gpus"] == 2 and d["value"] > 0
+    assert d["cpu_baseline"]["kind"] == "reference" and d["config"]["points"] == 1 << 16
