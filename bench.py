@@ -420,6 +420,18 @@ def convert_block(vp, device, stream):
         ref = oracle.Reference()
     except Exception:
         ref = None
+    # the C-ABI call's own host-visible cost, from a C++ caller (regular n-gons)
+    cxx = {}
+    try:
+        out = subprocess.run([str(ROOT / "paper_2007_15385_b200" / "bin" / "prepare_timing"), "8",
+                              "32", "1024"], capture_output=True, text=True, timeout=120,
+                             env={**os.environ, "CUDA_VISIBLE_DEVICES":
+                                  os.environ.get("CUDA_VISIBLE_DEVICES", str(device))})
+        for line in out.stdout.splitlines():
+            r = json.loads(line)
+            cxx[r["n"]] = r
+    except Exception:
+        pass
     single = []
     for n, (vx, vy) in polys:
         vx, vy = np.ascontiguousarray(vx, np.float64), np.ascontiguousarray(vy, np.float64)
@@ -440,6 +452,9 @@ def convert_block(vp, device, stream):
                 rdy.append(t2 - t0)
         e = {"n": n, "prepare_enqueue_us": statistics.median(enq) * 1e6,
              "prepare_ready_us": statistics.median(rdy) * 1e6}
+        if n in cxx:
+            e["cxx_prepare_enqueue_us"] = cxx[n]["prepare_enqueue_us"]
+            e["cxx_prepare_ready_us"] = cxx[n]["prepare_ready_us"]
         if ref is not None:
             tv, tc = ref.time_convert(vx, vy)
             e.update({"reference_validate_us": tv / 1e3, "reference_to_voronoi_us": tc / 1e3})
@@ -466,7 +481,8 @@ def convert_block(vp, device, stream):
     return {"single": single, "c4": c4, "ctypes_call_us": statistics.median(ct) * 1e6,
             "what": "warm medians; GPU: vpipg_prepare = host validate_polygon + enqueued device "
                     "conversion (generators, f32 tables), ready = until vpipg_poly_status "
-                    "returns; C4: vpipg_prepare_csr of the 65,536-polygon database. Reference: "
+                    "returns, timed through ctypes and (cxx_*) by a C++ caller "
+                    "(bin/prepare_timing, regular n-gons); C4: vpipg_prepare_csr of the 65,536-polygon database. Reference: "
                     "validate_polygon and to_voronoi (the convert phase of bench.cpp:165-170) "
                     "of the same polygons, single-threaded as run_benchmark runs them"}
 

@@ -106,6 +106,12 @@ def build(verbose: bool = False) -> Path:
         _run(["g++", *CXX_FLAGS, str(cli_src), "-o", str(cli), f"-L{LIB.parent}", "-lvpipg",
               f"-L{CUDA_HOME / 'lib64'}", "-lcudart", "-Wl,-rpath,$ORIGIN/../lib",
               f"-Wl,-rpath,{CUDA_HOME / 'lib64'}"])
+    timing = PKG / "bin" / "prepare_timing"
+    timing_src = CSRC / "cli" / "prepare_timing.cpp"
+    if _stale(timing, [timing_src, LIB] + hdrs):
+        _run(["g++", *CXX_FLAGS, str(timing_src), "-o", str(timing), f"-L{LIB.parent}", "-lvpipg",
+              f"-L{CUDA_HOME / 'lib64'}", "-lcudart", "-Wl,-rpath,$ORIGIN/../lib",
+              f"-Wl,-rpath,{CUDA_HOME / 'lib64'}"])
     if verbose:
         print(f"built {LIB}")
     return LIB

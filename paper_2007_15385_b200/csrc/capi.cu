@@ -106,13 +106,15 @@ class PinnedArena {
     }
     if (size > kChunk) {  // large: its own allocation
       void* h = nullptr;
-      if (cudaHostAlloc(&h, size, cudaHostAllocPortable) != cudaSuccess) return nullptr;
+      if (cudaHostAlloc(&h, size, cudaHostAllocPortable | cudaHostAllocMapped) != cudaSuccess)
+        return nullptr;
       *got = size;
       return static_cast<char*>(h);
     }
     if (left_ < size) {
       void* h = nullptr;
-      if (cudaHostAlloc(&h, kChunk, cudaHostAllocPortable) != cudaSuccess) return nullptr;
+      if (cudaHostAlloc(&h, kChunk, cudaHostAllocPortable | cudaHostAllocMapped) != cudaSuccess)
+        return nullptr;
       cur_ = static_cast<char*>(h);
       left_ = kChunk;
     }
@@ -249,8 +251,16 @@ int build(vpipg_poly* p, const double* vv, const double* vr, const double* gen, 
   a.cross_vert = reinterpret_cast<float4*>(b + o_cross);
   a.lines = reinterpret_cast<double4*>(b + o_lines);
   a.meta = reinterpret_cast<PrepMeta*>(b + o_meta);
+  // the kernel writes the status, counts and small tables straight into the
+  // mapped pinned block (unified addressing: the host pointer is valid on the
+  // device), so no download call is enqueued
+  (void)dl;
+  a.host_out = p->host + p->dl_meta;
+  a.out_slab[0] = static_cast<uint32_t>(o_s0 - o_meta);
+  a.out_slab[1] = static_cast<uint32_t>(o_s1 - o_meta);
+  a.out_cross = static_cast<uint32_t>(o_cross - o_meta);
+  a.tables_out = p->host_tables ? 1 : 0;
   VPIPG_TRY(launch_prep(a, inline_in ? &inl : nullptr, s));
-  VPIPG_TRY(cudaMemcpyAsync(p->host + p->dl_meta, b + o_meta, dl, cudaMemcpyDeviceToHost, s));
   VPIPG_TRY(cudaEventRecord(p->ready, s));
   p->state.store(-1, std::memory_order_release);
   return kOk;

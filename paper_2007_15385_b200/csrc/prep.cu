@@ -345,6 +345,20 @@ __global__ void __launch_bounds__(kPrepThreads) prep_kernel(const PrepArgs a0,
   }
   __syncthreads();
   if (tid == 0) a.meta->status = (s_fail == INT_MAX) ? 0 : (s_fail & 7);
+  if (a.host_out) {  // straight into the caller's mapped pinned block
+    __syncthreads();
+    const uint32_t* mw = reinterpret_cast<const uint32_t*>(a.meta);
+    uint32_t* hm = reinterpret_cast<uint32_t*>(a.host_out);
+    for (int i = tid; i < static_cast<int>(sizeof(PrepMeta) / 4); i += kPrepThreads) hm[i] = mw[i];
+    if (a.tables_out) {
+      for (int e = 0; e < 2; ++e) {
+        float2* h = reinterpret_cast<float2*>(a.host_out + a.out_slab[e]);
+        for (int i = tid; i < n + 4; i += kPrepThreads) h[i] = a.slab_coef[e][i];
+      }
+      float4* hc = reinterpret_cast<float4*>(a.host_out + a.out_cross);
+      for (int i = tid; i < n; i += kPrepThreads) hc[i] = a.cross_vert[i];
+    }
+  }
 }
 
 }  // namespace

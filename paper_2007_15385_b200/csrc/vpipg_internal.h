@@ -26,6 +26,12 @@ struct PrepArgs {
   float4* cross_vert;
   double4* lines;        // n unit-normal edge lines (band metric)
   PrepMeta* meta;
+  // the handle's pinned, mapped host block: the kernel copies the final
+  // PrepMeta there and, when tables_out, the slab tables (n + 4 pairs each)
+  // and the crossing table at the given byte offsets (no download call)
+  char* host_out;
+  uint32_t out_slab[2], out_cross;
+  int tables_out;
 };
 
 // Small prepare inputs in the prep kernel's parameter bank (no upload call):
