@@ -230,7 +230,8 @@ __device__ __forceinline__ void test_pair(const DbTables& t, bool ok, uint32_t i
   }
   for (uint32_t g = 1; 8 * g < n; ++g) {
     const float2* b = r + 4 + 12 * g;
-    const Rows4 r0 = ld256(b), r1 = ld256(b + 4);
+    // the second row chunk only when the group has more than 4 edges
+    const Rows4 r0 = ld256(b), r1 = 8 * g + 4 < n ? ld256(b + 4) : Rows4{};
     const Rows4 f0 = kV ? ld256(b + 8) : Rows4{};
     group(g, r0, r1, f0);
   }
