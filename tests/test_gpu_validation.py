@@ -176,3 +176,38 @@ def test_c2_full_scale_vs_reference_library():
             assert par["outside_band"] == 0, (e, par)
             assert abs(c.item() - ref[e]["inside"]) <= par["disagree"]
             print(f"C2 engine {e}: {par['disagree']} band disagreements vs the reference")
+
+
+@pytest.mark.parametrize("nv", [40, 200])
+def test_non_convex_crossing_full_scale_vs_reference_library(nv):
+    """Ray crossing on a random star-shaped (non-convex) polygon, 2^24 f32
+    points, against the unmodified reference library's
+    ray_crossing_contains_batch on the same points (raw vertices, any simple
+    polygon, vpip.cpp:120-128): every disagreement lies inside the band. Both
+    table placements (parameter bank at 40 vertices, shared memory at 200)."""
+    import bench_cpu as BC
+    import oracle
+    try:
+        ref = oracle.Reference()
+    except FileNotFoundError:
+        pytest.skip("oracle/_ref not built")
+    rng = np.random.default_rng(nv)
+    ang = np.sort(rng.uniform(0, 2 * np.pi, nv))
+    rad = rng.uniform(0.3, 1.0, nv)
+    vx, vy = 3.0 + rad * np.cos(ang), -2.0 + rad * np.sin(ang)
+    m = 1 << 24
+    xs = torch.empty(m, dtype=torch.float32, device=DEV)
+    ys = torch.empty(m, dtype=torch.float32, device=DEV)
+    vp.fill_uniform_points(1234 + nv, 0, xs, ys, (2.0, -3.0, 4.0, -1.0))
+    hx, hy = xs.cpu().numpy(), ys.cpu().numpy()
+    want = ref.full_pass(vx, vy, hx, hy, BC.cores(), engines=(2,))[0]
+    with vp.PreparedPolygon.prepare(vx, vy, vp.KIND_CROSSING) as p:
+        w = torch.zeros(m // 32, dtype=torch.int32, device=DEV)
+        c = torch.zeros(1, dtype=torch.int64, device=DEV)
+        p.test(2, xs, ys, words=w, count=c)
+        torch.cuda.synchronize()
+    par = BC.parity_entry(w, want["words"], hx, hy, vx, vy, m, BC.EPS32)
+    assert par["outside_band"] == 0, par
+    assert abs(c.item() - want["inside"]) <= par["disagree"]
+    assert 0.1 < want["inside"] / m < 0.6
+    print(f"non-convex {nv}-gon: {par['disagree']} band disagreements vs the reference")
