@@ -844,3 +844,44 @@ def test_prepare_is_asynchronous_and_reports_device_status_on_first_use():
     torch.cuda.synchronize()
     assert c.item() == 64  # (0, 0) is inside
     q.close()
+
+
+def test_first_use_of_a_fresh_handle_from_many_threads():
+    """The asynchronous prepare is finished exactly once even when several host
+    threads make the first call on a handle at the same time (ensure_ready),
+    each on its own stream: every result equals a sequential run."""
+    import threading
+    vx, vy = W.c5_polygon(vp.random_convex_polygon)
+    m = 1 << 20
+    xs = torch.empty(m, dtype=torch.float32, device=DEV)
+    ys = torch.empty_like(xs)
+    vp.fill_uniform_points(99, 0, xs, ys, W.C5_BOX)
+    with vp.PreparedPolygon.prepare(vx, vy, vp.KIND_ALL) as p:
+        want = []
+        for e in range(3):
+            w = torch.zeros(m // 32, dtype=torch.int32, device=DEV)
+            p.test(e, xs, ys, words=w)
+            want.append(w)
+        torch.cuda.synchronize()
+    for rep in range(5):
+        with vp.PreparedPolygon.prepare(vx, vy, vp.KIND_ALL) as p:  # pending
+            outs, errors = [None] * 12, []
+
+            def worker(i):
+                try:
+                    s = torch.cuda.Stream()
+                    w = torch.zeros(m // 32, dtype=torch.int32, device=DEV)
+                    p.test(i % 3, xs, ys, words=w, stream=s)
+                    s.synchronize()
+                    outs[i] = w
+                except Exception as ex:
+                    errors.append(ex)
+
+            threads = [threading.Thread(target=worker, args=(i,)) for i in range(12)]
+            for th in threads:
+                th.start()
+            for th in threads:
+                th.join()
+            assert not errors, errors
+            for i, w in enumerate(outs):
+                assert torch.equal(w, want[i % 3]), (rep, i)
