@@ -885,3 +885,56 @@ def test_first_use_of_a_fresh_handle_from_many_threads():
             assert not errors, errors
             for i, w in enumerate(outs):
                 assert torch.equal(w, want[i % 3]), (rep, i)
+
+
+@pytest.mark.parametrize("n", [3, 4, 5, 6, 7, 8])
+@pytest.mark.parametrize("form", ["y_only", "x_only", "far"])
+@pytest.mark.parametrize("m", [(1 << 20) + 77, 1 << 22])
+def test_small_polygon_fused_route(orc, n, form, m):
+    """Polygons of at most 8 vertices whose slab tables have one section take
+    the straight-line small-polygon kernel (test_f32.cu tri_small_kernel: edge
+    count and padded group size compile-time, tables as constant-bank
+    operands). Its words and counts equal the three per-engine kernels' bit
+    for bit -- y-only and x-only tables (an exactly vertical edge forces the
+    latter), the local-frame shift of a polygon far from the origin, and a
+    ragged tail -- and every engine equals the oracle outside the band."""
+    rng = np.random.default_rng(4000 + 10 * n + len(form))
+    t = np.sort(rng.uniform(0.0, 2.0 * np.pi, n)) + np.linspace(0.0, 0.5 / n, n)
+    vx, vy = np.cos(t), np.sin(t)
+    if form == "x_only":  # turn edge 0 -> 1 exactly vertical: no y-only table
+        vx, vy = _rot(vx, vy, 0.5 * np.pi - np.arctan2(vy[1] - vy[0], vx[1] - vx[0]))
+        vx[1] = vx[0]
+    cx, cy = (300.0, -700.0) if form == "far" else (0.0, 0.0)
+    vx, vy = vx + cx, vy + cy
+    if form == "x_only":
+        assert _offset_table_mode(vx, vy) == 2
+    else:
+        assert _offset_table_mode(vx, vy) != 0
+    xs = (cx + rng.uniform(-1.3, 1.3, m)).astype(np.float32)
+    ys = (cy + rng.uniform(-1.3, 1.3, m)).astype(np.float32)
+    nw = (m + 31) // 32
+    xt, yt = torch.as_tensor(xs, device=DEV), torch.as_tensor(ys, device=DEV)
+    with vp.PreparedPolygon.prepare(vx, vy, vp.KIND_ALL) as p:
+        assert p.multi_fused(xt, yt)
+        ref = []
+        for e in range(3):
+            w = torch.zeros(nw, dtype=torch.int32, device=DEV)
+            c = torch.zeros(1, dtype=torch.int64, device=DEV)
+            p.test(e, xt, yt, words=w, count=c)
+            ref.append((w, c))
+        ws = [torch.zeros(nw, dtype=torch.int32, device=DEV) for _ in range(3)]
+        cs = [torch.zeros(1, dtype=torch.int64, device=DEV) for _ in range(3)]
+        p.test_multi(xt, yt, (0, 1, 2), words=ws, counts=cs)
+        torch.cuda.synchronize()
+        for e in range(3):
+            assert torch.equal(ws[e], ref[e][0]), (n, form, e)
+            assert cs[e].item() == ref[e][1].item() > 0, (n, form, e)
+    k = 1 << 18  # oracle on a prefix
+    xd, yd = xs[:k].astype(np.float64), ys[:k].astype(np.float64)
+    want = orc.masks(vx, vy, xd, yd)
+    ext = max(np.ptp(vx), np.ptp(vy))
+    ulp = np.spacing(np.maximum(np.abs(xs[:k]), np.abs(ys[:k]))).astype(np.float64)
+    band = orc.edge_line_distances(vx, vy, xd, yd) <= EPS32 * max(1.0, ext) + 2 * ulp
+    for e in range(3):
+        got = words_to_mask(ws[e].cpu().numpy().view(np.uint32), m)[:k]
+        assert not ((got != want[e]) & ~band).any(), (n, form, e)
