@@ -26,6 +26,7 @@
 #include <cstring>
 #include <type_traits>
 
+#include "f32_common.cuh"
 #include "tma_pipe.cuh"
 #include "vpipg_device.cuh"
 #include "vpipg_internal.h"
@@ -50,31 +51,12 @@
 #ifndef VPIPG_CROSS_UNROLL
 #define VPIPG_CROSS_UNROLL 1
 #endif
-#define VPIPG_PRAGMA(x) _Pragma(#x)
-#define VPIPG_UNROLL(n) VPIPG_PRAGMA(unroll n)
 
 namespace vpipg {
 
 namespace {
 
-constexpr int kWarps = 8;             // warps per CTA
-constexpr int kThreads = kWarps * 32;
 constexpr int kStages = 2;            // per-warp ring depth
-constexpr int kGroupXlo = 0, kGroupYlo = 2;  // slab group order (vpipg_device.cuh)
-
-// NaN-propagating three-input max / min (FMNMX3 .NAN, same issue cost): a
-// point with a NaN coordinate turns every bound of its sections into NaN, so
-// the final compare sees NaN and the engine's NaN rule decides (below)
-__device__ __forceinline__ float fmax3(float a, float b, float c) {
-  float r;
-  asm("max.NaN.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
-  return r;
-}
-__device__ __forceinline__ float fmin3(float a, float b, float c) {
-  float r;
-  asm("min.NaN.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
-  return r;
-}
 
 // ---------------------------------------------------------------------------
 #ifndef VPIPG_LOCAL_FRAME
@@ -116,9 +98,6 @@ struct SlabParams {
 // read them with uniform constant loads (LDCU) into uniform registers, so the
 // per-edge FFMA / FADD operands come from the uniform datapath and no vector
 // register or shared-memory load is spent on table values.
-#ifndef VPIPG_INLINE
-#define VPIPG_INLINE 1
-#endif
 constexpr int kInlineMax = 128;
 struct SlabParamsInl {
   SlabTable tab;
@@ -244,31 +223,6 @@ struct SlabEngine {
   }
 };
 
-// ---------------------------------------------------------------------------
-// Crossing engine (engines.cpp:165-204). For edge w = v[k-1] -> u = v[k]:
-//   in_range <=> (u.y > qy) != (w.y > qy) <=> sign(h_k) ^ sign(h_{k-1}),
-//                h = qy - v.y (a -0.0 from qy = -0.0 merely moves vertex k to
-//                "above" for both of its edges at once, which keeps the parity)
-//   on_left  <=> qx < x-of-edge-at-qy <=> d = (a.x - qx) + (qy - a.y) * dvx/dvy > 0
-//                for either endpoint a of the edge
-// crossing bit = (H_k ^ H_{k-1}) & ~D (one LOP3), XOR-reduced into the parity
-// word's bit 31 two bits per LOP3.
-//
-// Paired anchoring: edges k (v[k-1] -> v[k]) and k+1 (v[k] -> v[k+1]) both
-// take their x-intercept from their shared vertex v[k], so g = v[k].x - qx is
-// formed for every other vertex only and h_k serves both d's: per edge
-// 1 FADD (h) + 1/2 FADD (g) + 1 FFMA (d) + 3/2 LOP3, 5.5 dispatch cycles
-// against 6 for one g per vertex (B200, profiles/crossing_forms_r02.json:
-// C5 crossing 12.18 -> 11.20 ms at P = 12). The per-edge constants come from
-// the parameter bank as uniform registers (VPIPG_INLINE), so the FFMA has two
-// vector sources: with three (table in shared memory) it issues at 0.61 per
-// cycle instead of 0.96 (tools/pipe_peaks2.cu).
-// Points exactly on an edge line lie inside the 1e-5 parity band, so the
-// reference's closed-boundary latch (engines.cpp:194-196) is repeated only by
-// the exact f64 kernel.
-__device__ __forceinline__ uint32_t cross_bit(float h, float hprev, float d) {
-  return (__float_as_uint(h) ^ __float_as_uint(hprev)) & ~__float_as_uint(d);
-}
 struct CrossParams {
   CrossTable tab;
   float ox, oy;
@@ -377,57 +331,6 @@ struct CrossEngine {
   }
 };
 
-// ---------------------------------------------------------------------------
-// Output: ballot words (PIPM order), optional byte mask, per-lane inside count.
-// The P words of a slice are warp-uniform; lane 0 writes them with 16-byte
-// streaming stores (a slice's words are 64 contiguous, 64-byte aligned bytes).
-// kVote 0: inside = (a >= b); 1: (a >= b or unordered), the NaN-inside rule;
-// 2: a's bit pattern is negative as an int (the crossing parity word, no
-// float conversion). One compare feeds both the ballot and a predicated count.
-// Per-lane inside counts: integer-valued floats (VPIPG_FCOUNT, the predicated
-// FADD issues at full rate on the FMA pipe) or u32; exact either way below
-// 2^24 points per lane (2^24 x 75,776 resident lanes per launch).
-#ifndef VPIPG_FCOUNT
-#define VPIPG_FCOUNT 1
-#endif
-using cnt_t = std::conditional_t<VPIPG_FCOUNT != 0, float, uint32_t>;
-#if VPIPG_FCOUNT
-#define VPIPG_CNT_ADD "@q add.f32 %1, %1, 0f3F800000;\n\t}"
-#define VPIPG_CNT_C "+f"
-#else
-#define VPIPG_CNT_ADD "@q add.u32 %1, %1, 1;\n\t}"
-#define VPIPG_CNT_C "+r"
-#endif
-template <int kVote>
-__device__ __forceinline__ uint32_t vote_in(float a, float b, cnt_t& cnt) {
-  uint32_t w;
-  if (kVote == 2)
-    asm volatile(
-        "{\n\t.reg .pred q;\n\t"
-        "setp.lt.s32 q, %2, 0;\n\t"
-        "vote.sync.ballot.b32 %0, q, 0xffffffff;\n\t"
-        VPIPG_CNT_ADD
-        : "=r"(w), VPIPG_CNT_C(cnt)
-        : "r"(__float_as_uint(a)));
-  else if (kVote == 1)
-    asm volatile(
-        "{\n\t.reg .pred q;\n\t"
-        "setp.geu.f32 q, %2, %3;\n\t"
-        "vote.sync.ballot.b32 %0, q, 0xffffffff;\n\t"
-        VPIPG_CNT_ADD
-        : "=r"(w), VPIPG_CNT_C(cnt)
-        : "f"(a), "f"(b));
-  else
-    asm volatile(
-        "{\n\t.reg .pred q;\n\t"
-        "setp.ge.f32 q, %2, %3;\n\t"
-        "vote.sync.ballot.b32 %0, q, 0xffffffff;\n\t"
-        VPIPG_CNT_ADD
-        : "=r"(w), VPIPG_CNT_C(cnt)
-        : "f"(a), "f"(b));
-  return w;
-}
-
 // live == false (a warp whose slot in the last round is past the end; warp-
 // uniform): the votes run, nothing is stored or counted
 template <bool kGuard, int kVote, int P>
@@ -465,13 +368,6 @@ __device__ __forceinline__ cnt_t emit(float (&av)[P], const float (&bv)[P], uint
   return cnt;
 }
 
-__device__ __forceinline__ void flush_count(cnt_t fcnt, const TestArgs& a) {
-  uint32_t cnt = static_cast<uint32_t>(fcnt);
-#pragma unroll
-  for (int s = 16; s > 0; s >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, s);
-  if ((threadIdx.x & 31) == 0 && a.inside && cnt) atomicAdd(a.inside, (unsigned long long)cnt);
-}
-
 // Guarded warp tile straight from global memory (tails, unaligned inputs).
 template <class Eng, bool kShift = Eng::kShiftIn>
 __device__ __forceinline__ cnt_t guarded_tile(const typename Eng::Params& prm, const float4* tab,
@@ -491,28 +387,6 @@ __device__ __forceinline__ cnt_t guarded_tile(const typename Eng::Params& prm, c
   Eng::eval(prm, tab, x, y, va, vb);
   return emit<true, Eng::kVote, P>(va, vb, base, a, lane);
 }
-
-// Persistent slice schedule: warp w of CTA b takes slices (b + r * grid) *
-// kWarps + w for rounds r = 0 .. rounds - 1. `rounds` depends on the CTA
-// only, so every loop over it is uniform control flow for the compiler (the
-// per-edge table reads can then use the uniform datapath); a warp whose slot
-// in the last round lies past the end re-reads the last full slice and stores
-// nothing (emit's `live`).
-struct SliceRounds {
-  uint64_t W, b0, g0, rounds, last;
-  __device__ SliceRounds(uint64_t full_slices, int warp) {
-    W = (uint64_t)gridDim.x * kWarps;
-    b0 = (uint64_t)blockIdx.x * kWarps;
-    g0 = b0 + warp;
-    rounds = full_slices > b0 ? (full_slices - b0 + W - 1) / W : 0;
-    last = full_slices ? full_slices - 1 : 0;
-  }
-  __device__ uint64_t slice(uint64_t r) const {
-    const uint64_t g = g0 + r * W;
-    return g < last ? g : last;
-  }
-  __device__ bool live(uint64_t r) const { return g0 + r * W <= last; }
-};
 
 // kSmemTab: the polygon table is staged in shared memory once per CTA (the
 // normal case); polygons whose table exceeds kSmemTableMax read it from global
@@ -596,10 +470,6 @@ __global__ void __launch_bounds__(kThreads, 2)
 // against the TMA ring: equal at C5 (compute-bound), 7 % faster at C3 n = 8
 // (memory-bound: 6.6 TB/s), so the slab engines use it; the crossing engine
 // keeps the ring (3 % faster there).
-__device__ __forceinline__ void prefetch_l2(const void* p) {
-  asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(p));
-}
-
 #ifndef VPIPG_LDG_MINB
 #define VPIPG_LDG_MINB 2
 #endif
@@ -804,192 +674,6 @@ __global__ void __launch_bounds__(kThreads, VPIPG_TRI_MINB)
   flush_count(cc, ac);
 }
 
-// ---------------------------------------------------------------------------
-// Small-polygon fused pass (tri_small_kernel): the three engines for polygons
-// of at most kSmallMaxN crossing vertices whose two slab tables share one
-// single-section form (y-only or x-only). The vertex count NC and the padded
-// record count K of the slab groups are compile-time, so every table value is
-// a constant-bank operand of its FFMA / FADD (no table loads, no edge loops,
-// no group-count branches) and each point runs straight-line code, point
-// after point. The arithmetic is the per-engine kernels' own: the crossing
-// pairs edges (0,1), (2,3), ... with the same anchoring (CrossEngine), and
-// a slab group padded with copies of its first record takes the same max /
-// min (both are exact and idempotent), so the masks equal the generic fused
-// kernel's bit for bit. At n = 3 the generic kernel issues 50.6 instructions
-// per point for the three engines, ~13 of them loop and group bookkeeping
-// (profiles/ncu_full_r02_c3n3.json).
-#ifndef VPIPG_TRI_SMALL_P
-#define VPIPG_TRI_SMALL_P 16
-#endif
-#ifndef VPIPG_TRI_SMALL
-#define VPIPG_TRI_SMALL 1
-#endif
-constexpr int kSmallP = VPIPG_TRI_SMALL_P;
-constexpr int kSmallMaxN = 8;
-// a single-section group of a convex NC-gon holds at most NC - 1 lines (the
-// other side holds at least one), i.e. ceil((NC - 1) / 2) records
-constexpr int small_kmax(int nc) { return nc / 2; }
-
-template <int NC, int K>
-struct TriSmallParams {
-  float ox, oy;          // local frame of the slab tables (0, 0: absolute)
-  float4 slab[2][2][K];  // [Voronoi | offset][lo | hi][record]: (B0, C0, B1, C1)
-  float4 cross[NC];      // crossing records in the absolute frame
-};
-
-// crossing parity word of one point (CrossEngine::eval, unrolled)
-template <int NC>
-__device__ __forceinline__ uint32_t cross_one(const float4 (&c)[NC], float x, float y) {
-  uint32_t par = 0;
-  float hp = y - c[NC - 1].y;
-#pragma unroll
-  for (int k = 0; k + 1 < NC; k += 2) {
-    const float h0 = y - c[k].y, g0 = c[k].x - x;
-    const float h1 = y - c[k + 1].y;
-    par ^= cross_bit(h0, hp, fmaf(h0, c[k].z, g0)) ^ cross_bit(h1, h0, fmaf(h0, c[k + 1].z, g0));
-    hp = h1;
-  }
-  if constexpr (NC & 1) {
-    const float h0 = y - c[NC - 1].y;
-    par ^= cross_bit(h0, hp, fmaf(h0, c[NC - 1].z, c[NC - 1].x - x));
-  }
-  return par;
-}
-
-// one single-section slab test (SlabEngine::section): MODE 1 bounds y by
-// lines in x, MODE 2 bounds x by lines in y; inside iff hi >= lo
-template <int K, int MODE>
-__device__ __forceinline__ void slab_one(const float4 (&t)[2][K], float x, float y, float& lo,
-                                         float& hi) {
-  const float v = MODE == 1 ? x : y, w = MODE == 1 ? y : x;
-  lo = w;
-  hi = w;
-#pragma unroll
-  for (int i = 0; i < K; ++i) {
-    const float4 a = t[0][i], b = t[1][i];
-    lo = fmax3(lo, fmaf(a.x, v, a.y), fmaf(a.z, v, a.w));
-    hi = fmin3(hi, fmaf(b.x, v, b.y), fmaf(b.z, v, b.w));
-  }
-}
-
-// votes, counts and stores of one engine over a slice, four words at a time
-// (f(p, a, b) gives point p's vote operands; see emit). Full slices store
-// their words with predicated 16-byte stores and no byte masks (small_plan
-// takes only 16-byte aligned word outputs and no byte outputs); the guarded
-// tail keeps emit's general stores.
-template <bool kGuard, int kVote, int P, class F>
-__device__ __forceinline__ cnt_t emit4(F&& f, uint64_t base, const TestArgs& a, int lane, bool live) {
-  static_assert(P % 4 == 0, "16-byte word stores need P % 4 == 0");
-  cnt_t cnt = 0;
-  const uint64_t w0 = base >> 5;
-  const bool st = live && lane == 0 && a.words != nullptr;
-#pragma unroll
-  for (int q = 0; q < P / 4; ++q) {
-    uint32_t w[4];
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int p = 4 * q + j;
-      float va, vb;
-      f(p, va, vb);
-      if (kGuard && base + 32u * p + lane >= a.m) va = kVote == 2 ? 0.f : -INFINITY;
-      w[j] = vote_in<kVote>(va, vb, cnt);
-    }
-    if constexpr (!kGuard) {
-      if (st) __stcs(reinterpret_cast<uint4*>(a.words + w0) + q, make_uint4(w[0], w[1], w[2], w[3]));
-    } else {
-      const uint64_t nwords = (a.m + 31) >> 5;
-      if (st) {
-#pragma unroll
-        for (int j = 0; j < 4; ++j)
-          if (w0 + 4 * q + j < nwords) a.words[w0 + 4 * q + j] = w[j];
-      }
-      if (live && a.bytes) {
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const uint64_t idx = base + 32u * (4 * q + j) + lane;
-          if (idx < a.m) a.bytes[idx] = (w[j] >> lane) & 1u;
-        }
-      }
-    }
-  }
-  return live ? cnt : 0;
-}
-
-template <int NC, int K, int MODE, bool kGuard, bool kShift>
-__device__ __forceinline__ void tri_small_slice(const TriSmallParams<NC, K>& prm, const TestArgs& av,
-                                                const TestArgs& ao, const TestArgs& ac,
-                                                uint64_t base, int lane, bool live, cnt_t& cv,
-                                                cnt_t& co, cnt_t& cc) {
-  constexpr int P = kSmallP;
-  const float* xs = static_cast<const float*>(av.xs) + base + lane;
-  const float* ys = static_cast<const float*>(av.ys) + base + lane;
-  float x[P], y[P];
-#pragma unroll
-  for (int p = 0; p < P; ++p) {
-    const bool ok = !kGuard || base + 32u * p + lane < av.m;
-    x[p] = ok ? __ldcs(xs + 32 * p) : 0.f;
-    y[p] = ok ? __ldcs(ys + 32 * p) : 0.f;
-  }
-  // crossing on the points as loaded (absolute-frame table), as tri_kernel
-  cc += emit4<kGuard, 2, P>(
-      [&](int p, float& a, float& b) {
-        a = __uint_as_float(cross_one<NC>(prm.cross, x[p], y[p]));
-        b = 0.f;
-      },
-      base, ac, lane, live);
-  if constexpr (kShift) {
-#pragma unroll
-    for (int p = 0; p < P; ++p) {
-      x[p] -= prm.ox;
-      y[p] -= prm.oy;
-    }
-  }
-  cv += emit4<kGuard, 0, P>([&](int p, float& a, float& b) { slab_one<K, MODE>(prm.slab[0], x[p], y[p], b, a); },
-                            base, av, lane, live);
-  co += emit4<kGuard, 1, P>([&](int p, float& a, float& b) { slab_one<K, MODE>(prm.slab[1], x[p], y[p], b, a); },
-                            base, ao, lane, live);
-}
-
-template <int NC, int K, int MODE>
-__global__ void __launch_bounds__(kThreads, 2)
-    tri_small_kernel(const __grid_constant__ TriSmallParams<NC, K> prm, const TestArgs av,
-                     const TestArgs ao, const TestArgs ac, const uint64_t full_slices) {
-  constexpr int P = kSmallP;
-  constexpr int kWarpPts = 32 * P;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const SliceRounds sr(full_slices, warp);
-  const float* xs = static_cast<const float*>(av.xs);
-  const float* ys = static_cast<const float*>(av.ys);
-  constexpr int kLines = kWarpPts * 4 / 128;
-  auto prefetch = [&](uint64_t r) {
-    if (r >= sr.rounds) return;
-    const uint64_t g = sr.slice(r);
-    for (int l = lane; l < 2 * kLines; l += 32)
-      prefetch_l2((l < kLines ? xs : ys) + g * kWarpPts + (l % kLines) * 32);
-  };
-  cnt_t cv = 0, co = 0, cc = 0;
-  // the slab engines' local-frame shift only where prep moved the origin
-  // (to_local's test, hoisted out of the slice loop)
-  auto run = [&](auto shift) {
-    constexpr bool S = decltype(shift)::value;
-    prefetch(0);
-    for (uint64_t r = 0; r < sr.rounds; ++r) {
-      prefetch(r + 1);
-      tri_small_slice<NC, K, MODE, false, S>(prm, av, ao, ac, sr.slice(r) * kWarpPts, lane,
-                                             sr.live(r), cv, co, cc);
-    }
-    if (sr.g0 == full_slices % sr.W) {
-      for (uint64_t base = full_slices * kWarpPts; base < av.m; base += kWarpPts)
-        tri_small_slice<NC, K, MODE, true, S>(prm, av, ao, ac, base, lane, true, cv, co, cc);
-    }
-  };
-  if (prm.ox != 0.f || prm.oy != 0.f) run(std::true_type{});
-  else run(std::false_type{});
-  flush_count(cv, av);
-  flush_count(co, ao);
-  flush_count(cc, ac);
-}
-
 template <class Eng, bool kSmemTab>
 __global__ void __launch_bounds__(kThreads) generic_kernel(const __grid_constant__ typename Eng::Params prm,
                                                           const TestArgs a) {
@@ -1064,81 +748,14 @@ cudaError_t launch(const typename Eng::Params& prm, const TestArgs& a, cudaStrea
 #define VPIPG_FUSE_MAX_N 96
 #endif
 
-// a crossing record (u.x, u.y, dvx/dvy, w.x) from the local frame of the
-// device tables to the absolute frame of the parameter-bank launches
 float4 cross_record_abs(const float4& r, float ox, float oy) {
   return make_float4(static_cast<float>(static_cast<double>(r.x) + ox),
                      static_cast<float>(static_cast<double>(r.y) + oy), r.z,
                      static_cast<float>(static_cast<double>(r.w) + ox));
 }
 
-// ---- small-polygon route (tri_small_kernel) ----
-using SmallLaunch = cudaError_t (*)(const DevTables&, const TestArgs*, cudaStream_t);
-
-template <int NC, int K, int MODE>
-cudaError_t launch_small(const DevTables& t, const TestArgs* a, cudaStream_t stream) {
-  constexpr int kWarpPts = 32 * kSmallP;
-  TriSmallParams<NC, K> prm{};
-  prm.ox = t.ox;
-  prm.oy = t.oy;
-  const int glo = MODE == 1 ? kGroupYlo : kGroupXlo;
-  for (int e = 0; e < 2; ++e)
-    for (int s = 0; s < 2; ++s) {
-      const float2* g = t.h_slab[e] + t.slab[e].off[glo + s];
-      const uint32_t c = t.slab[e].cnt[glo + s] / 2;
-      for (int i = 0; i < K; ++i)  // padded with copies of the first record
-        std::memcpy(&prm.slab[e][s][i], g + 2 * (i < (int)c ? i : 0), sizeof(float4));
-    }
-  for (int k = 0; k < NC; ++k) prm.cross[k] = cross_record_abs(t.h_cross[k], t.ox, t.oy);
-  auto kern = tri_small_kernel<NC, K, MODE>;
-  int sms = 0, per_sm = 0;
-  cudaError_t e = launch_config(reinterpret_cast<const void*>(kern), kThreads, 0, &sms, &per_sm);
-  if (e != cudaSuccess) return e;
-  const uint64_t full_slices = a[0].m / kWarpPts;
-  const uint64_t cap = (uint64_t)sms * per_sm;
-  const uint64_t want = (full_slices + kWarps - 1) / kWarps;
-  kern<<<(int)(want < cap ? want : cap), kThreads, 0, stream>>>(prm, a[0], a[1], a[2], full_slices);
-  return cudaGetLastError();
-}
-
-template <int NC, int MODE, int K = 1>
-SmallLaunch small_for_k(int k) {
-  if constexpr (K > small_kmax(NC)) return nullptr;
-  else return k == K ? launch_small<NC, K, MODE> : small_for_k<NC, MODE, K + 1>(k);
-}
-template <int MODE, int NC = 3>
-SmallLaunch small_for(int nc, int k) {
-  if constexpr (NC > kSmallMaxN) return nullptr;
-  else return nc == NC ? small_for_k<NC, MODE>(k) : small_for<MODE, NC + 1>(nc, k);
-}
-
-// the small kernel's launcher for these tables and this batch, or null
-SmallLaunch small_plan(const DevTables& t, const TestArgs* a) {
-  constexpr int kWarpPts = 32 * kSmallP;
-  if (!VPIPG_TRI_SMALL || !VPIPG_INLINE || !t.h_cross || !t.h_slab[0] || !t.h_slab[1] ||
-      t.cross.n < 3 || t.cross.n > (uint32_t)kSmallMaxN)
-    return nullptr;
-  const bool aligned =
-      ((reinterpret_cast<uintptr_t>(a[0].xs) | reinterpret_cast<uintptr_t>(a[0].ys)) & 15) == 0;
-  if (!aligned || a[0].m / kWarpPts < (uint64_t)kWarps) return nullptr;
-  for (int e = 0; e < 3; ++e)
-    if (a[e].bytes || (reinterpret_cast<uintptr_t>(a[e].words) & 15)) return nullptr;
-  auto form = [](const SlabTable& s) { return s.cnt[kGroupXlo] == 0 ? 1 : s.cnt[kGroupYlo] == 0 ? 2 : 0; };
-  const int mode = form(t.slab[0]);
-  if (mode == 0 || form(t.slab[1]) != mode) return nullptr;
-  const int glo = mode == 1 ? kGroupYlo : kGroupXlo;
-  uint32_t k = 0;
-  for (int e = 0; e < 2; ++e)
-    for (int s = 0; s < 2; ++s) {
-      const uint32_t c = t.slab[e].cnt[glo + s] / 2;
-      if (c == 0) return nullptr;
-      k = c > k ? c : k;
-    }
-  return mode == 1 ? small_for<1>((int)t.cross.n, (int)k) : small_for<2>((int)t.cross.n, (int)k);
-}
-
 bool test_f32_all_plan(const DevTables& t, const TestArgs* a, size_t* smem_out) {
-  if (small_plan(t, a)) {
+  if (test_f32_small_plan(t, a)) {
     if (smem_out) *smem_out = 0;
     return true;
   }
@@ -1156,7 +773,8 @@ cudaError_t launch_test_f32_all(const DevTables& t, const TestArgs* a, cudaStrea
   using TriV = SlabEngine<kTriP, false>;
   using TriO = SlabEngine<kTriP, true>;
   constexpr int kWarpPts = 32 * kTriP;
-  if (const SmallLaunch small = small_plan(t, a)) return small(t, a, stream);
+  const cudaError_t es = launch_test_f32_small(t, a, stream);
+  if (es != cudaErrorNotSupported) return es;
   if (!test_f32_all_plan(t, a, nullptr)) return cudaErrorNotSupported;
   TriParams prm{};
   prm.v = TriV::Params{t.slab[0], t.ox, t.oy};

@@ -119,6 +119,11 @@ cudaError_t launch_test_f32_all(const DevTables& t, const TestArgs* a, cudaStrea
 cudaError_t launch_test_f64_all(const DevTables& t, const TestArgs* a, cudaStream_t stream);
 // whether launch_test_f32_all takes this batch as one fused launch
 bool test_f32_all_plan(const DevTables& t, const TestArgs* a, size_t* smem);
+// the small-polygon fused kernel (tri_small.cu): at most 8 crossing vertices,
+// single-section slab tables of one form, 16-byte aligned points and word
+// outputs, no byte outputs; cudaErrorNotSupported otherwise
+bool test_f32_small_plan(const DevTables& t, const TestArgs* a);
+cudaError_t launch_test_f32_small(const DevTables& t, const TestArgs* a, cudaStream_t stream);
 cudaError_t launch_test_f64(const DevTables& t, int engine, const TestArgs& a, cudaStream_t stream);
 // ---- validation (validate.cu): run_validation (bench.cpp:279-308) on the device ----
 constexpr int kReportSamples = 100;

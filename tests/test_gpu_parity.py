@@ -887,14 +887,13 @@ def test_first_use_of_a_fresh_handle_from_many_threads():
                 assert torch.equal(w, want[i % 3]), (rep, i)
 
 
-@pytest.mark.parametrize("n", [3, 4, 5, 6, 7, 8])
+@pytest.mark.parametrize("n", [3, 4, 5, 6, 7, 8, 10, 11, 12])
 @pytest.mark.parametrize("form", ["y_only", "x_only", "far"])
 @pytest.mark.parametrize("m", [(1 << 20) + 77, 1 << 22])
 def test_small_polygon_fused_route(orc, n, form, m):
-    """Polygons of at most 8 vertices whose slab tables have one section take
-    the straight-line small-polygon kernel (test_f32.cu tri_small_kernel: edge
-    count and padded group size compile-time, tables as constant-bank
-    operands). Its words and counts equal the three per-engine kernels' bit
+    """Polygons of at most 12 vertices whose slab tables have one section take
+    the straight-line small-polygon kernel (tri_small.cu: edge count and
+    padded group size compile-time, tables as constant-bank operands). Its words and counts equal the three per-engine kernels' bit
     for bit -- y-only and x-only tables (an exactly vertical edge forces the
     latter), the local-frame shift of a polygon far from the origin, and a
     ragged tail -- and every engine equals the oracle outside the band."""
