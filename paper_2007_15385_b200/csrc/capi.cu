@@ -561,7 +561,7 @@ int vpipg_prepare_csr(const uint32_t* offsets, const double* vx, const double* v
   for (uint32_t i = 0; i < npoly; ++i) {
     rec[i] = static_cast<uint32_t>(units);
     const uint64_t nn = offsets[i + 1] - offsets[i];
-    const uint64_t u = 1 + 3 * std::max<uint64_t>(1, (nn + 7) / 8);  // header, 8-edge groups
+    const uint64_t u = 1 + std::max<uint64_t>(2, (nn + 3) / 4);  // header, >= two 4-row chunks
     units += u;
     umax = std::max(umax, u);
   }

@@ -17,14 +17,15 @@
 //   their polygon. For the edge v_j -> v_i of consecutive rows:
 //     Voronoi    outer generator g = p0' - f n (the mirror of the centroid
 //                across the edge line with normal n, reflect_generator's Eq. 8;
-//                prep stores the scalar f per edge, n comes from the two rows),
+//                f and n formed in registers from the two rows and p0'),
 //                inside iff |q'-g|^2 >= |q'-p0'|^2 for every edge
 //                (engines.cpp:85-98, ties inside)
-//     offset     s = (q - v_j) x (q - v_i) >= 0 in the validated (CCW) order,
-//                i.e. s <= 0 on raw rows that validation reversed
+//     offset     s = (q - v_j) x (q - v_i) >= 0 in the validated (CCW) order
 //                (engines.cpp:150-152)
 //     crossing   in_range = H_i ^ H_j, on_left = sign(s) ^ H_i (H = [v.y > qy]),
-//                parity by XOR (engines.cpp:187-196), on the raw order
+//                parity by XOR (engines.cpp:187-196); the rows are stored in
+//                the validated order, the reverse of a clockwise raw polygon,
+//                which leaves the crossing parity unchanged
 #include <climits>
 #include <cmath>
 #include <cstdint>
@@ -73,12 +74,6 @@ __global__ void prep_csr_kernel(CsrPrepArgs a) {
   // validated (CCW) order = the raw rows read backwards when reversed
   auto val = [&](int k) { return raw(rev ? n - 1 - k : k); };
   float2 p0 = make_float2(0.f, 0.f);
-  // record body: groups of 8 edges, group g at slot 4 + 12 g: its 8 rows, then
-  // its 8 f values (vpipg_internal.h)
-  auto row = [&](int k) -> float2& { return r[4 + 12 * (k >> 3) + (k & 7)]; };
-  auto fval = [&](int k) -> float& {
-    return reinterpret_cast<float*>(r + 12 + 12 * (k >> 3))[k & 7];
-  };
   if (status == 0 && (a.kinds & kKindVoronoi)) {
     double px, py;
     centroid_exact(val, n, &px, &py);
@@ -88,18 +83,6 @@ __global__ void prep_csr_kernel(CsrPrepArgs a) {
       double2 g;
       status = reflect_exact(val(k), val((k + 1) % n), px, py, &g);
       if (status == 0) a.outer[s + k] = g;
-    }
-    // the outer generator of raw edge v_{k-1} -> v_k as g = p0 - f_k n_k with
-    // n_k = (v_{k-1}.y - v_k.y, v_k.x - v_{k-1}.x) from the f32 rows the
-    // kernels read: f_k = -(g - p0).n_k / |n_k|^2 (g - p0 is parallel to n_k;
-    // the rows' rounding only turns it by < 1e-7 rad)
-    for (int k = 0; k < n && status == 0; ++k) {
-      const float2 vj = local(raw((k + n - 1) % n), cx, cy), vi = local(raw(k), cx, cy);
-      const double nx = static_cast<double>(vj.y) - vi.y, ny = static_cast<double>(vi.x) - vj.x;
-      const int vk = rev ? n - 1 - k : (k + n - 1) % n;  // the validated edge this raw edge is
-      const double2 g = a.outer[s + vk];
-      const double dd = nx * nx + ny * ny;
-      fval(k) = dd > 0.0 ? static_cast<float>(-((g.x - px) * nx + (g.y - py) * ny) / dd) : 0.f;
     }
   }
   a.status[i] = status;
@@ -111,8 +94,13 @@ __global__ void prep_csr_kernel(CsrPrepArgs a) {
   r[1] = make_float2(fcx, fcy);
   r[2] = p0;
   if (n > 0) {
-    r[3] = local(raw(n - 1), cx, cy);
-    for (int k = 0; k < n; ++k) row(k) = local(raw(k), cx, cy);
+    // the rows in the validated order (the crossing parity does not depend
+    // on the direction of travel), padded to whole 4-row chunks with copies
+    // of the last row: a repeated row is an empty edge every engine ignores
+    const float2 last = local(val(n - 1), cx, cy);
+    r[3] = last;
+    for (int k = 0; k < n; ++k) r[4 + k] = local(val(k), cx, cy);
+    for (int k = n; k < 4 * ((n + 3) / 4); ++k) r[4 + k] = last;
   }
 }
 
@@ -123,7 +111,7 @@ __global__ void prep_csr_kernel(CsrPrepArgs a) {
 #define VPIPG_GSTREAM_AHEAD 1
 #endif
 #ifndef VPIPG_GMINB_ALL
-#define VPIPG_GMINB_ALL 4
+#define VPIPG_GMINB_ALL 5
 #endif
 constexpr int kGThreads = 256;
 
@@ -143,48 +131,74 @@ __device__ __forceinline__ Rows4 ld256(const float2* p) {
 }
 
 
+// MUFU.RCP (about 1 ulp): the generator it places is off by ~1e-7 of the
+// polygon's extent, far inside the band
+__device__ __forceinline__ float rcp_approx(float x) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+
+// three-input minimum (FMNMX3; NaN operands are ignored)
+__device__ __forceinline__ float min3(float a, float b, float c) {
+  float r;
+  asm("min.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+  return r;
+}
+
 // The three engines' state for one pair over one polygon's edges.
 template <bool kV, bool kO, bool kC>
 struct PairAcc {
   float qx, qy;       // q' (local frame)
   float qpx, qpy;     // q' - p0' (p0' the inner generator)
   float d0;           // |q' - p0'|^2
+  float tgx, tgy;     // 2 p0'
   float pa, pb;       // q' - v_j of the previous row
-  float px, py;       // v_j' itself (the Voronoi edge normal)
-  uint32_t vor = 0;   // sign bits of |q'-g|^2 - |q'-p0'|^2 (any set: outside)
-  uint32_t off = 0;   // sign bits of the oriented cross products (any set: outside)
+  float px, py;       // v_j' itself
+  // running minima of |q'-g|^2 - |q'-p0'|^2 and of the cross products over
+  // the edges so far (negative: outside), two edges per three-input min (it
+  // issues like one LOP3 per two edges instead of one per edge)
+  float vor = INFINITY, off = INFINITY;
   uint32_t par = 0;   // crossing parity (bit 31)
-  uint32_t flip = 0;  // 0x80000000 when the raw rows run clockwise
 
   __device__ __forceinline__ void start(float x, float y, float cx, float cy, float gx, float gy,
-                                        float lx, float ly, uint32_t rev) {
+                                        float lx, float ly) {
     qx = x - cx;  // exact for points near their polygon (Sterbenz)
     qy = y - cy;
     if (kV) {
       qpx = qx - gx;
       qpy = qy - gy;
       d0 = fmaf(qpx, qpx, qpy * qpy);
+      tgx = gx + gx;
+      tgy = gy + gy;
     }
     pa = qx - lx;
     pb = qy - ly;
     px = lx;
     py = ly;
-    flip = rev ? 0x80000000u : 0u;
   }
-  // edge v_j -> v_i with v_j the previous row, v_i = (rx, ry) and f the
-  // edge's generator coefficient (the outer generator g = p0' - f n)
-  __device__ __forceinline__ void edge(float rx, float ry, float f) {
+  // edge v_j -> v_i, v_j the previous row and v_i = (rx, ry), in the validated
+  // (counter-clockwise) order. A repeated row (the chunk padding) is an empty
+  // edge: n = 0 gives f = 0 and g = p0', s = +0, no crossing.
+  __device__ __forceinline__ void edge(float rx, float ry, float& dv, float& s) {
     const float a = qx - rx, b = qy - ry;
+    dv = INFINITY;
+    s = 0.f;
     if (kV) {
-      // n = (v_j.y - v_i.y, v_i.x - v_j.x), the edge line's normal
-      // (edge_coefficients, voronoi.cpp:23-31); q' - g = (q' - p0') + f n
+      // the outer generator g = p0' - f n, the mirror of p0' across the edge
+      // line (reflect_generator, voronoi.cpp:46-58) with n = (v_j.y - v_i.y,
+      // v_i.x - v_j.x) (edge_coefficients, voronoi.cpp:23-31) and
+      // f = 2 (p0' - v_j).n / |n|^2, formed in registers from the two rows
       const float nx = py - ry, ny = rx - px;
-      const float ex = fmaf(f, nx, qpx), ey = fmaf(f, ny, qpy);
-      vor |= __float_as_uint(fmaf(ex, ex, ey * ey) - d0);  // |q'-g|^2 - |q'-p0'|^2
+      const float dx = fmaf(-2.f, px, tgx), dy = fmaf(-2.f, py, tgy);  // 2 (p0' - v_j)
+      const float nn = fmaf(nx, nx, fmaf(ny, ny, 1e-30f));
+      const float f = fmaf(dx, nx, dy * ny) * rcp_approx(nn);
+      const float ex = fmaf(f, nx, qpx), ey = fmaf(f, ny, qpy);  // q' - g = (q' - p0') + f n
+      dv = fmaf(ex, ex, ey * ey) - d0;  // |q'-g|^2 - |q'-p0'|^2
     }
     if (kO || kC) {
-      const float s = fmaf(pa, b, -(a * pb));  // (q - v_j) x (q - v_i)
-      if (kO) off |= __float_as_uint(s) ^ flip;
+      // (q - v_j) x (q - v_i), exactly +0 for v_i = v_j (no contraction)
+      s = __fsub_rn(__fmul_rn(pa, b), __fmul_rn(a, pb));
       if (kC) {
         const uint32_t hi = __float_as_uint(b), hj = __float_as_uint(pb);
         par ^= (hi ^ hj) & (__float_as_uint(s) ^ hi);
@@ -194,6 +208,16 @@ struct PairAcc {
     pb = b;
     px = rx;
     py = ry;
+  }
+  __device__ __forceinline__ void chunk(const Rows4& c) {
+#pragma unroll
+    for (int u = 0; u < 4; u += 2) {
+      float v0, s0, v1, s1;
+      edge(c.v[2 * u], c.v[2 * u + 1], v0, s0);
+      edge(c.v[2 * u + 2], c.v[2 * u + 3], v1, s1);
+      if (kV) vor = min3(vor, v0, v1);
+      if (kO) off = min3(off, s0, s1);
+    }
   }
 };
 
@@ -207,38 +231,27 @@ __device__ __forceinline__ void test_pair(const DbTables& t, bool ok, uint32_t i
   // are uniform enough; per-polygon offsets otherwise (one dependent load more)
   const uint64_t unit = t.stride ? (uint64_t)id * t.stride : (uint64_t)(ok ? __ldg(t.rec + id) : 0u);
   const float2* r = t.recs + 4 * (ok ? unit : 0u);
-  const Rows4 h = ld256(r);
+  // the header and the first two 4-row chunks in one round trip (their
+  // addresses do not depend on n; every record holds at least two chunks),
+  // later chunks two at a time once n is known
+  const Rows4 h = ld256(r), c0 = ld256(r + 4), c1 = ld256(r + 8);
   const uint32_t nf = __float_as_uint(h.v[0]);
   const uint32_t n = ok ? nf & kNMask : 0u;
   PairAcc<kV, kO, kC> acc;
-  acc.start(x, y, h.v[2], h.v[3], h.v[4], h.v[5], h.v[6], h.v[7], nf & kReversed);
-  // group 0 (edges 0..7) is read together with the header -- its address does
-  // not depend on n -- and later groups after it, three 32-byte loads each
-  auto group = [&](uint32_t g, const Rows4& h0, const Rows4& h1, const Rows4& f) {
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      if (8 * g + u < n) {
-        const Rows4& q = u < 4 ? h0 : h1;
-        acc.edge(q.v[2 * (u & 3)], q.v[2 * (u & 3) + 1], kV ? f.v[u] : 0.f);
-      }
-    }
-  };
-  {
-    const Rows4 r0 = ld256(r + 4), r1 = ld256(r + 8);
-    const Rows4 f0 = kV ? ld256(r + 12) : Rows4{};
-    group(0, r0, r1, f0);
-  }
-  for (uint32_t g = 1; 8 * g < n; ++g) {
-    const float2* b = r + 4 + 12 * g;
-    // the second row chunk only when the group has more than 4 edges
-    const Rows4 r0 = ld256(b), r1 = 8 * g + 4 < n ? ld256(b + 4) : Rows4{};
-    const Rows4 f0 = kV ? ld256(b + 8) : Rows4{};
-    group(g, r0, r1, f0);
+  acc.start(x, y, h.v[2], h.v[3], h.v[4], h.v[5], h.v[6], h.v[7]);
+  acc.chunk(c0);
+  if (n > 4) acc.chunk(c1);
+  for (uint32_t c = 2; 4 * c < n; c += 2) {
+    const Rows4 ca = ld256(r + 4 + 4 * c);
+    const bool two = 4 * c + 4 < n;
+    const Rows4 cb = two ? ld256(r + 8 + 4 * c) : Rows4{};
+    acc.chunk(ca);
+    if (two) acc.chunk(cb);
   }
   const bool convex_ok = n > 0 && !(nf & kRangeInvalid);
   const bool nan = acc.qx != acc.qx || acc.qy != acc.qy;
-  in[0] = kV && convex_ok && !nan && !(acc.vor >> 31);
-  in[1] = kO && convex_ok && (nan || !(acc.off >> 31));
+  in[0] = kV && convex_ok && !nan && !(acc.vor < 0.f);
+  in[1] = kO && convex_ok && (nan || !(acc.off < 0.f));
   in[2] = kC && n > 0 && (acc.par >> 31);
 }
 

@@ -62,16 +62,16 @@ constexpr uint32_t kNMask = 0x3fffffffu;
 //   slot 1   frame origin c (f32 centre of the bounding box)
 //   slot 2   p0' = centroid - c (f32; the Voronoi inner generator)
 //   slot 3   v_{n-1}' (closes the ring)
-//   then groups of 8 edges, group g at slot 4 + 12 g: the rows v_{8g}' ..
-//   v_{8g+7}' (the RAW vertices relative to c, 64 bytes) and 8 floats f_k (32
-//   bytes): the outer generator of raw edge v_{k-1} -> v_k is p0' - f_k n_k,
-//   n_k the edge's normal; group 0 is present (and read) for every polygon
-// so a pair reads one header (the first 32-byte load brings slots 0-3) and one
-// walk of n rows for all three engines: crossing on the raw order
-// (vpip.cpp:120-128), sign-of-offset on the same rows with the orientation
-// taken from kReversed (the validated order is their reverse), Voronoi with
-// each outer generator rebuilt from its edge's rows and f_k (4 bytes per edge
-// instead of an 8-byte generator row).
+//   slot 4 + k  the row v_k' (f32, relative to c) in the VALIDATED
+//            (counter-clockwise) order, padded with copies of v_{n-1}' to
+//            whole 4-row (32-byte) chunks, at least two chunks per record
+// so a pair reads one header and one walk of n rows for all three engines:
+// sign-of-offset and Voronoi in the validated order the reference tests them
+// in, the crossing on the same rows (for a clockwise raw polygon that is the
+// raw ring travelled backwards, which leaves the crossing parity unchanged),
+// Voronoi with each outer generator rebuilt in registers from its edge's two
+// rows and p0' (12.125 bytes of stream and ~4.3 32-byte sectors of record per
+// C4 pair).
 struct CsrPrepArgs {
   const uint32_t* offsets;  // npoly + 1 (input CSR)
   const double* vx;         // raw vertices (device)
