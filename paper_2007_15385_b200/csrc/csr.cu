@@ -256,8 +256,10 @@ __device__ __forceinline__ void test_pair(const DbTables& t, bool ok, uint32_t i
 }
 
 // kMask: bit e = engine e (Voronoi, offset, crossing) of this launch; a[e]
-// its outputs (all share xs, ys, ids, m)
-template <int kMask>
+// its outputs (all share xs, ys, ids, m). kBytes: some engine wants a byte
+// mask (decided per launch, so the common words-only launch carries no byte
+// stores or their address arithmetic).
+template <int kMask, bool kBytes>
 __global__ void __launch_bounds__(kGThreads, kMask == 7 ? VPIPG_GMINB_ALL : VPIPG_GMINB)
     gather_kernel(const DbTables t, const GatherArgs av, const GatherArgs ao, const GatherArgs ac) {
   constexpr bool kV = kMask & 1, kO = kMask & 2, kC = kMask & 4;
@@ -265,6 +267,8 @@ __global__ void __launch_bounds__(kGThreads, kMask == 7 ? VPIPG_GMINB_ALL : VPIP
   const int lane = threadIdx.x & 31;
   const uint64_t gwarp = (uint64_t)blockIdx.x * (kGThreads / 32) + (threadIdx.x >> 5);
   const uint64_t stride = (uint64_t)gridDim.x * (kGThreads / 32) * 32;
+  // warp-wide inside counts: every lane adds the popcount of the (uniform)
+  // ballot word, lane 0 flushes
   uint32_t cnt[3] = {0, 0, 0};
   // the next pair's stream words are loaded one iteration ahead
   auto load = [&](uint64_t j, uint32_t& id, float& x, float& y) {
@@ -292,19 +296,16 @@ __global__ void __launch_bounds__(kGThreads, kMask == 7 ? VPIPG_GMINB_ALL : VPIP
       if (!(kMask & (1 << e))) continue;
       const GatherArgs& a = *args[e];
       const uint32_t w = __ballot_sync(0xffffffffu, in[e]);
-      cnt[e] += in[e];
+      cnt[e] += __popc(w);
       if (a.words && lane == 0) a.words[base >> 5] = w;
-      if (a.bytes && j < a.m) a.bytes[j] = in[e] ? 1 : 0;
+      if (kBytes && a.bytes && j < a.m) a.bytes[j] = in[e] ? 1 : 0;
     }
   }
   const GatherArgs* args[3] = {&av, &ao, &ac};
 #pragma unroll
   for (int e = 0; e < 3; ++e) {
     if (!(kMask & (1 << e))) continue;
-    uint32_t c = cnt[e];
-#pragma unroll
-    for (int s = 16; s > 0; s >>= 1) c += __shfl_xor_sync(0xffffffffu, c, s);
-    if (lane == 0 && args[e]->inside && c) atomicAdd(args[e]->inside, (unsigned long long)c);
+    if (lane == 0 && args[e]->inside && cnt[e]) atomicAdd(args[e]->inside, (unsigned long long)cnt[e]);
   }
 }
 
@@ -344,7 +345,8 @@ template <int kMask>
 cudaError_t launch_gather_mask(const DbTables& t, const GatherArgs& av, const GatherArgs& ao,
                                const GatherArgs& ac, uint64_t m, cudaStream_t stream) {
   int sms = 0, per_sm = 0;
-  auto k = gather_kernel<kMask>;
+  const bool bytes = ((kMask & 1) && av.bytes) || ((kMask & 2) && ao.bytes) || ((kMask & 4) && ac.bytes);
+  auto k = bytes ? gather_kernel<kMask, true> : gather_kernel<kMask, false>;
   const cudaError_t e = launch_config(reinterpret_cast<const void*>(k), kGThreads, 0, &sms, &per_sm);
   if (e != cudaSuccess) return e;
   const uint64_t warps = (m + 31) / 32;

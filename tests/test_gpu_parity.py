@@ -893,10 +893,12 @@ def test_first_use_of_a_fresh_handle_from_many_threads():
 def test_small_polygon_fused_route(orc, n, form, m):
     """Polygons of at most 12 vertices whose slab tables have one section take
     the straight-line small-polygon kernel (tri_small.cu: edge count and
-    padded group size compile-time, tables as constant-bank operands). Its words and counts equal the three per-engine kernels' bit
-    for bit -- y-only and x-only tables (an exactly vertical edge forces the
-    latter), the local-frame shift of a polygon far from the origin, and a
-    ragged tail -- and every engine equals the oracle outside the band."""
+    padded group size compile-time, tables as constant-bank operands). Its
+    words and counts equal the three per-engine kernels' bit for bit --
+    y-only and x-only tables (an exactly vertical edge forces the latter),
+    the local-frame shift of a polygon far from the origin, a ragged tail and
+    non-finite coordinates -- and every engine equals the oracle outside the
+    band."""
     rng = np.random.default_rng(4000 + 10 * n + len(form))
     t = np.sort(rng.uniform(0.0, 2.0 * np.pi, n)) + np.linspace(0.0, 0.5 / n, n)
     vx, vy = np.cos(t), np.sin(t)
@@ -911,6 +913,12 @@ def test_small_polygon_fused_route(orc, n, form, m):
         assert _offset_table_mode(vx, vy) != 0
     xs = (cx + rng.uniform(-1.3, 1.3, m)).astype(np.float32)
     ys = (cy + rng.uniform(-1.3, 1.3, m)).astype(np.float32)
+    # non-finite coordinates past the oracle prefix: the engines' NaN / inf
+    # rules must come out of the small kernel exactly as from the per-engine ones
+    bad = rng.choice(np.arange(1 << 18, m), 97, replace=False)
+    xs[bad[0::3]] = np.nan
+    ys[bad[1::3]] = np.inf
+    xs[bad[2::3]] = -np.inf
     nw = (m + 31) // 32
     xt, yt = torch.as_tensor(xs, device=DEV), torch.as_tensor(ys, device=DEV)
     with vp.PreparedPolygon.prepare(vx, vy, vp.KIND_ALL) as p:
