@@ -150,8 +150,7 @@ __device__ __forceinline__ float min3(float a, float b, float c) {
 template <bool kV, bool kO, bool kC>
 struct PairAcc {
   float qx, qy;       // q' (local frame)
-  float qpx, qpy;     // q' - p0' (p0' the inner generator)
-  float d0;           // |q' - p0'|^2
+  float qpx, qpy;     // 2 (q' - p0') (p0' the inner generator)
   float tgx, tgy;     // 2 p0'
   float pa, pb;       // q' - v_j of the previous row
   float px, py;       // v_j' itself
@@ -166,9 +165,8 @@ struct PairAcc {
     qx = x - cx;  // exact for points near their polygon (Sterbenz)
     qy = y - cy;
     if (kV) {
-      qpx = qx - gx;
-      qpy = qy - gy;
-      d0 = fmaf(qpx, qpx, qpy * qpy);
+      qpx = 2.f * (qx - gx);
+      qpy = 2.f * (qy - gy);
       tgx = gx + gx;
       tgy = gy + gy;
     }
@@ -193,8 +191,9 @@ struct PairAcc {
       const float dx = fmaf(-2.f, px, tgx), dy = fmaf(-2.f, py, tgy);  // 2 (p0' - v_j)
       const float nn = fmaf(nx, nx, fmaf(ny, ny, 1e-30f));
       const float f = fmaf(dx, nx, dy * ny) * rcp_approx(nn);
-      const float ex = fmaf(f, nx, qpx), ey = fmaf(f, ny, qpy);  // q' - g = (q' - p0') + f n
-      dv = fmaf(ex, ex, ey * ey) - d0;  // |q'-g|^2 - |q'-p0'|^2
+      // |q'-g|^2 - |q'-p0'|^2 = |(q'-p0') + f n|^2 - |q'-p0'|^2
+      //                      = f (f |n|^2 + 2 (q'-p0').n), expanded (no cancellation)
+      dv = f * fmaf(f, nn, fmaf(qpx, nx, qpy * ny));
     }
     if (kO || kC) {
       // (q - v_j) x (q - v_i), exactly +0 for v_i = v_j (no contraction)
