@@ -56,12 +56,10 @@ ISSUE_CYCLES_PER_PE = {"voronoi": 2.0, "sign_of_offset": 2.0, "ray_crossing": 5.
 # the exact f64 kernels (test_f64.cu): the reference's own operation sequence
 # on the FP64 pipe (16 lanes per SMSP: every DADD / DMUL / DSETP holds it 2
 # cycles): Voronoi 3 DADD + 2 DMUL + DSETP, offset 2 DMUL + DADD + DSETP,
-# crossing 2 DMUL + DADD + 3 DSETP (in range, lhs > rhs, lhs == rhs; the
-# on-segment box only on a tie) -- the FP64-pipe bound, not counting the
-# predicate / integer logic around it
-# (ncu, profiles/ncu_full_r02_c5f64.json: 17.44 DADD / DMUL / DSETP per
-# point-edge over the three engines, crossing's share 7.44 with its tie test)
-ISSUE_CYCLES_PER_PE_F64 = {"voronoi": 12.0, "sign_of_offset": 8.0, "ray_crossing": 14.9}
+# crossing 2 DMUL + DADD + 4 DSETP (u.y > qy, w.y > qy, on_left, lhs == rhs;
+# the on-segment box only on a tie) -- the FP64-pipe bound, not counting the
+# predicate / integer logic around it (ncu, profiles/ncu_full_r02_c5f64.json)
+ISSUE_CYCLES_PER_PE_F64 = {"voronoi": 12.0, "sign_of_offset": 8.0, "ray_crossing": 14.0}
 HBM_FALLBACK_GBS = 6650.0
 # FFMA lane-ops per SM per clock on sm_100a (tools/pipe_peaks.cu: 3.79 warp-inst/clk/SM)
 FFMA_PER_SM_CLK = 128
@@ -899,7 +897,7 @@ def main():
                                    "of this kernel on this workload, scaled to this launch)",
                  "issue_model_frac": dk.get("issue_model_frac"),
                  "issue_model": ("FP64-pipe cycles per point-edge (2 per DADD / DMUL / DSETP): "
-                                 "Voronoi 12, offset 8, crossing 14.9 "
+                                 "Voronoi 12, offset 8, crossing 14 "
                                  "(profiles/ncu_full_r02_c5f64.json)" if f64 else
                                  "dispatch cycles per point-edge: slab 2 (FFMA + FMNMX3/2), "
                                  "crossing 5.5 (1.5 FADD + FFMA + 1.5 LOP3, paired anchoring); the "

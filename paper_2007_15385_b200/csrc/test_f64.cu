@@ -11,6 +11,7 @@
 //   ray_kernel     (engines.cpp:165-204): parity | on-segment latch
 // Same warp-tile / ballot / fused-count structure as test_f32.cu.
 #include <cstdint>
+#include <type_traits>
 
 #include "vpipg_device.cuh"
 #include "vpipg_internal.h"
@@ -28,6 +29,23 @@ constexpr int kWarps = kThreads / 32;
 __device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
 __device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
 __device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a, b); }
+
+// The offset engine's per-point step as explicit PTX, so the comparison
+// feeds a predicated increment (one ALU op) instead of an add and a select.
+// The arithmetic is the reference's, individually rounded.
+//
+// offset (engines.cpp:150-153): flags += (qy*dvx - qx*dvy < rhs)
+__device__ __forceinline__ void offset_step(double x, double y, double dvx, double dvy, double rhs,
+                                            uint32_t& flags) {
+  asm("{\n\t.reg .pred c;\n\t.reg .f64 t0, t1;\n\t"
+      "mul.rn.f64 t0, %2, %3;\n\t"
+      "mul.rn.f64 t1, %1, %4;\n\t"
+      "sub.rn.f64 t0, t0, t1;\n\t"
+      "setp.lt.f64 c, t0, %5;\n\t"
+      "@c add.u32 %0, %0, 1;\n\t}"
+      : "+r"(flags)
+      : "d"(x), "d"(y), "d"(dvx), "d"(dvy), "d"(rhs));
+}
 
 template <int P>
 __device__ __forceinline__ uint32_t emit_words(const bool (&in)[P], uint64_t base, uint64_t m,
@@ -59,7 +77,10 @@ __device__ __forceinline__ void flush_count(uint32_t cnt, const TestArgs& a) {
 
 // One engine's test of P points per lane against its per-edge records
 // (`tab`: shared or global memory), exactly as the reference computes it.
-template <int kEngine, int P>
+// kPtxStep: the offset engine's step as explicit PTX (offset_step) -- 8 %
+// faster in the per-engine kernel, 4 % slower inside the fused kernel (C5
+// in f64), so only the per-engine kernel takes it
+template <int kEngine, int P, bool kPtxStep = false>
 __device__ __forceinline__ void exact_eval(uint32_t n, double inner_x, double inner_y,
                                            const void* tab, const double (&x)[P],
                                            const double (&y)[P], bool (&in)[P]) {
@@ -90,51 +111,64 @@ __device__ __forceinline__ void exact_eval(uint32_t n, double inner_x, double in
       const OffsetEdgeF64 r = s[e];
 #pragma unroll
       for (int p = 0; p < P; ++p) {
-        const double lhs = dsub(dmul(y[p], r.dvx), dmul(x[p], r.dvy));
-        flags[p] += lhs < r.rhs;
+        if constexpr (kPtxStep) {
+          offset_step(x[p], y[p], r.dvx, r.dvy, r.rhs, flags[p]);
+        } else {
+          const double lhs = dsub(dmul(y[p], r.dvx), dmul(x[p], r.dvy));
+          flags[p] += lhs < r.rhs;
+        }
       }
     }
 #pragma unroll
     for (int p = 0; p < P; ++p) in[p] = (flags[p] == 0u) | (flags[p] == n);
   } else {
-    // The same comparisons with the same operands as ray_kernel, fewer issued:
-    //  - (w.y > qy) of edge e is (u.y > qy) of edge e-1 (record e's wy is
-    //    record e-1's uy, the same vertex): carried, one DSETP per edge;
-    //  - lhs != rhs is !(lhs == rhs) (IEEE, NaN included): one DSETP less;
-    //  - the on-segment box (four DSETP) is evaluated only when some point of
-    //    the warp lies exactly on the edge line (lhs == rhs), i.e. almost never.
+    // The reference's comparisons with the same operands (ray_kernel), laid
+    // out so every per-point boolean is a short-lived predicate (P = 4
+    // points would otherwise carry more predicates than the SM has, and the
+    // compiler round-trips them through registers: ~9 SEL / ISETP / LOP3 per
+    // point-edge):
+    //  - (u.y > qy) and (w.y > qy) both evaluated per edge, as the reference
+    //    does, instead of carrying the vertex's bit from the previous edge;
+    //  - on_left = (lhs != rhs) & ((lhs > rhs) == going_up) is `lhs > rhs`
+    //    for an upward edge and `!(lhs >= rhs)` for a downward one (NaN
+    //    included); going_up is uniform, so one comparison per point;
+    //  - lhs == rhs only feeds a warp-wide flag; the on-segment box runs (with
+    //    lhs recomputed) only when some point of the warp lies exactly on the
+    //    edge line, i.e. almost never;
+    //  - the parity is an integer toggled under the crossing predicate.
     const RayEdgeF64* s = static_cast<const RayEdgeF64*>(tab);
-    bool parity[P], on_edge[P], above[P];
+    uint32_t parity[P], on_edge[P];
 #pragma unroll
     for (int p = 0; p < P; ++p) {
-      parity[p] = false;
-      on_edge[p] = false;
-      above[p] = n > 0 && s[n - 1].uy > y[p];
+      parity[p] = 0;
+      on_edge[p] = 0;
     }
     for (uint32_t e = 0; e < n; ++e) {
       const RayEdgeF64 r = s[e];
-      bool eq[P];
       bool any_eq = false;
+      auto edge = [&](auto up) {
 #pragma unroll
-      for (int p = 0; p < P; ++p) {
-        const bool above_u = r.uy > y[p];
-        const bool in_range = above_u != above[p];
-        above[p] = above_u;
-        const double lhs = dsub(dmul(y[p], r.dvx), dmul(x[p], r.dvy));
-        eq[p] = lhs == r.rhs;
-        const bool on_left = !eq[p] & ((lhs > r.rhs) == (r.going_up != 0));
-        parity[p] ^= in_range & on_left;
-        any_eq |= eq[p];
-      }
+        for (int p = 0; p < P; ++p) {
+          const bool in_range = (r.uy > y[p]) != (r.wy > y[p]);
+          const double lhs = dsub(dmul(y[p], r.dvx), dmul(x[p], r.dvy));
+          const bool on_left = decltype(up)::value ? lhs > r.rhs : !(lhs >= r.rhs);
+          any_eq |= lhs == r.rhs;
+          if (in_range & on_left) parity[p] ^= 1u;
+        }
+      };
+      if (r.going_up) edge(std::true_type{});
+      else edge(std::false_type{});
       if (__builtin_expect(__any_sync(0xffffffffu, any_eq), 0)) {
 #pragma unroll
-        for (int p = 0; p < P; ++p)
-          on_edge[p] |= eq[p] & (x[p] >= r.min_x) & (x[p] <= r.max_x) & (y[p] >= r.min_y) &
-                        (y[p] <= r.max_y);
+        for (int p = 0; p < P; ++p) {
+          const double lhs = dsub(dmul(y[p], r.dvx), dmul(x[p], r.dvy));
+          on_edge[p] |= (lhs == r.rhs) & (x[p] >= r.min_x) & (x[p] <= r.max_x) &
+                        (y[p] >= r.min_y) & (y[p] <= r.max_y);
+        }
       }
     }
 #pragma unroll
-    for (int p = 0; p < P; ++p) in[p] = on_edge[p] | parity[p];
+    for (int p = 0; p < P; ++p) in[p] = (on_edge[p] | parity[p]) != 0u;
   }
 }
 
@@ -186,7 +220,7 @@ __global__ void __launch_bounds__(kThreads) exact_kernel(const DevTables t, cons
     double x[P], y[P];
     bool in[P];
     load_tile<P>(a, base, lane, x, y);
-    exact_eval<kEngine, P>(n, t.inner_x, t.inner_y, s_tab, x, y, in);
+    exact_eval<kEngine, P, true>(n, t.inner_x, t.inner_y, s_tab, x, y, in);
 #pragma unroll
     for (int p = 0; p < P; ++p) in[p] = in[p] & (base + 32u * p + lane < a.m);
     count += emit_words<P>(in, base, a.m, a, lane);

@@ -870,7 +870,8 @@ def test_first_use_of_a_fresh_handle_from_many_threads():
             def worker(i):
                 try:
                     s = torch.cuda.Stream()
-                    w = torch.zeros(m // 32, dtype=torch.int32, device=DEV)
+                    with torch.cuda.stream(s):  # the zero fill ordered before the test
+                        w = torch.zeros(m // 32, dtype=torch.int32, device=DEV)
                     p.test(i % 3, xs, ys, words=w, stream=s)
                     s.synchronize()
                     outs[i] = w
