@@ -23,7 +23,7 @@ namespace {
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
 #ifndef VPIPG_F64_P
-#define VPIPG_F64_P 4  // points per lane (4 measured best on C1)
+#define VPIPG_F64_P 8  // points per lane (C5 in f64: 8 -> 83.1 ms, 4 -> 84.9, 2 -> 94.7; C1 equal)
 #endif
 
 __device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
@@ -123,7 +123,7 @@ __device__ __forceinline__ void exact_eval(uint32_t n, double inner_x, double in
     for (int p = 0; p < P; ++p) in[p] = (flags[p] == 0u) | (flags[p] == n);
   } else {
     // The reference's comparisons with the same operands (ray_kernel), laid
-    // out so every per-point boolean is a short-lived predicate (P = 4
+    // out so every per-point boolean is a short-lived predicate (P = 4 or 8
     // points would otherwise carry more predicates than the SM has, and the
     // compiler round-trips them through registers: ~9 SEL / ISETP / LOP3 per
     // point-edge):
