@@ -132,12 +132,16 @@ int vpipg_test_multi(const vpipg_poly* poly, uint32_t engines, int dtype, const 
                      uint8_t* const* mask_bytes, unsigned long long* const* d_inside,
                      void* stream);
 
-/* 1 when vpipg_test_multi would run this batch as ONE fused launch: all three
- * engines and either float64 points (the exact kernels, any n) or float32
- * points in 16-byte-aligned buffers of at least one slice per warp with a
- * polygon of at most VPIPG_FUSE_MAX_N (96) edges whose tables fit the kernel
- * parameter bank or shared memory (above that the per-engine kernels are
- * faster); else 0. Pure query: no device work. */
+/* Nonzero when vpipg_test_multi would run this batch as ONE fused launch: all
+ * three engines and either float64 points (the exact kernels, any n) or
+ * float32 points in 16-byte-aligned buffers of at least one slice per warp
+ * with a polygon of at most VPIPG_FUSE_MAX_N (96) edges whose tables fit the
+ * kernel parameter bank or shared memory (above that the per-engine kernels
+ * are faster); else 0. The value names the kernel: 2 for the small-polygon
+ * kernel (float32, at most 12 vertices, single-section slab tables of one
+ * form, word outputs only), 1 for the general fused kernels -- the route
+ * depends on the outputs too, so the answer assumes 16-byte-aligned word
+ * outputs and no byte outputs. Pure query: no device work. */
 int vpipg_test_multi_fused(const vpipg_poly* poly, uint32_t engines, int dtype, const void* xs,
                            const void* ys, uint64_t m);
 

@@ -30,7 +30,7 @@ NVCC_FLAGS = ARCH + [
 CXX_FLAGS = ["-std=c++20", "-O2", "-fPIC", "-ffp-contract=off", "-Wall",
              f"-I{ROOT / 'include'}", f"-I{CSRC}", f"-I{CUDA_HOME / 'include'}"]
 
-CU_SOURCES = ["prep.cu", "test_f32.cu", "tri_small.cu", "test_f64.cu", "fill.cu", "csr.cu", "validate.cu", "capi.cu",
+CU_SOURCES = ["prep.cu", "test_f32.cu", "tri_small.cu", "tri_small_hi.cu", "test_f64.cu", "fill.cu", "csr.cu", "validate.cu", "capi.cu",
               "hostpipe.cu"]
 CXX_SOURCES = ["vpip_api.cpp", "comm.cpp"]
 

@@ -163,13 +163,18 @@ class PreparedPolygon:
 
     def multi_fused(self, xs, ys, engines=(0, 1, 2)) -> bool:
         """Whether test_multi runs this batch as one fused kernel (vpipg_test_multi_fused)."""
+        return self.multi_route(xs, ys, engines) != 0
+
+    def multi_route(self, xs, ys, engines=(0, 1, 2)) -> int:
+        """vpipg_test_multi_fused's answer: 0 one engine at a time, 1 a general
+        fused kernel, 2 the small-polygon kernel (word outputs only)."""
         import torch
         mask = 0
         for e in engines:
             mask |= 1 << _engine_id(e)
         dtype = F32 if xs.dtype == torch.float32 else F64
-        return bool(load().vpipg_test_multi_fused(self._h, mask, dtype, C.c_void_p(xs.data_ptr()),
-                                                  C.c_void_p(ys.data_ptr()), xs.numel()))
+        return int(load().vpipg_test_multi_fused(self._h, mask, dtype, C.c_void_p(xs.data_ptr()),
+                                                 C.c_void_p(ys.data_ptr()), xs.numel()))
 
     def test_multi(self, xs, ys, engines=(0, 1, 2), words=None, bytes_=None, counts=None,
                    stream=None) -> None:

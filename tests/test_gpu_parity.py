@@ -693,17 +693,25 @@ def test_multi_partial_engine_sets_f64_and_missing_outputs(golden):
 def test_multi_fused_plan():
     """vpipg_test_multi_fused reports the route vpipg_test_multi takes: one
     fused launch for all three engines on float32 batches of polygons with at
-    most 96 edges and on any float64 batch, per-engine kernels otherwise."""
+    most 96 edges (the small-polygon kernel, route 2, for single-section
+    polygons of at most 12 vertices) and on any float64 batch, per-engine
+    kernels otherwise."""
     m = 1 << 20
     xs = torch.zeros(m, dtype=torch.float32, device=DEV)
     ys = torch.zeros_like(xs)
     vx, vy = W.c5_polygon(vp.random_convex_polygon)  # 32 edges
     with vp.PreparedPolygon.prepare(vx, vy, vp.KIND_ALL) as p:
         assert p.multi_fused(xs, ys)
+        assert p.multi_route(xs, ys) == 1                 # 32 edges: the general fused kernel
         assert not p.multi_fused(xs, ys, (0, 2))
         assert p.multi_fused(xs.double(), ys.double())       # the exact f64 kernels fuse at any n
         assert not p.multi_fused(xs[:100], ys[:100])      # fewer slices than warps
         assert not p.multi_fused(xs[1:], ys[1:])          # not 16-byte aligned
+    _, (vx, vy) = W.c3_named("c3:3")
+    with vp.PreparedPolygon.prepare(vx, vy, vp.KIND_ALL) as p:
+        assert p.multi_route(xs, ys) == 2                 # triangle: the small-polygon kernel
+        assert p.multi_route(xs.double(), ys.double()) == 1  # f64: the exact fused kernel
+        assert p.multi_route(xs[:100], ys[:100]) == 0
     _, (vx, vy) = W.c3_named("c3x:128")
     with vp.PreparedPolygon.prepare(vx, vy, vp.KIND_ALL) as p:
         assert not p.multi_fused(xs, ys)                  # 128 edges: separate kernels are faster
@@ -923,7 +931,7 @@ def test_small_polygon_fused_route(orc, n, form, m):
     nw = (m + 31) // 32
     xt, yt = torch.as_tensor(xs, device=DEV), torch.as_tensor(ys, device=DEV)
     with vp.PreparedPolygon.prepare(vx, vy, vp.KIND_ALL) as p:
-        assert p.multi_fused(xt, yt)
+        assert p.multi_route(xt, yt) == 2  # the small-polygon kernel
         ref = []
         for e in range(3):
             w = torch.zeros(nw, dtype=torch.int32, device=DEV)
