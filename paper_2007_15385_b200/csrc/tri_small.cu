@@ -15,7 +15,7 @@ SmallLaunch small_for(int nc, int k) {
 
 // the small kernel's launcher for these tables and this batch, or null
 SmallLaunch small_plan(const DevTables& t, const TestArgs* a) {
-  constexpr int kWarpPts = 32 * kSmallP;
+  const uint64_t kWarpPts = 32u * small_p((int)t.cross.n);
   if (!VPIPG_TRI_SMALL || !VPIPG_INLINE || !t.h_cross || !t.h_slab[0] || !t.h_slab[1] ||
       t.cross.n < 3 || t.cross.n > (uint32_t)kSmallMaxN)
     return nullptr;

@@ -43,7 +43,14 @@ namespace {
 #ifndef VPIPG_TRI_SMALL
 #define VPIPG_TRI_SMALL 1
 #endif
-constexpr int kSmallP = VPIPG_TRI_SMALL_P;
+// points per lane per slice: 16 up to 8 vertices; 12 above (C2, n = 12 and
+// 2^24 points: 74 us against 77 at P = 16 and 76 at P = 8, whose unrolled
+// slices also stall less on instruction fetch; at 2^28 points P = 16 is
+// ~1 % faster for 10-12 vertices)
+#ifndef VPIPG_TRI_SMALL_P_HI
+#define VPIPG_TRI_SMALL_P_HI 12
+#endif
+constexpr int small_p(int nc) { return nc <= 8 ? VPIPG_TRI_SMALL_P : VPIPG_TRI_SMALL_P_HI; }
 constexpr int kSmallMaxN = 12;
 // padded slab group sizes K (records of two lines) instantiated per vertex
 // count: a single-section group of a convex NC-gon holds at most NC - 1
@@ -144,7 +151,7 @@ __device__ __forceinline__ void tri_small_slice(const TriSmallParams<NC, K>& prm
                                                 const TestArgs& ao, const TestArgs& ac,
                                                 uint64_t base, int lane, bool live, cnt_t& cv,
                                                 cnt_t& co, cnt_t& cc) {
-  constexpr int P = kSmallP;
+  constexpr int P = small_p(NC);
   const float* xs = static_cast<const float*>(av.xs) + base + lane;
   const float* ys = static_cast<const float*>(av.ys) + base + lane;
   float x[P], y[P];
@@ -181,7 +188,7 @@ template <int NC, int K, int MODE>
 __global__ void __launch_bounds__(kThreads, VPIPG_TRI_SMALL_MINB)
     tri_small_kernel(const __grid_constant__ TriSmallParams<NC, K> prm, const TestArgs av,
                      const TestArgs ao, const TestArgs ac, const uint64_t full_slices) {
-  constexpr int P = kSmallP;
+  constexpr int P = small_p(NC);
   constexpr int kWarpPts = 32 * P;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const SliceRounds sr(full_slices, warp);
@@ -219,7 +226,7 @@ __global__ void __launch_bounds__(kThreads, VPIPG_TRI_SMALL_MINB)
 
 template <int NC, int K, int MODE>
 cudaError_t launch_small(const DevTables& t, const TestArgs* a, cudaStream_t stream) {
-  constexpr int kWarpPts = 32 * kSmallP;
+  constexpr int kWarpPts = 32 * small_p(NC);
   TriSmallParams<NC, K> prm{};
   prm.ox = t.ox;
   prm.oy = t.oy;
