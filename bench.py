@@ -766,9 +766,13 @@ def main():
     sep_ms = None
     if fused:
         # per-engine breakdown: K eager steps of the three separate kernels
-        # (same inputs, same flush), outside the timed region
+        # (same inputs, same flush), outside the timed region, after one
+        # untimed pass (their first launches load the kernels' modules)
         sep = []
         with torch.cuda.stream(stream):
+            vp.zero_counts(counts, stream)
+            for e in range(3):
+                job.launch(e, words[e], counts[e:e + 1], stream)
             for _ in range(args.steps):
                 if flush is not None:
                     flush_sink.copy_(flush.view(torch.int64).sum(dtype=torch.int64).view(1))
