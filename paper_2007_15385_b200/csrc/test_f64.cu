@@ -31,7 +31,8 @@ __device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a,
 __device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a, b); }
 
 // The offset engine's per-point step as explicit PTX, so the comparison
-// feeds a predicated increment (one ALU op) instead of an add and a select.
+// feeds a predicated increment (one ALU op) instead of an add and a select
+// (per-engine kernel at C5 in f64: 21.9 -> 20.1 ms).
 // The arithmetic is the reference's, individually rounded.
 //
 // offset (engines.cpp:150-153): flags += (qy*dvx - qx*dvy < rhs)
@@ -77,10 +78,7 @@ __device__ __forceinline__ void flush_count(uint32_t cnt, const TestArgs& a) {
 
 // One engine's test of P points per lane against its per-edge records
 // (`tab`: shared or global memory), exactly as the reference computes it.
-// kPtxStep: the offset engine's step as explicit PTX (offset_step) -- 8 %
-// faster in the per-engine kernel, 4 % slower inside the fused kernel (C5
-// in f64), so only the per-engine kernel takes it
-template <int kEngine, int P, bool kPtxStep = false>
+template <int kEngine, int P>
 __device__ __forceinline__ void exact_eval(uint32_t n, double inner_x, double inner_y,
                                            const void* tab, const double (&x)[P],
                                            const double (&y)[P], bool (&in)[P]) {
@@ -111,12 +109,7 @@ __device__ __forceinline__ void exact_eval(uint32_t n, double inner_x, double in
       const OffsetEdgeF64 r = s[e];
 #pragma unroll
       for (int p = 0; p < P; ++p) {
-        if constexpr (kPtxStep) {
-          offset_step(x[p], y[p], r.dvx, r.dvy, r.rhs, flags[p]);
-        } else {
-          const double lhs = dsub(dmul(y[p], r.dvx), dmul(x[p], r.dvy));
-          flags[p] += lhs < r.rhs;
-        }
+        offset_step(x[p], y[p], r.dvx, r.dvy, r.rhs, flags[p]);
       }
     }
 #pragma unroll
@@ -220,7 +213,7 @@ __global__ void __launch_bounds__(kThreads) exact_kernel(const DevTables t, cons
     double x[P], y[P];
     bool in[P];
     load_tile<P>(a, base, lane, x, y);
-    exact_eval<kEngine, P, true>(n, t.inner_x, t.inner_y, s_tab, x, y, in);
+    exact_eval<kEngine, P>(n, t.inner_x, t.inner_y, s_tab, x, y, in);
 #pragma unroll
     for (int p = 0; p < P; ++p) in[p] = in[p] & (base + 32u * p + lane < a.m);
     count += emit_words<P>(in, base, a.m, a, lane);
