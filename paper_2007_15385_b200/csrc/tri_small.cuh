@@ -161,13 +161,23 @@ __device__ __forceinline__ void tri_small_slice(const TriSmallParams<NC, K>& prm
     x[p] = ok ? __ldcs(xs + 32 * p) : 0.f;
     y[p] = ok ? __ldcs(ys + 32 * p) : 0.f;
   }
-  // crossing on the points as loaded (absolute-frame table), as tri_kernel
-  cc += emit4<kGuard, 2, P>(
-      [&](int p, float& a, float& b) {
-        a = __uint_as_float(cross_one<NC>(prm.cross, x[p], y[p]));
-        b = 0.f;
-      },
-      base, ac, lane, live);
+  // crossing on the points as loaded (absolute-frame table), as tri_kernel;
+  // from five vertices on (and no local-frame shift, which must follow it)
+  // after the two slab engines, which measured faster there (C3 n = 8:
+  // 0.735 -> 0.710 ms; n = 5-7 1-3 %; n = 3-4 5-6 % slower, so first there)
+  auto crossing = [&] {
+    cc += emit4<kGuard, 2, P>(
+        [&](int p, float& a, float& b) {
+          a = __uint_as_float(cross_one<NC>(prm.cross, x[p], y[p]));
+          b = 0.f;
+        },
+        base, ac, lane, live);
+  };
+#ifndef VPIPG_SMALL_CROSS_LAST_N
+#define VPIPG_SMALL_CROSS_LAST_N 5
+#endif
+  constexpr bool kCrossLast = !kShift && NC >= VPIPG_SMALL_CROSS_LAST_N;
+  if constexpr (!kCrossLast) crossing();
   if constexpr (kShift) {
 #pragma unroll
     for (int p = 0; p < P; ++p) {
@@ -179,6 +189,7 @@ __device__ __forceinline__ void tri_small_slice(const TriSmallParams<NC, K>& prm
                             base, av, lane, live);
   co += emit4<kGuard, 1, P>([&](int p, float& a, float& b) { slab_one<K, MODE>(prm.slab[1], x[p], y[p], b, a); },
                             base, ao, lane, live);
+  if constexpr (kCrossLast) crossing();
 }
 
 #ifndef VPIPG_TRI_SMALL_MINB
