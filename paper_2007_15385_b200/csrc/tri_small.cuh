@@ -162,9 +162,10 @@ __device__ __forceinline__ void tri_small_slice(const TriSmallParams<NC, K>& prm
     y[p] = ok ? __ldcs(ys + 32 * p) : 0.f;
   }
   // crossing on the points as loaded (absolute-frame table), as tri_kernel;
-  // from five vertices on (and no local-frame shift, which must follow it)
-  // after the two slab engines, which measured faster there (C3 n = 8:
-  // 0.735 -> 0.710 ms; n = 5-7 1-3 %; n = 3-4 5-6 % slower, so first there)
+  // for 5-8 vertices (and no local-frame shift, which must follow it) after
+  // the two slab engines, which measured faster there (C3 n = 8: 0.735 ->
+  // 0.710 ms; n = 5-7 1-3 %); first below (n = 3-4: 5-6 % slower last) and
+  // above (C2, n = 12: 1 % slower last)
   auto crossing = [&] {
     cc += emit4<kGuard, 2, P>(
         [&](int p, float& a, float& b) {
@@ -173,10 +174,7 @@ __device__ __forceinline__ void tri_small_slice(const TriSmallParams<NC, K>& prm
         },
         base, ac, lane, live);
   };
-#ifndef VPIPG_SMALL_CROSS_LAST_N
-#define VPIPG_SMALL_CROSS_LAST_N 5
-#endif
-  constexpr bool kCrossLast = !kShift && NC >= VPIPG_SMALL_CROSS_LAST_N;
+  constexpr bool kCrossLast = !kShift && NC >= 5 && NC <= 8;
   if constexpr (!kCrossLast) crossing();
   if constexpr (kShift) {
 #pragma unroll
