@@ -73,6 +73,42 @@ def _check_device_batch(xs, ys, dtypes, outs=(), ids=None, device=None) -> None:
                            "masks and int64 counters of sufficient size are required")
 
 
+def _host_view(a):
+    """(dtype name, numel, 1-D contiguous host buffer, element size) of a numpy
+    array or a CPU torch tensor; None for anything else."""
+    if isinstance(a, np.ndarray):
+        return a.dtype.name, a.size, a.ndim == 1 and a.flags.c_contiguous, a.itemsize
+    if hasattr(a, "is_cuda") and hasattr(a, "element_size"):
+        return (str(a.dtype).rsplit(".", 1)[-1], a.numel(),
+                a.dim() == 1 and a.is_contiguous() and not a.is_cuda, a.element_size())
+    return None
+
+
+def _check_host_batch(xs, ys, dtypes, ids=None, words=None) -> None:
+    """The host-buffer calls read m elements of xs / ys (/ ids) and write
+    ceil(m/32) words per engine through raw pointers, so the mirror checks what
+    the C-ABI cannot see (InvalidParameter, code 6): 1-D contiguous host
+    buffers of one floating dtype and one length, 4-byte integer ids, and
+    caller-provided word buffers of 4-byte elements large enough for the batch."""
+    vx, vy = _host_view(xs), _host_view(ys)
+    ok = (vx is not None and vy is not None and vx[2] and vy[2] and vx[0] in dtypes
+          and vy[0] == vx[0] and vy[1] == vx[1])
+    m = vx[1] if ok else 0
+    if ok and ids is not None:
+        vi = _host_view(ids)
+        ok = vi is not None and vi[2] and vi[1] == m and vi[0] in ("int32", "uint32")
+    for w in (words or ()):
+        if w is None or not ok:
+            continue
+        vw = _host_view(w)
+        ok = (vw is not None and vw[2] and vw[3] == 4 and vw[0] in ("int32", "uint32")
+              and vw[1] >= (m + 31) // 32)
+    if not ok:
+        raise VpipError(6, "host batch: 1-D contiguous host buffers (numpy or CPU tensors) of "
+                           f"matching length and dtype ({', '.join(dtypes)}), 32-bit ids and "
+                           "32-bit mask-word buffers of ceil(m/32) elements are required")
+
+
 def _engine_id(engine) -> int:
     return ENGINES[engine] if isinstance(engine, str) else int(engine)
 
@@ -202,6 +238,7 @@ class PreparedPolygon:
     def test_host(self, engine, xs: np.ndarray, ys: np.ndarray, words: bool = True,
                   bytes_: bool = False):
         """Host-buffer drop-in (vpipg_test_host): returns (words|None, bytes|None, count)."""
+        _check_host_batch(xs, ys, ("float32", "float64"))
         dtype = F32 if xs.dtype == np.float32 else F64
         m = xs.size
         w = np.zeros((m + 31) // 32, dtype=np.uint32) if words else None
@@ -246,6 +283,7 @@ class PreparedPolygon:
 
         `words`: optional list of 3 preallocated uint32 arrays (e.g. pinned
         buffers); returns (words list, counts list)."""
+        _check_host_batch(xs, ys, ("float32", "float64"), words=words)
         is_np = isinstance(xs, np.ndarray)
         dtype = F32 if str(xs.dtype).endswith("float32") else F64
         m = xs.size if is_np else xs.numel()
@@ -268,8 +306,10 @@ class PreparedPolygon:
 class PolygonDB:
     """A CSR batch of polygons prepared on the device (vpipg_prepare_csr)."""
 
-    def __init__(self, handle: C.c_void_p, npoly: int, status: np.ndarray, device: int = 0):
+    def __init__(self, handle: C.c_void_p, npoly: int, status: np.ndarray, device: int = 0,
+                 offsets: np.ndarray | None = None):
         self._h = handle
+        self.offsets = offsets
         self.npoly = npoly
         self.status = status
         self.device = device
@@ -280,12 +320,18 @@ class PolygonDB:
         vx = np.ascontiguousarray(vx, dtype=np.float64)
         vy = np.ascontiguousarray(vy, dtype=np.float64)
         npoly = offsets.size - 1
+        # the C-ABI checks that offsets start at 0 and never decrease, but it
+        # cannot see the vertex arrays' length: it reads offsets[-1] of each
+        if (offsets.ndim != 1 or npoly < 0 or vx.ndim != 1 or vx.shape != vy.shape
+                or int(offsets[-1]) > vx.size):
+            raise VpipError(6, "prepare_csr: 1-D offsets of npoly + 1 entries whose last entry "
+                               "does not exceed the length of vx == length of vy")
         status = np.zeros(max(npoly, 1), dtype=np.int32)
         h = C.c_void_p()
         check(load().vpipg_prepare_csr(C.c_void_p(offsets.ctypes.data), _dptr(vx), _dptr(vy),
                                        npoly, kinds, device, _stream_ptr(stream), C.byref(h),
                                        C.c_void_p(status.ctypes.data)), "vpipg_prepare_csr")
-        return cls(h, npoly, status[:npoly], device)
+        return cls(h, npoly, status[:npoly], device, offsets.copy())
 
     def close(self) -> None:
         if self._h:
@@ -304,8 +350,15 @@ class PolygonDB:
     def __exit__(self, *exc):
         self.close()
 
-    def generators(self, poly: int, n: int):
-        inner, outer = np.zeros(2), np.zeros((n, 2))
+    def generators(self, poly: int, n: int | None = None):
+        """(inner[2], outer[n, 2]) of polygon `poly`; n is its vertex count
+        (taken from the offsets; a caller's n must agree with it)."""
+        if not 0 <= poly < self.npoly or self.offsets is None:
+            raise VpipError(6, "generators: polygon index out of range (or no offsets)")
+        size = int(self.offsets[poly + 1]) - int(self.offsets[poly])
+        if n is not None and n != size:
+            raise VpipError(6, f"generators: polygon {poly} has {size} vertices, not {n}")
+        inner, outer = np.zeros(2), np.zeros((size, 2))
         check(load().vpipg_db_generators(self._h, poly, _dptr(inner), _dptr(outer)), "generators")
         return inner, outer
 
@@ -346,6 +399,7 @@ class PolygonDB:
         """The join over host buffers (vpipg_test_gather_host): float32 xs / ys and
         uint32 / int32 ids, numpy arrays or (pinned) CPU tensors. Returns
         (words list, counts list)."""
+        _check_host_batch(xs, ys, ("float32",), ids=ids, words=words)
         m = xs.size if isinstance(xs, np.ndarray) else xs.numel()
         mask = 0
         for e in engines:

@@ -139,3 +139,42 @@ def test_python_mirror_rejects_bad_device_batches():
     with pytest.raises(vp.VpipError) as e:
         db.test(0, x, x, torch.zeros(63, dtype=torch.int32))
     assert e.value.code == 6
+
+
+def test_python_mirror_rejects_bad_host_batches():
+    """The host-buffer calls read m elements through raw pointers: the mirror
+    rejects mismatched lengths / dtypes, non-float points, short or wide
+    caller word buffers, bad join ids, and CSR offsets past the vertex arrays
+    (code 6) before anything reaches the C-ABI."""
+    import torch
+    p = object.__new__(vp.PreparedPolygon)
+    p._h, p.device = None, 0
+    x32, x64 = np.zeros(100, np.float32), np.zeros(100, np.float64)
+    bad = [
+        lambda: p.test_host(0, x32, x32[:99]),                 # short ys
+        lambda: p.test_host(0, x32, x64),                      # mixed dtypes
+        lambda: p.test_host(0, np.zeros(100, np.int64), np.zeros(100, np.int64)),
+        lambda: p.test_host(0, np.zeros((10, 10), np.float32), np.zeros((10, 10), np.float32)),
+        lambda: p.test_host(0, x64[::2], x64[::2]),            # strided
+        lambda: p.test_host_multi(x32, x32, words=[np.zeros(3, np.uint32), None, None]),
+        lambda: p.test_host_multi(x32, x32, words=[np.zeros(4, np.uint64), None, None]),
+        lambda: p.test_host_multi(torch.zeros(100), torch.zeros(99)),
+        lambda: p.test_host_multi([0.0] * 100, [0.0] * 100),
+    ]
+    db = object.__new__(vp.PolygonDB)
+    db._h, db.device, db.npoly, db.offsets = None, 0, 2, np.array([0, 4, 9], np.uint32)
+    ids = np.zeros(100, np.uint32)
+    bad += [
+        lambda: db.test_host(x64, x64, ids),                   # join points are f32
+        lambda: db.test_host(x32, x32, ids[:50]),
+        lambda: db.test_host(x32, x32, np.zeros(100, np.int64)),
+        lambda: db.generators(2),                              # index out of range
+        lambda: db.generators(1, 4),                           # polygon 1 has 5 vertices
+        lambda: vp.PolygonDB.prepare([0, 4, 9], np.zeros(8), np.zeros(8)),
+        lambda: vp.PolygonDB.prepare([0, 4], np.zeros(4), np.zeros(5)),
+        lambda: vp.PolygonDB.prepare([], np.zeros(4), np.zeros(4)),
+    ]
+    for i, f in enumerate(bad):
+        with pytest.raises(vp.VpipError) as e:
+            f()
+        assert e.value.code == 6, i
