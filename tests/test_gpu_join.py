@@ -323,3 +323,57 @@ def test_fused_join_on_the_c4_database(orc):
             db.test(e, xs, ys, ids, words=w, count=c)
             torch.cuda.synchronize()
             assert torch.equal(ws[e], w) and cs[e].item() == c.item(), e
+
+
+def _sized_db(sizes, seed=7):
+    """CSR database of vpip::random_convex_polygon(n_i) for the given sizes
+    (vpip::regular_polygon above 100 vertices, where the reference sampler
+    finds no well-spaced angle draw), centres in [0, 1000]^2 and radii in
+    [0.5, 5] (the C4 pair stream's box)."""
+    rng = np.random.default_rng(seed)
+    sizes = np.asarray(sizes, np.int64)
+    cx, cy = rng.uniform(0, 1000, sizes.size), rng.uniform(0, 1000, sizes.size)
+    r = rng.uniform(0.5, 5.0, sizes.size)
+    off = np.zeros(sizes.size + 1, np.uint32)
+    off[1:] = np.cumsum(sizes)
+    vx, vy = np.empty(int(off[-1])), np.empty(int(off[-1]))
+    for k, n in enumerate(sizes):
+        c = (float(cx[k]), float(cy[k]))
+        vx[off[k]:off[k + 1]], vy[off[k]:off[k + 1]] = (
+            vp.regular_polygon(int(n), float(r[k]), c) if n > 100 else
+            vp.random_convex_polygon(int(n), 1000 + k, float(r[k]), c))
+    return off, vx, vy, cx, cy, r
+
+
+@pytest.mark.parametrize("layout", ["packed", "fixed_wide"])
+def test_join_polygons_above_16_vertices(orc, layout):
+    """Polygons whose rows run past the header's first two 4-row chunks and the
+    loop's chunk pairs: a 4..16 database with a few 17..1000-gons (records
+    packed with per-polygon offsets, the largest record is far above 1.5x the
+    mean) and a 17..24-gon database (fixed stride). Every engine against the
+    oracle outside the band, and the fused join equal to the separate kernels."""
+    rng = np.random.default_rng(11)
+    if layout == "packed":
+        sizes = np.concatenate([rng.integers(4, 17, 1020), [17, 20, 33, 64, 100, 255, 500, 1000]])
+    else:
+        sizes = rng.integers(17, 25, 1024)
+    off, vx, vy, cx, cy, r = _sized_db(rng.permutation(sizes))
+    m = 1 << 18
+    _gather_vs_oracle(orc, m, off, vx, vy, cx, cy, r)
+    dcx, dcy, dr = (torch.as_tensor(a, device=DEV) for a in (cx, cy, r))
+    xs = torch.empty(m, dtype=torch.float32, device=DEV)
+    ys = torch.empty_like(xs)
+    ids = torch.empty(m, dtype=torch.int32, device=DEV)
+    vp.fill_join_pairs(W.c4_pair_seed(), 0, xs, ys, ids, dcx, dcy, dr)
+    nw = (m + 31) // 32
+    with vp.PolygonDB.prepare(off, vx, vy, vp.KIND_ALL) as db:
+        assert not db.status.any()
+        ws = [torch.zeros(nw, dtype=torch.int32, device=DEV) for _ in range(3)]
+        cs = [torch.zeros(1, dtype=torch.int64, device=DEV) for _ in range(3)]
+        db.test_multi(xs, ys, ids, words=ws, counts=cs)
+        for e in range(3):
+            w = torch.zeros(nw, dtype=torch.int32, device=DEV)
+            c = torch.zeros(1, dtype=torch.int64, device=DEV)
+            db.test(e, xs, ys, ids, words=w, count=c)
+            torch.cuda.synchronize()
+            assert torch.equal(ws[e], w) and cs[e].item() == c.item(), e
