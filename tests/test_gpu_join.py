@@ -215,7 +215,7 @@ def test_gather_nan_points(orc):
             assert np.array_equal(got, want), (e, got.tolist(), want.tolist())
 
 
-@pytest.mark.parametrize("m", [1, 33, 4099, 100003])
+@pytest.mark.parametrize("m", [0, 1, 33, 4099, 100003])
 def test_gather_outputs_have_no_stray_writes(m):
     """Canaries around the join's word / byte outputs stay untouched; bits past
     m in the last word are zero."""
@@ -264,7 +264,7 @@ def test_gather_host_buffers_equal_device_path(orc):
                 assert np.array_equal(words[e], ref[e][0]) and cnt[e] == ref[e][1], e
 
 
-@pytest.mark.parametrize("m", [1, 33, 4099, 1 << 20])
+@pytest.mark.parametrize("m", [0, 1, 33, 4099, 1 << 20])
 def test_fused_join_equals_separate_engines(m):
     """vpipg_test_gather_multi with all three engines (one fused kernel: offset
     and crossing share one walk over the vertex rows unless validation reversed
@@ -377,3 +377,20 @@ def test_join_polygons_above_16_vertices(orc, layout):
             db.test(e, xs, ys, ids, words=w, count=c)
             torch.cuda.synchronize()
             assert torch.equal(ws[e], w) and cs[e].item() == c.item(), e
+
+
+def test_empty_host_batches():
+    """m = 0 through every host-buffer entry point: no work, zero counts, empty
+    word arrays (the reference's batch calls accept an empty PointBatch)."""
+    off, vx, vy, cx, cy, r = _db_inputs(64)
+    e32, e64, eid = np.zeros(0, np.float32), np.zeros(0), np.zeros(0, np.uint32)
+    with vp.PolygonDB.prepare(off, vx, vy, vp.KIND_ALL) as db:
+        words, cnt = db.test_host(e32, e32, eid)
+        assert cnt == [0, 0, 0] and all(w.size == 0 for w in words)
+    pvx, pvy = W.c1_polygon()
+    with vp.PreparedPolygon.prepare(pvx, pvy, vp.KIND_ALL) as p:
+        for e in range(3):
+            w, b, c = p.test_host(e, e64, e64, words=True, bytes_=True)
+            assert w.size == 0 and b.size == 0 and c == 0
+        words, cnt = p.test_host_multi(e32, e32)
+        assert cnt == [0, 0, 0] and all(w.size == 0 for w in words)
