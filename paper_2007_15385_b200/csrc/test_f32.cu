@@ -138,72 +138,40 @@ struct SlabEngine {
   // third operand of the first FMNMX3 (prep.cu guarantees >= 1 pair per
   // group). With wlo = whi = w, afterwards lo >= w >= hi and the point
   // satisfies the section iff lo <= hi.
-  // kHyb (the fused kernel with parameter-bank tables): the slopes a.x / a.z
-  // come from the parameter-bank copy UA / UB of the same records (uniform
-  // registers), the intercepts a.y / a.w from shared memory (vector
-  // registers). An FFMA with three vector-register sources reads two registers
-  // from one bank and holds the dispatch for two cycles whenever the operand
-  // reuse cache misses (DESIGN 4.2); with the slope as a uniform operand it has
-  // two vector sources and issues every cycle.
-  template <bool kHyb = false>
   __device__ __forceinline__ static void section(const float4* A, uint32_t na, const float4* B,
                                                  uint32_t nb, const float (&v)[P],
                                                  const float (&wlo)[P], const float (&whi)[P],
-                                                 float (&lo)[P], float (&hi)[P],
-                                                 const float4* U = nullptr, uint32_t ua = 0,
-                                                 uint32_t ub = 0) {
-    // U[ua + i] / U[ub + i]: the parameter-bank copies of A[i] / B[i]. ua and
-    // ub are parameter words and run as their own counters, so that the slope
-    // addresses stay on the uniform datapath whatever registers the shared-
-    // memory addresses live in.
-    auto slopes = [&](const float4& rec, uint32_t ui, float& sx, float& sz) {
-      if constexpr (kHyb) {
-        sx = U[ui].x;
-        sz = U[ui].z;
-      } else {
-        sx = rec.x;
-        sz = rec.z;
-      }
-    };
+                                                 float (&lo)[P], float (&hi)[P]) {
     {
       const float4 a = A[0], b = B[0];
-      float ax, az, bx, bz;
-      slopes(a, ua, ax, az);
-      slopes(b, ub, bx, bz);
 #pragma unroll
       for (int p = 0; p < P; ++p) {
-        lo[p] = fmax3(wlo[p], fmaf(ax, v[p], a.y), fmaf(az, v[p], a.w));
-        hi[p] = fmin3(whi[p], fmaf(bx, v[p], b.y), fmaf(bz, v[p], b.w));
+        lo[p] = fmax3(wlo[p], fmaf(a.x, v[p], a.y), fmaf(a.z, v[p], a.w));
+        hi[p] = fmin3(whi[p], fmaf(b.x, v[p], b.y), fmaf(b.z, v[p], b.w));
       }
     }
-    const uint32_t nc = na < nb ? na : nb;  // >= 1 (prep.cu)
+    const uint32_t nc = na < nb ? na : nb;
+    uint32_t i = 1;
     VPIPG_UNROLL(VPIPG_SLAB_UNROLL)
-    for (uint32_t i = 1; i < nc; ++i) {
+    for (; i < nc; ++i) {
       const float4 a = A[i], b = B[i];
-      float ax, az, bx, bz;
-      slopes(a, ++ua, ax, az);
-      slopes(b, ++ub, bx, bz);
 #pragma unroll
       for (int p = 0; p < P; ++p) {
-        lo[p] = fmax3(lo[p], fmaf(ax, v[p], a.y), fmaf(az, v[p], a.w));
-        hi[p] = fmin3(hi[p], fmaf(bx, v[p], b.y), fmaf(bz, v[p], b.w));
+        lo[p] = fmax3(lo[p], fmaf(a.x, v[p], a.y), fmaf(a.z, v[p], a.w));
+        hi[p] = fmin3(hi[p], fmaf(b.x, v[p], b.y), fmaf(b.z, v[p], b.w));
       }
     }
 #pragma unroll 1
-    for (uint32_t j = nc; j < na; ++j) {
+    for (uint32_t j = i; j < na; ++j) {
       const float4 a = A[j];
-      float ax, az;
-      slopes(a, ++ua, ax, az);
 #pragma unroll
-      for (int p = 0; p < P; ++p) lo[p] = fmax3(lo[p], fmaf(ax, v[p], a.y), fmaf(az, v[p], a.w));
+      for (int p = 0; p < P; ++p) lo[p] = fmax3(lo[p], fmaf(a.x, v[p], a.y), fmaf(a.z, v[p], a.w));
     }
 #pragma unroll 1
-    for (uint32_t j = nc; j < nb; ++j) {
+    for (uint32_t j = i; j < nb; ++j) {
       const float4 b = B[j];
-      float bx, bz;
-      slopes(b, ++ub, bx, bz);
 #pragma unroll
-      for (int p = 0; p < P; ++p) hi[p] = fmin3(hi[p], fmaf(bx, v[p], b.y), fmaf(bz, v[p], b.w));
+      for (int p = 0; p < P; ++p) hi[p] = fmin3(hi[p], fmaf(b.x, v[p], b.y), fmaf(b.z, v[p], b.w));
     }
   }
 
@@ -216,40 +184,25 @@ struct SlabEngine {
   // section 1 did: y + f1 > y for every f1 that survives rounding against y,
   // and an f1 below half an ulp of y is a violation of < 6e-8 |y|, inside the
   // 1e-5 band. One compare per point decides both sections.
-  template <bool kHyb = false>
   __device__ __forceinline__ static void eval(const Params& prm, const float4* s,
                                               const float (&x)[P], const float (&y)[P],
-                                              float (&a)[P], float (&b)[P],
-                                              const float4* u = nullptr,
-                                              const uint32_t* uoff = nullptr) {
+                                              float (&a)[P], float (&b)[P]) {
     const SlabTable& t = prm.tab;
     float lo[P], hi[P];
-    // kHyb: group k's records in the parameter-bank copy; the offsets come from
-    // their own parameter words (uoff), so that the slope addresses stay on the
-    // uniform datapath (t.off also feeds the shared-memory addresses and ends
-    // up in vector registers)
-    auto grp = [&](int k) -> uint32_t {
-      if constexpr (kHyb) return uoff[k];
-      else return 0;
-    };
     // single-section tables: y alone, bounded by lines in x (mode 1), or x
     // alone, bounded by lines in y (mode 2)
     auto y_only = [&] {
-      section<kHyb>(s + t.off[2] / 2, t.cnt[2] / 2, s + t.off[3] / 2, t.cnt[3] / 2, x, y, y, lo, hi,
-                    u, grp(2), grp(3));
+      section(s + t.off[2] / 2, t.cnt[2] / 2, s + t.off[3] / 2, t.cnt[3] / 2, x, y, y, lo, hi);
     };
     auto x_only = [&] {
-      section<kHyb>(s + t.off[0] / 2, t.cnt[0] / 2, s + t.off[1] / 2, t.cnt[1] / 2, y, x, x, lo, hi,
-                    u, grp(0), grp(1));
+      section(s + t.off[0] / 2, t.cnt[0] / 2, s + t.off[1] / 2, t.cnt[1] / 2, y, x, x, lo, hi);
     };
     auto mixed = [&] {
-      section<kHyb>(s + t.off[0] / 2, t.cnt[0] / 2, s + t.off[1] / 2, t.cnt[1] / 2, y, x, x, lo, hi,
-                    u, grp(0), grp(1));
+      section(s + t.off[0] / 2, t.cnt[0] / 2, s + t.off[1] / 2, t.cnt[1] / 2, y, x, x, lo, hi);
       float seed[P];
 #pragma unroll
       for (int p = 0; p < P; ++p) seed[p] = y[p] + (lo[p] - hi[p]);
-      section<kHyb>(s + t.off[2] / 2, t.cnt[2] / 2, s + t.off[3] / 2, t.cnt[3] / 2, x, seed, y, lo, hi,
-                    u, grp(2), grp(3));
+      section(s + t.off[2] / 2, t.cnt[2] / 2, s + t.off[3] / 2, t.cnt[3] / 2, x, seed, y, lo, hi);
     };
     if constexpr (kMode == 0) {
       mixed();
@@ -620,7 +573,6 @@ struct TriParamsInl {   // the three tables in the parameter bank (VPIPG_INLINE)
   SlabParams v, o;
   CrossParams c;
   uint32_t off_o, off_c;  // float4 offsets of the offset / crossing tables in `t`
-  uint32_t uoff[8];       // float4 offsets in `t` of the four groups of the Voronoi / offset tables
   float4 t[kTriInlineMax];
 };
 
@@ -631,9 +583,6 @@ struct TriParamsInl {   // the three tables in the parameter bank (VPIPG_INLINE)
 // slab kernels) and only the crossing table read as uniform registers
 #ifndef VPIPG_TRI_SLAB_SMEM
 #define VPIPG_TRI_SLAB_SMEM 1
-#endif
-#ifndef VPIPG_TRI_SLAB_HYBRID
-#define VPIPG_TRI_SLAB_HYBRID 1
 #endif
 #ifndef VPIPG_TRI_MINB
 #define VPIPG_TRI_MINB 2
@@ -649,8 +598,6 @@ __global__ void __launch_bounds__(kThreads, VPIPG_TRI_MINB)
   static_assert(TriV::kRegStream && TriO::kRegStream, "slab engines stream through registers");
   constexpr int P = kTriP;
   constexpr int kWarpPts = 32 * P;
-  // slab slopes from the parameter bank, intercepts from shared memory
-  constexpr bool kHyb = kInline && VPIPG_TRI_SLAB_SMEM && VPIPG_TRI_SLAB_HYBRID;
   extern __shared__ __align__(128) unsigned char smem[];
   float4* s_tab = reinterpret_cast<float4*>(smem);
   const float4* tv;
@@ -706,11 +653,9 @@ __global__ void __launch_bounds__(kThreads, VPIPG_TRI_MINB)
       cc += emit<false, TriC::kVote, P>(va, vb, g * kWarpPts, ac, lane, live);
     }
     to_local(x, y, prm.v.ox, prm.v.oy);
-    if constexpr (kHyb) TriV::template eval<true>(prm.v, tv, x, y, va, vb, prm.t, prm.uoff);
-    else TriV::eval(prm.v, tv, x, y, va, vb);
+    TriV::eval(prm.v, tv, x, y, va, vb);
     cv += emit<false, TriV::kVote, P>(va, vb, g * kWarpPts, av, lane, live);
-    if constexpr (kHyb) TriO::template eval<true>(prm.o, to, x, y, va, vb, prm.t, prm.uoff + 4);
-    else TriO::eval(prm.o, to, x, y, va, vb);
+    TriO::eval(prm.o, to, x, y, va, vb);
     co += emit<false, TriO::kVote, P>(va, vb, g * kWarpPts, ao, lane, live);
     if constexpr (!kInline) {
       TriC::eval(prm.c, tc, x, y, va, vb);
@@ -867,10 +812,6 @@ cudaError_t launch_test_f32_all(const DevTables& t, const TestArgs* a, cudaStrea
     pi.c = prm.c;
     pi.off_o = prm.off_o;
     pi.off_c = prm.off_c;
-    for (int k = 0; k < 4; ++k) {
-      pi.uoff[k] = t.slab[0].off[k] / 2;
-      pi.uoff[4 + k] = prm.off_o + t.slab[1].off[k] / 2;
-    }
     std::memcpy(pi.t, t.h_slab[0], nv * sizeof(float4));
     std::memcpy(pi.t + nv, t.h_slab[1], no * sizeof(float4));
     for (size_t k = 0; k < nc; ++k) pi.t[nv + no + k] = cross_record_abs(t.h_cross[k], t.ox, t.oy);
