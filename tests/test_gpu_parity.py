@@ -518,6 +518,13 @@ def test_fused_multi_engine_pass_equals_separate_calls(m):
     xs = torch.empty(m, dtype=torch.float32, device=DEV)
     ys = torch.empty_like(xs)
     vp.fill_uniform_points(W.c5_point_seed(), 0, xs, ys, W.C5_BOX)
+    # non-finite coordinates too (full slices and the guarded tail alike): the
+    # fused kernel repeats the per-engine kernels' NaN / inf behaviour bit for bit
+    bad = torch.as_tensor(np.random.default_rng(m).choice(m, min(m, 96), replace=False), device=DEV)
+    xs[bad[0::4]] = float("nan")
+    ys[bad[1::4]] = float("nan")
+    xs[bad[2::4]] = float("inf")
+    ys[bad[3::4]] = float("-inf")
     nw = (m + 31) // 32
     with vp.PreparedPolygon.prepare(vx, vy, vp.KIND_ALL) as p:
         ref = []
@@ -535,6 +542,11 @@ def test_fused_multi_engine_pass_equals_separate_calls(m):
         for e in range(3):
             assert torch.equal(ws[e], ref[e][0]) and torch.equal(bs[e], ref[e][1]), e
             assert cs[e].item() == ref[e][2].item(), e
+        # the reference's IEEE answers on NaN coordinates (engines.cpp:85-98, :147-157,
+        # :176-199): Voronoi outside, sign-of-offset inside, crossing outside when qy is NaN
+        nan = torch.isnan(xs) | torch.isnan(ys)
+        assert nan.any() and not bs[0][nan].any() and bs[1][nan].all()
+        assert not bs[2][torch.isnan(ys)].any()
 
 
 def _offset_table_mode(vx, vy, steep=16):
