@@ -106,6 +106,15 @@ def test_f64_non_finite_points_bit_exact(golden, name):
             w, b, c = run_device(p, e, xs, ys)
             assert np.array_equal(b, want[e]), (name, e, b.tolist(), want[e].tolist())
             assert c == int(want[e].sum())
+        # and the fused exact kernel (one read of the points for all three engines)
+        xt, yt = torch.as_tensor(xs, device=DEV), torch.as_tensor(ys, device=DEV)
+        bs = [torch.zeros(xs.size, dtype=torch.uint8, device=DEV) for _ in range(3)]
+        cs = [torch.zeros(1, dtype=torch.int64, device=DEV) for _ in range(3)]
+        p.test_multi(xt, yt, bytes_=bs, counts=cs)
+        torch.cuda.synchronize()
+        for e in range(3):
+            assert np.array_equal(bs[e].cpu().numpy(), want[e]), (name, e)
+            assert cs[e].item() == int(want[e].sum())
 
 
 def test_f32_nan_points_follow_the_reference(golden, orc):
